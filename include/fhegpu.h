@@ -1,0 +1,129 @@
+/*
+ * fhegpu.h -- C ABI of the B200 engine for the encrypted-FFT hot path.
+ *
+ * The reference (arxiv 1611.08769, package `fhefft`, pure Python) has no FFI;
+ * its plugin boundary for this path is the duck-typed bit-engine protocol
+ * (fhefft/engine.py:69-214) over the scheme operators GswScheme.hom_nand /
+ * GswScheme.hom_not (fhefft/fhe.py:325-350).  This library is what a
+ * maintainer would bind (ctypes) to replace those two
+ * operators and the engine's gate-at-a-time evaluation:
+ *
+ *   fhegpu_nand_batch   replaces GswScheme.hom_nand   (fhe.py:325-341), batched
+ *   fhegpu_not_batch    replaces GswScheme.hom_not    (fhe.py:343-350), batched
+ *   fhegpu_prog_*       replaces FheEngine.nand/_fold  (engine.py:168-187) applied
+ *                       gate by gate: a whole levelised netlist (every gate of
+ *                       every butterfly of every signal) runs as one kernel per level
+ *   fhegpu_store_*      replaces the Ciphertext objects the engine keeps alive
+ *                       (engine.py:57-66, fhe.py:148-161): device-resident compact
+ *                       ciphertexts, read back for export_ct/read_back (engine.py:189-207)
+ *
+ * Ciphertext representation (bit-identical to the reference matrix): a
+ * reference ciphertext is the flattened N x N 0/1 matrix C = decompose(V); the
+ * library stores V, an N x k row-major matrix of u32 values in [0, q)
+ * (k = n + 1, N = k * ell).  Each ciphertext occupies ct_words u32 (N*k
+ * padded to a multiple of 4 so every ciphertext is 16-byte aligned for bulk
+ * copies).  NAND:  V = (G - bits(V1) V2) mod q.   NOT:  V = (G - V) mod q.
+ *
+ * Conventions: every call returns 0 (FHEGPU_OK) or an error code and sets a
+ * thread-local message (fhegpu_last_error).  Host arrays are borrowed for the
+ * duration of the call.  Device memory is owned by the context.  A context is
+ * bound to one device and one stream and is not thread safe.
+ */
+#ifndef FHEGPU_H
+#define FHEGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fhegpu_ctx fhegpu_ctx;
+typedef struct fhegpu_prog fhegpu_prog;
+
+typedef struct {
+  uint32_t n;    /* lattice dimension (SchemeParams.n); k = n + 1 */
+  uint32_t ell;  /* bits per Z_q value = bitlen(q - 1) (SchemeParams.ell) */
+  uint32_t q;    /* odd modulus, 8 <= q < 2^31 for this library */
+  uint32_t m;    /* public-key rows (SchemeParams.m); used by encryption only */
+} fhegpu_params;
+
+/* One netlist gate.  `left` is the operand the reference multiplies on the
+ * left AFTER its noise swap (fhe.py:336-337).  Flags bit 0 / bit 1 complement
+ * the left / right operand on load: that is how NOT gates (hom_not, produced
+ * only by folding NAND(x, 1), engine.py:180-187) are evaluated for free. */
+typedef struct {
+  uint32_t left;
+  uint32_t right;
+  uint32_t out;
+  uint32_t flags;
+} fhegpu_op;
+
+enum {
+  FHEGPU_OK = 0,
+  FHEGPU_EINVAL = 1,
+  FHEGPU_ECUDA = 2,
+  FHEGPU_ENOMEM = 3,
+  FHEGPU_EUNSUP = 4
+};
+
+enum {
+  FHEGPU_OP_COMPLEMENT_LEFT = 1u,
+  FHEGPU_OP_COMPLEMENT_RIGHT = 2u
+};
+
+enum {
+  FHEGPU_KERNEL_AUTO = 0,     /* tcgen05 when the parameter set has a build, else SIMT */
+  FHEGPU_KERNEL_SIMT = 1,     /* CUDA-core reference kernel (any k <= 16, ell <= 31) */
+  FHEGPU_KERNEL_TCGEN05 = 2   /* sm_100a tensor-core kernel (error if unavailable) */
+};
+
+const char *fhegpu_last_error(void);
+const char *fhegpu_version(void);
+
+/* Context: device, stream, parameter set.  Replaces GswScheme(params) (fhe.py:167-171). */
+int fhegpu_ctx_create(const fhegpu_params *params, int device, fhegpu_ctx **out);
+void fhegpu_ctx_destroy(fhegpu_ctx *ctx);
+int fhegpu_ctx_set_stream(fhegpu_ctx *ctx, void *cuda_stream); /* NULL = context's own stream */
+int fhegpu_ctx_set_kernel(fhegpu_ctx *ctx, int kernel);        /* FHEGPU_KERNEL_* */
+int fhegpu_ctx_kernel(const fhegpu_ctx *ctx);                  /* kernel a level launch will use */
+int fhegpu_ctx_set_debug(fhegpu_ctx *ctx, uint32_t dbg);       /* test knobs; 0 in production */
+uint32_t fhegpu_ct_words(const fhegpu_ctx *ctx);
+int fhegpu_sync(fhegpu_ctx *ctx);
+
+/* Device ciphertext store (indices are ciphertext numbers: slot * lanes + lane). */
+int fhegpu_store_reserve(fhegpu_ctx *ctx, uint64_t n_cts);     /* grows, keeps contents */
+uint64_t fhegpu_store_capacity(const fhegpu_ctx *ctx);
+uint64_t fhegpu_store_device_ptr(const fhegpu_ctx *ctx);      /* base address (for device-side producers) */
+int fhegpu_store_write(fhegpu_ctx *ctx, const uint64_t *idx, uint64_t count,
+                       const uint32_t *host_v /* count x N*k, dense */);
+int fhegpu_store_read(fhegpu_ctx *ctx, const uint64_t *idx, const uint8_t *complement,
+                      uint64_t count, uint32_t *host_v /* count x N*k */);
+/* Only row `row` of V (k words) per ciphertext: what decryption needs (fhe.py:259-286). */
+int fhegpu_store_read_rows(fhegpu_ctx *ctx, const uint64_t *idx, const uint8_t *complement,
+                           uint64_t count, uint32_t row, uint32_t *host_rows /* count x k */);
+
+/* Levelised netlist: ops[level_offsets[l] .. level_offsets[l+1]) are the gates of
+ * level l; every op of a level reads only slots written by earlier levels. */
+int fhegpu_prog_create(fhegpu_ctx *ctx, const fhegpu_op *ops, uint64_t n_ops,
+                       const uint64_t *level_offsets, uint32_t n_levels, fhegpu_prog **out);
+/* Run every level for `lanes` independent copies of the netlist (ciphertext
+ * index = slot * lanes + lane); one kernel launch per level, on the context stream. */
+int fhegpu_prog_run(fhegpu_ctx *ctx, fhegpu_prog *prog, uint32_t lanes);
+/* Run levels [first, last) only (profiling / partial evaluation). */
+int fhegpu_prog_run_range(fhegpu_ctx *ctx, fhegpu_prog *prog, uint32_t lanes,
+                          uint32_t first_level, uint32_t last_level);
+uint32_t fhegpu_prog_launches(const fhegpu_prog *prog);       /* launches one run issues */
+void fhegpu_prog_destroy(fhegpu_prog *prog);
+
+/* Scheme operators on host buffers (count independent gates, one launch).
+ * v1 is the left operand after the reference's swap.  Replace hom_nand / hom_not. */
+int fhegpu_nand_batch(fhegpu_ctx *ctx, const uint32_t *v1, const uint32_t *v2,
+                      uint32_t *out, uint64_t count);
+int fhegpu_not_batch(fhegpu_ctx *ctx, const uint32_t *v, uint32_t *out, uint64_t count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FHEGPU_H */

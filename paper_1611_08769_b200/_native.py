@@ -1,0 +1,214 @@
+"""ctypes binding of libfhegpu.so (include/fhegpu.h).
+
+There is deliberately no CPU fallback: if the library is missing or no CUDA
+device is present, every entry point raises ``DeviceError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import DeviceError, ParameterError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfhegpu.so")
+
+KERNEL_AUTO, KERNEL_SIMT, KERNEL_TCGEN05 = 0, 1, 2
+KERNEL_NAMES = {KERNEL_AUTO: "auto", KERNEL_SIMT: "simt", KERNEL_TCGEN05: "tcgen05"}
+
+OP_DTYPE = np.dtype([("left", "<u4"), ("right", "<u4"), ("out", "<u4"), ("flags", "<u4")])
+
+
+class _Params(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_uint32), ("ell", ctypes.c_uint32),
+                ("q", ctypes.c_uint32), ("m", ctypes.c_uint32)]
+
+
+_lib = None
+
+# (name, restype, argtypes) of every symbol include/fhegpu.h declares
+_P = ctypes.c_void_p
+_U32P = ctypes.POINTER(ctypes.c_uint32)
+_U64P = ctypes.POINTER(ctypes.c_uint64)
+_U8P = ctypes.POINTER(ctypes.c_uint8)
+SIGNATURES = [
+    ("fhegpu_last_error", ctypes.c_char_p, []),
+    ("fhegpu_version", ctypes.c_char_p, []),
+    ("fhegpu_ctx_create", ctypes.c_int, [ctypes.POINTER(_Params), ctypes.c_int, ctypes.POINTER(_P)]),
+    ("fhegpu_ctx_destroy", None, [_P]),
+    ("fhegpu_ctx_set_stream", ctypes.c_int, [_P, _P]),
+    ("fhegpu_ctx_set_kernel", ctypes.c_int, [_P, ctypes.c_int]),
+    ("fhegpu_ctx_kernel", ctypes.c_int, [_P]),
+    ("fhegpu_ctx_set_debug", ctypes.c_int, [_P, ctypes.c_uint32]),
+    ("fhegpu_ct_words", ctypes.c_uint32, [_P]),
+    ("fhegpu_sync", ctypes.c_int, [_P]),
+    ("fhegpu_store_reserve", ctypes.c_int, [_P, ctypes.c_uint64]),
+    ("fhegpu_store_capacity", ctypes.c_uint64, [_P]),
+    ("fhegpu_store_device_ptr", ctypes.c_uint64, [_P]),
+    ("fhegpu_store_write", ctypes.c_int, [_P, _U64P, ctypes.c_uint64, _U32P]),
+    ("fhegpu_store_read", ctypes.c_int, [_P, _U64P, _U8P, ctypes.c_uint64, _U32P]),
+    ("fhegpu_store_read_rows", ctypes.c_int, [_P, _U64P, _U8P, ctypes.c_uint64, ctypes.c_uint32, _U32P]),
+    ("fhegpu_prog_create", ctypes.c_int, [_P, _P, ctypes.c_uint64, _U64P, ctypes.c_uint32, ctypes.POINTER(_P)]),
+    ("fhegpu_prog_run", ctypes.c_int, [_P, _P, ctypes.c_uint32]),
+    ("fhegpu_prog_run_range", ctypes.c_int, [_P, _P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]),
+    ("fhegpu_prog_launches", ctypes.c_uint32, [_P]),
+    ("fhegpu_prog_destroy", None, [_P]),
+    ("fhegpu_nand_batch", ctypes.c_int, [_P, _U32P, _U32P, _U32P, ctypes.c_uint64]),
+    ("fhegpu_not_batch", ctypes.c_int, [_P, _U32P, _U32P, ctypes.c_uint64]),
+]
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libfhegpu.so and attach signatures (no device needed)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise DeviceError(f"CUDA library {path} not built; run __graft_entry__.build()")
+    try:
+        lib = ctypes.CDLL(path)
+    except OSError as exc:
+        raise DeviceError(f"cannot load {path}: {exc}") from exc
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = _lib.fhegpu_last_error().decode(errors="replace")
+        raise DeviceError(f"{what} failed (code {rc}): {msg}")
+
+
+def _ptr(arr, ctype):
+    return arr.ctypes.data_as(ctypes.POINTER(ctype))
+
+
+class Program:
+    """A levelised netlist resident on the device (fhegpu_prog)."""
+
+    def __init__(self, ctx: "DeviceContext", ops: np.ndarray, level_offsets: np.ndarray):
+        self.ctx = ctx
+        self.n_ops = int(len(ops))
+        self.n_levels = int(len(level_offsets) - 1)
+        ops = np.ascontiguousarray(ops, dtype=OP_DTYPE)
+        offs = np.ascontiguousarray(level_offsets, dtype=np.uint64)
+        h = ctypes.c_void_p()
+        _check(_lib.fhegpu_prog_create(ctx.handle, ops.ctypes.data_as(ctypes.c_void_p),
+                                       self.n_ops, _ptr(offs, ctypes.c_uint64),
+                                       self.n_levels, ctypes.byref(h)), "prog_create")
+        self.handle = h
+        self.launches = int(_lib.fhegpu_prog_launches(h))
+
+    def run(self, lanes: int = 1, first: int = 0, last: int | None = None):
+        last = self.n_levels if last is None else last
+        _check(_lib.fhegpu_prog_run_range(self.ctx.handle, self.handle, lanes, first, last),
+               "prog_run")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and _lib is not None:
+            _lib.fhegpu_prog_destroy(h)
+            self.handle = None
+
+
+class DeviceContext:
+    """One fhegpu_ctx: device store + stream for one parameter set."""
+
+    def __init__(self, params, device: int = 0):
+        lib = load_library()
+        if params.q >= 1 << 31 or params.k > 16:
+            raise ParameterError("GPU library supports q < 2^31 and n <= 15")
+        self.params = params
+        cp = _Params(params.n, params.ell, params.q, params.m)
+        h = ctypes.c_void_p()
+        _check(lib.fhegpu_ctx_create(ctypes.byref(cp), device, ctypes.byref(h)), "ctx_create")
+        self.handle = h
+        self.device = device
+        self.ct_words = int(lib.fhegpu_ct_words(h))
+        self.words = params.n_ct * params.k
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and _lib is not None:
+            _lib.fhegpu_ctx_destroy(h)
+            self.handle = None
+
+    # -- configuration --------------------------------------------------------------
+    def set_stream(self, stream_ptr: int | None):
+        _check(_lib.fhegpu_ctx_set_stream(self.handle, ctypes.c_void_p(stream_ptr or 0)), "set_stream")
+
+    def set_kernel(self, kernel: int):
+        _check(_lib.fhegpu_ctx_set_kernel(self.handle, int(kernel)), "set_kernel")
+
+    @property
+    def kernel(self) -> str:
+        return KERNEL_NAMES[int(_lib.fhegpu_ctx_kernel(self.handle))]
+
+    def set_debug(self, dbg: int):
+        _check(_lib.fhegpu_ctx_set_debug(self.handle, int(dbg)), "set_debug")
+
+    def sync(self):
+        _check(_lib.fhegpu_sync(self.handle), "sync")
+
+    # -- store ----------------------------------------------------------------------
+    def reserve(self, n_cts: int):
+        _check(_lib.fhegpu_store_reserve(self.handle, int(n_cts)), "store_reserve")
+
+    @property
+    def capacity(self) -> int:
+        return int(_lib.fhegpu_store_capacity(self.handle))
+
+    @property
+    def store_ptr(self) -> int:
+        return int(_lib.fhegpu_store_device_ptr(self.handle))
+
+    def write(self, idx, values: np.ndarray):
+        idx = np.ascontiguousarray(idx, dtype=np.uint64)
+        vals = np.ascontiguousarray(values, dtype=np.uint32).reshape(len(idx), self.words)
+        _check(_lib.fhegpu_store_write(self.handle, _ptr(idx, ctypes.c_uint64), len(idx),
+                                       _ptr(vals, ctypes.c_uint32)), "store_write")
+
+    def read(self, idx, complement=None) -> np.ndarray:
+        idx = np.ascontiguousarray(idx, dtype=np.uint64)
+        out = np.empty((len(idx), self.params.n_ct, self.params.k), dtype=np.uint32)
+        comp = None if complement is None else np.ascontiguousarray(complement, dtype=np.uint8)
+        _check(_lib.fhegpu_store_read(self.handle, _ptr(idx, ctypes.c_uint64),
+                                      None if comp is None else _ptr(comp, ctypes.c_uint8),
+                                      len(idx), _ptr(out, ctypes.c_uint32)), "store_read")
+        return out
+
+    def read_rows(self, idx, row: int, complement=None) -> np.ndarray:
+        idx = np.ascontiguousarray(idx, dtype=np.uint64)
+        out = np.empty((len(idx), self.params.k), dtype=np.uint32)
+        comp = None if complement is None else np.ascontiguousarray(complement, dtype=np.uint8)
+        _check(_lib.fhegpu_store_read_rows(self.handle, _ptr(idx, ctypes.c_uint64),
+                                           None if comp is None else _ptr(comp, ctypes.c_uint8),
+                                           len(idx), int(row), _ptr(out, ctypes.c_uint32)),
+               "store_read_rows")
+        return out
+
+    # -- programs and scheme operators ------------------------------------------------
+    def program(self, ops: np.ndarray, level_offsets) -> Program:
+        return Program(self, ops, np.asarray(level_offsets))
+
+    def nand_batch(self, v1: np.ndarray, v2: np.ndarray) -> np.ndarray:
+        v1 = np.ascontiguousarray(v1, dtype=np.uint32)
+        v2 = np.ascontiguousarray(v2, dtype=np.uint32)
+        out = np.empty_like(v1)
+        _check(_lib.fhegpu_nand_batch(self.handle, _ptr(v1, ctypes.c_uint32), _ptr(v2, ctypes.c_uint32),
+                                      _ptr(out, ctypes.c_uint32), len(v1)), "nand_batch")
+        return out
+
+    def not_batch(self, v: np.ndarray) -> np.ndarray:
+        v = np.ascontiguousarray(v, dtype=np.uint32)
+        out = np.empty_like(v)
+        _check(_lib.fhegpu_not_batch(self.handle, _ptr(v, ctypes.c_uint32), _ptr(out, ctypes.c_uint32),
+                                     len(v)), "not_batch")
+        return out

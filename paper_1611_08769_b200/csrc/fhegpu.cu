@@ -1,0 +1,459 @@
+// fhegpu.cu -- C ABI of the B200 engine (declared in include/fhegpu.h).
+//
+// Owns: the device ciphertext store, the context stream, levelised programs
+// (op tables resident in HBM) and the kernel dispatch (tcgen05 kernel for the
+// parameter sets it is instantiated for, CUDA-core kernel otherwise).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fhegpu.h"
+#include "common.cuh"
+#include "simt_nand.cuh"
+#include "tc_nand.cuh"
+
+using namespace fhegpu;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                       \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      return fail(FHEGPU_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));        \
+  } while (0)
+
+constexpr size_t kStagingCap = size_t(256) << 20;  // bytes per staged transfer chunk
+
+}  // namespace
+
+struct fhegpu_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  DevParams p{};
+  uint32_t n = 0, m = 0;
+  int kernel_pref = FHEGPU_KERNEL_AUTO;
+  bool tc_capable = false;  // sm_100 device and a kernel instantiated for (k, ell)
+  int num_sms = 0;
+  uint32_t *store = nullptr;
+  uint64_t capacity = 0;  // ciphertexts
+  // staging
+  uint32_t *d_stage = nullptr;
+  size_t stage_bytes = 0;
+  uint64_t *d_idx = nullptr;
+  size_t idx_cap = 0;
+  uint8_t *d_comp = nullptr;
+  size_t comp_cap = 0;
+  OpRec *d_tmp_ops = nullptr;
+  size_t tmp_ops_cap = 0;
+};
+
+struct fhegpu_prog {
+  OpRec *d_ops = nullptr;
+  std::vector<uint64_t> offsets;  // n_levels + 1
+  uint64_t n_ops = 0;
+};
+
+namespace {
+
+int ensure(void **ptr, size_t *cap, size_t need) {
+  if (*cap >= need) return FHEGPU_OK;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  *cap = 0;
+  size_t sz = std::max(need, size_t(1) << 20);
+  cudaError_t e = cudaMalloc(ptr, sz);
+  if (e != cudaSuccess) return fail(FHEGPU_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  *cap = sz;
+  return FHEGPU_OK;
+}
+
+bool tc_instantiated(uint32_t k, uint32_t ell) {
+  return (k == 9 && ell == 29) || (k == 3 && ell == 17);
+}
+
+template <int K, int ELL>
+int launch_tc(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes) {
+  using G = tc::Geo<K, ELL>;
+  static bool attr_done = false;
+  // 100 KB requested so at most two CTAs (2 x 256 TMEM columns) share an SM
+  const int smem = std::max(G::SMEM, 100 * 1024);
+  if (!attr_done) {
+    CUDA_TRY(cudaFuncSetAttribute(tc::level_tc_kernel<K, ELL>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_done = true;
+  }
+  const uint64_t items = (uint64_t)n_ops * lanes;
+  const uint64_t grid = std::min<uint64_t>(items, (uint64_t)c->num_sms * 2);
+  tc::level_tc_kernel<K, ELL><<<(unsigned)grid, G::THREADS, smem, c->stream>>>(store, ops, n_ops,
+                                                                               lanes, c->p);
+  CUDA_TRY(cudaGetLastError());
+  return FHEGPU_OK;
+}
+
+int launch_simt(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes) {
+  const size_t smem = size_t(2) * c->p.words * sizeof(uint32_t);
+  const uint64_t items = (uint64_t)n_ops * lanes;
+  const uint64_t grid = std::min<uint64_t>(items, (uint64_t)c->num_sms * 8);
+  if (c->p.k <= 4) {
+    if (smem > 48 * 1024)
+      CUDA_TRY(cudaFuncSetAttribute(level_simt_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    level_simt_kernel<4><<<(unsigned)grid, 256, smem, c->stream>>>(store, ops, n_ops, lanes, c->p);
+  } else {
+    if (smem > 48 * 1024)
+      CUDA_TRY(cudaFuncSetAttribute(level_simt_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+    level_simt_kernel<16><<<(unsigned)grid, 256, smem, c->stream>>>(store, ops, n_ops, lanes, c->p);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return FHEGPU_OK;
+}
+
+int effective_kernel(const fhegpu_ctx *c) {
+  if (c->kernel_pref == FHEGPU_KERNEL_SIMT) return FHEGPU_KERNEL_SIMT;
+  if (c->kernel_pref == FHEGPU_KERNEL_TCGEN05) return FHEGPU_KERNEL_TCGEN05;
+  return c->tc_capable ? FHEGPU_KERNEL_TCGEN05 : FHEGPU_KERNEL_SIMT;
+}
+
+int launch_level(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes) {
+  if (n_ops == 0 || lanes == 0) return FHEGPU_OK;
+  const int kern = effective_kernel(c);
+  if (kern == FHEGPU_KERNEL_TCGEN05) {
+    if (!c->tc_capable)
+      return fail(FHEGPU_EUNSUP, "tcgen05 kernel requested but not available for this device/params");
+    if (c->p.k == 9 && c->p.ell == 29) return launch_tc<9, 29>(c, store, ops, n_ops, lanes);
+    if (c->p.k == 3 && c->p.ell == 17) return launch_tc<3, 17>(c, store, ops, n_ops, lanes);
+    return fail(FHEGPU_EUNSUP, "no tcgen05 instantiation for these params");
+  }
+  return launch_simt(c, store, ops, n_ops, lanes);
+}
+
+unsigned grid_for(uint64_t work, int num_sms) {
+  uint64_t g = (work + 255) / 256;
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, (uint64_t)num_sms * 16));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *fhegpu_last_error(void) { return g_err.c_str(); }
+const char *fhegpu_version(void) { return "fhegpu 0.1 (sm_100a)"; }
+
+int fhegpu_ctx_create(const fhegpu_params *params, int device, fhegpu_ctx **out) {
+  if (!params || !out) return fail(FHEGPU_EINVAL, "null argument");
+  *out = nullptr;
+  const uint32_t k = params->n + 1, ell = params->ell, q = params->q;
+  if (params->n < 1 || k > 16) return fail(FHEGPU_EUNSUP, "library supports 1 <= n <= 15");
+  if (q < 8 || (q & 1u) == 0 || q >= (1u << 31))
+    return fail(FHEGPU_EUNSUP, "library supports odd 8 <= q < 2^31");
+  if (ell != (uint32_t)(32 - __builtin_clz(q - 1)))
+    return fail(FHEGPU_EINVAL, "ell must equal bitlen(q - 1)");
+  CUDA_TRY(cudaSetDevice(device));
+  auto *c = new fhegpu_ctx();
+  c->device = device;
+  c->n = params->n;
+  c->m = params->m;
+  c->p.k = k;
+  c->p.ell = ell;
+  c->p.q = q;
+  c->p.rows = k * ell;
+  c->p.words = k * ell * k;
+  c->p.ct_words = (c->p.words + 3u) & ~3u;
+  c->p.mu = ~0ull / q;  // floor((2^64 - 1) / q) == floor(2^64 / q) for odd q
+  c->p.dbg = 0;
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(FHEGPU_ECUDA, std::string("cudaGetDeviceProperties: ") + cudaGetErrorString(e));
+  }
+  c->num_sms = prop.multiProcessorCount;
+  c->tc_capable = (prop.major == 10 && prop.minor == 0) && tc_instantiated(k, ell);
+  e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(FHEGPU_ECUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+  }
+  c->stream = c->own_stream;
+  *out = c;
+  return FHEGPU_OK;
+}
+
+void fhegpu_ctx_destroy(fhegpu_ctx *c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  cudaFree(c->store);
+  cudaFree(c->d_stage);
+  cudaFree(c->d_idx);
+  cudaFree(c->d_comp);
+  cudaFree(c->d_tmp_ops);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+}
+
+int fhegpu_ctx_set_stream(fhegpu_ctx *c, void *stream) {
+  if (!c) return fail(FHEGPU_EINVAL, "null ctx");
+  c->stream = stream ? (cudaStream_t)stream : c->own_stream;
+  return FHEGPU_OK;
+}
+
+int fhegpu_ctx_set_kernel(fhegpu_ctx *c, int kernel) {
+  if (!c) return fail(FHEGPU_EINVAL, "null ctx");
+  if (kernel < 0 || kernel > 2) return fail(FHEGPU_EINVAL, "unknown kernel id");
+  if (kernel == FHEGPU_KERNEL_TCGEN05 && !c->tc_capable)
+    return fail(FHEGPU_EUNSUP, "tcgen05 kernel unavailable for this device/params");
+  c->kernel_pref = kernel;
+  return FHEGPU_OK;
+}
+
+int fhegpu_ctx_kernel(const fhegpu_ctx *c) { return c ? effective_kernel(c) : -1; }
+
+int fhegpu_ctx_set_debug(fhegpu_ctx *c, uint32_t dbg) {
+  if (!c) return fail(FHEGPU_EINVAL, "null ctx");
+  c->p.dbg = dbg;
+  return FHEGPU_OK;
+}
+
+uint32_t fhegpu_ct_words(const fhegpu_ctx *c) { return c ? c->p.ct_words : 0; }
+
+int fhegpu_sync(fhegpu_ctx *c) {
+  if (!c) return fail(FHEGPU_EINVAL, "null ctx");
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FHEGPU_OK;
+}
+
+int fhegpu_store_reserve(fhegpu_ctx *c, uint64_t n_cts) {
+  if (!c) return fail(FHEGPU_EINVAL, "null ctx");
+  if (n_cts <= c->capacity) return FHEGPU_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  uint32_t *nw = nullptr;
+  const size_t bytes = (size_t)n_cts * c->p.ct_words * sizeof(uint32_t);
+  cudaError_t e = cudaMalloc(&nw, bytes);
+  if (e != cudaSuccess)
+    return fail(FHEGPU_ENOMEM, "store_reserve: cannot allocate " + std::to_string(bytes) + " bytes");
+  if (c->store) {
+    CUDA_TRY(cudaMemcpyAsync(nw, c->store, (size_t)c->capacity * c->p.ct_words * 4,
+                             cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    cudaFree(c->store);
+  }
+  c->store = nw;
+  c->capacity = n_cts;
+  return FHEGPU_OK;
+}
+
+uint64_t fhegpu_store_capacity(const fhegpu_ctx *c) { return c ? c->capacity : 0; }
+
+uint64_t fhegpu_store_device_ptr(const fhegpu_ctx *c) { return c ? (uint64_t)(uintptr_t)c->store : 0; }
+
+static int check_idx(fhegpu_ctx *c, const uint64_t *idx, uint64_t count) {
+  for (uint64_t i = 0; i < count; ++i)
+    if (idx[i] >= c->capacity)
+      return fail(FHEGPU_EINVAL, "ciphertext index " + std::to_string(idx[i]) + " beyond capacity " +
+                                     std::to_string(c->capacity));
+  return FHEGPU_OK;
+}
+
+int fhegpu_store_write(fhegpu_ctx *c, const uint64_t *idx, uint64_t count, const uint32_t *host_v) {
+  if (!c || (count && (!idx || !host_v))) return fail(FHEGPU_EINVAL, "null argument");
+  if (int rc = check_idx(c, idx, count)) return rc;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t per = (size_t)c->p.words * 4;
+  const uint64_t chunk = std::max<uint64_t>(1, kStagingCap / per);
+  for (uint64_t s = 0; s < count; s += chunk) {
+    const uint64_t n = std::min(chunk, count - s);
+    if (int rc = ensure((void **)&c->d_stage, &c->stage_bytes, n * per)) return rc;
+    if (int rc = ensure((void **)&c->d_idx, &c->idx_cap, n * 8)) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->d_stage, host_v + s * c->p.words, n * per, cudaMemcpyHostToDevice,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->d_idx, idx + s, n * 8, cudaMemcpyHostToDevice, c->stream));
+    scatter_kernel<<<grid_for(n * c->p.ct_words, c->num_sms), 256, 0, c->stream>>>(
+        c->store, c->d_idx, c->d_stage, n, c->p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(c->stream));  // staging is reused by the next chunk
+  }
+  return FHEGPU_OK;
+}
+
+static int read_impl(fhegpu_ctx *c, const uint64_t *idx, const uint8_t *comp, uint64_t count, int row,
+                     uint32_t *host) {
+  if (!c || (count && (!idx || !host))) return fail(FHEGPU_EINVAL, "null argument");
+  if (row >= (int)c->p.rows) return fail(FHEGPU_EINVAL, "row out of range");
+  if (int rc = check_idx(c, idx, count)) return rc;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const uint32_t per_words = row < 0 ? c->p.words : c->p.k;
+  const size_t per = (size_t)per_words * 4;
+  const uint64_t chunk = std::max<uint64_t>(1, kStagingCap / per);
+  for (uint64_t s = 0; s < count; s += chunk) {
+    const uint64_t n = std::min(chunk, count - s);
+    if (int rc = ensure((void **)&c->d_stage, &c->stage_bytes, n * per)) return rc;
+    if (int rc = ensure((void **)&c->d_idx, &c->idx_cap, n * 8)) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->d_idx, idx + s, n * 8, cudaMemcpyHostToDevice, c->stream));
+    const uint8_t *dcomp = nullptr;
+    if (comp) {
+      if (int rc = ensure((void **)&c->d_comp, &c->comp_cap, n)) return rc;
+      CUDA_TRY(cudaMemcpyAsync(c->d_comp, comp + s, n, cudaMemcpyHostToDevice, c->stream));
+      dcomp = c->d_comp;
+    }
+    gather_kernel<<<grid_for(n * per_words, c->num_sms), 256, 0, c->stream>>>(
+        c->store, c->d_idx, dcomp, c->d_stage, n, row, c->p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(host + s * per_words, c->d_stage, n * per, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  return FHEGPU_OK;
+}
+
+int fhegpu_store_read(fhegpu_ctx *c, const uint64_t *idx, const uint8_t *comp, uint64_t count,
+                      uint32_t *host_v) {
+  return read_impl(c, idx, comp, count, -1, host_v);
+}
+
+int fhegpu_store_read_rows(fhegpu_ctx *c, const uint64_t *idx, const uint8_t *comp, uint64_t count,
+                           uint32_t row, uint32_t *host_rows) {
+  return read_impl(c, idx, comp, count, (int)row, host_rows);
+}
+
+int fhegpu_prog_create(fhegpu_ctx *c, const fhegpu_op *ops, uint64_t n_ops,
+                       const uint64_t *level_offsets, uint32_t n_levels, fhegpu_prog **out) {
+  if (!c || !out || (n_ops && !ops) || !level_offsets) return fail(FHEGPU_EINVAL, "null argument");
+  *out = nullptr;
+  if (level_offsets[0] != 0 || level_offsets[n_levels] != n_ops)
+    return fail(FHEGPU_EINVAL, "level offsets must span [0, n_ops]");
+  for (uint32_t l = 0; l < n_levels; ++l)
+    if (level_offsets[l + 1] < level_offsets[l]) return fail(FHEGPU_EINVAL, "level offsets not sorted");
+  for (uint64_t i = 0; i < n_ops; ++i) {
+    const uint32_t mx = std::max(ops[i].left, std::max(ops[i].right, ops[i].out));
+    if (mx >= (1u << 31) || (ops[i].flags & ~3u))
+      return fail(FHEGPU_EINVAL, "bad op record " + std::to_string(i));
+  }
+  CUDA_TRY(cudaSetDevice(c->device));
+  auto *pr = new fhegpu_prog();
+  pr->n_ops = n_ops;
+  pr->offsets.assign(level_offsets, level_offsets + n_levels + 1);
+  if (n_ops) {
+    cudaError_t e = cudaMalloc(&pr->d_ops, n_ops * sizeof(OpRec));
+    if (e != cudaSuccess) {
+      delete pr;
+      return fail(FHEGPU_ENOMEM, "prog_create: cannot allocate op table");
+    }
+    e = cudaMemcpyAsync(pr->d_ops, ops, n_ops * sizeof(OpRec), cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+      cudaFree(pr->d_ops);
+      delete pr;
+      return fail(FHEGPU_ECUDA, std::string("prog_create upload: ") + cudaGetErrorString(e));
+    }
+  }
+  *out = pr;
+  return FHEGPU_OK;
+}
+
+int fhegpu_prog_run_range(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes, uint32_t first,
+                          uint32_t last) {
+  if (!c || !pr) return fail(FHEGPU_EINVAL, "null argument");
+  const uint32_t n_levels = (uint32_t)pr->offsets.size() - 1;
+  last = std::min(last, n_levels);
+  CUDA_TRY(cudaSetDevice(c->device));
+  for (uint32_t l = first; l < last; ++l) {
+    const uint64_t a = pr->offsets[l], b = pr->offsets[l + 1];
+    if (int rc = launch_level(c, c->store, pr->d_ops + a, (uint32_t)(b - a), lanes)) return rc;
+  }
+  return FHEGPU_OK;
+}
+
+int fhegpu_prog_run(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
+  if (!pr) return fail(FHEGPU_EINVAL, "null prog");
+  return fhegpu_prog_run_range(c, pr, lanes, 0, (uint32_t)pr->offsets.size() - 1);
+}
+
+uint32_t fhegpu_prog_launches(const fhegpu_prog *pr) {
+  if (!pr) return 0;
+  uint32_t n = 0;
+  for (size_t l = 0; l + 1 < pr->offsets.size(); ++l) n += pr->offsets[l + 1] > pr->offsets[l];
+  return n;
+}
+
+void fhegpu_prog_destroy(fhegpu_prog *pr) {
+  if (!pr) return;
+  cudaFree(pr->d_ops);
+  delete pr;
+}
+
+int fhegpu_nand_batch(fhegpu_ctx *c, const uint32_t *v1, const uint32_t *v2, uint32_t *out,
+                      uint64_t count) {
+  if (!c || (count && (!v1 || !v2 || !out))) return fail(FHEGPU_EINVAL, "null argument");
+  if (count == 0) return FHEGPU_OK;
+  if (count >= (1u << 29)) return fail(FHEGPU_EINVAL, "batch too large");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t ctb = (size_t)c->p.ct_words * 4;
+  uint32_t *buf = nullptr;
+  CUDA_TRY(cudaMalloc(&buf, 3 * count * ctb));
+  std::vector<OpRec> ops(count);
+  for (uint64_t i = 0; i < count; ++i)
+    ops[i] = OpRec{(uint32_t)i, (uint32_t)(count + i), (uint32_t)(2 * count + i), 0u};
+  int rc = ensure((void **)&c->d_tmp_ops, &c->tmp_ops_cap, count * sizeof(OpRec));
+  cudaError_t e = cudaSuccess;
+  if (!rc) {
+    // dense host rows -> padded device ciphertexts
+    e = cudaMemset2DAsync(buf, ctb, 0, ctb, 3 * count, c->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(buf, ctb, v1, (size_t)c->p.words * 4, (size_t)c->p.words * 4, count,
+                            cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(buf + count * c->p.ct_words, ctb, v2, (size_t)c->p.words * 4,
+                            (size_t)c->p.words * 4, count, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(c->d_tmp_ops, ops.data(), count * sizeof(OpRec), cudaMemcpyHostToDevice,
+                          c->stream);
+    if (e == cudaSuccess) rc = launch_level(c, buf, c->d_tmp_ops, (uint32_t)count, 1);
+    if (e == cudaSuccess && !rc)
+      e = cudaMemcpy2DAsync(out, (size_t)c->p.words * 4, buf + 2 * count * c->p.ct_words, ctb,
+                            (size_t)c->p.words * 4, count, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess && !rc) e = cudaStreamSynchronize(c->stream);
+  }
+  cudaFree(buf);
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(FHEGPU_ECUDA, std::string("nand_batch: ") + cudaGetErrorString(e));
+  return FHEGPU_OK;
+}
+
+int fhegpu_not_batch(fhegpu_ctx *c, const uint32_t *v, uint32_t *out, uint64_t count) {
+  if (!c || (count && (!v || !out))) return fail(FHEGPU_EINVAL, "null argument");
+  if (count == 0) return FHEGPU_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t per = (size_t)c->p.words * 4;
+  uint32_t *buf = nullptr;
+  CUDA_TRY(cudaMalloc(&buf, 2 * count * per));
+  cudaError_t e = cudaMemcpyAsync(buf, v, count * per, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) {
+    complement_kernel<<<grid_for(count * c->p.words, c->num_sms), 256, 0, c->stream>>>(
+        buf, buf + count * c->p.words, count, c->p);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out, buf + count * c->p.words, count * per, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(buf);
+  if (e != cudaSuccess) return fail(FHEGPU_ECUDA, std::string("not_batch: ") + cudaGetErrorString(e));
+  return FHEGPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,112 @@
+// simt_nand.cuh -- CUDA-core level kernel (reference implementation on the GPU).
+//
+// One CTA evaluates one (gate, lane) item at a time, grid-striding over the
+// level's items.  Compact NAND:
+//     out[r][i] = (G[r][i] - sum_c bit_c(row r of V1) * V2[c][i]) mod q
+// where bit c of row r is bit (c mod ell) of V1[r][c / ell].  Operands are
+// complemented on load ((G - V) mod q) when the op's flags say so -- the fused
+// hom_not of fhe.py:343-350.  This kernel serves parameter sets without a
+// tensor-core build and is the GPU cross-check of the tcgen05 kernel.
+#pragma once
+
+#include "common.cuh"
+
+namespace fhegpu {
+
+template <int KMAX>
+__global__ void __launch_bounds__(256)
+level_simt_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uint32_t n_ops,
+                  uint32_t lanes, DevParams p) {
+  extern __shared__ uint32_t smem[];
+  uint32_t *sA = smem;              // V1 (effective), rows x k
+  uint32_t *sB = smem + p.words;    // V2 (effective)
+  const uint64_t n_items = (uint64_t)n_ops * lanes;
+  for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const uint32_t op_i = (uint32_t)(item / lanes);
+    const uint32_t lane = (uint32_t)(item - (uint64_t)op_i * lanes);
+    const OpRec op = ops[op_i];
+    const uint32_t *g1 = store + ((uint64_t)op.left * lanes + lane) * p.ct_words;
+    const uint32_t *g2 = store + ((uint64_t)op.right * lanes + lane) * p.ct_words;
+    uint32_t *go = store + ((uint64_t)op.out * lanes + lane) * p.ct_words;
+    const bool c1 = op.flags & 1u, c2 = op.flags & 2u;
+    for (uint32_t w = threadIdx.x; w < p.words; w += blockDim.x) {
+      const uint32_t r = w / p.k, i = w - r * p.k;
+      const uint32_t g = gadget(p, r, i);
+      uint32_t a = g1[w], b = g2[w];
+      sA[w] = c1 ? sub_mod(g, a, p.q) : a;
+      sB[w] = c2 ? sub_mod(g, b, p.q) : b;
+    }
+    __syncthreads();
+    for (uint32_t r = threadIdx.x; r < p.rows; r += blockDim.x) {
+      uint64_t acc[KMAX];
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) acc[i] = 0;
+      for (uint32_t blk = 0; blk < p.k; ++blk) {
+        uint32_t bits = sA[r * p.k + blk];
+        while (bits) {
+          const uint32_t j = __ffs(bits) - 1;
+          bits &= bits - 1;
+          const uint32_t *vrow = sB + (blk * p.ell + j) * p.k;
+#pragma unroll
+          for (int i = 0; i < KMAX; ++i)
+            if (i < (int)p.k) acc[i] += vrow[i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) {
+        if (i < (int)p.k) {
+          const uint32_t s = mod_u64(acc[i], p.q, p.mu);
+          go[r * p.k + i] = sub_mod(gadget(p, r, i), s, p.q);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// out = (G - in) mod q elementwise over `count` ciphertexts (dense N*k each in
+// and out of a staging buffer).
+__global__ void complement_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out,
+                                  uint64_t count, DevParams p) {
+  const uint64_t total = count * p.words;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t w = (uint32_t)(t % p.words);
+    const uint32_t r = w / p.k, i = w - r * p.k;
+    out[t] = sub_mod(gadget(p, r, i), in[t], p.q);
+  }
+}
+
+// store[idx[c]] <- dense[c] (zero the padding words).
+__global__ void scatter_kernel(uint32_t *__restrict__ store, const uint64_t *__restrict__ idx,
+                               const uint32_t *__restrict__ dense, uint64_t count, DevParams p) {
+  const uint64_t total = count * p.ct_words;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = t / p.ct_words;
+    const uint32_t w = (uint32_t)(t - c * p.ct_words);
+    store[idx[c] * p.ct_words + w] = (w < p.words) ? dense[c * p.words + w] : 0u;
+  }
+}
+
+// dense[c] <- store[idx[c]] (complemented when comp[c]); row >= 0 selects one row only.
+__global__ void gather_kernel(const uint32_t *__restrict__ store, const uint64_t *__restrict__ idx,
+                              const uint8_t *__restrict__ comp, uint32_t *__restrict__ dense,
+                              uint64_t count, int row, DevParams p) {
+  const uint32_t per = row < 0 ? p.words : p.k;
+  const uint64_t total = count * per;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = t / per;
+    const uint32_t j = (uint32_t)(t - c * per);
+    const uint32_t w = row < 0 ? j : (uint32_t)row * p.k + j;
+    uint32_t v = store[idx[c] * p.ct_words + w];
+    if (comp != nullptr && comp[c]) {
+      const uint32_t r = w / p.k, i = w - r * p.k;
+      v = sub_mod(gadget(p, r, i), v, p.q);
+    }
+    dense[t] = v;
+  }
+}
+
+}  // namespace fhegpu

@@ -1,0 +1,472 @@
+"""GPU bit engine: the reference's bit-engine protocol over a levelised netlist.
+
+Drop-in for ``fhefft.engine.FheEngine`` (engine.py:124-214): same attributes
+(``batch_size``, ``nand_count``, ``max_depth``, ``stats``), same methods
+(``constant``, ``input_bit``, ``nand``, ``read_back``, ``export_ct``,
+``import_ct``, ``map_parallel``), same folding rules, operand swap, level and
+noise bookkeeping, and the same error classes.  What changes is *when* gates
+run: ``nand`` only records the gate.  On ``flush`` (triggered by
+``read_back`` / ``export_ct`` or explicitly) every pending gate is grouped by
+its level (the reference's ``level`` = NAND depth), ciphertext slots are
+assigned by liveness, and each level executes as ONE kernel launch over every
+gate of that level and every lane (independent signal) -- never one gate per
+launch.
+
+Folded NOTs (NAND(x, const 1) -> hom_not, engine.py:180-187) cost nothing:
+a handle is (node, complement flag) and the complement is applied when a
+kernel loads the operand, which is bit-identical to the reference's
+``flatten(I - C)`` because (G - (G - V) mod q) mod q = V.
+
+Lanes: ``batch_size`` > 1 evaluates the same netlist for that many
+independent inputs (like the reference's ``CleartextEngine`` lane packing):
+``input_bit`` takes the lane bits packed in an int (bit l = lane l) and
+``read_back`` returns them packed the same way.  Lane l draws its encryption
+randomness from ``lane_rngs[l]`` (or the single ``rng``, lane-major).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import CapabilityError, NoiseOverflowError, UsageError
+from .scheme import Ciphertext, GswScheme, KeyPair
+
+_UPLOAD_BATCH_BYTES = 256 << 20
+
+
+@dataclass(frozen=True)
+class GateStats:
+    """Snapshot of the gate accounting (engine.py:37-42)."""
+
+    nand_count: int
+    max_depth: int
+
+
+class GpuBit:
+    """One circuit wire: a device ciphertext node (+ complement flag) or a public constant."""
+
+    __slots__ = ("engine", "node", "neg", "const", "plain", "wire")
+
+    def __init__(self, engine, node: int, neg: int, const: bool, plain, wire: int):
+        self.engine = engine
+        self.node = node
+        self.neg = neg
+        self.const = const
+        self.plain = plain
+        self.wire = wire
+        if node >= 0:
+            engine._refs[node] += 1
+
+    def __del__(self):
+        if self.node >= 0:
+            try:
+                self.engine._refs[self.node] -= 1
+            except Exception:  # interpreter shutdown
+                pass
+
+    @property
+    def ct(self):
+        """The reference handle's ``.ct``: this wire's ciphertext (flushes)."""
+        return None if self.const else self.engine.export_ct(self)
+
+
+class GpuEngine:
+    """Lazy, levelised FHE bit engine on one B200."""
+
+    def __init__(self, scheme: GswScheme, keys: KeyPair | None = None, public_key=None,
+                 rng=None, threads: int = 1, batch_size: int = 1, lane_rngs=None,
+                 cse: bool = False, keep_all: bool = False, record_trace: bool = False,
+                 dry_run: bool = False):
+        if threads < 1:
+            raise UsageError("threads must be >= 1")
+        if batch_size < 1:
+            raise UsageError("batch_size must be >= 1")
+        if lane_rngs is not None and len(lane_rngs) != batch_size:
+            raise UsageError("need one rng per lane")
+        self.scheme = scheme
+        self.params = scheme.params
+        self.public_key = keys.public_key if keys is not None else public_key
+        self.secret_key = keys.secret_key if keys is not None else None
+        self.rng = rng if rng is not None else np.random.default_rng()
+        self.lane_rngs = lane_rngs
+        self.threads = threads
+        self.batch_size = batch_size
+        self.mask = (1 << batch_size) - 1
+        self.nand_count = 0
+        self.max_depth = 0
+        self.executed_nands = 0
+        self.cse = cse
+        self.keep_all = keep_all
+        self.trace = [] if record_trace else None
+        self._wire = 0
+        # node tables (python lists: appended per gate)
+        self._level: list[int] = []
+        self._est: list[int] = []
+        self._slot: list[int] = []
+        self._refs: list[int] = []
+        self._pending_ops: list[int] = []       # flat: left, lneg, right, rneg, out
+        self._pending_in_idx: list[np.ndarray] = []
+        self._pending_in_val: list[np.ndarray] = []
+        self._pending_in_bytes = 0
+        self._cse_map: dict | None = {} if cse else None
+        self._free: list[int] = []
+        self._n_slots = 0
+        self.last_program = None
+        self.programs_run = 0
+        self.launches = 0
+        self._fresh_noise = self.params.m * self.params.noise_bound
+        # dry_run: record and compile only (no encryption, no device) -- used to
+        # test netlists and slot allocation on machines without a GPU
+        self.dry_run = dry_run
+        self.dry_inputs: list[tuple[int, int]] = []     # (slot, packed lane bits)
+        self.dry_programs: list[dict] = []
+
+    # -- protocol attributes -----------------------------------------------------------
+
+    @property
+    def stats(self) -> GateStats:
+        return GateStats(self.nand_count, self.max_depth)
+
+    @property
+    def ctx(self):
+        return self.scheme.ctx
+
+    # -- nodes and slots ---------------------------------------------------------------
+
+    def _new_wire(self) -> int:
+        w = self._wire
+        self._wire += 1
+        return w
+
+    def _new_node(self, level: int, est: int) -> int:
+        self._level.append(level)
+        self._est.append(est)
+        self._slot.append(-1)
+        self._refs.append(0)
+        return len(self._level) - 1
+
+    def _alloc_slot(self) -> int:
+        if self._free:
+            return self._free.pop()
+        s = self._n_slots
+        self._n_slots += 1
+        return s
+
+    def _lane_idx(self, slot: int) -> np.ndarray:
+        return slot * self.batch_size + np.arange(self.batch_size, dtype=np.uint64)
+
+    def _ensure_capacity(self):
+        need = self._n_slots * self.batch_size
+        if self.ctx.capacity < need:
+            self.ctx.reserve(max(need, int(self.ctx.capacity * 1.25) + self.batch_size))
+
+    def _queue_upload(self, node: int, values: np.ndarray):
+        """values: (lanes, N, k) compact ciphertexts of one node."""
+        slot = self._alloc_slot()
+        self._slot[node] = slot
+        self._pending_in_idx.append(self._lane_idx(slot))
+        self._pending_in_val.append(np.ascontiguousarray(values, dtype=np.uint32))
+        self._pending_in_bytes += values.nbytes
+        if self._pending_in_bytes >= _UPLOAD_BATCH_BYTES:
+            self._upload_inputs()
+
+    def _upload_inputs(self):
+        if not self._pending_in_idx:
+            return
+        self._ensure_capacity()
+        idx = np.concatenate(self._pending_in_idx)
+        vals = np.concatenate([v.reshape(-1, self.params.n_ct * self.params.k)
+                               for v in self._pending_in_val])
+        self.ctx.write(idx, vals)
+        self._pending_in_idx.clear()
+        self._pending_in_val.clear()
+        self._pending_in_bytes = 0
+
+    # -- bit-engine protocol ----------------------------------------------------------
+
+    def constant(self, bit: int) -> GpuBit:
+        if bit not in (0, 1):
+            raise UsageError(f"constant must be 0 or 1, got {bit!r}")
+        return GpuBit(self, -1, 0, True, bit, -1)
+
+    def input_bit(self, bits: int) -> GpuBit:
+        """Encrypt one wire; ``bits`` is 0/1 (batch 1) or the lanes packed in an int."""
+        if self.batch_size == 1:
+            if bits not in (0, 1):
+                raise UsageError(f"input bit must be 0 or 1, got {bits!r}")
+        elif not 0 <= bits <= self.mask:
+            raise UsageError(f"lane value {bits:#x} out of range for batch_size={self.batch_size}")
+        if self.public_key is None and not self.dry_run:
+            raise CapabilityError("encrypting inputs needs the public key")
+        lanes = self.batch_size
+        if self.dry_run:
+            node = self._new_node(0, self._fresh_noise)
+            slot = self._alloc_slot()
+            self._slot[node] = slot
+            self.dry_inputs.append((slot, bits))
+            wire = self._new_wire()
+            if self.trace is not None:
+                self.trace.append((2, -1, -1, wire, node, 0))
+            return GpuBit(self, node, 0, False, None, wire)
+        if self.lane_rngs is None:
+            mus = [(bits >> l) & 1 for l in range(lanes)]
+            vals = self.scheme.encrypt_many(self.public_key, mus, self.rng)
+        else:
+            vals = np.empty((lanes, self.params.n_ct, self.params.k), dtype=np.uint32)
+            for l in range(lanes):
+                vals[l] = self.scheme.encrypt_many(self.public_key, [(bits >> l) & 1],
+                                                   self.lane_rngs[l])[0]
+        return self._input_values(vals, 0, self._fresh_noise)
+
+    def input_values(self, values: np.ndarray, level: int = 0, noise_est: int | None = None) -> GpuBit:
+        """New wire from precomputed compact ciphertexts, one per lane: (lanes, N, k)."""
+        values = np.asarray(values, dtype=np.uint32)
+        if values.shape != (self.batch_size, self.params.n_ct, self.params.k):
+            raise UsageError(f"expected {(self.batch_size, self.params.n_ct, self.params.k)}, "
+                             f"got {values.shape}")
+        return self._input_values(values, level, self._fresh_noise if noise_est is None else noise_est)
+
+    def _input_values(self, values, level, est) -> GpuBit:
+        node = self._new_node(level, est)
+        self._queue_upload(node, values)
+        wire = self._new_wire()
+        if self.trace is not None:
+            self.trace.append((2, -1, -1, wire, node, 0))
+        return GpuBit(self, node, 0, False, None, wire)
+
+    def import_ct(self, ct) -> GpuBit:
+        """Wire from a Ciphertext (batch 1) or a list of one Ciphertext per lane."""
+        cts = ct if isinstance(ct, (list, tuple)) else [ct]
+        if len(cts) != self.batch_size:
+            raise UsageError(f"import_ct needs {self.batch_size} ciphertexts (one per lane)")
+        vals = np.stack([np.asarray(c.v, dtype=np.uint32) for c in cts])
+        node = self._new_node(max(c.level for c in cts), max(c.noise_est for c in cts))
+        self._queue_upload(node, vals)
+        return GpuBit(self, node, 0, False, None, -1)
+
+    def nand(self, a: GpuBit, b: GpuBit) -> GpuBit:
+        if a.engine is not self or b.engine is not self:
+            raise UsageError("cannot mix handles from different engines")
+        if a.const or b.const:
+            return self._fold(a, b)
+        la, lb = self._level[a.node], self._level[b.node]
+        level = (la if la >= lb else lb) + 1
+        if level > self.params.depth_budget:
+            raise NoiseOverflowError(
+                f"NAND at level {level} would exceed depth budget {self.params.depth_budget}")
+        ea, eb = self._est[a.node], self._est[b.node]
+        if eb > ea:                                   # fhe.py:336-337: noisier operand left
+            a, b, ea, eb = b, a, eb, ea
+        est = ea + self.params.n_ct * eb
+        if est > self.params.q:
+            est = self.params.q
+        self.nand_count += 1
+        if level > self.max_depth:
+            self.max_depth = level
+        key = (a.node, a.neg, b.node, b.neg)
+        node = self._cse_map.get(key, -1) if self._cse_map is not None else -1
+        if node < 0:
+            node = self._new_node(level, est)
+            self._pending_ops.extend((a.node, a.neg, b.node, b.neg, node))
+            self.executed_nands += 1
+            if self._cse_map is not None:
+                self._cse_map[key] = node
+        wire = self._new_wire()
+        if self.trace is not None:
+            self.trace.append((0, a.wire, b.wire, wire, node, 0))
+        return GpuBit(self, node, 0, False, None, wire)
+
+    def _fold(self, a: GpuBit, b: GpuBit) -> GpuBit:
+        """engine.py:180-187: const/const -> const; NAND(x,0) -> 1; NAND(x,1) -> NOT x."""
+        if a.const and b.const:
+            return self.constant(0 if (a.plain and b.plain) else 1)
+        if b.const:
+            a, b = b, a
+        if a.plain == 0:
+            return self.constant(1)
+        wire = self._new_wire()
+        if self.trace is not None:
+            self.trace.append((1, b.wire, b.wire, wire, b.node, b.neg ^ 1))
+        return GpuBit(self, b.node, b.neg ^ 1, False, None, wire)
+
+    def map_parallel(self, fn, items):
+        """Gates only record here; the GPU provides the parallelism at flush."""
+        return [fn(x) for x in items]
+
+    # -- read back ------------------------------------------------------------------------
+
+    def _decrypt_row(self) -> int:
+        p = self.params
+        return p.n * p.ell + (p.q // 2).bit_length() - 1
+
+    def read_back(self, h: GpuBit) -> int:
+        if h.engine is not self:
+            raise UsageError("handle belongs to a different engine")
+        if h.const:
+            return h.plain if self.batch_size == 1 else (self.mask if h.plain else 0)
+        return int(self.read_back_many([h])[0])
+
+    def read_back_many(self, handles) -> list[int]:
+        """Packed lane bits of many wires with one device gather (vectorised decrypt)."""
+        bits = self.read_back_bits(handles)
+        if self.batch_size == 1:
+            return [int(b) for b in bits[:, 0]]
+        weights = [1 << l for l in range(self.batch_size)]
+        return [sum(w for w, b in zip(weights, row) if b) for row in bits.tolist()]
+
+    def read_back_bits(self, handles) -> np.ndarray:
+        """Decrypted bits of many wires, shape (len(handles), lanes), one device gather."""
+        lanes = self.batch_size
+        out = np.zeros((len(handles), lanes), dtype=np.uint8)
+        var = []
+        for i, h in enumerate(handles):
+            if h.engine is not self:
+                raise UsageError("handle belongs to a different engine")
+            if h.const:
+                out[i] = h.plain
+            else:
+                var.append(i)
+        if not var:
+            return out
+        if self.secret_key is None:
+            raise CapabilityError("read_back needs the secret key")
+        self.flush()
+        for i in var:
+            lvl = self._level[handles[i].node]
+            if lvl > self.params.depth_budget:
+                raise NoiseOverflowError(
+                    f"ciphertext level {lvl} exceeds depth budget {self.params.depth_budget}")
+        slots = np.array([self._slot[handles[i].node] for i in var], dtype=np.uint64)
+        idx = (slots[:, None] * np.uint64(lanes) + np.arange(lanes, dtype=np.uint64)).ravel()
+        comp = np.repeat(np.array([handles[i].neg for i in var], dtype=np.uint8), lanes)
+        rows = self.ctx.read_rows(idx, self._decrypt_row(), comp)
+        bits = self.scheme.decrypt_bits_from_rows(self.secret_key, rows).reshape(len(var), lanes)
+        out[var] = bits
+        return out
+
+    def node_values(self, handles) -> np.ndarray:
+        """Compact ciphertexts (n, lanes, N, k) of variable wires (flushes)."""
+        return self.read_nodes([h.node for h in handles], [h.neg for h in handles])
+
+    def read_nodes(self, nodes, negs, lanes=None) -> np.ndarray:
+        """Compact ciphertexts (n, len(lanes), N, k) of raw (node, complement) pairs."""
+        self.flush()
+        lanes = np.arange(self.batch_size, dtype=np.uint64) if lanes is None else \
+            np.asarray(lanes, dtype=np.uint64)
+        slots = np.asarray([self._slot[n] for n in nodes], dtype=np.int64)
+        if (slots < 0).any():
+            raise UsageError("node has no live ciphertext (released); use keep_all=True")
+        idx = (slots.astype(np.uint64)[:, None] * np.uint64(self.batch_size) + lanes).ravel()
+        comp = np.repeat(np.asarray(negs, dtype=np.uint8), len(lanes))
+        vals = self.ctx.read(idx, comp)
+        return vals.reshape(len(nodes), len(lanes), self.params.n_ct, self.params.k)
+
+    def export_ct(self, h: GpuBit):
+        """Ciphertext of a wire (constants become trivial ciphertexts); a list per lane if batched."""
+        if h.engine is not self:
+            raise UsageError("handle belongs to a different engine")
+        if h.const:
+            ct = self.scheme.trivial_encrypt_bit(h.plain)
+            return ct if self.batch_size == 1 else [ct] * self.batch_size
+        vals = self.node_values([h])[0]
+        lvl, est = self._level[h.node], self._est[h.node]
+        cts = [Ciphertext(vals[l], lvl, est, self.params) for l in range(self.batch_size)]
+        return cts[0] if self.batch_size == 1 else cts
+
+    # -- compile + run ------------------------------------------------------------------------
+
+    def flush(self):
+        """Evaluate every pending gate: one kernel launch per level over all lanes."""
+        if not self.dry_run:
+            self._upload_inputs()
+        if not self._pending_ops:
+            return None
+        prog = self._compile()
+        self._pending_ops = []
+        if self._cse_map is not None:
+            self._cse_map = {}
+        self.last_compile = prog
+        if self.dry_run:
+            self.dry_programs.append(prog)
+            return prog
+        self._ensure_capacity()
+        program = self.ctx.program(prog["ops"], prog["offsets"])
+        program.run(self.batch_size)
+        self.last_program = program
+        self.last_compile = prog
+        self.programs_run += 1
+        self.launches += program.launches
+        return program
+
+    def _compile(self):
+        """Level-sort the pending gates and assign ciphertext slots by liveness.
+
+        A slot read at level L is released before the launch of level L + 1 at
+        the earliest, so no launch ever writes a slot another gate of the same
+        launch reads.  Nodes still referenced by a live handle keep their slot.
+        """
+        ops = np.asarray(self._pending_ops, dtype=np.int64).reshape(-1, 5)
+        level = np.asarray(self._level, dtype=np.int64)
+        slot = np.asarray(self._slot, dtype=np.int64)
+        refs = np.asarray(self._refs, dtype=np.int64)
+        n_nodes = len(level)
+        op_level = level[ops[:, 4]]
+        order = np.argsort(op_level, kind="stable")
+        ops = ops[order]
+        op_level = op_level[order]
+        left, lneg, right, rneg, out = ops.T
+        # last level at which each node is read by a pending gate
+        last_use = np.full(n_nodes, -1, dtype=np.int64)
+        np.maximum.at(last_use, left, op_level)
+        np.maximum.at(last_use, right, op_level)
+        # release point of each slot: the level before whose launch it becomes free
+        never = np.iinfo(np.int64).max
+        free_at = np.full(n_nodes, never, dtype=np.int64)
+        if not self.keep_all:
+            dead = refs <= 0
+            old = (slot >= 0) & dead
+            free_at[old] = np.where(last_use[old] >= 0, last_use[old] + 1, 0)
+            new_dead = np.zeros(n_nodes, dtype=bool)
+            new_dead[out] = True
+            new_dead &= dead
+            free_at[new_dead] = np.maximum(last_use[new_dead], level[new_dead]) + 1
+        cand = np.nonzero(free_at != never)[0]
+        cand = cand[np.argsort(free_at[cand], kind="stable")]
+        cand_at = free_at[cand]
+        lv_vals, lv_start = np.unique(op_level, return_index=True)
+        lv_end = np.append(lv_start[1:], len(op_level))
+        ptr = 0
+        free = self._free
+        for lv, s, e in zip(lv_vals.tolist(), lv_start.tolist(), lv_end.tolist()):
+            hi = int(np.searchsorted(cand_at, lv, side="right"))
+            if hi > ptr:
+                rel = slot[cand[ptr:hi]]
+                free.extend(rel[rel >= 0].tolist())
+                ptr = hi
+            cnt = e - s
+            take = min(cnt, len(free))
+            new_slots = np.empty(cnt, dtype=np.int64)
+            if take:
+                new_slots[:take] = free[len(free) - take:]
+                del free[len(free) - take:]
+            if cnt > take:
+                new_slots[take:] = np.arange(self._n_slots, self._n_slots + cnt - take)
+                self._n_slots += cnt - take
+            slot[out[s:e]] = new_slots
+        table = np.empty(len(out), dtype=[("left", "<u4"), ("right", "<u4"),
+                                          ("out", "<u4"), ("flags", "<u4")])
+        table["left"] = slot[left]
+        table["right"] = slot[right]
+        table["out"] = slot[out]
+        table["flags"] = lneg | (rneg << 1)
+        if ptr < len(cand):                       # released after the last launch
+            rel = slot[cand[ptr:]]
+            free.extend(rel[rel >= 0].tolist())
+        released = cand                            # every released node loses its slot
+        slot[released] = -1
+        self._slot = slot.tolist()
+        offsets = np.append(lv_start, len(out)).astype(np.uint64)
+        return {"ops": table, "offsets": offsets, "levels": lv_vals,
+                "widths": np.diff(offsets).astype(np.int64)}

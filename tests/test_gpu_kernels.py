@@ -1,0 +1,122 @@
+"""GPU kernel parity: tcgen05 and SIMT level kernels vs the CPU oracle (bit-exact)."""
+
+import numpy as np
+import pytest
+
+from oracle import gsw
+from paper_1611_08769_b200 import DEFAULT_PARAMS, EXACT_PARAMS, GswScheme, SchemeParams
+from paper_1611_08769_b200 import _native
+from tests.helpers import golden_json, golden_npz
+
+pytestmark = pytest.mark.gpu
+
+ORACLE = {EXACT_PARAMS: gsw.EXACT, DEFAULT_PARAMS: gsw.DEFAULT}
+
+
+def _ctx(params, kernel):
+    s = GswScheme(params)
+    ctx = s.ctx
+    ctx.set_kernel(kernel)
+    return s, ctx
+
+
+def _random_cts(p, count, rng, extremes=True):
+    v = rng.integers(0, p.q, (count, p.n_ct, p.k), dtype=np.int64)
+    if extremes and count >= 4:
+        v[0] = 0                      # all-zero (C = 0)
+        v[1] = p.q - 1                # all bits set below q
+        v[2] = gsw.gadget(gsw.Params(p.n, p.q, p.m, p.noise_bound, p.depth_budget))  # trivial 1
+        v[3] = rng.integers(0, 2, v[3].shape)
+    return v.astype(np.uint32)
+
+
+def _oracle_nand(p, a, b, ca, cb):
+    op = ORACLE[p]
+    a = gsw.hom_not_compact(op, a) if ca else a.astype(np.int64)
+    b = gsw.hom_not_compact(op, b) if cb else b.astype(np.int64)
+    return gsw.hom_nand_compact(op, a, b)
+
+
+@pytest.mark.parametrize("params", [DEFAULT_PARAMS, EXACT_PARAMS], ids=["default", "exact"])
+@pytest.mark.parametrize("kernel", [_native.KERNEL_TCGEN05, _native.KERNEL_SIMT], ids=["tc", "simt"])
+def test_level_kernel_random_operands(params, kernel):
+    """A 2-level program over random operands, all complement combinations, many lanes."""
+    s, ctx = _ctx(params, kernel)
+    rng = np.random.default_rng(1234)
+    lanes, n_in = 3, 8
+    vals = _random_cts(params, n_in * lanes, rng)
+    ctx.reserve(64 * lanes)
+    ctx.write(np.arange(n_in * lanes, dtype=np.uint64), vals)
+    ops = []
+    flags_cycle = [0, 1, 2, 3]
+    for i in range(n_in):                     # level 1: slots 8..15
+        ops.append((i, (i * 3 + 1) % n_in, 8 + i, flags_cycle[i % 4]))
+    lvl1 = len(ops)
+    for i in range(6):                        # level 2 reads level-1 outputs and inputs
+        ops.append((8 + i, (i + 5) % n_in if i % 2 else 8 + (i + 1) % 8, 16 + i, flags_cycle[(i + 1) % 4]))
+    table = np.array(ops, dtype=np.uint32).view(_native.OP_DTYPE).reshape(-1)
+    prog = ctx.program(table, [0, lvl1, len(ops)])
+    prog.run(lanes)
+    ctx.sync()
+    v = vals.reshape(n_in, lanes, params.n_ct, params.k)
+    store = {i: v[i] for i in range(n_in)}
+    for (l, r, o, f) in ops:
+        store[o] = np.stack([_oracle_nand(params, store[l][ln], store[r][ln], f & 1, f & 2)
+                             for ln in range(lanes)])
+    for o in sorted({op[2] for op in ops}):
+        got = ctx.read(o * lanes + np.arange(lanes, dtype=np.uint64))
+        assert np.array_equal(got.astype(np.int64), store[o]), f"slot {o}"
+
+
+@pytest.mark.parametrize("params", [DEFAULT_PARAMS, EXACT_PARAMS], ids=["default", "exact"])
+def test_nand_batch_and_not_batch_vs_oracle(params):
+    s = GswScheme(params)
+    rng = np.random.default_rng(99)
+    a = _random_cts(params, 37, rng)
+    b = _random_cts(params, 37, rng)
+    got = s.ctx.nand_batch(a, b)
+    for i in range(37):
+        assert np.array_equal(got[i].astype(np.int64), _oracle_nand(params, a[i], b[i], 0, 0))
+    nt = s.ctx.not_batch(a)
+    for i in range(37):
+        assert np.array_equal(nt[i].astype(np.int64), gsw.hom_not_compact(ORACLE[params], a[i]))
+
+
+@pytest.mark.parametrize("name,params", [("default", DEFAULT_PARAMS), ("exact", EXACT_PARAMS)])
+def test_scheme_hom_nand_reproduces_reference_ciphertexts(name, params):
+    """GswScheme.hom_nand/hom_not on the GPU == the reference's ciphertexts (golden KAT)."""
+    kat = golden_npz(f"scheme_{name}.npz")
+    meta = golden_json("scheme_kat.json")[name]
+    s = GswScheme(params)
+    from paper_1611_08769_b200 import Ciphertext
+    fresh = meta["fresh_noise_est"]
+    cts = [Ciphertext(kat[f"ct{i}"], 0, fresh, params) for i in range(5)]
+    n01 = s.hom_nand(cts[0], cts[1])
+    n12 = s.hom_nand(cts[1], cts[2])
+    x = s.hom_nand(n01, cts[3])
+    y = s.hom_nand(cts[4], n12)
+    nt = s.hom_not(y)
+    for nm, c in (("n01", n01), ("n12", n12), ("x", x), ("y", y), ("nt", nt)):
+        assert np.array_equal(c.v, kat[nm]), nm
+    assert [n01.level, n12.level, x.level, y.level, nt.level] == meta["levels"]
+    assert [n01.noise_est, n12.noise_est, x.noise_est, y.noise_est, nt.noise_est] == meta["noise_est"]
+    batch = s.hom_nand_many([(cts[0], cts[1]), (n01, cts[3])])
+    assert np.array_equal(batch[1].v, kat["x"])
+
+
+def test_generic_params_use_simt_kernel():
+    p = SchemeParams(n=3, q=2**13 - 1, m=8, noise_bound=0, depth_budget=10**9)
+    s = GswScheme(p)
+    assert s.ctx.kernel == "simt"
+    rng = np.random.default_rng(5)
+    a = rng.integers(0, p.q, (5, p.n_ct, p.k)).astype(np.uint32)
+    b = rng.integers(0, p.q, (5, p.n_ct, p.k)).astype(np.uint32)
+    op = gsw.Params(p.n, p.q, p.m, p.noise_bound, p.depth_budget)
+    got = s.ctx.nand_batch(a, b)
+    for i in range(5):
+        assert np.array_equal(got[i].astype(np.int64), gsw.hom_nand_compact(op, a[i], b[i]))
+
+
+def test_default_kernel_is_tcgen05_on_b200():
+    assert GswScheme(DEFAULT_PARAMS).ctx.kernel == "tcgen05"
+    assert GswScheme(EXACT_PARAMS).ctx.kernel == "tcgen05"

@@ -1,0 +1,140 @@
+"""Netlist parity (CPU): the circuits built on the GPU engine emit the reference's
+gate sequence, and the levelised + slot-allocated programs compute the right bits."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from paper_1611_08769_b200 import (DEFAULT0_PARAMS, DEFAULT_PARAMS, EXACT_PARAMS, FixedFormat,
+                                   GpuEngine, GswScheme, and_, fft_1d, fft_2d, input_signal, xor_)
+from paper_1611_08769_b200.fft import signal_words
+from tests.helpers import (FFT_CONFIGS, config_signal, golden_json, golden_npz, model_outputs,
+                           read_dry, replay_dry)
+
+PARAMS = {"EXACT": EXACT_PARAMS, "DEFAULT0": DEFAULT0_PARAMS}
+
+
+def _build(cfg, lanes=1, keep_all=False, values=None):
+    pname, seed, (F, f), dims, _ = FFT_CONFIGS[cfg]
+    scheme = GswScheme(PARAMS[pname])
+    eng = GpuEngine(scheme, dry_run=True, record_trace=True, batch_size=lanes, keep_all=keep_all)
+    if values is None:
+        values = config_signal(cfg)[1]
+    sig = input_signal(eng, values, FixedFormat(F, f), dims=dims if isinstance(dims, tuple) else None)
+    out = fft_2d(sig) if isinstance(dims, tuple) else fft_1d(sig)
+    return eng, out
+
+
+def _ops_digest(trace):
+    ops = [t[:4] for t in trace if t[0] in (0, 1)]
+    return hashlib.sha256(np.asarray(ops, dtype="<i8").tobytes()).hexdigest()[:16], ops
+
+
+def test_cfg0_trace_matches_reference_gate_for_gate():
+    eng, out = _build("cfg0")
+    ref = golden_npz("trace_cfg0.npz")
+    dig, ops = _ops_digest(eng.trace)
+    assert np.array_equal(np.asarray(ops), ref["ops"])
+    meta = golden_json("trace_cfg0.json")
+    assert dig == meta["ops_digest"]
+    assert (eng.nand_count, eng.max_depth) == (meta["nand_count"], meta["max_depth"])
+    # output wires in reference order
+    wires = [h.wire if not h.const else (-2 if h.plain else -1)
+             for w in signal_words(out) for h in w.bits]
+    assert wires == meta["outputs"]
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3", "cfg4"])
+def test_trace_digest_matches_reference(cfg):
+    eng, out = _build(cfg)
+    meta = golden_json(f"trace_{cfg}.json")
+    dig, ops = _ops_digest(eng.trace)
+    assert (eng.nand_count, eng.max_depth) == (meta["nand_count"], meta["max_depth"])
+    assert len(ops) == meta["n_ops"] and sum(o[0] == 1 for o in ops) == meta["n_not"]
+    assert dig == meta["ops_digest"]
+    wires = [h.wire if not h.const else (-2 if h.plain else -1)
+             for w in signal_words(out) for h in w.bits]
+    assert wires == meta["outputs"]
+
+
+def test_cfg1_pair_trace_matches_reference_with_swaps():
+    """DEFAULT params: the noise rule swaps operands exactly like the reference."""
+    meta = golden_json("trace_cfg1.json")
+    scheme = GswScheme(DEFAULT_PARAMS)
+    eng = GpuEngine(scheme, dry_run=True, record_trace=True)
+    hs = [(eng.input_bit(0), eng.input_bit(1)) for _ in range(meta["pairs"])]
+    outs = [(xor_(a, b), and_(a, b)) for a, b in hs]
+    ops = [list(t[:4]) for t in eng.trace if t[0] in (0, 1)]
+    assert ops == meta["ops"]
+    assert [[x.wire, y.wire] for x, y in outs] == meta["outputs"]
+    assert (eng.nand_count, eng.max_depth) == (meta["nand_count"], meta["max_depth"])
+
+
+@pytest.mark.parametrize("cfg", ["cfg0", "cfg3"])
+@pytest.mark.parametrize("keep_all", [False, True])
+def test_compiled_program_replay_matches_oracle(cfg, keep_all):
+    """Levelised ops + liveness slot reuse evaluate to the oracle's words (cleartext replay)."""
+    eng, out = _build(cfg, keep_all=keep_all)
+    eng.flush()
+    store = replay_dry(eng)
+    handles = [h for w in signal_words(out) for h in w.bits]
+    bits = read_dry(eng, store, handles)
+    F = FFT_CONFIGS[cfg][2][0]
+    words = []
+    for i in range(0, len(bits), F):
+        u = sum((b & 1) << k for k, b in enumerate(bits[i:i + F]))
+        words.append(u - (1 << F) if u >> (F - 1) else u)
+    want = model_outputs(cfg, config_signal(cfg)[1][None])[0]
+    assert words == want.tolist()
+    comp = eng.dry_programs[0]
+    assert comp["widths"].sum() == eng.executed_nands == eng.nand_count
+    if not keep_all:
+        assert eng._n_slots < len(eng._level) // 4      # slots are reused
+
+
+def test_lanes_replay_and_slot_reuse_cfg4_subset():
+    lanes = 8
+    vals = np.array([config_signal("cfg4", l)[1] for l in range(lanes)])
+    eng, out = _build("cfg4", lanes=lanes, values=vals)
+    eng.flush()
+    store = replay_dry(eng)
+    handles = [h for w in signal_words(out) for h in w.bits]
+    masks = read_dry(eng, store, handles)
+    want = model_outputs("cfg4", vals)
+    for lane in range(lanes):
+        words = []
+        for i in range(0, len(masks), 16):
+            u = sum(((m >> lane) & 1) << k for k, m in enumerate(masks[i:i + 16]))
+            words.append(u - (1 << 16) if u >> 15 else u)
+        assert words == want[lane].tolist()
+
+
+def test_incremental_flushes_and_dead_handles():
+    """Several flushes with handles dropped in between keep results exact."""
+    scheme = GswScheme(EXACT_PARAMS)
+    eng = GpuEngine(scheme, dry_run=True, batch_size=4)
+    a = eng.input_bit(0b0011)
+    b = eng.input_bit(0b0101)
+    x = xor_(a, b)
+    eng.flush()
+    y = and_(x, a)
+    del a
+    eng.flush()
+    z = xor_(y, b)
+    del x
+    eng.flush()
+    store = replay_dry(eng)
+    got = read_dry(eng, store, [y, z])
+    assert got == [0b0010, 0b0111]
+
+
+def test_cse_keeps_reference_counts():
+    scheme = GswScheme(DEFAULT_PARAMS)
+    eng = GpuEngine(scheme, dry_run=True, cse=True, batch_size=4)
+    a, b = eng.input_bit(0b0011), eng.input_bit(0b0101)
+    x, y = xor_(a, b), and_(a, b)
+    assert eng.nand_count == 6 and eng.executed_nands == 5 and eng.max_depth == 3
+    eng.flush()
+    store = replay_dry(eng)
+    assert read_dry(eng, store, [x, y]) == [0b0110, 0b0001]
