@@ -84,7 +84,8 @@ const char *fhegpu_version(void);
 /* Context: device, stream, parameter set.  Replaces GswScheme(params) (fhe.py:167-171). */
 int fhegpu_ctx_create(const fhegpu_params *params, int device, fhegpu_ctx **out);
 void fhegpu_ctx_destroy(fhegpu_ctx *ctx);
-int fhegpu_ctx_set_stream(fhegpu_ctx *ctx, void *cuda_stream); /* NULL = context's own stream */
+int fhegpu_ctx_set_stream(fhegpu_ctx *ctx, void *cuda_stream); /* NULL = legacy default stream */
+void *fhegpu_ctx_own_stream(const fhegpu_ctx *ctx);           /* the stream a new context starts on */
 int fhegpu_ctx_set_kernel(fhegpu_ctx *ctx, int kernel);        /* FHEGPU_KERNEL_* */
 int fhegpu_ctx_kernel(const fhegpu_ctx *ctx);                  /* kernel a level launch will use */
 int fhegpu_ctx_set_debug(fhegpu_ctx *ctx, uint32_t dbg);       /* test knobs; 0 in production */

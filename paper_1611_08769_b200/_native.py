@@ -40,6 +40,7 @@ SIGNATURES = [
     ("fhegpu_ctx_create", ctypes.c_int, [ctypes.POINTER(_Params), ctypes.c_int, ctypes.POINTER(_P)]),
     ("fhegpu_ctx_destroy", None, [_P]),
     ("fhegpu_ctx_set_stream", ctypes.c_int, [_P, _P]),
+    ("fhegpu_ctx_own_stream", _P, [_P]),
     ("fhegpu_ctx_set_kernel", ctypes.c_int, [_P, ctypes.c_int]),
     ("fhegpu_ctx_kernel", ctypes.c_int, [_P]),
     ("fhegpu_ctx_set_debug", ctypes.c_int, [_P, ctypes.c_uint32]),
@@ -142,7 +143,17 @@ class DeviceContext:
 
     # -- configuration --------------------------------------------------------------
     def set_stream(self, stream_ptr: int | None):
-        _check(_lib.fhegpu_ctx_set_stream(self.handle, ctypes.c_void_p(stream_ptr or 0)), "set_stream")
+        """Launch on this CUDA stream handle (0 = legacy default stream, None = own stream)."""
+        if stream_ptr is None:
+            stream_ptr = _lib.fhegpu_ctx_own_stream(self.handle) or 0
+        _check(_lib.fhegpu_ctx_set_stream(self.handle, ctypes.c_void_p(stream_ptr)), "set_stream")
+
+    def use_torch_stream(self, stream=None):
+        """Launch on a torch CUDA stream (default: torch's current stream)."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream()
+        self.set_stream(int(st.cuda_stream))
+        return st
 
     def set_kernel(self, kernel: int):
         _check(_lib.fhegpu_ctx_set_kernel(self.handle, int(kernel)), "set_kernel")

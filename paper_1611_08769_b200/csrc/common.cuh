@@ -16,6 +16,7 @@ struct DevParams {
   uint32_t words;     // N * k (dense words)
   uint64_t mu;        // floor(2^64 / q) for Barrett reduction
   uint32_t dbg;       // debug knobs (bit 0: swap B descriptor strides); 0 in production
+  uint32_t pm_c;      // 2^ell - q (pseudo-Mersenne epilogue constant)
 };
 
 // Gadget entry G[r][i] = 2^(r mod ell) if i == r / ell else 0 (fhe.py:200-208, mu = 1).

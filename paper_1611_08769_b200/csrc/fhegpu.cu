@@ -85,23 +85,41 @@ bool tc_instantiated(uint32_t k, uint32_t ell) {
   return (k == 9 && ell == 29) || (k == 3 && ell == 17);
 }
 
-template <int K, int ELL>
-int launch_tc(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes) {
+// Pseudo-Mersenne epilogue applies when the folded sum of finish_value stays < 2q.
+bool pm_ok(uint32_t q, uint32_t ell) {
+  if (ell < 17 || ell > 31) return false;
+  const uint64_t c = (1ull << ell) - q;
+  const uint64_t bh_max = ((1ull << 26) - 1) >> (ell - 16);
+  const uint64_t t_max = ((1ull << 26) - 1) + (((1ull << (ell - 16)) - 1) << 16) + c * bh_max;
+  return c * bh_max < (1ull << 32) && t_max < 2ull * q && t_max < (1ull << 32);
+}
+
+template <int K, int ELL, bool PM>
+int launch_tc_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes) {
   using G = tc::Geo<K, ELL>;
   static bool attr_done = false;
   // 100 KB requested so at most two CTAs (2 x 256 TMEM columns) share an SM
   const int smem = std::max(G::SMEM, 100 * 1024);
   if (!attr_done) {
-    CUDA_TRY(cudaFuncSetAttribute(tc::level_tc_kernel<K, ELL>,
+    CUDA_TRY(cudaFuncSetAttribute(tc::level_tc_kernel<K, ELL, PM>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_done = true;
   }
   const uint64_t items = (uint64_t)n_ops * lanes;
   const uint64_t grid = std::min<uint64_t>(items, (uint64_t)c->num_sms * 2);
-  tc::level_tc_kernel<K, ELL><<<(unsigned)grid, G::THREADS, smem, c->stream>>>(store, ops, n_ops,
-                                                                               lanes, c->p);
+  tc::level_tc_kernel<K, ELL, PM><<<(unsigned)grid, G::THREADS, smem, c->stream>>>(
+      store, ops, n_ops, lanes, c->p);
   CUDA_TRY(cudaGetLastError());
   return FHEGPU_OK;
+}
+
+template <int K, int ELL>
+int launch_tc(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes) {
+  if constexpr ((ELL + 7) / 8 == 4) {
+    if (pm_ok(c->p.q, c->p.ell) && !(c->p.dbg & 2u))  // dbg bit 1 forces the generic epilogue
+      return launch_tc_impl<K, ELL, true>(c, store, ops, n_ops, lanes);
+  }
+  return launch_tc_impl<K, ELL, false>(c, store, ops, n_ops, lanes);
 }
 
 int launch_simt(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes) {
@@ -176,6 +194,7 @@ int fhegpu_ctx_create(const fhegpu_params *params, int device, fhegpu_ctx **out)
   c->p.ct_words = (c->p.words + 3u) & ~3u;
   c->p.mu = ~0ull / q;  // floor((2^64 - 1) / q) == floor(2^64 / q) for odd q
   c->p.dbg = 0;
+  c->p.pm_c = (uint32_t)((1ull << ell) - q);
   cudaDeviceProp prop;
   cudaError_t e = cudaGetDeviceProperties(&prop, device);
   if (e != cudaSuccess) {
@@ -209,9 +228,11 @@ void fhegpu_ctx_destroy(fhegpu_ctx *c) {
 
 int fhegpu_ctx_set_stream(fhegpu_ctx *c, void *stream) {
   if (!c) return fail(FHEGPU_EINVAL, "null ctx");
-  c->stream = stream ? (cudaStream_t)stream : c->own_stream;
+  c->stream = (cudaStream_t)stream;  // NULL = the legacy default stream
   return FHEGPU_OK;
 }
+
+void *fhegpu_ctx_own_stream(const fhegpu_ctx *c) { return c ? (void *)c->own_stream : nullptr; }
 
 int fhegpu_ctx_set_kernel(fhegpu_ctx *c, int kernel) {
   if (!c) return fail(FHEGPU_EINVAL, "null ctx");

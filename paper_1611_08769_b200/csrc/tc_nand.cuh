@@ -143,6 +143,17 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint
       : "memory");
 }
 
+// D[tmem] (+)= A[smem desc] * B[smem desc], kind::i8, cta_group::1.
+__device__ __forceinline__ void mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -166,9 +177,10 @@ struct Geo {
   static constexpr int ROWS = K * ELL;
   static constexpr int FULL = ROWS / 128;
   static constexpr int REM = ROWS % 128;
-  static constexpr bool CORE_TAIL = (FULL >= 1) && (REM > 0) && (REM <= 16);
-  static constexpr int MT = CORE_TAIL ? FULL : (FULL + (REM > 0 ? 1 : 0));  // MMA tiles
-  static constexpr int TAIL = CORE_TAIL ? REM : 0;        // rows done on CUDA cores
+  // rows past the last full 128-row tile: a third MMA with A from an 8-row smem block
+  static constexpr bool SMEM_TAIL = (FULL >= 1) && (REM > 0) && (REM <= 8);
+  static constexpr int MT = SMEM_TAIL ? FULL : (FULL + (REM > 0 ? 1 : 0));  // TMEM-A tiles
+  static constexpr int TAIL = SMEM_TAIL ? REM : 0;
   static constexpr int MMA_ROWS = MT * 128;
   static constexpr int THREADS = 128 * MT;
   static constexpr int NDIG = (ELL + 7) / 8;               // byte digits per value
@@ -176,9 +188,11 @@ struct Geo {
   static constexpr int NPAD = ((NCOL + 15) / 16) * 16 < 16 ? 16 : ((NCOL + 15) / 16) * 16;
   static constexpr int NCH = NPAD / 16;                    // 16-byte MN chunks of B
   static constexpr int KB = 32 * K;                        // K extent in bytes
-  static constexpr uint32_t SBO = 128;                     // MN-chunk stride (bytes)
-  static constexpr uint32_t LBO = NCH * 128;               // 8-row K-group stride (bytes)
+  static constexpr uint32_t SBO = 128;                     // B: MN-chunk stride (bytes)
+  static constexpr uint32_t LBO = NCH * 128;               // B: 8-row K-group stride (bytes)
   static constexpr int B_BYTES = KB * NPAD;
+  static constexpr uint32_t TA_LBO = 128;                  // tail A: 16-byte K-chunk stride
+  static constexpr int TA_BYTES = (KB / 16) * 128;         // 8 rows x KB, K-major core matrices
   static constexpr int WORDS = ROWS * K;
   static constexpr int CT_WORDS = (WORDS + 3) & ~3;
   static constexpr int CT_BYTES = CT_WORDS * 4;
@@ -190,17 +204,17 @@ struct Geo {
   // idesc: c_format S32 (bits 4-5 = 2), a/b u8, A K-major, B MN-major (bit 16), N>>3, M>>4.
   static constexpr uint32_t IDESC =
       (2u << 4) | (1u << 16) | ((uint32_t)(NPAD >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  // tail split: each (tail row, column) sum is shared by TSPLIT threads
-  static constexpr int TSPLIT = 4;
-  // smem carve-up (bytes, all 128-aligned)
+  // smem carve-up (bytes, 128-aligned)
   static constexpr int OFF_IN = 0;                                   // [2 stages][2 operands]
   static constexpr int OFF_B = OFF_IN + 4 * CT_BYTES;
-  static constexpr int OFF_OUT = ((OFF_B + B_BYTES + 127) / 128) * 128;  // [2]
+  static constexpr int OFF_TA = ((OFF_B + B_BYTES + 127) / 128) * 128;
+  static constexpr int OFF_OUT = ((OFF_TA + (TAIL ? TA_BYTES : 0) + 127) / 128) * 128;  // [2]
   static constexpr int OFF_BAR = ((OFF_OUT + 2 * CT_BYTES + 127) / 128) * 128;
   static constexpr int SMEM = OFF_BAR + 128;
-  static_assert(K <= 16 && ELL <= 31 && ELL >= 4, "geometry out of range");
+  static_assert(K <= 16 && ELL <= 31 && ELL >= 17, "geometry out of range");
   static_assert(NPAD <= 256, "N too large for one MMA");
   static_assert(TMEM_NEED <= 256, "TMEM budget is 256 columns per CTA (2 CTAs/SM)");
+  static_assert(!TAIL || 8 * K >= NPAD, "tail accumulator reuses tile-0 A columns");
   static_assert(CT_BYTES % 16 == 0, "bulk copies need 16-byte multiples");
 };
 
@@ -222,7 +236,41 @@ __device__ __forceinline__ uint32_t b_word(const uint32_t *vals, int wi) {
   }
 }
 
-template <int K, int ELL>
+// The 32 bits of one compact word spread to 32 u8 in {0, 128}: byte slot 8g + p holds
+// bit 8g + 7 - p (multiply-spread: copies at stride 9 never overlap, so no carries).
+__device__ __forceinline__ void spread_word(uint32_t w, uint32_t (&out)[8]) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const uint32_t x = __byte_perm(w, 0u, 0x4440u + g);
+    out[2 * g] = (x * 0x08040201u) & 0x80808080u;      // bits 7,6,5,4
+    out[2 * g + 1] = (x * 0x80402010u) & 0x80808080u;  // bits 3,2,1,0
+  }
+}
+
+// Reduce one output value.  d[] holds the NDIG s32 accumulators of column i
+// (each 128 * digit sum).  Returns (G - S) mod q.
+template <int ELL, int NDIG, bool PM>
+__device__ __forceinline__ uint32_t finish_value(const uint32_t *d, uint32_t g, const DevParams &p) {
+  uint32_t r;
+  if constexpr (PM && NDIG == 4) {
+    // S = A + B 2^16, A = S0 + S1 2^8, B = S2 + S3 2^8 (both < 2^26);
+    // 2^ELL = c (mod q):  S = A + Bl 2^16 + c Bh  with B = Bh 2^(ELL-16) + Bl.  (< 2q, host-checked)
+    const uint32_t a = (d[0] >> 7) + (d[1] << 1);
+    const uint32_t b = (d[2] >> 7) + (d[3] << 1);
+    const uint32_t bl = b & ((1u << (ELL - 16)) - 1u);
+    const uint32_t bh = b >> (ELL - 16);
+    const uint32_t t = a + (bl << 16) + p.pm_c * bh;
+    r = t >= p.q ? t - p.q : t;
+  } else {
+    uint64_t s = 0;
+#pragma unroll
+    for (int dg = 0; dg < NDIG; ++dg) s += (uint64_t)d[dg] << (8 * dg);
+    r = mod_u64(s >> 7, p.q, p.mu);
+  }
+  return sub_mod(g, r, p.q);
+}
+
+template <int K, int ELL, bool PM>
 __global__ void __launch_bounds__(Geo<K, ELL>::THREADS, 2)
 level_tc_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uint32_t n_ops,
                 uint32_t lanes, DevParams p) {
@@ -230,8 +278,9 @@ level_tc_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uin
   extern __shared__ __align__(1024) uint8_t smem[];
   uint32_t *s_in = reinterpret_cast<uint32_t *>(smem + G::OFF_IN);
   uint8_t *s_b = smem + G::OFF_B;
+  uint8_t *s_ta = smem + G::OFF_TA;
   uint32_t *s_out = reinterpret_cast<uint32_t *>(smem + G::OFF_OUT);
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + G::OFF_BAR);  // [0,1] loads, [2] mma
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + G::OFF_BAR);  // 0,1 loads; 2 main; 3 tail
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + G::OFF_BAR + 64);
 
   const int tid = threadIdx.x;
@@ -240,21 +289,23 @@ level_tc_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uin
 
   if (warp == 0) tmem_alloc<G::TMEM_COLS>(tmem_slot);
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    mbar_init(&bar[2], 1);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
     fence_mbar_init();
   }
-  // zero output staging once (its padding words are stored with every ciphertext)
+  // zero once: B (its K-padding rows stay zero), tail A (rows TAIL..7), output padding
+  for (int w = tid; w < G::B_BYTES / 4; w += G::THREADS) reinterpret_cast<uint32_t *>(s_b)[w] = 0u;
+  if constexpr (G::TAIL > 0)
+    for (int w = tid; w < G::TA_BYTES / 4; w += G::THREADS) reinterpret_cast<uint32_t *>(s_ta)[w] = 0u;
   for (int w = tid; w < 2 * G::CT_WORDS; w += G::THREADS) s_out[w] = 0u;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t lane_quad = (uint32_t)(warp & 3) * 32u;
-  const uint32_t t_row_addr = tmem_base + (lane_quad << 16);  // this warp's TMEM lanes
-  const int tile = warp >> 2;                                  // MMA tile of this thread's row
-  const int row = tid;                                         // row within the ciphertext
+  const uint32_t lane_off = ((uint32_t)(warp & 3) * 32u) << 16;  // this warp's TMEM lanes
+  const int tile = warp >> 2;                                      // MMA tile of this thread's row
+  const int row = tid;                                             // ciphertext row of this thread
+  const int row_blk = row / ELL, row_bit = row - row_blk * ELL;
 
   auto item_ptrs = [&](uint64_t item, const uint32_t *&a, const uint32_t *&b, uint32_t *&o,
                        uint32_t &flags) {
@@ -301,67 +352,61 @@ level_tc_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uin
     const bool comp1 = flags & 1u, comp2 = flags & 2u;
     uint32_t *out_st = s_out + stage * G::CT_WORDS;
 
-    // ---- phase 1a: B operand (MN-major canonical layout, K slots permuted) ----
-    for (int e = tid; e < G::KB * G::NCH; e += G::THREADS) {
-      const int kr = e / G::NCH, ch = e - kr * G::NCH;
+    // ---- phase 1a: B operand: one K row (= one compact row of V2) per thread ----
+    for (int kr = tid; kr < G::KB; kr += G::THREADS) {
       const int w = kr >> 5, kk = kr & 31;
       const int j = (kk & ~7) + 7 - (kk & 7);
-      uint4 val = make_uint4(0u, 0u, 0u, 0u);
-      if (j < ELL) {
-        const int c = w * ELL + j;
-        if constexpr (G::NDIG == 4) {
-          uint32_t q4[4];
+      if (j >= ELL) continue;                 // K padding rows: zero since init
+      const int c = w * ELL + j;
+      uint32_t vals[K];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int wi = 4 * ch + u;
-            uint32_t v = 0u;
-            if (wi < K) {
-              v = v2[c * K + wi];
-              if (comp2) v = sub_mod(gadget_ct<ELL>(c, wi), v, p.q);
-            }
-            q4[u] = v;
-          }
-          val = make_uint4(q4[0], q4[1], q4[2], q4[3]);
-        } else {
-          uint32_t vals[K];
+      for (int i = 0; i < K; ++i) vals[i] = v2[c * K + i];
+      if (comp2) {                            // (G - V) mod q, G[c][i] = 2^j iff i == w
 #pragma unroll
-          for (int i = 0; i < K; ++i) {
-            const uint32_t v = v2[c * K + i];
-            vals[i] = comp2 ? sub_mod(gadget_ct<ELL>(c, i), v, p.q) : v;
-          }
-          val.x = b_word<K, G::NDIG>(vals, 4 * ch + 0);
-          val.y = b_word<K, G::NDIG>(vals, 4 * ch + 1);
-          val.z = b_word<K, G::NDIG>(vals, 4 * ch + 2);
-          val.w = b_word<K, G::NDIG>(vals, 4 * ch + 3);
-        }
+        for (int i = 0; i < K; ++i) vals[i] = sub_mod(i == w ? (1u << j) : 0u, vals[i], p.q);
       }
-      uint8_t *dst = s_b + (kr >> 3) * G::LBO + ch * G::SBO + (kr & 7) * 16;
-      *reinterpret_cast<uint4 *>(dst) = val;
+      uint8_t *dst = s_b + (kr >> 3) * G::LBO + (kr & 7) * 16;
+#pragma unroll
+      for (int ch = 0; ch < G::NCH; ++ch) {
+        uint4 val;
+        val.x = b_word<K, G::NDIG>(vals, 4 * ch + 0);
+        val.y = b_word<K, G::NDIG>(vals, 4 * ch + 1);
+        val.z = b_word<K, G::NDIG>(vals, 4 * ch + 2);
+        val.w = b_word<K, G::NDIG>(vals, 4 * ch + 3);
+        *reinterpret_cast<uint4 *>(dst + ch * G::SBO) = val;
+      }
     }
 
-    // ---- phase 1b: A operand, bits of row `row` spread to bytes, into TMEM ----
+    // ---- phase 1b: A operand of the TMEM tiles: this thread's row, spread, into TMEM ----
     {
       uint32_t words[K];
 #pragma unroll
-      for (int i = 0; i < K; ++i) {
-        uint32_t v = 0u;
-        if (row < G::ROWS) {
-          v = v1[row * K + i];
-          if (comp1) v = sub_mod(gadget_ct<ELL>(row, i), v, p.q);
-        }
-        words[i] = v;
+      for (int i = 0; i < K; ++i) words[i] = (row < G::ROWS) ? v1[row * K + i] : 0u;
+      if (comp1 && row < G::ROWS) {
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+          words[i] = sub_mod(i == row_blk ? (1u << row_bit) : 0u, words[i], p.q);
       }
-      const uint32_t a_col = tmem_base + G::D_COLS + tile * 8 * K;
+      const uint32_t a_addr = tmem_base + lane_off + G::D_COLS + tile * 8 * K;
 #pragma unroll
       for (int w = 0; w < K; ++w) {
-        uint32_t spread[8];
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const uint32_t x = (words[w] >> (8 * g)) & 0xFFu;
-          spread[2 * g] = (x * 0x08040201u) & 0x80808080u;      // bits 7,6,5,4 -> bytes 0..3
-          spread[2 * g + 1] = (x * 0x80402010u) & 0x80808080u;  // bits 3,2,1,0 -> bytes 0..3
-        }
-        tmem_st8((t_row_addr & 0xFFFF0000u) | ((a_col + 8 * w) & 0xFFFFu), spread);
+        uint32_t sp[8];
+        spread_word(words[w], sp);
+        tmem_st8(a_addr + 8 * w, sp);
+      }
+    }
+    // ---- phase 1c: A operand of the smem tail tile (rows MMA_ROWS .. ROWS-1) ----
+    if constexpr (G::TAIL > 0) {
+      if (tid < G::TAIL * K) {
+        const int m = tid / K, w = tid - m * K;
+        const int r = G::MMA_ROWS + m;
+        uint32_t v = v1[r * K + w];
+        if (comp1) v = sub_mod(w == r / ELL ? (1u << (r % ELL)) : 0u, v, p.q);
+        uint32_t sp[8];
+        spread_word(v, sp);
+        uint8_t *dst = s_ta + (2 * w) * G::TA_LBO + m * 16;
+        *reinterpret_cast<uint4 *>(dst) = make_uint4(sp[0], sp[1], sp[2], sp[3]);
+        *reinterpret_cast<uint4 *>(dst + G::TA_LBO) = make_uint4(sp[4], sp[5], sp[6], sp[7]);
       }
     }
     tmem_wait_st();
@@ -369,7 +414,7 @@ level_tc_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uin
     tc_fence_before();
     __syncthreads();
 
-    // ---- phase 2: MMA issue (one thread) || CUDA-core tail rows ----
+    // ---- phase 2: MMA issue (one thread) ----
     if (tid == 0) {
       tc_fence_after();
       const uint32_t b_base = smem_u32(s_b);
@@ -386,29 +431,20 @@ level_tc_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uin
         }
       }
       mma_commit(&bar[2]);
-    }
-    if constexpr (G::TAIL > 0) {
-      constexpr int UNITS = G::TAIL * K;
-      const int unit = tid / G::TSPLIT, sub = tid % G::TSPLIT;
-      const bool active = unit < UNITS;
-      const int tr = G::MMA_ROWS + (active ? unit / K : 0), i = active ? unit % K : 0;
-      uint64_t acc = 0;
-      if (active) {
-        for (int blk = 0; blk < K; ++blk) {
-          uint32_t wv = v1[tr * K + blk];
-          if (comp1) wv = sub_mod(gadget_ct<ELL>(tr, blk), wv, p.q);
-          for (int j = sub; j < ELL; j += G::TSPLIT) {
-            const int c = blk * ELL + j;
-            uint32_t v = v2[c * K + i];
-            if (comp2) v = sub_mod(gadget_ct<ELL>(c, i), v, p.q);
-            acc += ((wv >> j) & 1u) ? v : 0u;
-          }
-        }
-      }
+      if constexpr (G::TAIL > 0) {
+        // tail accumulator lives in tile 0's A columns: wait until those MMAs are done
+        mbar_wait(&bar[2], t & 1u);
+        tc_fence_after();
+        const uint32_t ta_base = smem_u32(s_ta);
+        const uint32_t d_tail = tmem_base + G::D_COLS;
 #pragma unroll
-      for (int o = 1; o < G::TSPLIT; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (active && sub == 0)
-        out_st[tr * K + i] = sub_mod(gadget_ct<ELL>(tr, i), mod_u64(acc, p.q, p.mu), p.q);
+        for (int s = 0; s < K; ++s) {
+          const uint64_t ad = smem_desc(ta_base + s * 2 * G::TA_LBO, G::TA_LBO, 0u);
+          const uint64_t bd = smem_desc(b_base + s * 4 * G::LBO, G::LBO, G::SBO);
+          mma_i8_ss(d_tail, ad, bd, G::IDESC, s > 0 ? 1u : 0u);
+        }
+        mma_commit(&bar[3]);
+      }
     }
 
     // ---- phase 3: epilogue, TMEM -> registers -> (G - S) mod q -> smem ----
@@ -419,8 +455,7 @@ level_tc_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uin
 #pragma unroll
       for (int c = 0; c < G::NCH; ++c) {
         uint32_t chunk[16];
-        tmem_ld16((t_row_addr & 0xFFFF0000u) | ((tmem_base + tile * G::NPAD + 16 * c) & 0xFFFFu),
-                  chunk);
+        tmem_ld16(tmem_base + lane_off + tile * G::NPAD + 16 * c, chunk);
 #pragma unroll
         for (int x = 0; x < 16; ++x) d[16 * c + x] = chunk[x];
       }
@@ -428,11 +463,32 @@ level_tc_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uin
       if (row < G::ROWS) {
 #pragma unroll
         for (int i = 0; i < K; ++i) {
-          uint64_t s = 0;
+          const uint32_t g = (i == row_blk) ? (1u << row_bit) : 0u;
+          out_st[row * K + i] = finish_value<ELL, G::NDIG, PM>(&d[i * G::NDIG], g, p);
+        }
+      }
+    }
+    if constexpr (G::TAIL > 0) {
+      if (warp == 0) {
+        mbar_wait(&bar[3], t & 1u);
+        tc_fence_after();
+        uint32_t d[G::NPAD];
 #pragma unroll
-          for (int dg = 0; dg < G::NDIG; ++dg) s += (uint64_t)d[i * G::NDIG + dg] << (8 * dg);
-          s >>= 7;  // A bytes are 128
-          out_st[row * K + i] = sub_mod(gadget_ct<ELL>(row, i), mod_u64(s, p.q, p.mu), p.q);
+        for (int c = 0; c < G::NCH; ++c) {
+          uint32_t chunk[16];
+          tmem_ld16(tmem_base + G::D_COLS + 16 * c, chunk);
+#pragma unroll
+          for (int x = 0; x < 16; ++x) d[16 * c + x] = chunk[x];
+        }
+        tmem_wait_ld();
+        if (tid < G::TAIL) {
+          const int r = G::MMA_ROWS + tid;
+          const int rb = r / ELL, rbit = r - rb * ELL;
+#pragma unroll
+          for (int i = 0; i < K; ++i) {
+            const uint32_t g = (i == rb) ? (1u << rbit) : 0u;
+            out_st[r * K + i] = finish_value<ELL, G::NDIG, PM>(&d[i * G::NDIG], g, p);
+          }
         }
       }
     }

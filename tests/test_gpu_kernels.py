@@ -38,10 +38,12 @@ def _oracle_nand(p, a, b, ca, cb):
 
 
 @pytest.mark.parametrize("params", [DEFAULT_PARAMS, EXACT_PARAMS], ids=["default", "exact"])
-@pytest.mark.parametrize("kernel", [_native.KERNEL_TCGEN05, _native.KERNEL_SIMT], ids=["tc", "simt"])
-def test_level_kernel_random_operands(params, kernel):
+@pytest.mark.parametrize("kernel,dbg", [(_native.KERNEL_TCGEN05, 0), (_native.KERNEL_TCGEN05, 2),
+                                        (_native.KERNEL_SIMT, 0)], ids=["tc", "tc-generic-epilogue", "simt"])
+def test_level_kernel_random_operands(params, kernel, dbg):
     """A 2-level program over random operands, all complement combinations, many lanes."""
     s, ctx = _ctx(params, kernel)
+    ctx.set_debug(dbg)
     rng = np.random.default_rng(1234)
     lanes, n_in = 3, 8
     vals = _random_cts(params, n_in * lanes, rng)
