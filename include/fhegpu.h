@@ -123,6 +123,20 @@ int fhegpu_nand_batch(fhegpu_ctx *ctx, const uint32_t *v1, const uint32_t *v2,
                       uint32_t *out, uint64_t count);
 int fhegpu_not_batch(fhegpu_ctx *ctx, const uint32_t *v, uint32_t *out, uint64_t count);
 
+/* Fresh encryption on the device, stream-exact with numpy's Generator(PCG64)
+ * (replaces GswScheme._encrypt / encrypt_bit / encrypt_value, fhe.py:227-242).
+ * Ciphertext e draws its N x m bits starting u32_offset[e] 32-bit draws after
+ * streams[stream_idx[e]] (a numpy PCG64 state with has_uint32 == 0), exactly as
+ * rng.integers(0, 2, (N, m)) would, and stores V = (R pk + mu G) mod q at store
+ * index target[e].  pk: m x k row-major, entries < q; mu[e] < q. */
+typedef struct {
+  uint64_t state_lo, state_hi, inc_lo, inc_hi;
+} fhegpu_pcg64;
+
+int fhegpu_encrypt(fhegpu_ctx *ctx, const uint32_t *pk, const fhegpu_pcg64 *streams,
+                   uint32_t n_streams, const uint32_t *stream_idx, const uint64_t *u32_offset,
+                   const uint32_t *mu, const uint64_t *target, uint64_t count);
+
 #ifdef __cplusplus
 }
 #endif

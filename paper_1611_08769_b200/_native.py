@@ -59,7 +59,24 @@ SIGNATURES = [
     ("fhegpu_prog_destroy", None, [_P]),
     ("fhegpu_nand_batch", ctypes.c_int, [_P, _U32P, _U32P, _U32P, ctypes.c_uint64]),
     ("fhegpu_not_batch", ctypes.c_int, [_P, _U32P, _U32P, ctypes.c_uint64]),
+    ("fhegpu_encrypt", ctypes.c_int, [_P, _U32P, _P, ctypes.c_uint32, _U32P, _U64P, _U32P, _U64P,
+                                      ctypes.c_uint64]),
 ]
+
+PCG_DTYPE = np.dtype([("state_lo", "<u8"), ("state_hi", "<u8"), ("inc_lo", "<u8"), ("inc_hi", "<u8")])
+
+
+def pcg64_stream(rng) -> tuple:
+    """(state_lo, state_hi, inc_lo, inc_hi) of a numpy Generator(PCG64) at its current
+    position; requires no buffered 32-bit half (has_uint32 == 0)."""
+    st = rng.bit_generator.state
+    if st.get("bit_generator") != "PCG64":
+        raise ParameterError("device encryption reproduces numpy's PCG64 only")
+    if st["has_uint32"]:
+        raise ParameterError("generator holds a buffered 32-bit half; draw an even number first")
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    m = (1 << 64) - 1
+    return (s & m, s >> 64, inc & m, inc >> 64)
 
 
 def load_library(path: str = LIB_PATH):
@@ -216,6 +233,19 @@ class DeviceContext:
         _check(_lib.fhegpu_nand_batch(self.handle, _ptr(v1, ctypes.c_uint32), _ptr(v2, ctypes.c_uint32),
                                       _ptr(out, ctypes.c_uint32), len(v1)), "nand_batch")
         return out
+
+    def encrypt(self, public_key, streams, stream_idx, u32_offset, mu, target):
+        """Device encryption (fhegpu_encrypt): ciphertext e -> store index target[e]."""
+        pk = np.ascontiguousarray(np.asarray(public_key) % self.params.q, dtype=np.uint32)
+        st = np.ascontiguousarray(np.array([tuple(x) for x in streams], dtype=PCG_DTYPE))
+        idx = np.ascontiguousarray(stream_idx, dtype=np.uint32)
+        off = np.ascontiguousarray(u32_offset, dtype=np.uint64)
+        mus = np.ascontiguousarray(mu, dtype=np.uint32)
+        tgt = np.ascontiguousarray(target, dtype=np.uint64)
+        _check(_lib.fhegpu_encrypt(self.handle, _ptr(pk, ctypes.c_uint32), st.ctypes.data_as(ctypes.c_void_p),
+                                   len(st), _ptr(idx, ctypes.c_uint32), _ptr(off, ctypes.c_uint64),
+                                   _ptr(mus, ctypes.c_uint32), _ptr(tgt, ctypes.c_uint64), len(idx)),
+               "encrypt")
 
     def not_batch(self, v: np.ndarray) -> np.ndarray:
         v = np.ascontiguousarray(v, dtype=np.uint32)

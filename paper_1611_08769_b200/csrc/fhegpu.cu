@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "simt_nand.cuh"
 #include "tc_nand.cuh"
+#include "encrypt.cuh"
 
 using namespace fhegpu;
 
@@ -59,6 +60,7 @@ struct fhegpu_ctx {
   size_t comp_cap = 0;
   OpRec *d_tmp_ops = nullptr;
   size_t tmp_ops_cap = 0;
+  JumpTable *d_jump = nullptr;  // PCG64 jump-ahead constants (lazily uploaded)
 };
 
 struct fhegpu_prog {
@@ -222,6 +224,7 @@ void fhegpu_ctx_destroy(fhegpu_ctx *c) {
   cudaFree(c->d_idx);
   cudaFree(c->d_comp);
   cudaFree(c->d_tmp_ops);
+  cudaFree(c->d_jump);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }
@@ -474,6 +477,66 @@ int fhegpu_not_batch(fhegpu_ctx *c, const uint32_t *v, uint32_t *out, uint64_t c
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   cudaFree(buf);
   if (e != cudaSuccess) return fail(FHEGPU_ECUDA, std::string("not_batch: ") + cudaGetErrorString(e));
+  return FHEGPU_OK;
+}
+
+int fhegpu_encrypt(fhegpu_ctx *c, const uint32_t *pk, const fhegpu_pcg64 *streams, uint32_t n_streams,
+                   const uint32_t *stream_idx, const uint64_t *u32_offset, const uint32_t *mu,
+                   const uint64_t *target, uint64_t count) {
+  if (!c || (count && (!pk || !streams || !stream_idx || !u32_offset || !mu || !target)))
+    return fail(FHEGPU_EINVAL, "null argument");
+  if (count == 0) return FHEGPU_OK;
+  if (c->m == 0 || c->m > 4096) return fail(FHEGPU_EINVAL, "bad m");
+  for (uint64_t e = 0; e < count; ++e) {
+    if (stream_idx[e] >= n_streams) return fail(FHEGPU_EINVAL, "stream index out of range");
+    if (target[e] >= c->capacity) return fail(FHEGPU_EINVAL, "encrypt target beyond store capacity");
+    if (mu[e] >= c->p.q) return fail(FHEGPU_EINVAL, "plaintext must be < q");
+  }
+  for (uint32_t i = 0; i < c->m * c->p.k; ++i)
+    if (pk[i] >= c->p.q) return fail(FHEGPU_EINVAL, "public key entries must be < q");
+  for (uint32_t i = 0; i < n_streams; ++i)
+    if ((streams[i].inc_lo & 1u) == 0) return fail(FHEGPU_EINVAL, "PCG64 increment must be odd");
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (!c->d_jump) {
+    JumpTable h;
+    const u128 mult = ((u128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+    u128 a = mult, g = 1;
+    for (int j = 0; j < 64; ++j) {
+      h.a[j] = a;
+      h.g[j] = g;
+      g = g * (a + 1);
+      a = a * a;
+    }
+    CUDA_TRY(cudaMalloc(&c->d_jump, sizeof(JumpTable)));
+    CUDA_TRY(cudaMemcpy(c->d_jump, &h, sizeof(JumpTable), cudaMemcpyHostToDevice));
+  }
+  // one staging allocation: streams | stream_idx | offsets | mu | target | pk
+  const size_t b_str = (size_t)n_streams * sizeof(StreamRec), b_idx = count * 4, b_off = count * 8,
+               b_mu = count * 4, b_tgt = count * 8, b_pk = (size_t)c->m * c->p.k * 4;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t total = al(b_str) + al(b_idx) + al(b_off) + al(b_mu) + al(b_tgt) + al(b_pk);
+  uint8_t *buf = nullptr;
+  CUDA_TRY(cudaMalloc(&buf, total));
+  uint8_t *q = buf;
+  auto put = [&](const void *src, size_t n) {
+    uint8_t *dst = q;
+    cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, c->stream);
+    q += al(n);
+    return dst;
+  };
+  auto *d_str = (const StreamRec *)put(streams, b_str);
+  auto *d_idx = (const uint32_t *)put(stream_idx, b_idx);
+  auto *d_off = (const uint64_t *)put(u32_offset, b_off);
+  auto *d_mu = (const uint32_t *)put(mu, b_mu);
+  auto *d_tgt = (const uint64_t *)put(target, b_tgt);
+  auto *d_pk = (const uint32_t *)put(pk, b_pk);
+  const uint64_t work = count * c->p.rows;
+  encrypt_kernel<<<grid_for(work, c->num_sms), 256, b_pk, c->stream>>>(
+      c->store, c->d_jump, d_str, d_idx, d_off, d_mu, d_tgt, d_pk, count, c->m, c->p);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(buf);
+  if (e != cudaSuccess) return fail(FHEGPU_ECUDA, std::string("encrypt: ") + cudaGetErrorString(e));
   return FHEGPU_OK;
 }
 

@@ -78,7 +78,7 @@ class GpuEngine:
     def __init__(self, scheme: GswScheme, keys: KeyPair | None = None, public_key=None,
                  rng=None, threads: int = 1, batch_size: int = 1, lane_rngs=None,
                  cse: bool = False, keep_all: bool = False, record_trace: bool = False,
-                 dry_run: bool = False):
+                 dry_run: bool = False, device_encrypt: bool = False):
         if threads < 1:
             raise UsageError("threads must be >= 1")
         if batch_size < 1:
@@ -122,6 +122,13 @@ class GpuEngine:
         self.dry_run = dry_run
         self.dry_inputs: list[tuple[int, int]] = []     # (slot, packed lane bits)
         self.dry_programs: list[dict] = []
+        # device_encrypt: fresh encryptions are generated on the GPU (stream-exact with
+        # numpy's PCG64); the host only snapshots generator positions and advances them.
+        self.device_encrypt = device_encrypt
+        self._enc_streams: list[tuple] = []
+        self._enc_stream_id: dict = {}
+        self._enc_rows: list[np.ndarray] = []     # per chunk: (stream_idx, u32_off, mu, target)
+        self._draws_per_ct = self.params.n_ct * self.params.m
 
     # -- protocol attributes -----------------------------------------------------------
 
@@ -173,6 +180,14 @@ class GpuEngine:
             self._upload_inputs()
 
     def _upload_inputs(self):
+        if self._enc_rows:
+            self._ensure_capacity()
+            rows = np.concatenate(self._enc_rows, axis=1)
+            self.ctx.encrypt(self.public_key, self._enc_streams, rows[0], rows[1], rows[2], rows[3])
+            self._enc_rows.clear()
+            self._enc_streams.clear()
+            self._enc_stream_id.clear()
+            self._pending_in_bytes = 0
         if not self._pending_in_idx:
             return
         self._ensure_capacity()
@@ -210,6 +225,9 @@ class GpuEngine:
             if self.trace is not None:
                 self.trace.append((2, -1, -1, wire, node, 0))
             return GpuBit(self, node, 0, False, None, wire)
+        if self.device_encrypt:
+            mus = np.array([(bits >> l) & 1 for l in range(lanes)], dtype=np.int64)
+            return self.input_block(mus[:, None])[0]
         if self.lane_rngs is None:
             mus = [(bits >> l) & 1 for l in range(lanes)]
             vals = self.scheme.encrypt_many(self.public_key, mus, self.rng)
@@ -219,6 +237,64 @@ class GpuEngine:
                 vals[l] = self.scheme.encrypt_many(self.public_key, [(bits >> l) & 1],
                                                    self.lane_rngs[l])[0]
         return self._input_values(vals, 0, self._fresh_noise)
+
+    def input_block(self, bits) -> list:
+        """Fresh wires for a (lanes, n) block of plaintext bits, encrypted on the device.
+
+        Draw order: with ``lane_rngs`` lane l's generator encrypts its n bits in order;
+        with the single ``rng`` the block is drawn lane-major (lane 0's n inputs, then
+        lane 1's, ...) -- e.g. the pair-major a0, b0, a1, b1, ... of the gate benchmark.
+        Identical ciphertexts to encrypting one by one with the reference."""
+        bits = np.asarray(bits, dtype=np.int64)
+        lanes = self.batch_size
+        if bits.ndim != 2 or bits.shape[0] != lanes:
+            raise UsageError(f"expected a ({lanes}, n) bit block")
+        if ((bits != 0) & (bits != 1)).any():
+            raise UsageError("input bits must be 0 or 1")
+        if self.public_key is None:
+            raise CapabilityError("encrypting inputs needs the public key")
+        if self._draws_per_ct % 2:
+            raise UsageError("device encryption needs N*m even")
+        from ._native import pcg64_stream
+        n = bits.shape[1]
+        step = self._draws_per_ct
+        nodes = [self._new_node(0, self._fresh_noise) for _ in range(n)]
+        slots = np.array([self._alloc_slot() for _ in range(n)], dtype=np.uint64)
+        for node, slot in zip(nodes, slots.tolist()):
+            self._slot[node] = slot
+        lane_ix = np.arange(lanes, dtype=np.uint64)
+        target = (slots[None, :] * np.uint64(lanes) + lane_ix[:, None])        # (lanes, n)
+        if self.lane_rngs is None:
+            sid = self._stream_id(pcg64_stream(self.rng))
+            stream_idx = np.full((lanes, n), sid, dtype=np.uint32)
+            off = (np.arange(lanes * n, dtype=np.uint64) * np.uint64(step)).reshape(lanes, n)
+            self.rng.bit_generator.advance(lanes * n * step // 2)
+        else:
+            stream_idx = np.empty((lanes, n), dtype=np.uint32)
+            for l, g in enumerate(self.lane_rngs):
+                stream_idx[l, :] = self._stream_id(pcg64_stream(g))
+                g.bit_generator.advance(n * step // 2)
+            off = np.broadcast_to(np.arange(n, dtype=np.uint64) * np.uint64(step), (lanes, n))
+        self._enc_rows.append(np.stack([stream_idx.ravel().astype(np.uint64), off.ravel(),
+                                        bits.ravel().astype(np.uint64), target.ravel()]))
+        self._pending_in_bytes += lanes * n * 32
+        out = []
+        for node in nodes:
+            wire = self._new_wire()
+            if self.trace is not None:
+                self.trace.append((2, -1, -1, wire, node, 0))
+            out.append(GpuBit(self, node, 0, False, None, wire))
+        if self._pending_in_bytes >= _UPLOAD_BATCH_BYTES:
+            self._upload_inputs()
+        return out
+
+    def _stream_id(self, st: tuple) -> int:
+        sid = self._enc_stream_id.get(st)
+        if sid is None:
+            sid = len(self._enc_streams)
+            self._enc_streams.append(st)
+            self._enc_stream_id[st] = sid
+        return sid
 
     def input_values(self, values: np.ndarray, level: int = 0, noise_est: int | None = None) -> GpuBit:
         """New wire from precomputed compact ciphertexts, one per lane: (lanes, N, k)."""

@@ -1,0 +1,157 @@
+"""Config-level GPU parity: ciphertexts gate by gate and decrypted outputs vs the reference.
+
+Golden digests come from running the reference itself (tests/golden/make_golden.py);
+the gate-by-gate chain covers every hom_nand / hom_not the reference evaluated, in order.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import digest
+from paper_1611_08769_b200 import (DEFAULT0_PARAMS, DEFAULT_PARAMS, EXACT_PARAMS, FixedFormat,
+                                   GpuEngine, GswScheme, and_, fft_1d, fft_2d, input_signal, xor_)
+from paper_1611_08769_b200.fft import read_signal_ints, signal_words
+from tests.helpers import GOLDEN, FFT_CONFIGS, config_signal, golden_json, golden_npz, model_outputs
+
+pytestmark = pytest.mark.gpu
+
+PARAMS = {"EXACT": EXACT_PARAMS, "DEFAULT0": DEFAULT0_PARAMS}
+
+
+def gate_digests(eng, lane=0, chunk=16384):
+    """Digest of every hom_nand / hom_not output in reference order, plus input digests."""
+    trace = eng.trace
+    ins = [t for t in trace if t[0] == 2]
+    gates = [t for t in trace if t[0] in (0, 1)]
+
+    def digs(entries):
+        out = []
+        for s in range(0, len(entries), chunk):
+            part = entries[s:s + chunk]
+            vals = eng.read_nodes([t[4] for t in part], [t[5] for t in part], lanes=[lane])
+            out.extend(digest.digest_compact(v[0]) for v in vals)
+        return out
+    return digs(ins), digs(gates)
+
+
+def run_fft_config(cfg, device_encrypt, keep_all=True, lanes=1):
+    pname, seed, (F, f), dims, _ = FFT_CONFIGS[cfg]
+    params = PARAMS[pname]
+    scheme = GswScheme(params)
+    keys = scheme.keygen(seed)
+    if lanes == 1:
+        rng, x = config_signal(cfg)
+        eng = GpuEngine(scheme, keys=keys, rng=rng, keep_all=keep_all, record_trace=keep_all,
+                        device_encrypt=device_encrypt)
+        values = x
+    else:
+        rngs, vals = [], []
+        for lane in range(lanes):
+            r, x = config_signal(cfg, lane)
+            rngs.append(r)
+            vals.append(x)
+        eng = GpuEngine(scheme, keys=keys, batch_size=lanes, lane_rngs=rngs,
+                        device_encrypt=device_encrypt, keep_all=keep_all, record_trace=keep_all)
+        values = np.array(vals)
+    sig = input_signal(eng, values, FixedFormat(F, f), dims=dims if isinstance(dims, tuple) else None)
+    out = fft_2d(sig) if isinstance(dims, tuple) else fft_1d(sig)
+    eng.flush()
+    return eng, out, values
+
+
+@pytest.mark.parametrize("device_encrypt", [False, True], ids=["host-enc", "device-enc"])
+def test_cfg0_gate_by_gate(device_encrypt):
+    eng, out, x = run_fft_config("cfg0", device_encrypt)
+    ref = golden_json("cts_cfg0.json")
+    ins, gates = gate_digests(eng)
+    assert digest.chain_digest(ins) == ref["inputs_chain"]
+    gd = golden_npz("cts_cfg0.npz")["gate_digests"].view(np.uint8).reshape(-1, 8)
+    want = [bytes(r).hex() for r in gd]
+    first_bad = next((i for i, (a, b) in enumerate(zip(gates, want)) if a != b), None)
+    assert first_bad is None, f"first differing gate {first_bad}"
+    assert digest.chain_digest(gates) == ref["gates_chain"]
+    assert read_signal_ints(eng, out)[0].tolist() == ref["output_words"]
+    assert (eng.nand_count, eng.max_depth) == (ref["nand_count"], ref["max_depth"])
+
+
+def test_cfg1_sample_pairs_bit_exact():
+    """First 4096 pairs of the 2^20-pair gate benchmark: every XOR/AND ciphertext."""
+    ref = golden_json("cts_cfg1.json")
+    pairs = ref["pairs"]
+    scheme = GswScheme(DEFAULT_PARAMS)
+    keys = scheme.keygen(1)
+    rng = np.random.default_rng(1)
+    bits = rng.integers(0, 2, (1 << 20, 2))
+    eng = GpuEngine(scheme, keys=keys, rng=rng, batch_size=pairs, device_encrypt=True,
+                    keep_all=True, record_trace=True)
+    a, b = eng.input_block(bits[:pairs])
+    x = xor_(a, b)
+    y = and_(a, b)
+    assert eng.read_back_bits([x])[0].tolist() == (bits[:pairs, 0] ^ bits[:pairs, 1]).tolist()
+    assert eng.read_back_bits([y])[0].tolist() == (bits[:pairs, 0] & bits[:pairs, 1]).tolist()
+    vx = eng.node_values([x])[0]
+    vy = eng.node_values([y])[0]
+    assert [digest.digest_compact(v) for v in vx] == ref["xor_digests"]
+    assert [digest.digest_compact(v) for v in vy] == ref["and_digests"]
+    gates = [t for t in eng.trace if t[0] in (0, 1)]
+    assert len(gates) == 6
+    vals = eng.read_nodes([t[4] for t in gates], [t[5] for t in gates])     # (6, pairs, N, k)
+    per_pair = [digest.digest_compact(vals[g, p]) for p in range(pairs) for g in range(6)]
+    assert per_pair[:len(ref["first_gates"])] == ref["first_gates"]
+    assert digest.chain_digest(per_pair) == ref["gates_chain"]
+    assert eng.nand_count == 6 and eng.max_depth == 3
+
+
+def test_cfg4_all_lanes_outputs():
+    """1024 signals as lanes (device encryption, per-lane generators): all outputs bit-exact."""
+    eng, out, vals = run_fft_config("cfg4", device_encrypt=True, keep_all=False, lanes=1024)
+    got = read_signal_ints(eng, out)
+    want = golden_npz("clear_cfg4.npz")["words"]
+    assert np.array_equal(got, want)
+    assert np.array_equal(got, model_outputs("cfg4", vals))
+    assert eng.nand_count == golden_json("trace_cfg4.json")["nand_count"]
+    assert eng.launches == golden_json("trace_cfg4.json")["max_depth"]   # one launch per level
+
+
+def test_cfg4_lane0_gate_by_gate():
+    eng, out, _ = run_fft_config("cfg4", device_encrypt=True)
+    ref = golden_json("cts_cfg4.json")
+    ins, gates = gate_digests(eng)
+    assert digest.chain_digest(ins) == ref["inputs_chain"]
+    every = ref["checkpoint_every"]
+    cps = [digest.chain_digest(gates[:i]) for i in range(every, len(gates) + 1, every)]
+    assert cps == ref["gates_checkpoints"]
+    assert digest.chain_digest(gates) == ref["gates_chain"]
+    assert read_signal_ints(eng, out)[0].tolist() == ref["output_words"]
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg2"])
+def test_fft_config_gate_by_gate(cfg):
+    path = os.path.join(GOLDEN, f"cts_{cfg}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"golden {cfg} ciphertext digests not generated")
+    eng, out, x = run_fft_config(cfg, device_encrypt=True)
+    ref = golden_json(f"cts_{cfg}.json")
+    ins, gates = gate_digests(eng)
+    assert digest.chain_digest(ins) == ref["inputs_chain"]
+    assert digest.chain_digest(gates) == ref["gates_chain"]
+    assert read_signal_ints(eng, out)[0].tolist() == ref["output_words"]
+    assert read_signal_ints(eng, out)[0].tolist() == golden_npz(f"clear_{cfg}.npz")["words"][0].tolist()
+
+
+def test_device_encryption_equals_host_encryption():
+    for params, seed in ((DEFAULT_PARAMS, 1), (EXACT_PARAMS, 3)):
+        s = GswScheme(params)
+        keys = s.keygen(seed)
+        r_host = np.random.default_rng(42)
+        r_dev = np.random.default_rng(42)
+        bits = r_host.integers(0, 2, (3, 5))
+        r_dev.integers(0, 2, (3, 5))
+        host = s.encrypt_many(keys.public_key, bits.ravel(), r_host)
+        eng = GpuEngine(s, keys=keys, rng=r_dev, batch_size=3, device_encrypt=True)
+        hs = eng.input_block(bits)
+        dev = eng.node_values(hs)                                    # (5, 3, N, k)
+        assert np.array_equal(dev.transpose(1, 0, 2, 3).reshape(-1, params.n_ct, params.k), host)
+        assert r_host.bit_generator.state == r_dev.bit_generator.state
