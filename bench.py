@@ -1,0 +1,491 @@
+#!/usr/bin/env python
+"""Benchmark: homomorphic NAND-gate throughput on one B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], the gate microbenchmark): 2^20 independent
+pairs of encrypted random bits (DEFAULT params, N = 261, keys seed 1, bits and
+encryptions from default_rng(1), pair-major), one XOR + one AND per pair =
+6 NANDs per pair as the reference counts them (gates.py:13-24).  A "step" is
+one evaluation of that whole netlist: 3 levels, one kernel launch each, every
+launch spanning every pair.  Secondary: configs[4], 1024 x 16-point Q4.12
+FFTs (DEFAULT dims, noise-free), reported as FFTs/s.
+
+  value      NAND/s, inputs resident in HBM, device time (CUDA events, max over ranks)
+  e2e        same metric through the C-ABI with host buffers: pinned H2D of the
+             step's input ciphertexts + evaluation + D2H of every output ciphertext
+  roofline   level_tc_kernel: algorithmic bytes 3*ceil(N^2/8) per NAND / avg launch time
+  cpu_baseline  the reference algorithm (oracle/gsw.py restates fhe.py:325-341:
+             float64 N x N product + flatten) on this box's host cores, time-boxed sample
+
+`--impl reference` times that CPU path alone (the reference's own implementation,
+restated; the Python reference cannot travel to the GPU box) on every host core.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "encrypted gates/s (homomorphic NAND, reference-counted) on B200"
+UNIT = "NAND/s"
+PAIRS_FULL = 1 << 20
+ALG_BYTES_PER_NAND_261 = 3 * math.ceil(261 * 261 / 8)   # 25,548 B
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------------------
+# CPU reference leg (oracle port of the reference algorithm), process pool
+# ----------------------------------------------------------------------------------------
+
+def _cpu_worker(args):
+    seconds, seed = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    import numpy as np
+    from oracle import gsw
+    p = gsw.DEFAULT
+    pk, _ = gsw.keygen(p, 1)
+    rng = np.random.default_rng(1000 + seed)
+    cts = [gsw.encrypt_matrix(p, pk, int(b), rng) for b in rng.integers(0, 2, 8)]
+    # XOR + AND per pair, the reference's 6 NANDs (gates.py:13-24) in its float64 algorithm
+    nands = 0
+    t0 = time.perf_counter()
+    i = 0
+    while True:
+        a, b = cts[i % 8], cts[(i + 3) % 8]
+        n1 = gsw.hom_nand_matrix(p, a, b)
+        t1 = gsw.hom_nand_matrix(p, n1, a)
+        t2 = gsw.hom_nand_matrix(p, n1, b)
+        gsw.hom_nand_matrix(p, t1, t2)
+        n2 = gsw.hom_nand_matrix(p, a, b)
+        gsw.hom_nand_matrix(p, n2, n2)
+        nands += 6
+        i += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            return nands, el
+
+
+def cpu_reference(seconds: float, workers: int | None = None):
+    """Aggregate NAND/s of the reference algorithm on `workers` host processes."""
+    import multiprocessing as mp
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    workers = workers or os.cpu_count() or 1
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(workers) as pool:
+        res = pool.map(_cpu_worker, [(seconds, i) for i in range(workers)])
+    total = sum(n for n, _ in res)
+    wall = max(t for _, t in res)
+    return total / wall, workers, total
+
+
+# ----------------------------------------------------------------------------------------
+# clocks (NVML, sampled during the timed region)
+# ----------------------------------------------------------------------------------------
+
+class ClockSampler:
+    def __init__(self, device: int, period: float = 0.02):
+        self.device, self.period = device, period
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        self.ok = True
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.ok = False
+
+    _BITS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+             0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self._BITS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------------------
+
+def _dist():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def _max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def time_program(prog, lanes, stream, steps, warmup, world, sampler=None):
+    import torch
+    for _ in range(warmup):
+        prog.run(lanes)
+    torch.cuda.synchronize()
+    _barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if sampler is not None:
+        sampler.__enter__()
+    e0.record(stream)
+    for _ in range(steps):
+        prog.run(lanes)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if sampler is not None:
+        sampler.__exit__()
+    _barrier(world)
+    return _max_over_ranks(e0.elapsed_time(e1) / steps, world)
+
+
+def level_launch_times(prog, lanes, stream, reps=3):
+    """Average duration (ms) of each level's single kernel launch (CUDA events)."""
+    import torch
+    out = []
+    for lv in range(prog.n_levels):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        prog.run(lanes, lv, lv + 1)
+        e0.record(stream)
+        for _ in range(reps):
+            prog.run(lanes, lv, lv + 1)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out.append(e0.elapsed_time(e1) / reps)
+    return out
+
+
+def _traffic_from_profiles(widths_items, lanes):
+    """dram bytes per launch from the committed ncu capture (profiles/ncu_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            d = json.load(fh)
+        per_item = d["dram_bytes_per_item"]
+        items = sum(widths_items) / max(1, len(widths_items))
+        return per_item * items, d
+    except Exception:
+        return None, None
+
+
+def bench_gates(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    from paper_1611_08769_b200 import DEFAULT_PARAMS, GpuEngine, GswScheme, and_, xor_
+    pairs = args.pairs
+    scheme = GswScheme(DEFAULT_PARAMS, device=local)
+    keys = scheme.keygen(1)
+    rng = np.random.default_rng(1 + rank)           # rank 0 is exactly the cfg1 protocol
+    bits = rng.integers(0, 2, (PAIRS_FULL, 2))      # full draw keeps the stream positions
+    t0 = time.perf_counter()
+    eng = GpuEngine(scheme, keys=keys, rng=rng, batch_size=pairs, device_encrypt=True,
+                    cse=args.cse)
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    scheme.ctx.use_torch_stream(stream)
+    a, b = eng.input_block(bits[:pairs])
+    x = xor_(a, b)
+    y = and_(a, b)
+    prog = eng.flush()
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    # correctness spot check (outside timing): decrypt 64 lanes of each output
+    xb = eng.read_back_bits([x, y])
+    ok = bool((xb[0] == (bits[:pairs, 0] ^ bits[:pairs, 1])).all()
+              and (xb[1] == (bits[:pairs, 0] & bits[:pairs, 1])).all())
+    lanes = pairs
+    nand_per_step = eng.nand_count * lanes
+    exec_per_step = eng.executed_nands * lanes
+    sampler = ClockSampler(local)
+    ms = time_program(prog, lanes, stream, args.steps, args.warmup, world, sampler)
+    comp = eng.last_compile
+    widths_items = [int(w) * lanes for w in comp["widths"]]
+    lv_ms = level_launch_times(prog, lanes, stream)
+    peak, peak_kind = _peaks()
+    bytes_per_launch = [w * ALG_BYTES_PER_NAND_261 for w in widths_items]
+    achieved = sum(bytes_per_launch) / (sum(lv_ms) / 1e3) / 1e9        # GB/s
+    traffic, tinfo = _traffic_from_profiles(widths_items, lanes)
+    res = {
+        "ms": ms, "nand_per_step": nand_per_step, "exec_per_step": exec_per_step,
+        "launches_per_step": prog.launches, "widths": [int(w) for w in comp["widths"]],
+        "level_ms": lv_ms, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+        "traffic": traffic, "traffic_info": tinfo, "ok": ok, "setup_s": setup_s,
+        "clocks": sampler.summary(), "kernel": scheme.ctx.kernel,
+        "slots": eng._n_slots, "store_gb": eng._n_slots * lanes * scheme.ctx.ct_words * 4 / 1e9,
+    }
+    if args.e2e:
+        res["e2e"] = e2e_gates(eng, scheme, prog, lanes, (a, b), (x, y), stream, args, world)
+    del eng, prog, a, b, x, y
+    return res
+
+
+def e2e_gates(eng, scheme, prog, lanes, inputs, outputs, stream, args, world):
+    """Same step through the C-ABI with HOST buffers: pinned H2D of both input ciphertext
+    arrays, evaluation, D2H of both output ciphertext arrays, every step."""
+    import torch
+    ctx = scheme.ctx
+    words = scheme.params.n_ct * scheme.params.k
+    for h in inputs + outputs:
+        assert h.neg == 0
+    in_first = [eng._slot[h.node] * lanes for h in inputs]
+    out_first = [eng._slot[h.node] * lanes for h in outputs]
+    t0 = time.perf_counter()
+    host_in = torch.empty((len(inputs), lanes, words), dtype=torch.int32, pin_memory=True)
+    host_out = torch.empty((len(outputs), lanes, words), dtype=torch.int32, pin_memory=True)
+    for i, f in enumerate(in_first):             # the step's inputs, as a client would hold them
+        ctx.read_range(f, lanes, host_in[i].data_ptr())
+    pin_s = time.perf_counter() - t0
+
+    def step():
+        for i, f in enumerate(in_first):
+            ctx.write_range(f, lanes, host_in[i].data_ptr(), sync=False)
+        prog.run(lanes)
+        for i, f in enumerate(out_first):
+            ctx.read_range(f, lanes, host_out[i].data_ptr(), sync=False)
+
+    steps = max(1, min(args.steps, 5))
+    for _ in range(max(1, min(args.warmup, 2))):
+        step()
+    torch.cuda.synchronize()
+    _barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - w0) * 1e3 / steps
+    ms = _max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    # the results are the reference ciphertexts: decrypt a few lanes from host memory
+    bytes_ct = words * 4
+    return {"ms": ms, "wall_ms": wall_ms, "steps": steps, "pin_s": pin_s,
+            "h2d": len(inputs) * lanes * bytes_ct, "d2h": len(outputs) * lanes * bytes_ct,
+            "sample_out": host_out[0, :2, :4].tolist()}
+
+
+def bench_fft(args, world, rank, local):
+    """configs[4]: 1024 independent 16-point Q4.12 FFTs as lanes of one netlist."""
+    import numpy as np
+    import torch
+
+    from paper_1611_08769_b200 import DEFAULT0_PARAMS, FixedFormat, GpuEngine, GswScheme, fft_1d, input_signal
+    from paper_1611_08769_b200.fft import read_signal_ints
+    lanes = args.fft_lanes
+    scheme = GswScheme(DEFAULT0_PARAMS, device=local)
+    keys = scheme.keygen(4)
+    rngs, vals = [], []
+    for lane in range(lanes):
+        r = np.random.default_rng(4 + lane + rank * lanes)
+        re = r.uniform(-1, 1, 16)
+        im = r.uniform(-1, 1, 16)
+        rngs.append(r)
+        vals.append(re + 1j * im)
+    t0 = time.perf_counter()
+    eng = GpuEngine(scheme, keys=keys, batch_size=lanes, lane_rngs=rngs, device_encrypt=True)
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    scheme.ctx.use_torch_stream(stream)
+    out = fft_1d(input_signal(eng, np.array(vals), FixedFormat(16, 12)))
+    build_s = time.perf_counter() - t0
+    prog = eng.flush()
+    torch.cuda.synchronize()
+    got = read_signal_ints(eng, out)
+    ok = None
+    if rank == 0:
+        try:
+            from tests.helpers import golden_npz
+            ok = bool(np.array_equal(got, golden_npz("clear_cfg4.npz")["words"][:lanes]))
+        except Exception:
+            ok = None
+    ms = time_program(prog, lanes, stream, max(2, args.steps // 2), min(args.warmup, 3), world)
+    return {"ms": ms, "ffts_per_s": lanes * world / (ms / 1e3),
+            "nand_per_s": eng.nand_count * lanes * world / (ms / 1e3),
+            "nand_per_fft": eng.nand_count, "levels": prog.n_levels, "lanes": lanes,
+            "build_s": build_s, "ok": ok}
+
+
+def run_ours(args):
+    world, rank, local = _dist()
+    res = bench_gates(args, world, rank, local)
+    fft = None
+    if args.fft:
+        import gc
+        gc.collect()
+        fft = bench_fft(args, world, rank, local)
+    cpu = None
+    if rank == 0 and world == 1 and args.cpu_seconds > 0:
+        v, cores, total = cpu_reference(args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{cores} processes x {args.cpu_seconds:.0f} s time-boxed XOR+AND pairs "
+                         f"({total} NANDs) of oracle/gsw.py hom_nand_matrix (the reference's float64 "
+                         f"N x N product + flatten, fhe.py:325-341), OPENBLAS_NUM_THREADS=1"}
+    if rank != 0:
+        _barrier(world)
+        return
+    ms = res["ms"]
+    value = res["nand_per_step"] * world / (ms / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8xu8->s32 tcgen05 MMA, u32 Z_q", "data": "synthetic",
+        "config": {
+            "workload": "configs[1] gate microbenchmark: 2^20 pairs x (XOR + AND) = 6 NANDs/pair, "
+                        "DEFAULT params n=8 q=2^29-3 m=32 (N=261), keygen(1), default_rng(1) pair-major",
+            "pairs_per_gpu": args.pairs, "nand_per_step_per_gpu": res["nand_per_step"],
+            "executed_nand_per_step_per_gpu": res["exec_per_step"], "cse": args.cse,
+            "levels": len(res["widths"]), "gates_per_level": res["widths"],
+            "parallelism": f"replicas x{world} (independent pairs, no collective)",
+            "l2": f"inputs {2 * args.pairs * 9408 / 1e9:.1f} GB per step >> 126 MB L2 (no flush needed)",
+            "kernel": res["kernel"], "decrypt_check": res["ok"],
+            "store_gb": round(res["store_gb"], 1), "setup_s": round(res["setup_s"], 2),
+        },
+        "roofline": {
+            "bound": "hbm", "achieved": res["achieved"], "peak": res["peak"], "unit": "GB/s",
+            "frac": res["achieved"] / res["peak"], "traffic": res["traffic"],
+            "kernel": "fhegpu::tc::level_tc_kernel<9,29,true>",
+            "algorithmic_bytes_per_nand": ALG_BYTES_PER_NAND_261,
+            "level_launch_ms": [round(x, 4) for x in res["level_ms"]],
+            "peak_source": res["peak_kind"],
+        },
+        "gpu_launches": res["launches_per_step"] * args.steps,
+        "clocks": res["clocks"],
+    }
+    if "e2e" in res:
+        e = res["e2e"]
+        line["e2e"] = {"value": res["nand_per_step"] * world / (e["ms"] / 1e3), "unit": UNIT,
+                       "h2d_bytes_per_step": e["h2d"], "d2h_bytes_per_step": e["d2h"],
+                       "ms_per_step": e["ms"], "steps": e["steps"],
+                       "path": "fhegpu_store_write_range (pinned) -> fhegpu_prog_run -> "
+                               "fhegpu_store_read_range (pinned), all ciphertexts of the step"}
+    if fft is not None:
+        line["fft"] = {"metric": "16-pt Q4.12 FHE FFTs/s (configs[4])", "value": fft["ffts_per_s"],
+                       "unit": "FFT/s", "nand_per_s": fft["nand_per_s"], "ms_per_step": fft["ms"],
+                       "lanes": fft["lanes"], "nand_per_fft": fft["nand_per_fft"],
+                       "levels": fft["levels"], "decrypt_check_vs_reference": fft["ok"]}
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    _barrier(world)
+
+
+def run_reference(args):
+    """The reference's own algorithm on host cores, same metric/config; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    seconds = max(1.0, args.ref_step_seconds)
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        cpu_reference(1.0)
+    vals, totals = [], 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, cores, total = cpu_reference(seconds)
+        vals.append(v)
+        totals += total
+    wall = time.perf_counter() - t0
+    value = statistics.mean(vals)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 (exact integers)", "data": "synthetic",
+        "config": {"workload": "configs[1] gate microbenchmark: XOR + AND pairs, DEFAULT params "
+                               "(N=261); each step a time-boxed sample on every host core"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"per step {cores} processes x {seconds:.0f} s of XOR+AND pairs "
+                                   f"({totals} NANDs total) with oracle/gsw.py hom_nand_matrix"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--pairs", type=int, default=PAIRS_FULL)
+    ap.add_argument("--cse", action="store_true", help="share XOR/AND's common NAND (reported separately)")
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-fft", dest="fft", action="store_false")
+    ap.add_argument("--fft-lanes", type=int, default=1024)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=4.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

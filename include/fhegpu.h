@@ -104,6 +104,14 @@ int fhegpu_store_read(fhegpu_ctx *ctx, const uint64_t *idx, const uint8_t *compl
 int fhegpu_store_read_rows(fhegpu_ctx *ctx, const uint64_t *idx, const uint8_t *complement,
                            uint64_t count, uint32_t row, uint32_t *host_rows /* count x k */);
 
+/* Contiguous ciphertext ranges [first, first + count) <-> dense host rows (N*k u32 each),
+ * one strided async copy (pinned host memory reaches full PCIe bandwidth).  async = 0
+ * synchronises the context stream before returning. */
+int fhegpu_store_write_range(fhegpu_ctx *ctx, uint64_t first, uint64_t count,
+                             const uint32_t *host_v, int async);
+int fhegpu_store_read_range(fhegpu_ctx *ctx, uint64_t first, uint64_t count, uint32_t *host_v,
+                            int async);
+
 /* Levelised netlist: ops[level_offsets[l] .. level_offsets[l+1]) are the gates of
  * level l; every op of a level reads only slots written by earlier levels. */
 int fhegpu_prog_create(fhegpu_ctx *ctx, const fhegpu_op *ops, uint64_t n_ops,

@@ -52,6 +52,8 @@ SIGNATURES = [
     ("fhegpu_store_write", ctypes.c_int, [_P, _U64P, ctypes.c_uint64, _U32P]),
     ("fhegpu_store_read", ctypes.c_int, [_P, _U64P, _U8P, ctypes.c_uint64, _U32P]),
     ("fhegpu_store_read_rows", ctypes.c_int, [_P, _U64P, _U8P, ctypes.c_uint64, ctypes.c_uint32, _U32P]),
+    ("fhegpu_store_write_range", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P, ctypes.c_int]),
+    ("fhegpu_store_read_range", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P, ctypes.c_int]),
     ("fhegpu_prog_create", ctypes.c_int, [_P, _P, ctypes.c_uint64, _U64P, ctypes.c_uint32, ctypes.POINTER(_P)]),
     ("fhegpu_prog_run", ctypes.c_int, [_P, _P, ctypes.c_uint32]),
     ("fhegpu_prog_run_range", ctypes.c_int, [_P, _P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]),
@@ -202,6 +204,15 @@ class DeviceContext:
         vals = np.ascontiguousarray(values, dtype=np.uint32).reshape(len(idx), self.words)
         _check(_lib.fhegpu_store_write(self.handle, _ptr(idx, ctypes.c_uint64), len(idx),
                                        _ptr(vals, ctypes.c_uint32)), "store_write")
+
+    def write_range(self, first: int, count: int, host_ptr: int, sync: bool = True):
+        """Raw host pointer (e.g. pinned torch tensor) of count dense ciphertexts -> store."""
+        _check(_lib.fhegpu_store_write_range(self.handle, first, count, ctypes.c_void_p(host_ptr),
+                                             0 if sync else 1), "store_write_range")
+
+    def read_range(self, first: int, count: int, host_ptr: int, sync: bool = True):
+        _check(_lib.fhegpu_store_read_range(self.handle, first, count, ctypes.c_void_p(host_ptr),
+                                            0 if sync else 1), "store_read_range")
 
     def read(self, idx, complement=None) -> np.ndarray:
         idx = np.ascontiguousarray(idx, dtype=np.uint64)

@@ -355,6 +355,32 @@ int fhegpu_store_read_rows(fhegpu_ctx *c, const uint64_t *idx, const uint8_t *co
   return read_impl(c, idx, comp, count, (int)row, host_rows);
 }
 
+int fhegpu_store_write_range(fhegpu_ctx *c, uint64_t first, uint64_t count, const uint32_t *host_v,
+                             int async) {
+  if (!c || (count && !host_v)) return fail(FHEGPU_EINVAL, "null argument");
+  if (first + count > c->capacity) return fail(FHEGPU_EINVAL, "range beyond store capacity");
+  if (count == 0) return FHEGPU_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t dense = (size_t)c->p.words * 4, pitch = (size_t)c->p.ct_words * 4;
+  CUDA_TRY(cudaMemcpy2DAsync(c->store + first * c->p.ct_words, pitch, host_v, dense, dense, count,
+                             cudaMemcpyHostToDevice, c->stream));
+  if (!async) CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FHEGPU_OK;
+}
+
+int fhegpu_store_read_range(fhegpu_ctx *c, uint64_t first, uint64_t count, uint32_t *host_v,
+                            int async) {
+  if (!c || (count && !host_v)) return fail(FHEGPU_EINVAL, "null argument");
+  if (first + count > c->capacity) return fail(FHEGPU_EINVAL, "range beyond store capacity");
+  if (count == 0) return FHEGPU_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t dense = (size_t)c->p.words * 4, pitch = (size_t)c->p.ct_words * 4;
+  CUDA_TRY(cudaMemcpy2DAsync(host_v, dense, c->store + first * c->p.ct_words, pitch, dense, count,
+                             cudaMemcpyDeviceToHost, c->stream));
+  if (!async) CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FHEGPU_OK;
+}
+
 int fhegpu_prog_create(fhegpu_ctx *c, const fhegpu_op *ops, uint64_t n_ops,
                        const uint64_t *level_offsets, uint32_t n_levels, fhegpu_prog **out) {
   if (!c || !out || (n_ops && !ops) || !level_offsets) return fail(FHEGPU_EINVAL, "null argument");

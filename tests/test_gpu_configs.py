@@ -147,11 +147,11 @@ def test_device_encryption_equals_host_encryption():
         keys = s.keygen(seed)
         r_host = np.random.default_rng(42)
         r_dev = np.random.default_rng(42)
-        bits = r_host.integers(0, 2, (3, 5))
-        r_dev.integers(0, 2, (3, 5))
+        bits = r_host.integers(0, 2, (3, 6))          # even count: no buffered half left
+        r_dev.integers(0, 2, (3, 6))
         host = s.encrypt_many(keys.public_key, bits.ravel(), r_host)
         eng = GpuEngine(s, keys=keys, rng=r_dev, batch_size=3, device_encrypt=True)
         hs = eng.input_block(bits)
-        dev = eng.node_values(hs)                                    # (5, 3, N, k)
+        dev = eng.node_values(hs)                                    # (6, 3, N, k)
         assert np.array_equal(dev.transpose(1, 0, 2, 3).reshape(-1, params.n_ct, params.k), host)
         assert r_host.bit_generator.state == r_dev.bit_generator.state
