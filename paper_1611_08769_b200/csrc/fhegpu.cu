@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "simt_nand.cuh"
 #include "tc_nand.cuh"
+#include "tc_nand_ws.cuh"
 #include "encrypt.cuh"
 
 using namespace fhegpu;
@@ -115,8 +116,36 @@ int launch_tc_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_
   return FHEGPU_OK;
 }
 
+template <int K, int ELL, bool PM>
+int launch_tc_ws_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes) {
+  using G = tc::GeoWS<K, ELL, PM>;
+  static bool attr_done = false;
+  // > half of the SM's shared memory: exactly one CTA (512 TMEM columns) per SM
+  const int smem = std::max(G::SMEM, 120 * 1024);
+  if (!attr_done) {
+    CUDA_TRY(cudaFuncSetAttribute(tc::level_tc_ws_kernel<K, ELL, PM>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_done = true;
+  }
+  const uint64_t items = (uint64_t)n_ops * lanes;
+  if (items >= (1ull << 32)) return fail(FHEGPU_EINVAL, "level too large (>= 2^32 gate items)");
+  const uint64_t grid = std::min<uint64_t>(items, (uint64_t)c->num_sms);
+  tc::level_tc_ws_kernel<K, ELL, PM><<<(unsigned)grid, G::THREADS, smem, c->stream>>>(
+      store, ops, n_ops, lanes, c->p);
+  CUDA_TRY(cudaGetLastError());
+  return FHEGPU_OK;
+}
+
 template <int K, int ELL>
 int launch_tc(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes) {
+  if constexpr ((ELL + 7) / 8 == 4 && tc::Geo<K, ELL>::MT >= 1 &&
+                tc::Geo<K, ELL>::D_COLS + tc::Geo<K, ELL>::A_COLS <= 256) {
+    if (!(c->p.dbg & 4u)) {  // dbg bit 2 selects the two-CTA (v2) kernel
+      if (pm_ok(c->p.q, c->p.ell) && !(c->p.dbg & 2u))
+        return launch_tc_ws_impl<K, ELL, true>(c, store, ops, n_ops, lanes);
+      return launch_tc_ws_impl<K, ELL, false>(c, store, ops, n_ops, lanes);
+    }
+  }
   if constexpr ((ELL + 7) / 8 == 4) {
     if (pm_ok(c->p.q, c->p.ell) && !(c->p.dbg & 2u))  // dbg bit 1 forces the generic epilogue
       return launch_tc_impl<K, ELL, true>(c, store, ops, n_ops, lanes);

@@ -39,7 +39,9 @@ def _oracle_nand(p, a, b, ca, cb):
 
 @pytest.mark.parametrize("params", [DEFAULT_PARAMS, EXACT_PARAMS], ids=["default", "exact"])
 @pytest.mark.parametrize("kernel,dbg", [(_native.KERNEL_TCGEN05, 0), (_native.KERNEL_TCGEN05, 2),
-                                        (_native.KERNEL_SIMT, 0)], ids=["tc", "tc-generic-epilogue", "simt"])
+                                        (_native.KERNEL_TCGEN05, 4), (_native.KERNEL_TCGEN05, 6),
+                                        (_native.KERNEL_SIMT, 0)],
+                         ids=["tc-ws", "tc-ws-generic-epilogue", "tc-v2", "tc-v2-generic", "simt"])
 def test_level_kernel_random_operands(params, kernel, dbg):
     """A 2-level program over random operands, all complement combinations, many lanes."""
     s, ctx = _ctx(params, kernel)
