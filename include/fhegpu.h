@@ -145,6 +145,9 @@ int fhegpu_encrypt(fhegpu_ctx *ctx, const uint32_t *pk, const fhegpu_pcg64 *stre
                    uint32_t n_streams, const uint32_t *stream_idx, const uint64_t *u32_offset,
                    const uint32_t *mu, const uint64_t *target, uint64_t count);
 
+/* Debug only: timeline probe of the pipelined kernel (64 gates x 16 events, clock64). */
+int fhegpu_debug_ws_trace(uint64_t *host_out);
+
 #ifdef __cplusplus
 }
 #endif

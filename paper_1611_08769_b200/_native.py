@@ -61,6 +61,7 @@ SIGNATURES = [
     ("fhegpu_prog_destroy", None, [_P]),
     ("fhegpu_nand_batch", ctypes.c_int, [_P, _U32P, _U32P, _U32P, ctypes.c_uint64]),
     ("fhegpu_not_batch", ctypes.c_int, [_P, _U32P, _U32P, ctypes.c_uint64]),
+    ("fhegpu_debug_ws_trace", ctypes.c_int, [_U64P]),
     ("fhegpu_encrypt", ctypes.c_int, [_P, _U32P, _P, ctypes.c_uint32, _U32P, _U64P, _U32P, _U64P,
                                       ctypes.c_uint64]),
 ]

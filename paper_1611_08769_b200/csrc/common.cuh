@@ -17,6 +17,7 @@ struct DevParams {
   uint64_t mu;        // floor(2^64 / q) for Barrett reduction
   uint32_t dbg;       // debug knobs (bit 0: swap B descriptor strides); 0 in production
   uint32_t pm_c;      // 2^ell - q (pseudo-Mersenne epilogue constant)
+  uint32_t lanes_magic;  // floor((2^32 - 1) / lanes): item / lanes by multiply (set per launch)
 };
 
 // Gadget entry G[r][i] = 2^(r mod ell) if i == r / ell else 0 (fhe.py:200-208, mu = 1).
@@ -42,6 +43,17 @@ __device__ __forceinline__ uint32_t mod_u64(uint64_t x, uint32_t q, uint64_t mu)
   uint64_t qt = __umul64hi(x, mu);
   uint64_t r = x - qt * (uint64_t)q;
   return (uint32_t)(r >= q ? r - q : r);
+}
+
+// item / lanes and item % lanes for 32-bit items (magic = floor((2^32-1)/lanes)).
+__device__ __forceinline__ void div_lanes(uint32_t item, uint32_t lanes, uint32_t magic, uint32_t &q,
+                                          uint32_t &r) {
+  q = __umulhi(item, magic);
+  r = item - q * lanes;
+  if (r >= lanes) {
+    ++q;
+    r -= lanes;
+  }
 }
 
 struct OpRec {

@@ -130,8 +130,10 @@ int launch_tc_ws_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t
   const uint64_t items = (uint64_t)n_ops * lanes;
   if (items >= (1ull << 32)) return fail(FHEGPU_EINVAL, "level too large (>= 2^32 gate items)");
   const uint64_t grid = std::min<uint64_t>(items, (uint64_t)c->num_sms);
+  DevParams p = c->p;
+  p.lanes_magic = (uint32_t)(0xFFFFFFFFu / lanes);
   tc::level_tc_ws_kernel<K, ELL, PM><<<(unsigned)grid, G::THREADS, smem, c->stream>>>(
-      store, ops, n_ops, lanes, c->p);
+      store, ops, n_ops, lanes, p);
   CUDA_TRY(cudaGetLastError());
   return FHEGPU_OK;
 }
@@ -592,6 +594,13 @@ int fhegpu_encrypt(fhegpu_ctx *c, const uint32_t *pk, const fhegpu_pcg64 *stream
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   cudaFree(buf);
   if (e != cudaSuccess) return fail(FHEGPU_ECUDA, std::string("encrypt: ") + cudaGetErrorString(e));
+  return FHEGPU_OK;
+}
+
+// Debug: copy the warp-specialised kernel's timeline probe (64 x 16 clock64 values).
+int fhegpu_debug_ws_trace(uint64_t *host) {
+  if (!host) return fail(FHEGPU_EINVAL, "null argument");
+  CUDA_TRY(cudaMemcpyFromSymbol(host, tc::g_ws_trace, sizeof(uint64_t) * 64 * 16));
   return FHEGPU_OK;
 }
 

@@ -1,26 +1,32 @@
-// tc_nand_ws.cuh -- warp-specialised, pipelined tcgen05 level kernel (v3).
+// tc_nand_ws.cuh -- warp-specialised, pipelined tcgen05 level kernel (the production kernel).
 //
-// Same math as tc_nand.cuh (compact NAND: out = (G - bits(V1) V2) mod q, the
-// product on the tensor cores as a u8 GEMM), restructured so the phases of
-// different gates overlap inside one persistent CTA per SM:
+// Same math as tc_nand.cuh (compact NAND: out = (G - bits(V1) V2) mod q, the product on
+// the tensor cores as a u8 GEMM), restructured so the phases of different gates overlap
+// inside one persistent CTA per SM (608 threads):
 //
-//   warp 0        producer : cp.async.bulk of both operands into an S_IN-stage ring
-//   warp 1        MMA      : one thread issues tcgen05.mma (2 TMEM-A tiles + smem-A tail)
-//   warps 2..9    builders : B operand (smem, MN-major) + A operand (bits -> s8 {0,-1},
-//                            tcgen05.st into TMEM) for gate t while the MMA runs gate t-1
-//   warps 10..17  epilogue : tcgen05.ld of gate t-1's accumulators, mod-q fold,
-//                            bulk store -- while gate t builds
+//   warp 0        tail     : A of the 5 rows past the 2 MMA tiles (smem), their accumulator
+//                            read-out (TMEM lanes 0..4, hence a quadrant-0 warp) and the
+//                            st.global of those rows; frees the A buffer right after the read
+//   warp 1        producer : cp.async.bulk of both operands into an S_IN-stage ring
+//   warp 2        MMA      : one thread issues 2 x 9 TMEM-A tile MMAs + 9 smem-A tail MMAs
+//   warps 3..10   builders : B operand (smem, MN-major) + A operand (bits -> s8 {0,-1},
+//                            tcgen05.st into TMEM) of gate t while the MMAs of gate t-1 run
+//   warps 11..18  epilogue : tcgen05.ld of gate t-1's tile accumulators, mod-q fold,
+//                            one bulk store of rows 0..255
 //
-// TMEM (512 columns): two buffers of {D tile0, D tile1, A tile0, A tile1} (240 columns each);
-// the 5-row tail accumulates into the tile-0 A columns of its own buffer once the tile
-// MMAs are done.  Barriers (mbarrier): in_full/in_empty per input stage, op_full per
-// buffer (builders -> MMA), main_done/tail_done per buffer (tcgen05.commit -> epilogue
-// and MMA), epi_done per buffer (epilogue -> builders of gate t+2).
+// TMEM (512 columns): two buffers of {D tile0, D tile1, A tile0, A tile1} (240 columns);
+// the tail accumulates into the tile-0 A columns of its buffer, issued after the tile MMAs
+// (tcgen05.mma executes in issue order; the 9 tile-1 MMAs separate tile 0's last read of
+// those columns from the tail's writes).
 //
-// A operand: word w of row r spreads into 8 u32 (32 K slots).  Output o holds, in byte q,
-// bit 8q + o of w replicated to 0x00 / 0xFF by a sign-replicating PRMT of (w << (7 - o)),
-// i.e. the s8 value 0 or -1; D = -(sum of digits) and the epilogue negates.  K slot
-// 4o + q of word w therefore pairs with V2 row w * ELL + 8q + o in B.
+// mbarriers: in_full/in_empty per input stage; per TMEM buffer b: op_full (builders + tail
+// -> MMA), main_done (tcgen05.commit -> epilogue, tail), a_free (tail read-out -> builders
+// of gate t+2), d_free (epilogue tile read-out -> MMA of gate t+2).
+//
+// A operand: word w of row r spreads into 8 u32 (32 K slots); output o holds in byte q
+// the bit 8q + o of w replicated to 0x00/0xFF by a sign-replicating PRMT of (w << (7 - o)),
+// i.e. the s8 value 0 or -1, so D = -(digit sums) and the epilogue negates.  K slot 4o + q
+// of word w pairs with V2 row w * ELL + 8q + o in B.
 #pragma once
 
 #include "tc_nand.cuh"
@@ -28,24 +34,89 @@
 namespace fhegpu {
 namespace tc {
 
+// Pipeline timeline probe (dbg bit 14): CTA 0 records clock64 per (gate, event).
+__device__ uint64_t g_ws_trace[64 * 16];
+__device__ __forceinline__ void trace_ev(const DevParams &p, uint32_t t, int ev) {
+  if ((p.dbg & 16384u) && blockIdx.x == 0 && t < 64) g_ws_trace[t * 16 + ev] = clock64();
+}
+
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read_n() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// 32 bits of w -> 32 s8 K slots {0, -1}: out[o] byte q = -(bit 8q + o).
 __device__ __forceinline__ uint32_t prmt_sign(uint32_t x) {
   uint32_t r;  // default-mode prmt: selector nibble bit 3 replicates the selected byte's msb
   asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(r) : "r"(x));
   return r;
 }
 
+// 32 bits of w -> 32 s8 K slots {0, -1}: out[o] byte q = -(bit 8q + o).
 __device__ __forceinline__ void spread_word_sr(uint32_t w, uint32_t (&out)[8]) {
 #pragma unroll
   for (int o = 0; o < 8; ++o) out[o] = prmt_sign(w << (7 - o));
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t *v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+        "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+        "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t *v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31, %32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+      "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t *v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr)
+               : "memory");
+}
+
+// 36 accumulator columns (9 values x 4 digits) of this warp's 32 TMEM lanes.
+__device__ __forceinline__ void load_acc36(uint32_t taddr, uint32_t (&d)[36], bool skip) {
+  if (skip) {
+#pragma unroll
+    for (int i = 0; i < 36; ++i) d[i] = 0u;
+    return;
+  }
+  tmem_ld32(taddr, d);
+  tmem_ld4(taddr + 32, d + 32);
 }
 
 template <int K, int ELL, bool PM>
@@ -58,13 +129,18 @@ struct GeoWS {
   static constexpr int NPAD = B::NPAD, NCH = B::NCH, KB = B::KB, NDIG = B::NDIG;
   static constexpr uint32_t SBO = B::SBO, LBO = B::LBO, TA_LBO = B::TA_LBO;
   static constexpr int B_BYTES = B::B_BYTES, TA_BYTES = B::TA_BYTES;
+  static constexpr int WORDS = B::WORDS;
   static constexpr int CT_WORDS = B::CT_WORDS, CT_BYTES = B::CT_BYTES;
+  static constexpr int MAIN_BYTES = MMA_ROWS * K * 4;       // rows stored by the bulk copy
   static constexpr int D_COLS = B::D_COLS;                 // per buffer
   static constexpr int BUF_COLS = 256;                      // buffer stride in TMEM columns
   static constexpr int NB_WARPS = 4 * MT, NE_WARPS = 4 * MT;
-  static constexpr int WARP_BUILD0 = 2, WARP_EPI0 = 2 + NB_WARPS;
-  static constexpr int THREADS = 32 * (2 + NB_WARPS + NE_WARPS);
-  static constexpr int S_IN = 3;
+  static constexpr int WARP_TAIL = 0, WARP_PROD = 1, WARP_MMA = 2;
+  static constexpr int WARP_BUILD0 = 3, WARP_EPI0 = 3 + NB_WARPS;
+  static constexpr int THREADS = 32 * (3 + NB_WARPS + NE_WARPS);
+  static constexpr int S_IN = 7;                            // ~2.5 us load latency x bandwidth
+  static constexpr int N_OUT = 3;                           // output staging buffers
+  static constexpr uint32_t OP_ARRIVALS = NB_WARPS;
   // idesc: S32 accumulator, A s8 (bits 7-9 = 1), B u8, A K-major, B MN-major, N>>3, M>>4
   static constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 16) |
                                     ((uint32_t)(NPAD >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
@@ -72,10 +148,12 @@ struct GeoWS {
   static constexpr int OFF_B = OFF_IN + S_IN * 2 * CT_BYTES;
   static constexpr int OFF_TA = ((OFF_B + 2 * B_BYTES + 127) / 128) * 128;
   static constexpr int OFF_OUT = ((OFF_TA + (TAIL ? 2 * TA_BYTES : 0) + 127) / 128) * 128;
-  static constexpr int OFF_BAR = ((OFF_OUT + 2 * CT_BYTES + 127) / 128) * 128;
+  static constexpr int OFF_BAR = ((OFF_OUT + N_OUT * CT_BYTES + 127) / 128) * 128;
   static constexpr int SMEM = OFF_BAR + 256;
-  static_assert(NDIG == 4 && MT >= 1, "warp-specialised kernel covers 25..31-bit q with >= 128 rows");
+  static_assert(NDIG == 4 && B::NCOL <= 36, "warp-specialised kernel: 4 digits, <= 36 columns");
+  static_assert(MT >= 1 && TAIL <= 8, "two-tile geometry");
   static_assert(B::D_COLS + B::A_COLS <= BUF_COLS, "two TMEM buffers must fit 512 columns");
+  static_assert(MAIN_BYTES % 16 == 0, "bulk store size");
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
@@ -97,6 +175,22 @@ __device__ __forceinline__ uint32_t finish_neg(const uint32_t *d, uint32_t g, co
   return min(x, x + p.q);                           // (g - r) mod q for g, r < q
 }
 
+// Op record of gate item `item` (or a dummy past the end): issued one gate ahead so the
+// global-load latency never sits on a role's critical loop.
+__device__ __forceinline__ OpRec fetch_op(const OpRec *ops, uint32_t item, uint32_t n_items,
+                                          uint32_t lanes, uint32_t magic) {
+  if (item >= n_items) return OpRec{0u, 0u, 0u, 0u};
+  uint32_t q, r;
+  div_lanes(item, lanes, magic, q, r);
+  return ops[q];
+}
+
+__device__ __forceinline__ uint32_t lane_of(uint32_t item, uint32_t lanes, uint32_t magic) {
+  uint32_t q, r;
+  div_lanes(item, lanes, magic, q, r);
+  return r;
+}
+
 template <int K, int ELL, bool PM>
 __global__ void __launch_bounds__(GeoWS<K, ELL, PM>::THREADS, 1)
 level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uint32_t n_ops,
@@ -112,85 +206,150 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
   uint64_t *in_empty = bar + G::S_IN;         // [S_IN]
   uint64_t *op_full = bar + 2 * G::S_IN;      // [2]
   uint64_t *main_done = op_full + 2;          // [2]
-  uint64_t *tail_done = main_done + 2;        // [2]
-  uint64_t *epi_done = tail_done + 2;         // [2]
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(epi_done + 2);
+  uint64_t *a_free = main_done + 2;           // [2]
+  uint64_t *d_free = a_free + 2;              // [2]
+  uint64_t *out_free = d_free + 2;            // [N_OUT] staging o may take gate t's rows
+  uint64_t *tail_ready = out_free + G::N_OUT; // [N_OUT] tail rows of gate t are in staging o
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tail_ready + G::N_OUT);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const uint32_t n_items = n_ops * lanes;     // host guarantees < 2^32
 
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  if (warp == G::WARP_MMA) tmem_alloc<512>(tmem_slot);
   if (tid == 0) {
     for (int i = 0; i < G::S_IN; ++i) {
       mbar_init(&in_full[i], 1);
-      mbar_init(&in_empty[i], G::NB_WARPS);
+      mbar_init(&in_empty[i], G::OP_ARRIVALS);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&op_full[i], G::NB_WARPS);
+      mbar_init(&op_full[i], G::OP_ARRIVALS);
       mbar_init(&main_done[i], 1);
-      mbar_init(&tail_done[i], 1);
-      mbar_init(&epi_done[i], G::NE_WARPS);
+      mbar_init(&a_free[i], 1);
+      mbar_init(&d_free[i], G::NE_WARPS);
+    }
+    for (int i = 0; i < G::N_OUT; ++i) {
+      mbar_init(&out_free[i], 1);
+      mbar_init(&tail_ready[i], 1);
     }
     fence_mbar_init();
   }
   for (int w = tid; w < 2 * G::B_BYTES / 4; w += G::THREADS) reinterpret_cast<uint32_t *>(s_b)[w] = 0u;
   if constexpr (G::TAIL > 0)
     for (int w = tid; w < 2 * G::TA_BYTES / 4; w += G::THREADS) reinterpret_cast<uint32_t *>(s_ta)[w] = 0u;
-  for (int w = tid; w < 2 * G::CT_WORDS; w += G::THREADS) s_out[w] = 0u;
+  for (int w = tid; w < G::N_OUT * G::CT_WORDS; w += G::THREADS) s_out[w] = 0u;   // padding stays 0
+  fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == G::WARP_PROD) {
     // ------------------------------ producer ------------------------------
     if (lane == 0) {
       uint32_t t = 0;
+      OpRec op_next = fetch_op(ops, blockIdx.x, n_items, lanes, p.lanes_magic);
       for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
         const uint32_t s = t % G::S_IN, k = t / G::S_IN;
+        const OpRec op = op_next;
+        op_next = fetch_op(ops, item + gridDim.x, n_items, lanes, p.lanes_magic);
         mbar_wait(&in_empty[s], (k & 1u) ^ 1u);
-        const uint32_t op_i = item / lanes, ln = item - op_i * lanes;
-        const OpRec op = ops[op_i];
+        trace_ev(p, t, 0);
+        const uint32_t ln = lane_of(item, lanes, p.lanes_magic);
         uint32_t *dst = s_in + s * 2 * G::CT_WORDS;
+        if (p.dbg & 256u) {                       // timing experiment: no operand loads
+          mbar_arrive(&in_full[s]);
+          continue;
+        }
         mbar_expect_tx(&in_full[s], 2 * G::CT_BYTES);
         bulk_g2s(dst, store + ((uint64_t)op.left * lanes + ln) * G::CT_WORDS, G::CT_BYTES, &in_full[s]);
         bulk_g2s(dst + G::CT_WORDS, store + ((uint64_t)op.right * lanes + ln) * G::CT_WORDS,
                  G::CT_BYTES, &in_full[s]);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == G::WARP_MMA) {
     // ------------------------------ MMA issuer ------------------------------
-    if (lane == 0) {
+    // The whole warp runs the loop (descriptors stay warp-uniform, in uniform registers);
+    // one elected lane issues each tcgen05.mma / commit.
+    uint32_t t = 0;
+    const uint32_t idesc = (p.dbg & 8u) ? (G::IDESC & ~(7u << 7)) : G::IDESC;
+    const uint64_t bdesc0 = smem_desc(smem_u32(s_b), G::LBO, G::SBO);
+    const uint64_t tdesc0 = smem_desc(smem_u32(s_ta), G::TA_LBO, 0u);
+    for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
+      const uint32_t b = t & 1u, u = t >> 1;
+      mbar_wait(&op_full[b], u & 1u);
+      if (lane == 0) trace_ev(p, t, 2);
+      mbar_wait(&d_free[b], (u & 1u) ^ 1u);       // epilogue of gate t-2 has read D(b)
+      if (lane == 0) trace_ev(p, t, 3);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + b * G::BUF_COLS;
+      // descriptor address field is (addr >> 4): advance by adding byte offsets >> 4
+      const uint64_t bd_b = bdesc0 + ((b * G::B_BYTES) >> 4);
+      const uint64_t td_b = tdesc0 + ((b * G::TA_BYTES) >> 4);
+      if (!(p.dbg & 128u)) {
+        if (elect_one()) {
+#pragma unroll
+          for (int mt = 0; mt < G::MT; ++mt) {
+#pragma unroll
+            for (int s = 0; s < K; ++s)
+              mma_i8_ts(tb + mt * G::NPAD, tb + G::D_COLS + mt * 8 * K + 8 * s,
+                        bd_b + ((s * 4 * G::LBO) >> 4), idesc, s > 0 ? 1u : 0u);
+          }
+          if constexpr (G::TAIL > 0) {
+#pragma unroll
+            for (int s = 0; s < K; ++s)
+              mma_i8_ss(tb + G::D_COLS, td_b + ((s * 2 * G::TA_LBO) >> 4),
+                        bd_b + ((s * 4 * G::LBO) >> 4), idesc, s > 0 ? 1u : 0u);
+          }
+        }
+        __syncwarp();
+      }
+      if (elect_one()) {
+        mma_commit(&main_done[b]);
+        if constexpr (G::TAIL == 0) mma_commit(&a_free[b]);
+      }
+      __syncwarp();
+      if (lane == 0) trace_ev(p, t, 4);
+    }
+  } else if (warp == G::WARP_TAIL) {
+    // ------------------------------ tail rows ------------------------------
+    // Reads the tail accumulator of gate t right after its MMAs, frees the A buffer, then
+    // folds the 5 rows into the epilogue's staging buffer (the builders build the tail A).
+    if constexpr (G::TAIL > 0) {
       uint32_t t = 0;
       for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
         const uint32_t b = t & 1u, u = t >> 1;
-        mbar_wait(&op_full[b], u & 1u);
+        if (lane == 0) trace_ev(p, t, 12);
+        mbar_wait(&main_done[b], u & 1u);
+        if (lane == 0) trace_ev(p, t, 13);
         tc_fence_after();
-        const uint32_t tb = tmem_base + b * G::BUF_COLS;
-        const uint32_t b_base = smem_u32(s_b + b * G::B_BYTES);
-        const uint32_t idesc = (p.dbg & 8u) ? (G::IDESC & ~(7u << 7)) : G::IDESC;
+        uint32_t d[36];
+        load_acc36(tmem_base + b * G::BUF_COLS + G::D_COLS, d, false);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&a_free[b]);
+          trace_ev(p, t, 10);
+        }
+        const uint32_t o = t % G::N_OUT, ou = t / G::N_OUT;
+        mbar_wait(&out_free[o], ou & 1u);            // gate t-N_OUT's store has read staging o
+        uint32_t *out_st = s_out + o * G::CT_WORDS;
+        if (lane < G::TAIL && !(p.dbg & 1024u)) {
+          const int r = G::MMA_ROWS + lane;
+          const int rb = r / ELL, rbit = r - rb * ELL;
 #pragma unroll
-        for (int mt = 0; mt < G::MT; ++mt) {
-#pragma unroll
-          for (int s = 0; s < K; ++s) {
-            const uint64_t bd = smem_desc(b_base + s * 4 * G::LBO, G::LBO, G::SBO);
-            mma_i8_ts(tb + mt * G::NPAD, tb + G::D_COLS + mt * 8 * K + 8 * s, bd, idesc,
-                      s > 0 ? 1u : 0u);
+          for (int i = 0; i < K; ++i) {
+            const uint32_t g = (i == rb) ? (1u << rbit) : 0u;
+            out_st[r * K + i] = (p.dbg & 8u) ? finish_value<ELL, 4, PM>(&d[i * 4], g, p)
+                                             : finish_neg<ELL, PM>(&d[i * 4], g, p);
           }
         }
-        mma_commit(&main_done[b]);
-        if constexpr (G::TAIL > 0) {
-          mbar_wait(&main_done[b], u & 1u);       // tail accumulates into tile-0 A columns
-          tc_fence_after();
-          const uint32_t ta = smem_u32(s_ta + b * G::TA_BYTES);
-#pragma unroll
-          for (int s = 0; s < K; ++s) {
-            const uint64_t ad = smem_desc(ta + s * 2 * G::TA_LBO, G::TA_LBO, 0u);
-            const uint64_t bd = smem_desc(b_base + s * 4 * G::LBO, G::LBO, G::SBO);
-            mma_i8_ss(tb + G::D_COLS, ad, bd, idesc, s > 0 ? 1u : 0u);
-          }
-          mma_commit(&tail_done[b]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&tail_ready[o]);
+          trace_ev(p, t, 15);
         }
       }
     }
@@ -204,18 +363,68 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
     const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
     const int row_blk = row / ELL, row_bit = row - row_blk * ELL;
     uint32_t t = 0;
+    uint32_t flags_next = fetch_op(ops, blockIdx.x, n_items, lanes, p.lanes_magic).flags;
     for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
       const uint32_t s = t % G::S_IN, k = t / G::S_IN, b = t & 1u, u = t >> 1;
-      const uint32_t flags = ops[item / lanes].flags;
+      const uint32_t flags = flags_next;
+      flags_next = fetch_op(ops, item + gridDim.x, n_items, lanes, p.lanes_magic).flags;
       const bool comp1 = flags & 1u, comp2 = flags & 2u;
       mbar_wait(&in_full[s], k & 1u);
-      mbar_wait(&epi_done[b], (u & 1u) ^ 1u);          // gate t-2 is out of buffer b
+      if (bt == 0) trace_ev(p, t, 5);
+      mbar_wait(&a_free[b], (u & 1u) ^ 1u);            // gate t-2: MMAs done, tail read out
+      if (bt == 0) trace_ev(p, t, 6);
       tc_fence_after();
       const uint32_t *v1 = s_in + s * 2 * G::CT_WORDS;
       const uint32_t *v2 = v1 + G::CT_WORDS;
       uint8_t *bb = s_b + b * G::B_BYTES;
-      // B: K row kr <-> bit j = 8q + o of word w, kk = 4o + q
-      for (int kr = bt; kr < G::KB; kr += 128 * G::MT) {
+      // A (TMEM tiles): this thread's row
+      if (!(p.dbg & 16u)) {
+        uint32_t words[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) words[i] = v1[row * K + i];
+        if (comp1) {
+#pragma unroll
+          for (int i = 0; i < K; ++i) words[i] = sub_mod(i == row_blk ? (1u << row_bit) : 0u, words[i], p.q);
+        }
+        const uint32_t a_addr = tmem_base + b * G::BUF_COLS + lane_off + G::D_COLS + tile * 8 * K;
+#pragma unroll
+        for (int w0 = 0; w0 < K; w0 += 4) {
+          if (w0 + 4 <= K) {                     // 4 words -> one 32-column store
+            uint32_t sp[32];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint32_t one[8];
+              if (p.dbg & 8u) spread_word(words[w0 + j], one); else spread_word_sr(words[w0 + j], one);
+#pragma unroll
+              for (int x = 0; x < 8; ++x) sp[8 * j + x] = one[x];
+            }
+            tmem_st32(a_addr + 8 * w0, sp);
+          } else {
+#pragma unroll
+            for (int w = w0; w < K; ++w) {
+              uint32_t sp[8];
+              if (p.dbg & 8u) spread_word(words[w], sp); else spread_word_sr(words[w], sp);
+              tmem_st8(a_addr + 8 * w, sp);
+            }
+          }
+        }
+      }
+      // A of the smem tail tile (TA[b] was last read by the MMAs of gate t-2: a_free above)
+      if constexpr (G::TAIL > 0) {
+        if (bt < G::TAIL * K && !(p.dbg & 16u)) {
+          const int m = bt / K, w = bt - m * K;
+          const int r = G::MMA_ROWS + m;
+          uint32_t v = v1[r * K + w];
+          if (comp1) v = sub_mod(w == r / ELL ? (1u << (r % ELL)) : 0u, v, p.q);
+          uint32_t sp[8];
+          if (p.dbg & 8u) spread_word(v, sp); else spread_word_sr(v, sp);
+          uint8_t *dst = s_ta + b * G::TA_BYTES + (2 * w) * G::TA_LBO + m * 16;
+          *reinterpret_cast<uint4 *>(dst) = make_uint4(sp[0], sp[1], sp[2], sp[3]);
+          *reinterpret_cast<uint4 *>(dst + G::TA_LBO) = make_uint4(sp[4], sp[5], sp[6], sp[7]);
+        }
+      }
+      // B: K row kr <-> bit j of word w (j = 8q + o for kk = 4o + q; the u8 debug spread differs)
+      for (int kr = (p.dbg & 32u) ? G::KB : bt; kr < G::KB; kr += 128 * G::MT) {
         const int w = kr >> 5, kk = kr & 31;
         const int j = (p.dbg & 8u) ? (kk & ~7) + 7 - (kk & 7) : 8 * (kk & 3) + (kk >> 2);
         if (j >= ELL) continue;                         // padding rows stay zero
@@ -238,37 +447,6 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
           *reinterpret_cast<uint4 *>(dst + ch * G::SBO) = val;
         }
       }
-      // A (TMEM tiles): this thread's row
-      {
-        uint32_t words[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) words[i] = v1[row * K + i];
-        if (comp1) {
-#pragma unroll
-          for (int i = 0; i < K; ++i) words[i] = sub_mod(i == row_blk ? (1u << row_bit) : 0u, words[i], p.q);
-        }
-        const uint32_t a_addr = tmem_base + b * G::BUF_COLS + lane_off + G::D_COLS + tile * 8 * K;
-#pragma unroll
-        for (int w = 0; w < K; ++w) {
-          uint32_t sp[8];
-          if (p.dbg & 8u) spread_word(words[w], sp); else spread_word_sr(words[w], sp);
-          tmem_st8(a_addr + 8 * w, sp);
-        }
-      }
-      // A (smem tail tile)
-      if constexpr (G::TAIL > 0) {
-        if (bt < G::TAIL * K) {
-          const int m = bt / K, w = bt - m * K;
-          const int r = G::MMA_ROWS + m;
-          uint32_t v = v1[r * K + w];
-          if (comp1) v = sub_mod(w == r / ELL ? (1u << (r % ELL)) : 0u, v, p.q);
-          uint32_t sp[8];
-          if (p.dbg & 8u) spread_word(v, sp); else spread_word_sr(v, sp);
-          uint8_t *dst = s_ta + b * G::TA_BYTES + (2 * w) * G::TA_LBO + m * 16;
-          *reinterpret_cast<uint4 *>(dst) = make_uint4(sp[0], sp[1], sp[2], sp[3]);
-          *reinterpret_cast<uint4 *>(dst + G::TA_LBO) = make_uint4(sp[4], sp[5], sp[6], sp[7]);
-        }
-      }
       tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
@@ -277,6 +455,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
         mbar_arrive(&op_full[b]);
         mbar_arrive(&in_empty[s]);
       }
+      if (bt == 0) trace_ev(p, t, 7);
     }
   } else {
     // ------------------------------ epilogue ------------------------------
@@ -287,27 +466,30 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
     const int row = 128 * tile + 32 * quad + lane;
     const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
     const int row_blk = row / ELL, row_bit = row - row_blk * ELL;
-    const bool tail_warp = (G::TAIL > 0) && tile == 0 && quad == 0;
     constexpr uint32_t NE_THREADS = 32 * G::NE_WARPS;
+    if constexpr (G::TAIL > 0) {
+      if (et == 0) mbar_arrive(&out_free[0]);          // staging 0 is free for gate 0
+    }
     uint32_t t = 0;
+    OpRec op_next = fetch_op(ops, blockIdx.x, n_items, lanes, p.lanes_magic);
     for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
       const uint32_t b = t & 1u, u = t >> 1;
-      uint32_t *out_st = s_out + b * G::CT_WORDS;
-      if (et == 0) bulk_wait_read_le1();               // gate t-2's store has read its staging
-      named_bar(1, NE_THREADS);
+      const OpRec op_cur = op_next;
+      if (et == 0) op_next = fetch_op(ops, item + gridDim.x, n_items, lanes, p.lanes_magic);
+      const uint32_t o = t % G::N_OUT, ou = t / G::N_OUT;
+      uint32_t *out_st = s_out + o * G::CT_WORDS;
+      // staging o was released by et 0 before the previous gate's barrier (or is fresh)
+      if (et == 0) trace_ev(p, t, 8);
       mbar_wait(&main_done[b], u & 1u);
+      if (et == 0) trace_ev(p, t, 9);
       tc_fence_after();
-      const uint32_t tb = tmem_base + b * G::BUF_COLS;
-      {
-        uint32_t d[G::NPAD];
-#pragma unroll
-        for (int c = 0; c < G::NCH; ++c) {
-          uint32_t chunk[16];
-          tmem_ld16(tb + lane_off + tile * G::NPAD + 16 * c, chunk);
-#pragma unroll
-          for (int x = 0; x < 16; ++x) d[16 * c + x] = chunk[x];
-        }
-        tmem_wait_ld();
+      uint32_t d[36];
+      load_acc36(tmem_base + b * G::BUF_COLS + lane_off + tile * G::NPAD, d, (p.dbg & 4096u) != 0);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&d_free[b]);
+      if (!(p.dbg & 64u)) {
 #pragma unroll
         for (int i = 0; i < K; ++i) {
           const uint32_t g = (i == row_blk) ? (1u << row_bit) : 0u;
@@ -315,39 +497,22 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
                                              : finish_neg<ELL, PM>(&d[i * 4], g, p);
         }
       }
-      if constexpr (G::TAIL > 0) {
-        if (tail_warp) {
-          mbar_wait(&tail_done[b], u & 1u);
-          tc_fence_after();
-          uint32_t d[G::NPAD];
-#pragma unroll
-          for (int c = 0; c < G::NCH; ++c) {
-            uint32_t chunk[16];
-            tmem_ld16(tb + G::D_COLS + 16 * c, chunk);
-#pragma unroll
-            for (int x = 0; x < 16; ++x) d[16 * c + x] = chunk[x];
-          }
-          tmem_wait_ld();
-          if (lane < G::TAIL) {
-            const int r = G::MMA_ROWS + lane;
-            const int rb = r / ELL, rbit = r - rb * ELL;
-#pragma unroll
-            for (int i = 0; i < K; ++i)
-              out_st[r * K + i] = (p.dbg & 8u)
-                                      ? finish_value<ELL, 4, PM>(&d[i * 4], (i == rb) ? (1u << rbit) : 0u, p)
-                                      : finish_neg<ELL, PM>(&d[i * 4], (i == rb) ? (1u << rbit) : 0u, p);
-          }
-        }
-      }
-      tc_fence_before();
       fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&epi_done[b]);
-      named_bar(1, NE_THREADS);
       if (et == 0) {
-        const OpRec op = ops[item / lanes];
-        const uint32_t ln = item - (item / lanes) * lanes;
-        bulk_s2g(store + ((uint64_t)op.out * lanes + ln) * G::CT_WORDS, out_st, G::CT_BYTES);
+        // release the staging buffer gate t+1 will use (last written by gate t+1-N_OUT):
+        // at most N_OUT-2 older stores may still be reading; the barrier below orders this
+        // wait before any epilogue thread's writes of gate t+1
+        bulk_wait_read_n<G::N_OUT - 2>();
+        if constexpr (G::TAIL > 0) mbar_arrive(&out_free[(t + 1) % G::N_OUT]);
+      }
+      named_bar(1, NE_THREADS);
+      if (et == 0) trace_ev(p, t, 11);
+      if (et == 0) {
+        if constexpr (G::TAIL > 0) mbar_wait(&tail_ready[o], ou & 1u);
+      }
+      if (et == 0 && !(p.dbg & 512u)) {
+        const uint32_t ln = lane_of(item, lanes, p.lanes_magic);
+        bulk_s2g(store + ((uint64_t)op_cur.out * lanes + ln) * G::CT_WORDS, out_st, G::CT_BYTES);
       }
     }
     if (et == 0) bulk_wait_all();
@@ -356,7 +521,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc<512>(tmem_base);
+  if (warp == G::WARP_MMA) tmem_dealloc<512>(tmem_base);
 }
 
 }  // namespace tc
