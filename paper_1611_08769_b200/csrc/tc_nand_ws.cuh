@@ -272,7 +272,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
     // The whole warp runs the loop (descriptors stay warp-uniform, in uniform registers);
     // one elected lane issues each tcgen05.mma / commit.
     uint32_t t = 0;
-    const uint32_t idesc = (p.dbg & 8u) ? (G::IDESC & ~(7u << 7)) : G::IDESC;
+    const uint32_t idesc = G::IDESC;
     const uint64_t bdesc0 = smem_desc(smem_u32(s_b), G::LBO, G::SBO);
     const uint64_t tdesc0 = smem_desc(smem_u32(s_ta), G::TA_LBO, 0u);
     for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
@@ -334,6 +334,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
         }
         const uint32_t o = t % G::N_OUT, ou = t / G::N_OUT;
         mbar_wait(&out_free[o], ou & 1u);            // gate t-N_OUT's store has read staging o
+        if (lane == 0) trace_ev(p, t, 14);
         uint32_t *out_st = s_out + o * G::CT_WORDS;
         if (lane < G::TAIL && !(p.dbg & 1024u)) {
           const int r = G::MMA_ROWS + lane;
@@ -341,10 +342,10 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
 #pragma unroll
           for (int i = 0; i < K; ++i) {
             const uint32_t g = (i == rb) ? (1u << rbit) : 0u;
-            out_st[r * K + i] = (p.dbg & 8u) ? finish_value<ELL, 4, PM>(&d[i * 4], g, p)
-                                             : finish_neg<ELL, PM>(&d[i * 4], g, p);
+            out_st[r * K + i] = finish_neg<ELL, PM>(&d[i * 4], g, p);
           }
         }
+        if (lane == 0) trace_ev(p, t, 1);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -394,7 +395,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               uint32_t one[8];
-              if (p.dbg & 8u) spread_word(words[w0 + j], one); else spread_word_sr(words[w0 + j], one);
+              spread_word_sr(words[w0 + j], one);
 #pragma unroll
               for (int x = 0; x < 8; ++x) sp[8 * j + x] = one[x];
             }
@@ -403,7 +404,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
 #pragma unroll
             for (int w = w0; w < K; ++w) {
               uint32_t sp[8];
-              if (p.dbg & 8u) spread_word(words[w], sp); else spread_word_sr(words[w], sp);
+              spread_word_sr(words[w], sp);
               tmem_st8(a_addr + 8 * w, sp);
             }
           }
@@ -417,16 +418,16 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
           uint32_t v = v1[r * K + w];
           if (comp1) v = sub_mod(w == r / ELL ? (1u << (r % ELL)) : 0u, v, p.q);
           uint32_t sp[8];
-          if (p.dbg & 8u) spread_word(v, sp); else spread_word_sr(v, sp);
+          spread_word_sr(v, sp);
           uint8_t *dst = s_ta + b * G::TA_BYTES + (2 * w) * G::TA_LBO + m * 16;
           *reinterpret_cast<uint4 *>(dst) = make_uint4(sp[0], sp[1], sp[2], sp[3]);
           *reinterpret_cast<uint4 *>(dst + G::TA_LBO) = make_uint4(sp[4], sp[5], sp[6], sp[7]);
         }
       }
-      // B: K row kr <-> bit j of word w (j = 8q + o for kk = 4o + q; the u8 debug spread differs)
+      // B: K row kr <-> bit j = 8q + o of word w, kk = 4o + q (matches spread_word_sr)
       for (int kr = (p.dbg & 32u) ? G::KB : bt; kr < G::KB; kr += 128 * G::MT) {
         const int w = kr >> 5, kk = kr & 31;
-        const int j = (p.dbg & 8u) ? (kk & ~7) + 7 - (kk & 7) : 8 * (kk & 3) + (kk >> 2);
+        const int j = 8 * (kk & 3) + (kk >> 2);
         if (j >= ELL) continue;                         // padding rows stay zero
         const int c = w * ELL + j;
         uint32_t vals[K];
@@ -493,8 +494,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
 #pragma unroll
         for (int i = 0; i < K; ++i) {
           const uint32_t g = (i == row_blk) ? (1u << row_bit) : 0u;
-          out_st[row * K + i] = (p.dbg & 8u) ? finish_value<ELL, 4, PM>(&d[i * 4], g, p)
-                                             : finish_neg<ELL, PM>(&d[i * 4], g, p);
+          out_st[row * K + i] = finish_neg<ELL, PM>(&d[i * 4], g, p);
         }
       }
       fence_proxy_async_smem();

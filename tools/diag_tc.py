@@ -10,7 +10,7 @@ for params, op in ((EXACT_PARAMS, gsw.EXACT), (DEFAULT_PARAMS, gsw.DEFAULT)):
     b = rng.integers(0, params.q, (4, params.n_ct, params.k)).astype(np.uint32)
     want = [gsw.hom_nand_compact(op, a[i], b[i]) for i in range(4)]
     for kern in (1, 2):
-        for dbg in ((0, 1) if kern == 1 else (0, 8, 2, 10, 4)):
+        for dbg in ((0, 1) if kern == 1 else (0, 2, 4)):
             s.ctx.set_kernel(kern); s.ctx.set_debug(dbg)
             try:
                 got = s.ctx.nand_batch(a, b).astype(np.int64)

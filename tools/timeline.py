@@ -19,7 +19,7 @@ tr = buf.reshape(64, 16).astype(np.int64)
 t0 = tr[0, 0]
 names = {0: "P:got_empty", 2: "M:op_full", 3: "M:d_free", 4: "M:commit", 5: "B:in_full", 6: "B:a_free",
          7: "B:done", 8: "E:bar1", 9: "E:main_done", 11: "E:bar2",
-         12: "T:top", 13: "T:maindone", 10: "T:a_free", 15: "T:tail_ready"}
+         12: "T:top", 13: "T:maindone", 10: "T:a_free", 14: "T:out_free", 1: "T:math_done", 15: "T:tail_ready"}
 print("cycles relative to gate 0 producer start; per-gate rows")
 print("gate " + " ".join(f"{names[e]:>12s}" for e in sorted(names)))
 for g in range(16, 24):
