@@ -212,7 +212,7 @@ def cmd_trace(cfg):
         "seconds": round(time.time() - t0, 1),
     }
     save_json(f"trace_{cfg}.json", rec)
-    if cfg in ("cfg0", "cfg4"):
+    if cfg == "cfg0":
         np.savez_compressed(os.path.join(HERE, f"trace_{cfg}.npz"),
                             ops=ops.astype(np.int32),
                             levels=np.asarray(tap.levels, dtype=np.int32),
