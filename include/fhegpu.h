@@ -89,6 +89,7 @@ void *fhegpu_ctx_own_stream(const fhegpu_ctx *ctx);           /* the stream a ne
 int fhegpu_ctx_set_kernel(fhegpu_ctx *ctx, int kernel);        /* FHEGPU_KERNEL_* */
 int fhegpu_ctx_kernel(const fhegpu_ctx *ctx);                  /* kernel a level launch will use */
 int fhegpu_ctx_set_debug(fhegpu_ctx *ctx, uint32_t dbg);       /* test knobs; 0 in production */
+int fhegpu_ctx_set_graphs(fhegpu_ctx *ctx, int enable);        /* replay programs as CUDA graphs (default on) */
 uint32_t fhegpu_ct_words(const fhegpu_ctx *ctx);
 int fhegpu_sync(fhegpu_ctx *ctx);
 
@@ -117,7 +118,9 @@ int fhegpu_store_read_range(fhegpu_ctx *ctx, uint64_t first, uint64_t count, uin
 int fhegpu_prog_create(fhegpu_ctx *ctx, const fhegpu_op *ops, uint64_t n_ops,
                        const uint64_t *level_offsets, uint32_t n_levels, fhegpu_prog **out);
 /* Run every level for `lanes` independent copies of the netlist (ciphertext
- * index = slot * lanes + lane); one kernel launch per level, on the context stream. */
+ * index = slot * lanes + lane); one kernel launch per level, on the context stream.
+ * The first run on a non-default stream also captures the launches into a CUDA graph
+ * that later runs replay with one cudaGraphLaunch. */
 int fhegpu_prog_run(fhegpu_ctx *ctx, fhegpu_prog *prog, uint32_t lanes);
 /* Run levels [first, last) only (profiling / partial evaluation). */
 int fhegpu_prog_run_range(fhegpu_ctx *ctx, fhegpu_prog *prog, uint32_t lanes,

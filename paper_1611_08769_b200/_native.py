@@ -44,6 +44,7 @@ SIGNATURES = [
     ("fhegpu_ctx_set_kernel", ctypes.c_int, [_P, ctypes.c_int]),
     ("fhegpu_ctx_kernel", ctypes.c_int, [_P]),
     ("fhegpu_ctx_set_debug", ctypes.c_int, [_P, ctypes.c_uint32]),
+    ("fhegpu_ctx_set_graphs", ctypes.c_int, [_P, ctypes.c_int]),
     ("fhegpu_ct_words", ctypes.c_uint32, [_P]),
     ("fhegpu_sync", ctypes.c_int, [_P]),
     ("fhegpu_store_reserve", ctypes.c_int, [_P, ctypes.c_uint64]),
@@ -128,6 +129,9 @@ class Program:
         self.launches = int(_lib.fhegpu_prog_launches(h))
 
     def run(self, lanes: int = 1, first: int = 0, last: int | None = None):
+        if first == 0 and last is None:
+            _check(_lib.fhegpu_prog_run(self.ctx.handle, self.handle, lanes), "prog_run")
+            return
         last = self.n_levels if last is None else last
         _check(_lib.fhegpu_prog_run_range(self.ctx.handle, self.handle, lanes, first, last),
                "prog_run")
@@ -181,6 +185,9 @@ class DeviceContext:
     @property
     def kernel(self) -> str:
         return KERNEL_NAMES[int(_lib.fhegpu_ctx_kernel(self.handle))]
+
+    def set_graphs(self, enable: bool):
+        _check(_lib.fhegpu_ctx_set_graphs(self.handle, 1 if enable else 0), "set_graphs")
 
     def set_debug(self, dbg: int):
         _check(_lib.fhegpu_ctx_set_debug(self.handle, int(dbg)), "set_debug")

@@ -62,12 +62,20 @@ struct fhegpu_ctx {
   OpRec *d_tmp_ops = nullptr;
   size_t tmp_ops_cap = 0;
   JumpTable *d_jump = nullptr;  // PCG64 jump-ahead constants (lazily uploaded)
+  bool use_graphs = true;       // replay whole programs as CUDA graphs
 };
 
 struct fhegpu_prog {
   OpRec *d_ops = nullptr;
   std::vector<uint64_t> offsets;  // n_levels + 1
   uint64_t n_ops = 0;
+  // CUDA graph of one full run (all level launches), captured on first use per
+  // (lanes, stream, kernel choice, debug bits); replayed with a single cudaGraphLaunch
+  cudaGraphExec_t graph = nullptr;
+  uint32_t graph_lanes = 0;
+  cudaStream_t graph_stream = nullptr;
+  int graph_kernel = -1;
+  uint32_t graph_dbg = 0;
 };
 
 namespace {
@@ -462,7 +470,45 @@ int fhegpu_prog_run_range(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes, uint32
 
 int fhegpu_prog_run(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
   if (!pr) return fail(FHEGPU_EINVAL, "null prog");
-  return fhegpu_prog_run_range(c, pr, lanes, 0, (uint32_t)pr->offsets.size() - 1);
+  const uint32_t n_levels = (uint32_t)pr->offsets.size() - 1;
+  if (!c || !c->use_graphs || n_levels < 4 || c->stream == nullptr)
+    return fhegpu_prog_run_range(c, pr, lanes, 0, n_levels);
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int kern = effective_kernel(c);
+  if (!pr->graph || pr->graph_lanes != lanes || pr->graph_stream != c->stream ||
+      pr->graph_kernel != kern || pr->graph_dbg != c->p.dbg) {
+    if (pr->graph) {
+      cudaGraphExecDestroy(pr->graph);
+      pr->graph = nullptr;
+    }
+    // first use: run eagerly once (sets kernel attributes outside capture), then capture
+    if (int rc = fhegpu_prog_run_range(c, pr, lanes, 0, n_levels)) return rc;
+    cudaGraph_t g = nullptr;
+    CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = fhegpu_prog_run_range(c, pr, lanes, 0, n_levels);
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return fail(FHEGPU_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&pr->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(FHEGPU_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    pr->graph_lanes = lanes;
+    pr->graph_stream = c->stream;
+    pr->graph_kernel = kern;
+    pr->graph_dbg = c->p.dbg;
+    return FHEGPU_OK;                  // this call already ran the program once
+  }
+  CUDA_TRY(cudaGraphLaunch(pr->graph, c->stream));
+  return FHEGPU_OK;
+}
+
+int fhegpu_ctx_set_graphs(fhegpu_ctx *c, int enable) {
+  if (!c) return fail(FHEGPU_EINVAL, "null ctx");
+  c->use_graphs = enable != 0;
+  return FHEGPU_OK;
 }
 
 uint32_t fhegpu_prog_launches(const fhegpu_prog *pr) {
@@ -474,6 +520,7 @@ uint32_t fhegpu_prog_launches(const fhegpu_prog *pr) {
 
 void fhegpu_prog_destroy(fhegpu_prog *pr) {
   if (!pr) return;
+  if (pr->graph) cudaGraphExecDestroy(pr->graph);
   cudaFree(pr->d_ops);
   delete pr;
 }
