@@ -380,6 +380,30 @@ def cmd_scheme():
     print(json.dumps(out)[:600])
 
 
+def cmd_eft1():
+    """EFT1 containers written by the reference: an encrypted 4-point Q8.8 signal (EXACT,
+    keygen(1), default_rng(7)) and the container of its fft_1d output (the server step)."""
+    from fhefft import fileio
+    scheme = GswScheme(EXACT_PARAMS)
+    keys = scheme.keygen(seed=1)
+    rng = np.random.default_rng(7)
+    fmt = arith.FixedFormat(16, 8)
+    values = [0.5 + 0.25j, -0.75 + 0.125j, 0.0 + 0.0j, 1.5 - 1.0j]
+    eng = FheEngine(scheme, keys=keys, rng=rng)
+    sig = fft.input_signal(eng, values, fmt)
+    fileio.write_ciphertext_signal(os.path.join(HERE, "eft1_exact_in.eft"), EXACT_PARAMS, eng, sig, fmt)
+    server = FheEngine(scheme, public_key=keys.public_key, rng=np.random.default_rng(0))
+    loaded, fmt2 = fileio.read_ciphertext_signal(os.path.join(HERE, "eft1_exact_in.eft"), server)
+    out = fft.fft_1d(loaded)
+    fileio.write_ciphertext_signal(os.path.join(HERE, "eft1_exact_fft.eft"), EXACT_PARAMS, server, out, fmt2)
+    client = FheEngine(scheme, keys=keys)
+    res, _ = fileio.read_ciphertext_signal(os.path.join(HERE, "eft1_exact_fft.eft"), client)
+    words = _word_ints(client, _signal_words(res))[0]
+    save_json("eft1_exact.json", {"values_re": [v.real for v in values], "values_im": [v.imag for v in values],
+                                  "fft_words": [int(v) for v in words], "nand_count": server.nand_count})
+    print("eft1 ok", server.nand_count)
+
+
 if __name__ == "__main__":
     cmd = sys.argv[1]
     if cmd == "scheme":
@@ -390,5 +414,7 @@ if __name__ == "__main__":
         cmd_cts(sys.argv[2])
     elif cmd == "clear":
         cmd_clear(sys.argv[2])
+    elif cmd == "eft1":
+        cmd_eft1()
     else:
         raise SystemExit(__doc__)
