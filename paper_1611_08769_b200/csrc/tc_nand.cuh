@@ -25,6 +25,17 @@
 
 #include "common.cuh"
 
+#ifndef FHEGPU_WAIT_NS
+#define FHEGPU_WAIT_NS 0   // try_wait suspend-time hint (ns); 0 = no hint
+#endif
+#define FHEGPU_STR2(x) #x
+#define FHEGPU_STR(x) FHEGPU_STR2(x)
+#if FHEGPU_WAIT_NS > 0
+#define FHEGPU_WAIT_HINT ", " FHEGPU_STR(FHEGPU_WAIT_NS)
+#else
+#define FHEGPU_WAIT_HINT ""
+#endif
+
 namespace fhegpu {
 namespace tc {
 
@@ -49,7 +60,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1" FHEGPU_WAIT_HINT ";\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
       "r"(parity)
       : "memory");
