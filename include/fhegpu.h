@@ -125,6 +125,19 @@ int fhegpu_prog_run(fhegpu_ctx *ctx, fhegpu_prog *prog, uint32_t lanes);
 /* Run levels [first, last) only (profiling / partial evaluation). */
 int fhegpu_prog_run_range(fhegpu_ctx *ctx, fhegpu_prog *prog, uint32_t lanes,
                           uint32_t first_level, uint32_t last_level);
+/* Evaluate the program over `lanes` lanes held in HOST memory, streaming them through
+ * the device store in chunks of `chunk_lanes` (so a batch may exceed HBM).  host_in[i]
+ * holds `lanes` dense ciphertexts (N*k u32 each, lane-major) for the program input in
+ * slot in_slots[i]; host_out[i] receives the ciphertexts of slot out_slots[i].  Chunks
+ * rotate through 3 store regions (capacity >= 3 * slots * chunk_lanes): the copy-in of
+ * chunk c+1, the level kernels of chunk c and the copy-out of chunk c-1 overlap on
+ * separate streams (both PCIe directions busy).  Asynchronous w.r.t. the host; the
+ * context stream observes completion.  Resident store contents are overwritten.
+ * Host buffers should be pinned for the copies to overlap.  This is the batched
+ * equivalent of encrypt -> netlist of hom_nand (fhe.py:325-341) -> decrypt hand-off. */
+int fhegpu_prog_run_host(fhegpu_ctx *ctx, fhegpu_prog *prog, uint64_t lanes, uint32_t chunk_lanes,
+                         uint32_t n_in, const uint32_t *in_slots, const uint32_t *const *host_in,
+                         uint32_t n_out, const uint32_t *out_slots, uint32_t *const *host_out);
 uint32_t fhegpu_prog_launches(const fhegpu_prog *prog);       /* launches one run issues */
 void fhegpu_prog_destroy(fhegpu_prog *prog);
 

@@ -11,7 +11,7 @@ import os
 
 import numpy as np
 
-from .errors import DeviceError, ParameterError
+from .errors import DeviceError, ParameterError, UsageError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfhegpu.so")
@@ -59,6 +59,8 @@ SIGNATURES = [
     ("fhegpu_prog_run", ctypes.c_int, [_P, _P, ctypes.c_uint32]),
     ("fhegpu_prog_run_range", ctypes.c_int, [_P, _P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]),
     ("fhegpu_prog_launches", ctypes.c_uint32, [_P]),
+    ("fhegpu_prog_run_host", ctypes.c_int, [_P, _P, ctypes.c_uint64, ctypes.c_uint32,
+                                            ctypes.c_uint32, _P, _P, ctypes.c_uint32, _P, _P]),
     ("fhegpu_prog_destroy", None, [_P]),
     ("fhegpu_nand_batch", ctypes.c_int, [_P, _U32P, _U32P, _U32P, ctypes.c_uint64]),
     ("fhegpu_not_batch", ctypes.c_int, [_P, _U32P, _U32P, ctypes.c_uint64]),
@@ -135,6 +137,20 @@ class Program:
         last = self.n_levels if last is None else last
         _check(_lib.fhegpu_prog_run_range(self.ctx.handle, self.handle, lanes, first, last),
                "prog_run")
+
+    def run_host(self, lanes: int, chunk_lanes: int, in_slots, in_ptrs, out_slots, out_ptrs):
+        """fhegpu_prog_run_host: stream `lanes` host-resident lanes through the device in
+        chunks (copy-in / evaluate / copy-out overlapped).  *_ptrs are host addresses of
+        dense (lanes, N, k) u32 arrays (pinned for overlap).  Asynchronous."""
+        ni, no = len(in_slots), len(out_slots)
+        if len(in_ptrs) != ni or len(out_ptrs) != no:
+            raise UsageError("one host buffer per slot")
+        isl = (ctypes.c_uint32 * max(1, ni))(*[int(x) for x in in_slots])
+        osl = (ctypes.c_uint32 * max(1, no))(*[int(x) for x in out_slots])
+        ip = (ctypes.c_void_p * max(1, ni))(*[int(x) for x in in_ptrs])
+        op = (ctypes.c_void_p * max(1, no))(*[int(x) for x in out_ptrs])
+        _check(_lib.fhegpu_prog_run_host(self.ctx.handle, self.handle, int(lanes), int(chunk_lanes),
+                                         ni, isl, ip, no, osl, op), "prog_run_host")
 
     def __del__(self):
         h = getattr(self, "handle", None)

@@ -38,6 +38,7 @@ int fail(int code, const std::string &msg) {
   } while (0)
 
 constexpr size_t kStagingCap = size_t(256) << 20;  // bytes per staged transfer chunk
+constexpr int kStreamRegions = 3;                  // store regions rotated by fhegpu_prog_run_host
 
 }  // namespace
 
@@ -63,12 +64,19 @@ struct fhegpu_ctx {
   size_t tmp_ops_cap = 0;
   JumpTable *d_jump = nullptr;  // PCG64 jump-ahead constants (lazily uploaded)
   bool use_graphs = true;       // replay whole programs as CUDA graphs
+  // host streaming (fhegpu_prog_run_host): copy-in / copy-out streams + per-region events
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t ev_start = nullptr;
+  cudaEvent_t ev_in[kStreamRegions] = {}, ev_done[kStreamRegions] = {}, ev_free[kStreamRegions] = {};
+  uint32_t *d_hstage = nullptr;  // dense staging rows for contiguous host copies
+  size_t hstage_bytes = 0;
 };
 
 struct fhegpu_prog {
   OpRec *d_ops = nullptr;
   std::vector<uint64_t> offsets;  // n_levels + 1
   uint64_t n_ops = 0;
+  uint64_t n_slots = 0;           // 1 + the largest slot any op names
   // CUDA graph of one full run (all level launches), captured on first use per
   // (lanes, stream, kernel choice, debug bits); replayed with a single cudaGraphLaunch
   cudaGraphExec_t graph = nullptr;
@@ -265,6 +273,15 @@ void fhegpu_ctx_destroy(fhegpu_ctx *c) {
   cudaFree(c->d_tmp_ops);
   cudaFree(c->d_jump);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  cudaFree(c->d_hstage);
+  if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
+  if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
+  for (int r = 0; r < kStreamRegions; ++r) {
+    if (c->ev_in[r]) cudaEventDestroy(c->ev_in[r]);
+    if (c->ev_done[r]) cudaEventDestroy(c->ev_done[r]);
+    if (c->ev_free[r]) cudaEventDestroy(c->ev_free[r]);
+  }
   delete c;
 }
 
@@ -428,14 +445,17 @@ int fhegpu_prog_create(fhegpu_ctx *c, const fhegpu_op *ops, uint64_t n_ops,
     return fail(FHEGPU_EINVAL, "level offsets must span [0, n_ops]");
   for (uint32_t l = 0; l < n_levels; ++l)
     if (level_offsets[l + 1] < level_offsets[l]) return fail(FHEGPU_EINVAL, "level offsets not sorted");
+  uint64_t n_slots = 0;
   for (uint64_t i = 0; i < n_ops; ++i) {
     const uint32_t mx = std::max(ops[i].left, std::max(ops[i].right, ops[i].out));
     if (mx >= (1u << 31) || (ops[i].flags & ~3u))
       return fail(FHEGPU_EINVAL, "bad op record " + std::to_string(i));
+    n_slots = std::max<uint64_t>(n_slots, uint64_t(mx) + 1);
   }
   CUDA_TRY(cudaSetDevice(c->device));
   auto *pr = new fhegpu_prog();
   pr->n_ops = n_ops;
+  pr->n_slots = n_slots;
   pr->offsets.assign(level_offsets, level_offsets + n_levels + 1);
   if (n_ops) {
     cudaError_t e = cudaMalloc(&pr->d_ops, n_ops * sizeof(OpRec));
@@ -502,6 +522,100 @@ int fhegpu_prog_run(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
     return FHEGPU_OK;                  // this call already ran the program once
   }
   CUDA_TRY(cudaGraphLaunch(pr->graph, c->stream));
+  return FHEGPU_OK;
+}
+
+namespace {
+
+int ensure_streaming(fhegpu_ctx *c) {
+  if (c->h2d_stream) return FHEGPU_OK;
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+  for (int r = 0; r < kStreamRegions; ++r) {
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_in[r], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_done[r], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_free[r], cudaEventDisableTiming));
+  }
+  return FHEGPU_OK;
+}
+
+}  // namespace
+
+int fhegpu_prog_run_host(fhegpu_ctx *c, fhegpu_prog *pr, uint64_t lanes, uint32_t chunk_lanes,
+                         uint32_t n_in, const uint32_t *in_slots, const uint32_t *const *host_in,
+                         uint32_t n_out, const uint32_t *out_slots, uint32_t *const *host_out) {
+  if (!c || !pr || (n_in && (!in_slots || !host_in)) || (n_out && (!out_slots || !host_out)))
+    return fail(FHEGPU_EINVAL, "null argument");
+  if (lanes == 0) return FHEGPU_OK;
+  if (chunk_lanes == 0) return fail(FHEGPU_EINVAL, "chunk_lanes must be positive");
+  uint64_t n_slots = pr->n_slots;
+  for (uint32_t i = 0; i < n_in; ++i) {
+    if (!host_in[i]) return fail(FHEGPU_EINVAL, "null host input");
+    n_slots = std::max<uint64_t>(n_slots, uint64_t(in_slots[i]) + 1);
+  }
+  for (uint32_t i = 0; i < n_out; ++i) {
+    if (!host_out[i]) return fail(FHEGPU_EINVAL, "null host output");
+    n_slots = std::max<uint64_t>(n_slots, uint64_t(out_slots[i]) + 1);
+  }
+  const uint64_t chunk = std::min<uint64_t>(chunk_lanes, lanes);
+  const uint64_t n_chunks = (lanes + chunk - 1) / chunk;
+  const int regions = (int)std::min<uint64_t>(kStreamRegions, n_chunks);
+  const uint64_t region_cts = n_slots * chunk;
+  if (region_cts * regions > c->capacity)
+    return fail(FHEGPU_EINVAL, "store holds " + std::to_string(c->capacity) + " ciphertexts; streaming needs " +
+                                   std::to_string(region_cts * regions) + " (reserve more or use smaller chunks)");
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (int rc = ensure_streaming(c)) return rc;
+  const size_t dense = (size_t)c->p.words * 4;
+  // dense staging per region: n_in + n_out arrays of `chunk` rows (contiguous PCIe copies run
+  // ~10% faster than pitched ones; the repack to the store's padded rows is HBM-cheap)
+  const uint64_t stage_rows = (uint64_t)(n_in + n_out) * chunk;
+  if (int rc = ensure((void **)&c->d_hstage, &c->hstage_bytes, regions * stage_rows * dense)) return rc;
+  const uint32_t n_levels = (uint32_t)pr->offsets.size() - 1;
+  const unsigned repack_grid = (unsigned)std::max(1, c->num_sms * 8);
+  // everything queued on the context stream so far happens before the first copy
+  CUDA_TRY(cudaEventRecord(c->ev_start, c->stream));
+  CUDA_TRY(cudaStreamWaitEvent(c->h2d_stream, c->ev_start, 0));
+  CUDA_TRY(cudaStreamWaitEvent(c->d2h_stream, c->ev_start, 0));
+  for (uint64_t ch = 0; ch < n_chunks; ++ch) {
+    const int r = (int)(ch % regions);
+    const uint64_t lane0 = ch * chunk, cl = std::min(chunk, lanes - lane0);
+    uint32_t *base = c->store + (uint64_t)r * region_cts * c->p.ct_words;
+    uint32_t *stage = c->d_hstage + (uint64_t)r * stage_rows * c->p.words;
+    // copy-in: region r (store + staging) is free once chunk ch - regions was copied out
+    if (ch >= (uint64_t)regions) CUDA_TRY(cudaStreamWaitEvent(c->h2d_stream, c->ev_free[r], 0));
+    for (uint32_t i = 0; i < n_in; ++i)
+      CUDA_TRY(cudaMemcpyAsync(stage + (uint64_t)i * chunk * c->p.words, host_in[i] + lane0 * c->p.words,
+                               cl * dense, cudaMemcpyHostToDevice, c->h2d_stream));
+    CUDA_TRY(cudaEventRecord(c->ev_in[r], c->h2d_stream));
+    // evaluate: repack inputs, every level over this chunk's lanes (store layout
+    // slot * cl + lane inside region r), repack outputs
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_in[r], 0));
+    const unsigned g = (unsigned)std::min<uint64_t>(cl, repack_grid);
+    for (uint32_t i = 0; i < n_in; ++i)
+      dense_to_store_kernel<<<g, 256, 0, c->stream>>>(base + (uint64_t)in_slots[i] * cl * c->p.ct_words,
+                                                     stage + (uint64_t)i * chunk * c->p.words, cl, c->p);
+    CUDA_TRY(cudaGetLastError());
+    for (uint32_t l = 0; l < n_levels; ++l) {
+      const uint64_t a = pr->offsets[l], b = pr->offsets[l + 1];
+      if (int rc = launch_level(c, base, pr->d_ops + a, (uint32_t)(b - a), (uint32_t)cl)) return rc;
+    }
+    uint32_t *stage_out = stage + (uint64_t)n_in * chunk * c->p.words;
+    for (uint32_t i = 0; i < n_out; ++i)
+      store_to_dense_kernel<<<g, 256, 0, c->stream>>>(stage_out + (uint64_t)i * chunk * c->p.words,
+                                                     base + (uint64_t)out_slots[i] * cl * c->p.ct_words, cl, c->p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(c->ev_done[r], c->stream));
+    // copy-out
+    CUDA_TRY(cudaStreamWaitEvent(c->d2h_stream, c->ev_done[r], 0));
+    for (uint32_t i = 0; i < n_out; ++i)
+      CUDA_TRY(cudaMemcpyAsync(host_out[i] + lane0 * c->p.words, stage_out + (uint64_t)i * chunk * c->p.words,
+                               cl * dense, cudaMemcpyDeviceToHost, c->d2h_stream));
+    CUDA_TRY(cudaEventRecord(c->ev_free[r], c->d2h_stream));
+  }
+  // the context stream observes completion of every copy-out
+  for (int r = 0; r < regions; ++r) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_free[r], 0));
   return FHEGPU_OK;
 }
 

@@ -89,6 +89,22 @@ __global__ void scatter_kernel(uint32_t *__restrict__ store, const uint64_t *__r
   }
 }
 
+// Host-streaming repack (fhegpu_prog_run_host): rows of `words` u32 (dense, as the host
+// holds them) <-> store rows of ct_words (padding zeroed).  One row per block iteration.
+__global__ void dense_to_store_kernel(uint32_t *__restrict__ store, const uint32_t *__restrict__ dense,
+                                      uint64_t rows, DevParams p) {
+  for (uint64_t r = blockIdx.x; r < rows; r += gridDim.x)
+    for (uint32_t w = threadIdx.x; w < p.ct_words; w += blockDim.x)
+      store[r * p.ct_words + w] = w < p.words ? dense[r * p.words + w] : 0u;
+}
+
+__global__ void store_to_dense_kernel(uint32_t *__restrict__ dense, const uint32_t *__restrict__ store,
+                                      uint64_t rows, DevParams p) {
+  for (uint64_t r = blockIdx.x; r < rows; r += gridDim.x)
+    for (uint32_t w = threadIdx.x; w < p.words; w += blockDim.x)
+      dense[r * p.words + w] = store[r * p.ct_words + w];
+}
+
 // dense[c] <- store[idx[c]] (complemented when comp[c]); row >= 0 selects one row only.
 __global__ void gather_kernel(const uint32_t *__restrict__ store, const uint64_t *__restrict__ idx,
                               const uint8_t *__restrict__ comp, uint32_t *__restrict__ dense,

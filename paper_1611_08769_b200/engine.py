@@ -476,6 +476,73 @@ class GpuEngine:
         self.launches += program.launches
         return program
 
+    def run_host(self, program, inputs, outputs, chunk_lanes: int = 32768, out=None,
+                 sync: bool = True):
+        """Re-run a flushed `program` over lanes held in HOST memory (fhegpu_prog_run_host).
+
+        The netlist is compiled once (flush, at any batch size); here every input wire of
+        the program gets a host array of ``lanes`` dense compact ciphertexts (lanes, N, k)
+        u32 -- numpy, or torch pinned tensors for overlapped copies -- and every output
+        wire a host array of the same shape (allocated when ``out`` is None).  Lanes stream
+        through the device store in chunks; copy-in, the level kernels and copy-out overlap,
+        so batches larger than HBM work.  Resident values of this engine are overwritten:
+        call this after reading back what you need.  Returns the output arrays.
+        """
+        if program is None:
+            raise UsageError("run_host needs a flushed program")
+        p = self.params
+        shape_tail = (p.n_ct, p.k)
+        in_slots, in_ptrs, lanes = [], [], None
+        keep = []
+        for h, arr in inputs:
+            if h.const or h.neg or self._slot[h.node] < 0:
+                raise UsageError("run_host inputs must be resident, non-negated input wires")
+            arr = self._host_array(arr, shape_tail)
+            keep.append(arr)
+            if lanes is None:
+                lanes = len(arr)
+            elif len(arr) != lanes:
+                raise UsageError("every host input needs the same number of lanes")
+            in_slots.append(self._slot[h.node])
+            in_ptrs.append(arr.data_ptr() if hasattr(arr, "data_ptr") else arr.ctypes.data)
+        if lanes is None:
+            raise UsageError("run_host needs at least one input")
+        if out is None:
+            out = [np.empty((lanes,) + shape_tail, dtype=np.uint32) for _ in outputs]
+        out_slots, out_ptrs = [], []
+        for h, arr in zip(outputs, out):
+            if h.const or h.neg or self._slot[h.node] < 0:
+                raise UsageError("run_host outputs must be resident, non-negated wires")
+            arr = self._host_array(arr, shape_tail)
+            if len(arr) != lanes:
+                raise UsageError("output buffer lane count differs from the inputs'")
+            out_slots.append(self._slot[h.node])
+            out_ptrs.append(arr.data_ptr() if hasattr(arr, "data_ptr") else arr.ctypes.data)
+        n_slots = max([self._n_slots] + [s + 1 for s in in_slots + out_slots])
+        chunk = max(1, min(int(chunk_lanes), lanes))
+        regions = min(3, -(-lanes // chunk))
+        need = regions * n_slots * chunk
+        if self.ctx.capacity < need:
+            self.ctx.reserve(need)
+        program.run_host(lanes, chunk, in_slots, in_ptrs, out_slots, out_ptrs)
+        if sync:
+            self.ctx.sync()
+        return out
+
+    @staticmethod
+    def _host_array(arr, shape_tail):
+        if hasattr(arr, "data_ptr"):                      # torch tensor (ideally pinned)
+            if arr.device.type != "cpu" or not arr.is_contiguous() or arr.element_size() != 4:
+                raise UsageError("host tensors must be contiguous 32-bit CPU tensors")
+            if tuple(arr.shape[1:]) != shape_tail:
+                raise UsageError(f"host tensor shape {tuple(arr.shape)} is not (lanes,) + {shape_tail}")
+            return arr
+        if not isinstance(arr, np.ndarray) or arr.dtype != np.uint32 or not arr.flags.c_contiguous:
+            raise UsageError("host arrays must be C-contiguous uint32")
+        if arr.shape[1:] != shape_tail:
+            raise UsageError(f"host array shape {arr.shape} is not (lanes,) + {shape_tail}")
+        return arr
+
     def _compile(self):
         """Level-sort the pending gates and assign ciphertext slots by liveness.
 

@@ -124,3 +124,43 @@ def test_generic_params_use_simt_kernel():
 def test_default_kernel_is_tcgen05_on_b200():
     assert GswScheme(DEFAULT_PARAMS).ctx.kernel == "tcgen05"
     assert GswScheme(EXACT_PARAMS).ctx.kernel == "tcgen05"
+
+
+@pytest.mark.parametrize("pinned", [False, True], ids=["pageable", "pinned"])
+def test_run_host_streaming_matches_oracle(pinned):
+    """fhegpu_prog_run_host: XOR + AND compiled once at batch 1, then 1000 host lanes
+    streamed in chunks of 96 (11 chunks: 3 regions reused, ragged last chunk)."""
+    import torch
+    from paper_1611_08769_b200 import Ciphertext, GpuEngine, and_, xor_
+    p = DEFAULT_PARAMS
+    op = ORACLE[p]
+    s = GswScheme(p)
+    keys = s.keygen(1)
+    rng = np.random.default_rng(77)
+    eng = GpuEngine(s, keys=keys, rng=rng, batch_size=1)
+    seed_ct = s.encrypt_many(keys.public_key, [0, 1], rng)
+    a = eng.input_values(seed_ct[0:1], noise_est=64)
+    b = eng.input_values(seed_ct[1:2], noise_est=64)
+    x, y = xor_(a, b), and_(a, b)
+    prog = eng.flush()
+    lanes = 1000
+    bits = rng.integers(0, 2, (lanes, 2))
+    va = s.encrypt_many(keys.public_key, bits[:, 0], rng).astype(np.uint32)
+    vb = s.encrypt_many(keys.public_key, bits[:, 1], rng).astype(np.uint32)
+    if pinned:
+        ins = [torch.from_numpy(v.view(np.int32)).pin_memory() for v in (va, vb)]
+        outs = [torch.empty_like(ins[0]).pin_memory() for _ in range(2)]
+        eng.run_host(prog, [(a, ins[0]), (b, ins[1])], [x, y], chunk_lanes=96, out=outs)
+        ox, oy = (o.numpy().view(np.uint32) for o in outs)
+    else:
+        ox, oy = eng.run_host(prog, [(a, va), (b, vb)], [x, y], chunk_lanes=96)
+    for lane in list(range(0, lanes, 97)) + [lanes - 1]:
+        A, B = va[lane].astype(np.int64), vb[lane].astype(np.int64)
+        n1 = gsw.hom_nand_compact(op, A, B)
+        want_x = gsw.hom_nand_compact(op, gsw.hom_nand_compact(op, n1, A), gsw.hom_nand_compact(op, n1, B))
+        n2 = gsw.hom_nand_compact(op, A, B)
+        want_y = gsw.hom_nand_compact(op, n2, n2)           # not_ = NAND(x, x) (gates.py)
+        assert np.array_equal(ox[lane], want_x.astype(np.uint32)), lane
+        assert np.array_equal(oy[lane], want_y.astype(np.uint32)), lane
+    dec_x = [s.decrypt_bit(keys.secret_key, Ciphertext(ox[l], 3, 0, p)) for l in range(0, lanes, 7)]
+    assert dec_x == list(bits[::7, 0] ^ bits[::7, 1])

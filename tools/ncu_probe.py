@@ -14,6 +14,7 @@ a = eng.input_values(np.tile(base[0::2], (reps, 1, 1))[:lanes], noise_est=64)
 b = eng.input_values(np.tile(base[1::2], (reps, 1, 1))[:lanes], noise_est=64)
 x = xor_(a, b); y = and_(a, b)
 prog = eng.flush()
-prog.run(lanes)
+for _ in range(2):
+    prog.run(lanes)
 s.ctx.sync()
 print("ok", s.ctx.kernel)
