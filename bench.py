@@ -293,15 +293,26 @@ def e2e_gates(eng, scheme, prog, lanes, inputs, outputs, stream, args, world, bi
     import torch
     ctx = scheme.ctx
     p = scheme.params
-    words = p.n_ct * p.k
+    packed = args.e2e_format == "packed"
     for h in inputs + outputs:
         assert h.neg == 0
     in_first = [eng._slot[h.node] * lanes for h in inputs]
     t0 = time.perf_counter()
-    host_in = torch.empty((len(inputs), lanes, p.n_ct, p.k), dtype=torch.int32, pin_memory=True)
-    host_out = torch.empty((len(outputs), lanes, p.n_ct, p.k), dtype=torch.int32, pin_memory=True)
-    for i, f in enumerate(in_first):             # the step's inputs, as a client would hold them
-        ctx.read_range(f, lanes, host_in[i].data_ptr())
+    # host ciphertexts as a client holds them: the reference's serialised bytes (ceil(N^2/8)
+    # per ciphertext, fileio.py / EFT1 payload rows) or dense compact u32 rows
+    if packed:
+        bytes_ct = (p.n_ct * p.n_ct + 7) // 8
+        shape, dt = (lanes, bytes_ct), torch.uint8
+    else:
+        bytes_ct = p.n_ct * p.k * 4
+        shape, dt = (lanes, p.n_ct, p.k), torch.int32
+    host_in = [torch.empty(shape, dtype=dt, pin_memory=True) for _ in inputs]
+    host_out = [torch.empty(shape, dtype=dt, pin_memory=True) for _ in outputs]
+    for i, f in enumerate(in_first):
+        if packed:
+            ctx.read_packed(f, lanes, host_in[i].data_ptr())
+        else:
+            ctx.read_range(f, lanes, host_in[i].data_ptr())
     pin_s = time.perf_counter() - t0
 
     chunk = min(args.e2e_chunk, lanes)
@@ -310,7 +321,7 @@ def e2e_gates(eng, scheme, prog, lanes, inputs, outputs, stream, args, world, bi
         # fhegpu_prog_run_host: chunks of lanes stream host -> device -> host with copy-in,
         # the level kernels and copy-out overlapped on three streams (async; ends on `stream`)
         eng.run_host(prog, list(zip(inputs, host_in)), list(outputs), chunk_lanes=chunk,
-                     out=list(host_out), sync=False)
+                     out=host_out, sync=False, packed=packed)
 
     steps = max(1, min(args.steps, 5))
     for _ in range(max(1, min(args.warmup, 2))):
@@ -330,14 +341,19 @@ def e2e_gates(eng, scheme, prog, lanes, inputs, outputs, stream, args, world, bi
     from paper_1611_08769_b200 import Ciphertext
     sk = eng.secret_key
     sample = range(0, lanes, max(1, lanes // 64))
-    outs = [host_out[i].numpy().view(np.uint32) for i in range(len(outputs))]
-    ok = all(scheme.decrypt_bit(sk, Ciphertext(outs[0][l], 3, 0, p)) == (bits[l, 0] ^ bits[l, 1]) and
-             scheme.decrypt_bit(sk, Ciphertext(outs[1][l], 2, 0, p)) == (bits[l, 0] & bits[l, 1])
-             for l in sample)
-    bytes_ct = words * 4
+    sample = np.asarray(list(sample))
+    if packed:
+        from paper_1611_08769_b200.fileio import unpack_compact
+        outs = [unpack_compact(h.numpy()[sample], p) for h in host_out]
+    else:
+        outs = [h.numpy().view(np.uint32)[sample] for h in host_out]
+    ok = all(scheme.decrypt_bit(sk, Ciphertext(outs[0][j], 3, 0, p)) == (bits[l, 0] ^ bits[l, 1]) and
+             scheme.decrypt_bit(sk, Ciphertext(outs[1][j], 2, 0, p)) == (bits[l, 0] & bits[l, 1])
+             for j, l in enumerate(sample))
     return {"ms": ms, "wall_ms": wall_ms, "steps": steps, "pin_s": pin_s,
             "h2d": len(inputs) * lanes * bytes_ct, "d2h": len(outputs) * lanes * bytes_ct,
-            "chunk_lanes": chunk, "decrypt_check": ok,
+            "chunk_lanes": chunk, "decrypt_check": ok, "host_format": args.e2e_format,
+            "bytes_per_ciphertext": bytes_ct,
             }
 
 
@@ -434,8 +450,9 @@ def run_ours(args):
                        "h2d_bytes_per_step": e["h2d"], "d2h_bytes_per_step": e["d2h"],
                        "ms_per_step": e["ms"], "steps": e["steps"],
                        "chunk_lanes": e["chunk_lanes"], "decrypt_check": e["decrypt_check"],
-                       "path": "fhegpu_prog_run_host: pinned host inputs -> chunked H2D | level "
-                               "kernels | D2H of every output ciphertext, overlapped on 3 streams"}
+                       "host_format": e["host_format"], "bytes_per_ciphertext": e["bytes_per_ciphertext"],
+                       "path": "fhegpu_prog_run_host: pinned host ciphertexts (host_format) -> chunked H2D | unpack + level "
+                               "kernels + pack | D2H of every output ciphertext, overlapped on 3 streams"}
     if fft is not None:
         line["fft"] = {"metric": "16-pt Q4.12 FHE FFTs/s (configs[4])", "value": fft["ffts_per_s"],
                        "unit": "FFT/s", "nand_per_s": fft["nand_per_s"], "ms_per_step": fft["ms"],
@@ -488,6 +505,8 @@ def main():
     ap.add_argument("--cse", action="store_true", help="share XOR/AND's common NAND (reported separately)")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--e2e-chunk", type=int, default=32768, help="lanes per streamed chunk (e2e)")
+    ap.add_argument("--e2e-format", choices=["packed", "compact"], default="packed",
+                    help="host ciphertexts: reference-serialised bits (EFT1 rows) or compact u32")
     ap.add_argument("--no-fft", dest="fft", action="store_false")
     ap.add_argument("--fft-lanes", type=int, default=1024)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)

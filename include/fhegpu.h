@@ -113,6 +113,11 @@ int fhegpu_store_write_range(fhegpu_ctx *ctx, uint64_t first, uint64_t count,
 int fhegpu_store_read_range(fhegpu_ctx *ctx, uint64_t first, uint64_t count, uint32_t *host_v,
                             int async);
 
+/* Store range <-> the reference's serialised ciphertexts (FHEGPU_HOST_PACKED rows of
+ * ceil(N*N/8) bytes: fileio.py:72-79, one ciphertext of an EFT1 payload).  Synchronous. */
+int fhegpu_store_write_packed(fhegpu_ctx *ctx, uint64_t first, uint64_t count, const uint8_t *host_bytes);
+int fhegpu_store_read_packed(fhegpu_ctx *ctx, uint64_t first, uint64_t count, uint8_t *host_bytes);
+
 /* Levelised netlist: ops[level_offsets[l] .. level_offsets[l+1]) are the gates of
  * level l; every op of a level reads only slots written by earlier levels. */
 int fhegpu_prog_create(fhegpu_ctx *ctx, const fhegpu_op *ops, uint64_t n_ops,
@@ -125,19 +130,28 @@ int fhegpu_prog_run(fhegpu_ctx *ctx, fhegpu_prog *prog, uint32_t lanes);
 /* Run levels [first, last) only (profiling / partial evaluation). */
 int fhegpu_prog_run_range(fhegpu_ctx *ctx, fhegpu_prog *prog, uint32_t lanes,
                           uint32_t first_level, uint32_t last_level);
+/* Host ciphertext formats for fhegpu_prog_run_host. */
+enum {
+  FHEGPU_HOST_COMPACT = 0, /* dense compact V: N*k u32 per ciphertext (fhe.py:181-185 inverse) */
+  FHEGPU_HOST_PACKED = 1   /* the reference's serialised matrix: C = decompose(V) row-major,
+                              8 bits per byte MSB first, ceil(N*N/8) bytes per ciphertext --
+                              exactly one ciphertext of an EFT1 payload (fileio.py:72-79) */
+};
 /* Evaluate the program over `lanes` lanes held in HOST memory, streaming them through
  * the device store in chunks of `chunk_lanes` (so a batch may exceed HBM).  host_in[i]
- * holds `lanes` dense ciphertexts (N*k u32 each, lane-major) for the program input in
+ * holds `lanes` ciphertexts (lane-major, in `host_format`) for the program input in
  * slot in_slots[i]; host_out[i] receives the ciphertexts of slot out_slots[i].  Chunks
  * rotate through 3 store regions (capacity >= 3 * slots * chunk_lanes): the copy-in of
  * chunk c+1, the level kernels of chunk c and the copy-out of chunk c-1 overlap on
- * separate streams (both PCIe directions busy).  Asynchronous w.r.t. the host; the
+ * separate streams (both PCIe directions busy); copies are contiguous into device
+ * staging, repacked to store rows on the device.  Asynchronous w.r.t. the host; the
  * context stream observes completion.  Resident store contents are overwritten.
  * Host buffers should be pinned for the copies to overlap.  This is the batched
- * equivalent of encrypt -> netlist of hom_nand (fhe.py:325-341) -> decrypt hand-off. */
+ * equivalent of a netlist of hom_nand (fhe.py:325-341) over serialised ciphertexts. */
 int fhegpu_prog_run_host(fhegpu_ctx *ctx, fhegpu_prog *prog, uint64_t lanes, uint32_t chunk_lanes,
-                         uint32_t n_in, const uint32_t *in_slots, const uint32_t *const *host_in,
-                         uint32_t n_out, const uint32_t *out_slots, uint32_t *const *host_out);
+                         int host_format, uint32_t n_in, const uint32_t *in_slots,
+                         const void *const *host_in, uint32_t n_out, const uint32_t *out_slots,
+                         void *const *host_out);
 uint32_t fhegpu_prog_launches(const fhegpu_prog *prog);       /* launches one run issues */
 void fhegpu_prog_destroy(fhegpu_prog *prog);
 

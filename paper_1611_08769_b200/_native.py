@@ -17,6 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfhegpu.so")
 
 KERNEL_AUTO, KERNEL_SIMT, KERNEL_TCGEN05 = 0, 1, 2
+HOST_COMPACT, HOST_PACKED = 0, 1      # fhegpu_prog_run_host host formats
 KERNEL_NAMES = {KERNEL_AUTO: "auto", KERNEL_SIMT: "simt", KERNEL_TCGEN05: "tcgen05"}
 
 OP_DTYPE = np.dtype([("left", "<u4"), ("right", "<u4"), ("out", "<u4"), ("flags", "<u4")])
@@ -59,7 +60,9 @@ SIGNATURES = [
     ("fhegpu_prog_run", ctypes.c_int, [_P, _P, ctypes.c_uint32]),
     ("fhegpu_prog_run_range", ctypes.c_int, [_P, _P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]),
     ("fhegpu_prog_launches", ctypes.c_uint32, [_P]),
-    ("fhegpu_prog_run_host", ctypes.c_int, [_P, _P, ctypes.c_uint64, ctypes.c_uint32,
+    ("fhegpu_store_write_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
+    ("fhegpu_store_read_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
+    ("fhegpu_prog_run_host", ctypes.c_int, [_P, _P, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int,
                                             ctypes.c_uint32, _P, _P, ctypes.c_uint32, _P, _P]),
     ("fhegpu_prog_destroy", None, [_P]),
     ("fhegpu_nand_batch", ctypes.c_int, [_P, _U32P, _U32P, _U32P, ctypes.c_uint64]),
@@ -138,7 +141,8 @@ class Program:
         _check(_lib.fhegpu_prog_run_range(self.ctx.handle, self.handle, lanes, first, last),
                "prog_run")
 
-    def run_host(self, lanes: int, chunk_lanes: int, in_slots, in_ptrs, out_slots, out_ptrs):
+    def run_host(self, lanes: int, chunk_lanes: int, in_slots, in_ptrs, out_slots, out_ptrs,
+                 host_format: int = 0):
         """fhegpu_prog_run_host: stream `lanes` host-resident lanes through the device in
         chunks (copy-in / evaluate / copy-out overlapped).  *_ptrs are host addresses of
         dense (lanes, N, k) u32 arrays (pinned for overlap).  Asynchronous."""
@@ -150,7 +154,7 @@ class Program:
         ip = (ctypes.c_void_p * max(1, ni))(*[int(x) for x in in_ptrs])
         op = (ctypes.c_void_p * max(1, no))(*[int(x) for x in out_ptrs])
         _check(_lib.fhegpu_prog_run_host(self.ctx.handle, self.handle, int(lanes), int(chunk_lanes),
-                                         ni, isl, ip, no, osl, op), "prog_run_host")
+                                         int(host_format), ni, isl, ip, no, osl, op), "prog_run_host")
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -237,6 +241,16 @@ class DeviceContext:
     def read_range(self, first: int, count: int, host_ptr: int, sync: bool = True):
         _check(_lib.fhegpu_store_read_range(self.handle, first, count, ctypes.c_void_p(host_ptr),
                                             0 if sync else 1), "store_read_range")
+
+    def write_packed(self, first: int, count: int, host_ptr: int):
+        """Store range <- serialised ciphertexts (ceil(N^2/8) bytes each, fileio.pack_compact)."""
+        _check(_lib.fhegpu_store_write_packed(self.handle, first, count, ctypes.c_void_p(host_ptr)),
+               "store_write_packed")
+
+    def read_packed(self, first: int, count: int, host_ptr: int):
+        """Store range -> serialised ciphertexts (ceil(N^2/8) bytes each)."""
+        _check(_lib.fhegpu_store_read_packed(self.handle, first, count, ctypes.c_void_p(host_ptr)),
+               "store_read_packed")
 
     def read(self, idx, complement=None) -> np.ndarray:
         idx = np.ascontiguousarray(idx, dtype=np.uint64)

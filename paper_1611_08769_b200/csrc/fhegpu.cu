@@ -437,6 +437,62 @@ int fhegpu_store_read_range(fhegpu_ctx *c, uint64_t first, uint64_t count, uint3
   return FHEGPU_OK;
 }
 
+namespace {
+
+size_t packed_row_bytes(const fhegpu_ctx *c) { return ((size_t)c->p.rows * c->p.rows + 7) / 8; }
+
+int set_pack_smem(fhegpu_ctx *c) {
+  const size_t smem = std::max(packed_row_bytes(c), (size_t)c->p.words * 4);
+  if (smem > 48 * 1024) {
+    CUDA_TRY(cudaFuncSetAttribute(packed_to_store_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(cudaFuncSetAttribute(store_to_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  return FHEGPU_OK;
+}
+
+}  // namespace
+
+int fhegpu_store_write_packed(fhegpu_ctx *c, uint64_t first, uint64_t count, const uint8_t *host) {
+  if (!c || (count && !host)) return fail(FHEGPU_EINVAL, "null argument");
+  if (first + count > c->capacity) return fail(FHEGPU_EINVAL, "range beyond store capacity");
+  if (count == 0) return FHEGPU_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (int rc = set_pack_smem(c)) return rc;
+  const size_t per = packed_row_bytes(c);
+  const uint64_t chunk = std::max<uint64_t>(1, kStagingCap / per);
+  for (uint64_t s = 0; s < count; s += chunk) {
+    const uint64_t n = std::min(chunk, count - s);
+    if (int rc = ensure((void **)&c->d_stage, &c->stage_bytes, n * per)) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->d_stage, host + s * per, n * per, cudaMemcpyHostToDevice, c->stream));
+    packed_to_store_kernel<<<(unsigned)std::min<uint64_t>(n, c->num_sms * 8), 256, per, c->stream>>>(
+        c->store + (first + s) * c->p.ct_words, (const uint8_t *)c->d_stage, n, (uint32_t)per, c->p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(c->stream));  // staging is reused by the next chunk
+  }
+  return FHEGPU_OK;
+}
+
+int fhegpu_store_read_packed(fhegpu_ctx *c, uint64_t first, uint64_t count, uint8_t *host) {
+  if (!c || (count && !host)) return fail(FHEGPU_EINVAL, "null argument");
+  if (first + count > c->capacity) return fail(FHEGPU_EINVAL, "range beyond store capacity");
+  if (count == 0) return FHEGPU_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (int rc = set_pack_smem(c)) return rc;
+  const size_t per = packed_row_bytes(c);
+  const uint64_t chunk = std::max<uint64_t>(1, kStagingCap / per);
+  for (uint64_t s = 0; s < count; s += chunk) {
+    const uint64_t n = std::min(chunk, count - s);
+    if (int rc = ensure((void **)&c->d_stage, &c->stage_bytes, n * per)) return rc;
+    store_to_packed_kernel<<<(unsigned)std::min<uint64_t>(n, c->num_sms * 8), 256, (size_t)c->p.words * 4,
+                             c->stream>>>((uint8_t *)c->d_stage, c->store + (first + s) * c->p.ct_words, n,
+                                          (uint32_t)per, c->p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(host + s * per, c->d_stage, n * per, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  return FHEGPU_OK;
+}
+
 int fhegpu_prog_create(fhegpu_ctx *c, const fhegpu_op *ops, uint64_t n_ops,
                        const uint64_t *level_offsets, uint32_t n_levels, fhegpu_prog **out) {
   if (!c || !out || (n_ops && !ops) || !level_offsets) return fail(FHEGPU_EINVAL, "null argument");
@@ -543,12 +599,15 @@ int ensure_streaming(fhegpu_ctx *c) {
 }  // namespace
 
 int fhegpu_prog_run_host(fhegpu_ctx *c, fhegpu_prog *pr, uint64_t lanes, uint32_t chunk_lanes,
-                         uint32_t n_in, const uint32_t *in_slots, const uint32_t *const *host_in,
-                         uint32_t n_out, const uint32_t *out_slots, uint32_t *const *host_out) {
+                         int host_format, uint32_t n_in, const uint32_t *in_slots,
+                         const void *const *host_in, uint32_t n_out, const uint32_t *out_slots,
+                         void *const *host_out) {
   if (!c || !pr || (n_in && (!in_slots || !host_in)) || (n_out && (!out_slots || !host_out)))
     return fail(FHEGPU_EINVAL, "null argument");
   if (lanes == 0) return FHEGPU_OK;
   if (chunk_lanes == 0) return fail(FHEGPU_EINVAL, "chunk_lanes must be positive");
+  if (host_format != FHEGPU_HOST_COMPACT && host_format != FHEGPU_HOST_PACKED)
+    return fail(FHEGPU_EINVAL, "unknown host format");
   uint64_t n_slots = pr->n_slots;
   for (uint32_t i = 0; i < n_in; ++i) {
     if (!host_in[i]) return fail(FHEGPU_EINVAL, "null host input");
@@ -567,13 +626,17 @@ int fhegpu_prog_run_host(fhegpu_ctx *c, fhegpu_prog *pr, uint64_t lanes, uint32_
                                    std::to_string(region_cts * regions) + " (reserve more or use smaller chunks)");
   CUDA_TRY(cudaSetDevice(c->device));
   if (int rc = ensure_streaming(c)) return rc;
-  const size_t dense = (size_t)c->p.words * 4;
-  // dense staging per region: n_in + n_out arrays of `chunk` rows (contiguous PCIe copies run
-  // ~10% faster than pitched ones; the repack to the store's padded rows is HBM-cheap)
+  const bool packed = host_format == FHEGPU_HOST_PACKED;
+  const size_t row_bytes = packed ? ((size_t)c->p.rows * c->p.rows + 7) / 8 : (size_t)c->p.words * 4;
+  // staging per region: n_in + n_out arrays of `chunk` host-format rows (contiguous PCIe
+  // copies run ~10% faster than pitched ones; the repack to the store's padded rows is
+  // HBM-cheap and, for the packed format, cuts PCIe bytes by 1 - N^2/8 / (4 N k))
   const uint64_t stage_rows = (uint64_t)(n_in + n_out) * chunk;
-  if (int rc = ensure((void **)&c->d_hstage, &c->hstage_bytes, regions * stage_rows * dense)) return rc;
+  if (int rc = ensure((void **)&c->d_hstage, &c->hstage_bytes, regions * stage_rows * row_bytes)) return rc;
   const uint32_t n_levels = (uint32_t)pr->offsets.size() - 1;
   const unsigned repack_grid = (unsigned)std::max(1, c->num_sms * 8);
+  if (packed)
+    if (int rc = set_pack_smem(c)) return rc;
   // everything queued on the context stream so far happens before the first copy
   CUDA_TRY(cudaEventRecord(c->ev_start, c->stream));
   CUDA_TRY(cudaStreamWaitEvent(c->h2d_stream, c->ev_start, 0));
@@ -582,36 +645,47 @@ int fhegpu_prog_run_host(fhegpu_ctx *c, fhegpu_prog *pr, uint64_t lanes, uint32_
     const int r = (int)(ch % regions);
     const uint64_t lane0 = ch * chunk, cl = std::min(chunk, lanes - lane0);
     uint32_t *base = c->store + (uint64_t)r * region_cts * c->p.ct_words;
-    uint32_t *stage = c->d_hstage + (uint64_t)r * stage_rows * c->p.words;
+    uint8_t *stage = (uint8_t *)c->d_hstage + (uint64_t)r * stage_rows * row_bytes;
+    uint8_t *stage_out = stage + (uint64_t)n_in * chunk * row_bytes;
     // copy-in: region r (store + staging) is free once chunk ch - regions was copied out
     if (ch >= (uint64_t)regions) CUDA_TRY(cudaStreamWaitEvent(c->h2d_stream, c->ev_free[r], 0));
     for (uint32_t i = 0; i < n_in; ++i)
-      CUDA_TRY(cudaMemcpyAsync(stage + (uint64_t)i * chunk * c->p.words, host_in[i] + lane0 * c->p.words,
-                               cl * dense, cudaMemcpyHostToDevice, c->h2d_stream));
+      CUDA_TRY(cudaMemcpyAsync(stage + (uint64_t)i * chunk * row_bytes,
+                               (const uint8_t *)host_in[i] + lane0 * row_bytes, cl * row_bytes,
+                               cudaMemcpyHostToDevice, c->h2d_stream));
     CUDA_TRY(cudaEventRecord(c->ev_in[r], c->h2d_stream));
     // evaluate: repack inputs, every level over this chunk's lanes (store layout
     // slot * cl + lane inside region r), repack outputs
     CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_in[r], 0));
     const unsigned g = (unsigned)std::min<uint64_t>(cl, repack_grid);
-    for (uint32_t i = 0; i < n_in; ++i)
-      dense_to_store_kernel<<<g, 256, 0, c->stream>>>(base + (uint64_t)in_slots[i] * cl * c->p.ct_words,
-                                                     stage + (uint64_t)i * chunk * c->p.words, cl, c->p);
+    for (uint32_t i = 0; i < n_in; ++i) {
+      uint32_t *dst = base + (uint64_t)in_slots[i] * cl * c->p.ct_words;
+      const uint8_t *src = stage + (uint64_t)i * chunk * row_bytes;
+      if (packed)
+        packed_to_store_kernel<<<g, 256, row_bytes, c->stream>>>(dst, src, cl, (uint32_t)row_bytes, c->p);
+      else
+        dense_to_store_kernel<<<g, 256, 0, c->stream>>>(dst, (const uint32_t *)src, cl, c->p);
+    }
     CUDA_TRY(cudaGetLastError());
     for (uint32_t l = 0; l < n_levels; ++l) {
       const uint64_t a = pr->offsets[l], b = pr->offsets[l + 1];
       if (int rc = launch_level(c, base, pr->d_ops + a, (uint32_t)(b - a), (uint32_t)cl)) return rc;
     }
-    uint32_t *stage_out = stage + (uint64_t)n_in * chunk * c->p.words;
-    for (uint32_t i = 0; i < n_out; ++i)
-      store_to_dense_kernel<<<g, 256, 0, c->stream>>>(stage_out + (uint64_t)i * chunk * c->p.words,
-                                                     base + (uint64_t)out_slots[i] * cl * c->p.ct_words, cl, c->p);
+    for (uint32_t i = 0; i < n_out; ++i) {
+      uint8_t *dst = stage_out + (uint64_t)i * chunk * row_bytes;
+      const uint32_t *src = base + (uint64_t)out_slots[i] * cl * c->p.ct_words;
+      if (packed)
+        store_to_packed_kernel<<<g, 256, (size_t)c->p.words * 4, c->stream>>>(dst, src, cl, (uint32_t)row_bytes, c->p);
+      else
+        store_to_dense_kernel<<<g, 256, 0, c->stream>>>((uint32_t *)dst, src, cl, c->p);
+    }
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(c->ev_done[r], c->stream));
     // copy-out
     CUDA_TRY(cudaStreamWaitEvent(c->d2h_stream, c->ev_done[r], 0));
     for (uint32_t i = 0; i < n_out; ++i)
-      CUDA_TRY(cudaMemcpyAsync(host_out[i] + lane0 * c->p.words, stage_out + (uint64_t)i * chunk * c->p.words,
-                               cl * dense, cudaMemcpyDeviceToHost, c->d2h_stream));
+      CUDA_TRY(cudaMemcpyAsync((uint8_t *)host_out[i] + lane0 * row_bytes, stage_out + (uint64_t)i * chunk * row_bytes,
+                               cl * row_bytes, cudaMemcpyDeviceToHost, c->d2h_stream));
     CUDA_TRY(cudaEventRecord(c->ev_free[r], c->d2h_stream));
   }
   // the context stream observes completion of every copy-out

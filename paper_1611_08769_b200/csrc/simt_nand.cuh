@@ -105,6 +105,61 @@ __global__ void store_to_dense_kernel(uint32_t *__restrict__ dense, const uint32
       dense[r * p.words + w] = store[r * p.ct_words + w];
 }
 
+// Packed matrix bits: the reference's serialised ciphertext (fileio.py:72-79 / EFT1
+// payload): C = decompose(V) row-major, bit j of V[r][i] at stream position
+// r*N + i*ell + j, packed 8 per byte MSB first; ceil(N*N/8) bytes per ciphertext.
+__global__ void packed_to_store_kernel(uint32_t *__restrict__ store, const uint8_t *__restrict__ packed,
+                                       uint64_t rows, uint32_t row_bytes, DevParams p) {
+  extern __shared__ uint8_t s_bytes[];
+  for (uint64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const uint8_t *src = packed + r * row_bytes;
+    for (uint32_t b = threadIdx.x; b < row_bytes; b += blockDim.x) s_bytes[b] = src[b];
+    __syncthreads();
+    for (uint32_t w = threadIdx.x; w < p.ct_words; w += blockDim.x) {
+      uint32_t v = 0;
+      if (w < p.words) {
+        const uint32_t rr = w / p.k, i = w - rr * p.k;
+        const uint32_t b0 = rr * p.rows + i * p.ell;           // first stream bit (= bit 0 of v)
+        const uint32_t byte0 = b0 >> 3;
+        uint64_t u = 0;                                         // 5 bytes big-endian >= ell + 7 bits
+#pragma unroll
+        for (int t = 0; t < 5; ++t)
+          u = (u << 8) | (byte0 + t < row_bytes ? s_bytes[byte0 + t] : 0u);
+        const uint32_t x = (uint32_t)(u >> (40 - (b0 & 7) - p.ell)) & ((1u << p.ell) - 1u);
+        v = __brev(x) >> (32 - p.ell);                          // stream order is LSB first
+      }
+      store[r * p.ct_words + w] = v;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void store_to_packed_kernel(uint8_t *__restrict__ packed, const uint32_t *__restrict__ store,
+                                       uint64_t rows, uint32_t row_bytes, DevParams p) {
+  extern __shared__ uint32_t s_vals[];
+  const uint32_t n_bits = p.rows * p.rows;
+  for (uint64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    for (uint32_t w = threadIdx.x; w < p.words; w += blockDim.x) s_vals[w] = store[r * p.ct_words + w];
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < row_bytes; b += blockDim.x) {
+      uint32_t pos = b * 8, rr = pos / p.rows, col = pos - rr * p.rows;
+      uint32_t i = col / p.ell, j = col - i * p.ell;
+      uint32_t byte = 0;
+      for (int t = 0; t < 8; ++t, ++pos) {
+        uint32_t bit = 0;
+        if (pos < n_bits) bit = (s_vals[rr * p.k + i] >> j) & 1u;
+        byte |= bit << (7 - t);
+        if (++j == p.ell) {
+          j = 0;
+          if (++i == p.k) { i = 0; ++rr; }
+        }
+      }
+      packed[r * row_bytes + b] = (uint8_t)byte;
+    }
+    __syncthreads();
+  }
+}
+
 // dense[c] <- store[idx[c]] (complemented when comp[c]); row >= 0 selects one row only.
 __global__ void gather_kernel(const uint32_t *__restrict__ store, const uint64_t *__restrict__ idx,
                               const uint8_t *__restrict__ comp, uint32_t *__restrict__ dense,

@@ -477,7 +477,7 @@ class GpuEngine:
         return program
 
     def run_host(self, program, inputs, outputs, chunk_lanes: int = 32768, out=None,
-                 sync: bool = True):
+                 sync: bool = True, packed: bool = False):
         """Re-run a flushed `program` over lanes held in HOST memory (fhegpu_prog_run_host).
 
         The netlist is compiled once (flush, at any batch size); here every input wire of
@@ -487,17 +487,22 @@ class GpuEngine:
         through the device store in chunks; copy-in, the level kernels and copy-out overlap,
         so batches larger than HBM work.  Resident values of this engine are overwritten:
         call this after reading back what you need.  Returns the output arrays.
+
+        ``packed=True``: host arrays are (lanes, ceil(N^2/8)) uint8 -- each lane one
+        ciphertext serialised exactly as the reference writes it (fileio.pack_compact /
+        an EFT1 payload row); unpacking and packing run on the device.
         """
         if program is None:
             raise UsageError("run_host needs a flushed program")
         p = self.params
-        shape_tail = (p.n_ct, p.k)
+        shape_tail = ((p.n_ct * p.n_ct + 7) // 8,) if packed else (p.n_ct, p.k)
+        dtype = np.uint8 if packed else np.uint32
         in_slots, in_ptrs, lanes = [], [], None
         keep = []
         for h, arr in inputs:
             if h.const or h.neg or self._slot[h.node] < 0:
                 raise UsageError("run_host inputs must be resident, non-negated input wires")
-            arr = self._host_array(arr, shape_tail)
+            arr = self._host_array(arr, shape_tail, dtype)
             keep.append(arr)
             if lanes is None:
                 lanes = len(arr)
@@ -508,12 +513,12 @@ class GpuEngine:
         if lanes is None:
             raise UsageError("run_host needs at least one input")
         if out is None:
-            out = [np.empty((lanes,) + shape_tail, dtype=np.uint32) for _ in outputs]
+            out = [np.empty((lanes,) + shape_tail, dtype=dtype) for _ in outputs]
         out_slots, out_ptrs = [], []
         for h, arr in zip(outputs, out):
             if h.const or h.neg or self._slot[h.node] < 0:
                 raise UsageError("run_host outputs must be resident, non-negated wires")
-            arr = self._host_array(arr, shape_tail)
+            arr = self._host_array(arr, shape_tail, dtype)
             if len(arr) != lanes:
                 raise UsageError("output buffer lane count differs from the inputs'")
             out_slots.append(self._slot[h.node])
@@ -524,21 +529,23 @@ class GpuEngine:
         need = regions * n_slots * chunk
         if self.ctx.capacity < need:
             self.ctx.reserve(need)
-        program.run_host(lanes, chunk, in_slots, in_ptrs, out_slots, out_ptrs)
+        program.run_host(lanes, chunk, in_slots, in_ptrs, out_slots, out_ptrs,
+                         host_format=1 if packed else 0)
         if sync:
             self.ctx.sync()
         return out
 
     @staticmethod
-    def _host_array(arr, shape_tail):
+    def _host_array(arr, shape_tail, dtype=np.uint32):
+        size = np.dtype(dtype).itemsize
         if hasattr(arr, "data_ptr"):                      # torch tensor (ideally pinned)
-            if arr.device.type != "cpu" or not arr.is_contiguous() or arr.element_size() != 4:
-                raise UsageError("host tensors must be contiguous 32-bit CPU tensors")
+            if arr.device.type != "cpu" or not arr.is_contiguous() or arr.element_size() != size:
+                raise UsageError(f"host tensors must be contiguous {8 * size}-bit CPU tensors")
             if tuple(arr.shape[1:]) != shape_tail:
                 raise UsageError(f"host tensor shape {tuple(arr.shape)} is not (lanes,) + {shape_tail}")
             return arr
-        if not isinstance(arr, np.ndarray) or arr.dtype != np.uint32 or not arr.flags.c_contiguous:
-            raise UsageError("host arrays must be C-contiguous uint32")
+        if not isinstance(arr, np.ndarray) or arr.dtype != dtype or not arr.flags.c_contiguous:
+            raise UsageError(f"host arrays must be C-contiguous {np.dtype(dtype).name}")
         if arr.shape[1:] != shape_tail:
             raise UsageError(f"host array shape {arr.shape} is not (lanes,) + {shape_tail}")
         return arr

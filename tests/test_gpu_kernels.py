@@ -126,8 +126,9 @@ def test_default_kernel_is_tcgen05_on_b200():
     assert GswScheme(EXACT_PARAMS).ctx.kernel == "tcgen05"
 
 
-@pytest.mark.parametrize("pinned", [False, True], ids=["pageable", "pinned"])
-def test_run_host_streaming_matches_oracle(pinned):
+@pytest.mark.parametrize("pinned,packed", [(False, False), (True, False), (True, True), (False, True)],
+                         ids=["pageable", "pinned", "pinned-packed", "pageable-packed"])
+def test_run_host_streaming_matches_oracle(pinned, packed):
     """fhegpu_prog_run_host: XOR + AND compiled once at batch 1, then 1000 host lanes
     streamed in chunks of 96 (11 chunks: 3 regions reused, ragged last chunk)."""
     import torch
@@ -147,13 +148,20 @@ def test_run_host_streaming_matches_oracle(pinned):
     bits = rng.integers(0, 2, (lanes, 2))
     va = s.encrypt_many(keys.public_key, bits[:, 0], rng).astype(np.uint32)
     vb = s.encrypt_many(keys.public_key, bits[:, 1], rng).astype(np.uint32)
+    from paper_1611_08769_b200.fileio import pack_compact, unpack_compact
+    ha, hb = (pack_compact(va, p), pack_compact(vb, p)) if packed else (va, vb)
     if pinned:
-        ins = [torch.from_numpy(v.view(np.int32)).pin_memory() for v in (va, vb)]
+        ins = [torch.from_numpy(h.view(np.uint8 if packed else np.int32)).pin_memory() for h in (ha, hb)]
         outs = [torch.empty_like(ins[0]).pin_memory() for _ in range(2)]
-        eng.run_host(prog, [(a, ins[0]), (b, ins[1])], [x, y], chunk_lanes=96, out=outs)
-        ox, oy = (o.numpy().view(np.uint32) for o in outs)
+        eng.run_host(prog, [(a, ins[0]), (b, ins[1])], [x, y], chunk_lanes=96, out=outs, packed=packed)
+        ox, oy = (o.numpy() for o in outs)
     else:
-        ox, oy = eng.run_host(prog, [(a, va), (b, vb)], [x, y], chunk_lanes=96)
+        ox, oy = eng.run_host(prog, [(a, ha), (b, hb)], [x, y], chunk_lanes=96, packed=packed)
+    if packed:                                # the reference's serialised bytes, bit-exact
+        assert ox.shape == (lanes, (p.n_ct ** 2 + 7) // 8)
+        ox, oy = unpack_compact(ox, p), unpack_compact(oy, p)
+    else:
+        ox, oy = ox.view(np.uint32), oy.view(np.uint32)
     for lane in list(range(0, lanes, 97)) + [lanes - 1]:
         A, B = va[lane].astype(np.int64), vb[lane].astype(np.int64)
         n1 = gsw.hom_nand_compact(op, A, B)
@@ -164,3 +172,21 @@ def test_run_host_streaming_matches_oracle(pinned):
         assert np.array_equal(oy[lane], want_y.astype(np.uint32)), lane
     dec_x = [s.decrypt_bit(keys.secret_key, Ciphertext(ox[l], 3, 0, p)) for l in range(0, lanes, 7)]
     assert dec_x == list(bits[::7, 0] ^ bits[::7, 1])
+
+
+@pytest.mark.parametrize("params", [DEFAULT_PARAMS, EXACT_PARAMS], ids=["default", "exact"])
+def test_store_packed_io_matches_reference_serialisation(params):
+    """fhegpu_store_{write,read}_packed == fileio.pack_compact / unpack_compact (EFT1 rows)."""
+    from paper_1611_08769_b200.fileio import pack_compact
+    s = GswScheme(params)
+    ctx = s.ctx
+    rng = np.random.default_rng(5)
+    v = _random_cts(params, 300, rng)
+    packed = np.ascontiguousarray(pack_compact(v, params))
+    ctx.reserve(700)
+    ctx.write_packed(17, len(v), packed.ctypes.data)
+    assert np.array_equal(ctx.read(np.arange(17, 17 + len(v), dtype=np.uint64)), v)
+    ctx.write(np.arange(400, 400 + len(v), dtype=np.uint64), v)
+    back = np.empty_like(packed)
+    ctx.read_packed(400, len(v), back.ctypes.data)
+    assert np.array_equal(back, packed)
