@@ -10,6 +10,8 @@
  *
  *   fhegpu_nand_batch   replaces GswScheme.hom_nand   (fhe.py:325-341), batched
  *   fhegpu_not_batch    replaces GswScheme.hom_not    (fhe.py:343-350), batched
+ *   fhegpu_{add,mult,const_mult}_batch  replace hom_add / hom_mult / hom_const_mult
+ *                       (fhe.py:352-379), batched
  *   fhegpu_prog_*       replaces FheEngine.nand/_fold  (engine.py:168-187) applied
  *                       gate by gate: a whole levelised netlist (every gate of
  *                       every butterfly of every signal) runs as one kernel per level
@@ -160,6 +162,18 @@ void fhegpu_prog_destroy(fhegpu_prog *prog);
 int fhegpu_nand_batch(fhegpu_ctx *ctx, const uint32_t *v1, const uint32_t *v2,
                       uint32_t *out, uint64_t count);
 int fhegpu_not_batch(fhegpu_ctx *ctx, const uint32_t *v, uint32_t *out, uint64_t count);
+
+/* Z_q ring operators (replace GswScheme.hom_add / hom_const_mult / hom_mult,
+ * fhe.py:352-379; level / noise bookkeeping and hom_mult's swap stay host-side):
+ *   add:        (V1 + V2) mod q                       = recompose(C1 + C2)
+ *   mult:       C1 V2 mod q  (NAND product, complemented) = recompose(C1 C2)
+ *   const_mult: mult with left operand (k G) mod q    = recompose(decompose(kG) C)  */
+int fhegpu_add_batch(fhegpu_ctx *ctx, const uint32_t *v1, const uint32_t *v2,
+                     uint32_t *out, uint64_t count);
+int fhegpu_mult_batch(fhegpu_ctx *ctx, const uint32_t *v1, const uint32_t *v2,
+                      uint32_t *out, uint64_t count);
+int fhegpu_const_mult_batch(fhegpu_ctx *ctx, uint32_t k, const uint32_t *v, uint32_t *out,
+                            uint64_t count);
 
 /* Fresh encryption on the device, stream-exact with numpy's Generator(PCG64)
  * (replaces GswScheme._encrypt / encrypt_bit / encrypt_value, fhe.py:227-242).

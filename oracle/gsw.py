@@ -159,3 +159,36 @@ def hom_not_compact(p: Params, v: np.ndarray) -> np.ndarray:
 def noise_after_nand(p: Params, e_left: int, e_right: int) -> int:
     """fhe.py:339: est = min(e1 + N e2, q) with e1 the (post-swap) left operand."""
     return min(e_left + p.n_ct * e_right, p.q)
+
+
+# -- Z_q ring operations (SURVEY 8(f)3) -------------------------------------------------------
+
+def hom_add_matrix(p: Params, c1: np.ndarray, c2: np.ndarray) -> np.ndarray:
+    """fhe.py:352-356: flatten(C1 + C2)."""
+    return flatten(c1 + c2, p)
+
+
+def hom_const_mult_matrix(p: Params, c: np.ndarray, k: int) -> np.ndarray:
+    """fhe.py:358-364: flatten(decompose(scaled_gadget(k mod q) mod q) @ C)."""
+    mk = bits_of(gadget(p, k % p.q), p).astype(np.float64)   # decompose(kG mod q)
+    return flatten(mk @ c, p)
+
+
+def hom_mult_matrix(p: Params, c1: np.ndarray, c2: np.ndarray) -> np.ndarray:
+    """fhe.py:366-379: flatten(C1 @ C2) (c1 = left operand after the noise swap)."""
+    return flatten(c1 @ c2, p)
+
+
+def hom_add_compact(p: Params, v1: np.ndarray, v2: np.ndarray) -> np.ndarray:
+    """recompose(C1 + C2) = (V1 + V2) mod q (recompose is linear; each V < q < 2^ell)."""
+    return np.mod(np.asarray(v1, dtype=np.int64) + np.asarray(v2, dtype=np.int64), p.q)
+
+
+def hom_mult_compact(p: Params, v1: np.ndarray, v2: np.ndarray) -> np.ndarray:
+    """recompose(C1 C2) = C1 V2 mod q = NOT(NAND(V1, V2)): (G - (G - P)) mod q = P mod q."""
+    return np.mod(bits_of(v1, p) @ np.asarray(v2, dtype=np.int64), p.q)
+
+
+def hom_const_mult_compact(p: Params, v: np.ndarray, k: int) -> np.ndarray:
+    """hom_mult with the left operand V_k = (k G) mod q (the scaled gadget, fhe.py:200-208)."""
+    return hom_mult_compact(p, gadget(p, k % p.q), v)

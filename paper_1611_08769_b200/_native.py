@@ -67,6 +67,9 @@ SIGNATURES = [
     ("fhegpu_prog_destroy", None, [_P]),
     ("fhegpu_nand_batch", ctypes.c_int, [_P, _U32P, _U32P, _U32P, ctypes.c_uint64]),
     ("fhegpu_not_batch", ctypes.c_int, [_P, _U32P, _U32P, ctypes.c_uint64]),
+    ("fhegpu_add_batch", ctypes.c_int, [_P, _U32P, _U32P, _U32P, ctypes.c_uint64]),
+    ("fhegpu_mult_batch", ctypes.c_int, [_P, _U32P, _U32P, _U32P, ctypes.c_uint64]),
+    ("fhegpu_const_mult_batch", ctypes.c_int, [_P, ctypes.c_uint32, _U32P, _U32P, ctypes.c_uint64]),
     ("fhegpu_debug_ws_trace", ctypes.c_int, [_U64P]),
     ("fhegpu_encrypt", ctypes.c_int, [_P, _U32P, _P, ctypes.c_uint32, _U32P, _U64P, _U32P, _U64P,
                                       ctypes.c_uint64]),
@@ -295,6 +298,32 @@ class DeviceContext:
                                    len(st), _ptr(idx, ctypes.c_uint32), _ptr(off, ctypes.c_uint64),
                                    _ptr(mus, ctypes.c_uint32), _ptr(tgt, ctypes.c_uint64), len(idx)),
                "encrypt")
+
+    def _binary(self, fn, name, v1, v2):
+        v1 = np.ascontiguousarray(v1, dtype=np.uint32)
+        v2 = np.ascontiguousarray(v2, dtype=np.uint32)
+        if v1.shape != v2.shape:
+            raise UsageError(f"{name}: operand batches differ in shape")
+        out = np.empty_like(v1)
+        _check(fn(self.handle, _ptr(v1, ctypes.c_uint32), _ptr(v2, ctypes.c_uint32),
+                  _ptr(out, ctypes.c_uint32), len(v1)), name)
+        return out
+
+    def add_batch(self, v1: np.ndarray, v2: np.ndarray) -> np.ndarray:
+        """(V1 + V2) mod q per pair (hom_add, fhe.py:352-356)."""
+        return self._binary(_lib.fhegpu_add_batch, "add_batch", v1, v2)
+
+    def mult_batch(self, v1: np.ndarray, v2: np.ndarray) -> np.ndarray:
+        """bits(V1) V2 mod q per pair (hom_mult, fhe.py:366-379; v1 = left after the swap)."""
+        return self._binary(_lib.fhegpu_mult_batch, "mult_batch", v1, v2)
+
+    def const_mult_batch(self, k: int, v: np.ndarray) -> np.ndarray:
+        """hom_const_mult (fhe.py:358-364) of every ciphertext by the public constant k."""
+        v = np.ascontiguousarray(v, dtype=np.uint32)
+        out = np.empty_like(v)
+        _check(_lib.fhegpu_const_mult_batch(self.handle, int(k) % self.params.q, _ptr(v, ctypes.c_uint32),
+                                            _ptr(out, ctypes.c_uint32), len(v)), "const_mult_batch")
+        return out
 
     def not_batch(self, v: np.ndarray) -> np.ndarray:
         v = np.ascontiguousarray(v, dtype=np.uint32)

@@ -713,41 +713,100 @@ void fhegpu_prog_destroy(fhegpu_prog *pr) {
   delete pr;
 }
 
-int fhegpu_nand_batch(fhegpu_ctx *c, const uint32_t *v1, const uint32_t *v2, uint32_t *out,
-                      uint64_t count) {
+namespace {
+
+// One level of `count` products bits(V1) * V2 through the level kernels.  shared_left: v1 is
+// ONE ciphertext used as every product's left operand.  ring: return C1 V2 mod q instead of
+// NAND's (G - C1 V2) mod q, as the complement of the NAND result (fhe.py:366-379).
+int product_batch(fhegpu_ctx *c, const uint32_t *v1, bool shared_left, const uint32_t *v2, uint32_t *out,
+                  uint64_t count, bool ring, const char *what) {
   if (!c || (count && (!v1 || !v2 || !out))) return fail(FHEGPU_EINVAL, "null argument");
   if (count == 0) return FHEGPU_OK;
   if (count >= (1u << 29)) return fail(FHEGPU_EINVAL, "batch too large");
   CUDA_TRY(cudaSetDevice(c->device));
-  const size_t ctb = (size_t)c->p.ct_words * 4;
+  const size_t ctb = (size_t)c->p.ct_words * 4, dense = (size_t)c->p.words * 4;
+  const uint64_t n_left = shared_left ? 1 : count;
+  const uint64_t right0 = n_left, out0 = n_left + count;
   uint32_t *buf = nullptr;
-  CUDA_TRY(cudaMalloc(&buf, 3 * count * ctb));
+  CUDA_TRY(cudaMalloc(&buf, (out0 + count) * ctb));
   std::vector<OpRec> ops(count);
   for (uint64_t i = 0; i < count; ++i)
-    ops[i] = OpRec{(uint32_t)i, (uint32_t)(count + i), (uint32_t)(2 * count + i), 0u};
+    ops[i] = OpRec{(uint32_t)(shared_left ? 0 : i), (uint32_t)(right0 + i), (uint32_t)(out0 + i), 0u};
   int rc = ensure((void **)&c->d_tmp_ops, &c->tmp_ops_cap, count * sizeof(OpRec));
   cudaError_t e = cudaSuccess;
   if (!rc) {
     // dense host rows -> padded device ciphertexts
-    e = cudaMemset2DAsync(buf, ctb, 0, ctb, 3 * count, c->stream);
+    e = cudaMemset2DAsync(buf, ctb, 0, ctb, out0 + count, c->stream);
     if (e == cudaSuccess)
-      e = cudaMemcpy2DAsync(buf, ctb, v1, (size_t)c->p.words * 4, (size_t)c->p.words * 4, count,
+      e = cudaMemcpy2DAsync(buf, ctb, v1, dense, dense, n_left, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(buf + right0 * c->p.ct_words, ctb, v2, dense, dense, count,
                             cudaMemcpyHostToDevice, c->stream);
-    if (e == cudaSuccess)
-      e = cudaMemcpy2DAsync(buf + count * c->p.ct_words, ctb, v2, (size_t)c->p.words * 4,
-                            (size_t)c->p.words * 4, count, cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(c->d_tmp_ops, ops.data(), count * sizeof(OpRec), cudaMemcpyHostToDevice,
                           c->stream);
     if (e == cudaSuccess) rc = launch_level(c, buf, c->d_tmp_ops, (uint32_t)count, 1);
+    if (e == cudaSuccess && !rc && ring) {
+      complement_rows_kernel<<<grid_for(count * c->p.words, c->num_sms), 256, 0, c->stream>>>(
+          buf + out0 * c->p.ct_words, count, c->p);
+      e = cudaGetLastError();
+    }
     if (e == cudaSuccess && !rc)
-      e = cudaMemcpy2DAsync(out, (size_t)c->p.words * 4, buf + 2 * count * c->p.ct_words, ctb,
-                            (size_t)c->p.words * 4, count, cudaMemcpyDeviceToHost, c->stream);
+      e = cudaMemcpy2DAsync(out, dense, buf + out0 * c->p.ct_words, ctb, dense, count,
+                            cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess && !rc) e = cudaStreamSynchronize(c->stream);
   }
   cudaFree(buf);
   if (rc) return rc;
-  if (e != cudaSuccess) return fail(FHEGPU_ECUDA, std::string("nand_batch: ") + cudaGetErrorString(e));
+  if (e != cudaSuccess) return fail(FHEGPU_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return FHEGPU_OK;
+}
+
+}  // namespace
+
+int fhegpu_nand_batch(fhegpu_ctx *c, const uint32_t *v1, const uint32_t *v2, uint32_t *out,
+                      uint64_t count) {
+  return product_batch(c, v1, false, v2, out, count, false, "nand_batch");
+}
+
+int fhegpu_mult_batch(fhegpu_ctx *c, const uint32_t *v1, const uint32_t *v2, uint32_t *out,
+                      uint64_t count) {
+  return product_batch(c, v1, false, v2, out, count, true, "mult_batch");
+}
+
+int fhegpu_const_mult_batch(fhegpu_ctx *c, uint32_t k, const uint32_t *v, uint32_t *out, uint64_t count) {
+  if (!c) return fail(FHEGPU_EINVAL, "null ctx");
+  // left operand V_k = (k G) mod q: (k 2^j mod q) at row i*ell+j, column i (fhe.py:200-208)
+  const uint32_t q = c->p.q, kk = k % q;
+  std::vector<uint32_t> vk((size_t)c->p.words, 0u);
+  for (uint32_t r = 0; r < c->p.rows; ++r) {
+    const uint32_t i = r / c->p.ell, j = r % c->p.ell;
+    vk[(size_t)r * c->p.k + i] = (uint32_t)(((uint64_t)kk << j) % q);
+  }
+  return product_batch(c, vk.data(), true, v, out, count, true, "const_mult_batch");
+}
+
+int fhegpu_add_batch(fhegpu_ctx *c, const uint32_t *v1, const uint32_t *v2, uint32_t *out,
+                     uint64_t count) {
+  if (!c || (count && (!v1 || !v2 || !out))) return fail(FHEGPU_EINVAL, "null argument");
+  if (count == 0) return FHEGPU_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t per = (size_t)c->p.words * 4;
+  uint32_t *buf = nullptr;
+  CUDA_TRY(cudaMalloc(&buf, 3 * count * per));
+  cudaError_t e = cudaMemcpyAsync(buf, v1, count * per, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(buf + count * c->p.words, v2, count * per, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) {
+    add_kernel<<<grid_for(count * c->p.words, c->num_sms), 256, 0, c->stream>>>(
+        buf, buf + count * c->p.words, buf + 2 * count * c->p.words, count, c->p);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out, buf + 2 * count * c->p.words, count * per, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(buf);
+  if (e != cudaSuccess) return fail(FHEGPU_ECUDA, std::string("add_batch: ") + cudaGetErrorString(e));
   return FHEGPU_OK;
 }
 

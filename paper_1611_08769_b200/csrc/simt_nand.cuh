@@ -77,6 +77,30 @@ __global__ void complement_kernel(const uint32_t *__restrict__ in, uint32_t *__r
   }
 }
 
+// hom_add in compact form (fhe.py:352-356): out = (a + b) mod q, dense rows of p.words.
+__global__ void add_kernel(const uint32_t *__restrict__ a, const uint32_t *__restrict__ b,
+                           uint32_t *__restrict__ out, uint64_t count, DevParams p) {
+  const uint64_t total = count * p.words;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = a[t] + b[t];               // both < q < 2^31
+    out[t] = x >= p.q ? x - p.q : x;
+  }
+}
+
+// In-place complement of padded store rows: v <- (G - v) mod q.
+__global__ void complement_rows_kernel(uint32_t *__restrict__ rows, uint64_t count, DevParams p) {
+  const uint64_t total = count * p.words;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = t / p.words;
+    const uint32_t w = (uint32_t)(t - c * p.words);
+    const uint32_t r = w / p.k, i = w - r * p.k;
+    uint32_t *v = rows + c * p.ct_words + w;
+    *v = sub_mod(gadget(p, r, i), *v, p.q);
+  }
+}
+
 // store[idx[c]] <- dense[c] (zero the padding words).
 __global__ void scatter_kernel(uint32_t *__restrict__ store, const uint64_t *__restrict__ idx,
                                const uint32_t *__restrict__ dense, uint64_t count, DevParams p) {

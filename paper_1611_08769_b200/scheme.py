@@ -369,3 +369,53 @@ class GswScheme:
         """flatten(I - C) = (G - V) mod q; level and noise unchanged (fhe.py:343-350)."""
         out = self.ctx.not_batch(np.asarray(ct.v)[None])[0]
         return Ciphertext(out, ct.level, ct.noise_est, self.params)
+
+    # -- Z_q ring operations (fhe.py:352-379), on the GPU ----------------------------------
+
+    def add_meta(self, ct1: Ciphertext, ct2: Ciphertext):
+        """fhe.py:354-356: level = max, est = min(e1 + e2, q) -> (level, est)."""
+        return max(ct1.level, ct2.level), min(ct1.noise_est + ct2.noise_est, self.params.q)
+
+    def mult_meta(self, ct1: Ciphertext, ct2: Ciphertext):
+        """fhe.py:374-379: noisier operand left, est = min(e1 + N e2, q), level = max (no depth
+        check, unlike hom_nand) -> (left, right, level, est)."""
+        p = self.params
+        if ct2.noise_est > ct1.noise_est:
+            ct1, ct2 = ct2, ct1
+        est = min(ct1.noise_est + p.n_ct * ct2.noise_est, p.q)
+        return ct1, ct2, max(ct1.level, ct2.level), est
+
+    def hom_add(self, ct1: Ciphertext, ct2: Ciphertext) -> Ciphertext:
+        """Encrypts (m1 + m2) mod q: flatten(C1 + C2) = (V1 + V2) mod q (fhe.py:352-356)."""
+        return self.hom_add_many([(ct1, ct2)])[0]
+
+    def hom_add_many(self, pairs) -> list[Ciphertext]:
+        if not pairs:
+            return []
+        out = self.ctx.add_batch(np.stack([np.asarray(a.v) for a, _ in pairs]),
+                                 np.stack([np.asarray(b.v) for _, b in pairs]))
+        return [Ciphertext(o, *self.add_meta(a, b), self.params) for o, (a, b) in zip(out, pairs)]
+
+    def hom_const_mult(self, ct: Ciphertext, k: int) -> Ciphertext:
+        """Encrypts (k m) mod q: flatten(decompose(kG mod q) C) (fhe.py:358-364)."""
+        return self.hom_const_mult_many([ct], k)[0]
+
+    def hom_const_mult_many(self, cts, k: int) -> list[Ciphertext]:
+        """Every ciphertext times the same public constant k (one launch)."""
+        if not cts:
+            return []
+        p = self.params
+        out = self.ctx.const_mult_batch(int(k) % p.q, np.stack([np.asarray(c.v) for c in cts]))
+        return [Ciphertext(o, c.level, min(p.n_ct * c.noise_est, p.q), p) for o, c in zip(out, cts)]
+
+    def hom_mult(self, ct1: Ciphertext, ct2: Ciphertext) -> Ciphertext:
+        """Encrypts (m1 m2) mod q: flatten(C1 C2) = bits(V1) V2 mod q (fhe.py:366-379)."""
+        return self.hom_mult_many([(ct1, ct2)])[0]
+
+    def hom_mult_many(self, pairs) -> list[Ciphertext]:
+        metas = [self.mult_meta(a, b) for a, b in pairs]
+        if not metas:
+            return []
+        out = self.ctx.mult_batch(np.stack([np.asarray(m[0].v) for m in metas]),
+                                  np.stack([np.asarray(m[1].v) for m in metas]))
+        return [Ciphertext(o, m[2], m[3], self.params) for o, m in zip(out, metas)]

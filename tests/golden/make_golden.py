@@ -8,6 +8,7 @@ outputs travel instead):
     python tests/golden/make_golden.py trace cfg0    # op sequences (any cfg)
     python tests/golden/make_golden.py cts cfg0      # per-gate ciphertext digests
     python tests/golden/make_golden.py clear cfg4    # decrypted outputs (cleartext engine)
+    python tests/golden/make_golden.py ring          # Z_q ring ops (hom_add / const_mult / mult)
 
 The reference is instrumented, never modified: the methods of one
 ``GswScheme`` instance are wrapped so that every ciphertext the reference
@@ -404,6 +405,49 @@ def cmd_eft1():
     print("eft1 ok", server.nand_count)
 
 
+def cmd_ring():
+    """Z_q ring operations hom_add / hom_const_mult / hom_mult (fhe.py:352-379) as the
+    reference computes them, with fresh and non-fresh (swapped, leveled) operands."""
+    out = {}
+    for name, params in (("exact", EXACT_PARAMS), ("default", DEFAULT_PARAMS)):
+        scheme = GswScheme(params)
+        keys = scheme.keygen(seed=5)
+        rng = np.random.default_rng(11)
+        q = params.q
+        msgs = [3, 5, int(rng.integers(0, q)), int(rng.integers(0, 2 ** 7))]
+        cts = [scheme.encrypt_value(keys.public_key, m, rng) for m in msgs]
+        bits = [scheme.encrypt_bit(keys.public_key, b, rng) for b in (1, 0)]
+        nb = scheme.hom_nand(bits[0], bits[1])              # level 1, noisy
+        k_vals = [0, 1, 7, q - 1, int(rng.integers(0, q)), -3]
+        k, ell = params.n + 1, params.ell
+        comp = lambda c: compact_from_matrix(c.matrix, k, ell)  # noqa: E731
+        arrays = {f"ct{i}": comp(c) for i, c in enumerate(cts)}
+        arrays["b0"], arrays["b1"], arrays["nb"] = comp(bits[0]), comp(bits[1]), comp(nb)
+        results = {
+            "add01": scheme.hom_add(cts[0], cts[1]),
+            "add23": scheme.hom_add(cts[2], cts[3]),
+            "add_nb": scheme.hom_add(nb, bits[0]),
+            "mult03": scheme.hom_mult(cts[0], cts[3]),
+            "mult_b_nb": scheme.hom_mult(bits[1], nb),      # nb noisier => swapped
+            "mult_nb_b": scheme.hom_mult(nb, bits[0]),
+        }
+        for i, kv in enumerate(k_vals):
+            results[f"cmult{i}"] = scheme.hom_const_mult(cts[2] if i % 2 else nb, kv)
+        meta = {"params": [params.n, q, params.m, params.noise_bound, params.depth_budget],
+                "msgs": msgs, "k_vals": k_vals, "nb_level": nb.level, "nb_noise": nb.noise_est,
+                "fresh_noise": cts[0].noise_est, "results": {}}
+        for nm, c in results.items():
+            arrays[nm] = comp(c)
+            meta["results"][nm] = {"level": c.level, "noise_est": c.noise_est}
+        meta["decrypt"] = {"add01": scheme.decrypt_value(keys.secret_key, results["add01"]),
+                           "mult03": scheme.decrypt_value(keys.secret_key, results["mult03"])}
+        out[name] = meta
+        np.savez_compressed(os.path.join(HERE, f"ring_{name}.npz"),
+                            **{k2: np.asarray(v) for k2, v in arrays.items()})
+    save_json("ring_kat.json", out)
+    print(json.dumps(out)[:400])
+
+
 if __name__ == "__main__":
     cmd = sys.argv[1]
     if cmd == "scheme":
@@ -416,5 +460,7 @@ if __name__ == "__main__":
         cmd_clear(sys.argv[2])
     elif cmd == "eft1":
         cmd_eft1()
+    elif cmd == "ring":
+        cmd_ring()
     else:
         raise SystemExit(__doc__)

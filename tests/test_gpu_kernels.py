@@ -190,3 +190,48 @@ def test_store_packed_io_matches_reference_serialisation(params):
     back = np.empty_like(packed)
     ctx.read_packed(400, len(v), back.ctypes.data)
     assert np.array_equal(back, packed)
+
+
+@pytest.mark.parametrize("name,params", [("default", DEFAULT_PARAMS), ("exact", EXACT_PARAMS)])
+def test_ring_ops_reproduce_reference_ciphertexts(name, params):
+    """GPU hom_add / hom_const_mult / hom_mult == the reference's ciphertexts (fhe.py:352-379)."""
+    from paper_1611_08769_b200 import Ciphertext
+    meta = golden_json("ring_kat.json")[name]
+    z = golden_npz(f"ring_{name}.npz")
+    s = GswScheme(params)
+    fresh = lambda v: Ciphertext(v, 0, meta["fresh_noise"], params)          # noqa: E731
+    ct = [fresh(z[f"ct{i}"]) for i in range(4)]
+    b0, b1 = fresh(z["b0"]), fresh(z["b1"])
+    nb = Ciphertext(z["nb"], meta["nb_level"], meta["nb_noise"], params)
+    got = {"add01": s.hom_add(ct[0], ct[1]), "add23": s.hom_add(ct[2], ct[3]),
+           "add_nb": s.hom_add(nb, b0), "mult03": s.hom_mult(ct[0], ct[3]),
+           "mult_b_nb": s.hom_mult(b1, nb), "mult_nb_b": s.hom_mult(nb, b0)}
+    for i, k in enumerate(meta["k_vals"]):
+        got[f"cmult{i}"] = s.hom_const_mult(ct[2] if i % 2 else nb, k)
+    for key, c in got.items():
+        assert np.array_equal(c.v, z[key]), key
+        assert (c.level, c.noise_est) == (meta["results"][key]["level"], meta["results"][key]["noise_est"]), key
+
+
+def test_ring_ops_match_ring_oracle_like_reference_tests():
+    """The reference's own ring tests (tests/test_fhe.py:134-172), on the GPU operators."""
+    s = GswScheme(DEFAULT_PARAMS)
+    keys = s.keygen(1)
+    pk, sk = keys.public_key, keys.secret_key
+    rng = np.random.default_rng(3)
+    q = DEFAULT_PARAMS.q
+    assert s.decrypt_value(sk, s.hom_add(s.encrypt_value(pk, 3, rng), s.encrypt_value(pk, 5, rng))) == 8
+    m1, m2 = rng.integers(0, q, 40), rng.integers(0, q, 40)
+    outs = s.hom_add_many([(s.encrypt_value(pk, int(a), rng), s.encrypt_value(pk, int(b), rng))
+                           for a, b in zip(m1, m2)])
+    assert [s.decrypt_value(sk, c) for c in outs] == [int((a + b) % q) for a, b in zip(m1, m2)]
+    ct = s.encrypt_value(pk, 12345, rng)
+    assert s.decrypt_value(sk, s.hom_const_mult(ct, 0)) == 0
+    for _ in range(10):
+        m, k = int(rng.integers(0, q)), int(rng.integers(0, q))
+        out = s.hom_const_mult(s.encrypt_value(pk, m, rng), k)
+        assert s.decrypt_value(sk, out) == (m * k) % q
+    m1, m2 = rng.integers(0, 2 ** 15, 40), rng.integers(0, 2 ** 15, 40)
+    outs = s.hom_mult_many([(s.encrypt_value(pk, int(a), rng), s.encrypt_value(pk, int(b), rng))
+                            for a, b in zip(m1, m2)])
+    assert [s.decrypt_value(sk, c) for c in outs] == [int((a * b) % q) for a, b in zip(m1, m2)]

@@ -120,3 +120,38 @@ def test_integer_model_matches_reference_fhe_outputs():
     """cfg0's decrypted FHE outputs (real reference run) equal the model's words."""
     got = model_outputs("cfg0", config_signal("cfg0")[1][None])[0]
     assert got.tolist() == golden_json("cts_cfg0.json")["output_words"]
+
+
+def _ring_cases(p, z):
+    """(result name, op, operands in the order the reference call passed them)."""
+    return [("add01", "add", z["ct0"], z["ct1"]), ("add23", "add", z["ct2"], z["ct3"]),
+             ("add_nb", "add", z["nb"], z["b0"]), ("mult03", "mult", z["ct0"], z["ct3"]),
+             ("mult_b_nb", "mult", z["b1"], z["nb"]), ("mult_nb_b", "mult", z["nb"], z["b0"])]
+
+
+@pytest.mark.parametrize("name", ["exact", "default"])
+def test_oracle_ring_ops_known_answers(name):
+    """hom_add / hom_const_mult / hom_mult (fhe.py:352-379): the compact identities and the
+    restated matrix algorithm both reproduce the reference's ciphertexts bit for bit."""
+    meta = golden_json("ring_kat.json")[name]
+    z = golden_npz(f"ring_{name}.npz")
+    p = gsw.EXACT if name == "exact" else gsw.DEFAULT
+    for res, op, a, b in _ring_cases(p, z):
+        if op == "add":
+            got = gsw.hom_add_compact(p, a, b)
+            mat = gsw.hom_add_matrix(p, gsw.bits_of(a, p).astype(float), gsw.bits_of(b, p).astype(float))
+        else:
+            left, right = a, b
+            # the reference swaps when the right operand is noisier (fhe.py:374-375)
+            if res == "mult_b_nb" and meta["nb_noise"] > meta["fresh_noise"]:
+                left, right = b, a
+            got = gsw.hom_mult_compact(p, left, right)
+            mat = gsw.hom_mult_matrix(p, gsw.bits_of(left, p).astype(float), gsw.bits_of(right, p).astype(float))
+        assert np.array_equal(got, z[res]), res
+        assert np.array_equal(gsw.bits_of(got, p), mat), res
+    for i, k in enumerate(meta["k_vals"]):
+        src = z["ct2"] if i % 2 else z["nb"]
+        got = gsw.hom_const_mult_compact(p, src, k)
+        assert np.array_equal(got, z[f"cmult{i}"]), k
+        mat = gsw.hom_const_mult_matrix(p, gsw.bits_of(src, p).astype(float), k)
+        assert np.array_equal(gsw.bits_of(got, p), mat), k

@@ -69,3 +69,26 @@ def test_depth_budget_error_message():
         x = eng.nand(x, x)
     with pytest.raises(NoiseOverflowError, match="NAND at level 4 would exceed depth budget 3"):
         eng.nand(x, x)
+
+
+@pytest.mark.parametrize("name", ["exact", "default"])
+def test_ring_op_levels_and_noise_like_reference(name):
+    """hom_add / hom_const_mult / hom_mult bookkeeping (fhe.py:352-379) vs the reference's
+    recorded levels and noise estimates (host logic only; no device)."""
+    from tests.helpers import golden_json
+    meta = golden_json("ring_kat.json")[name]
+    params = EXACT_PARAMS if name == "exact" else DEFAULT_PARAMS
+    s = GswScheme(params)
+    z = np.zeros((params.n_ct, params.k), dtype=np.uint32)
+    fresh = Ciphertext(z, 0, meta["fresh_noise"], params)
+    nb = Ciphertext(z, meta["nb_level"], meta["nb_noise"], params)
+    r = meta["results"]
+    assert list(s.add_meta(fresh, fresh)) == [r["add01"]["level"], r["add01"]["noise_est"]]
+    assert list(s.add_meta(nb, fresh)) == [r["add_nb"]["level"], r["add_nb"]["noise_est"]]
+    for key, a, b in (("mult03", fresh, fresh), ("mult_b_nb", fresh, nb), ("mult_nb_b", nb, fresh)):
+        _, _, level, est = s.mult_meta(a, b)
+        assert (level, est) == (r[key]["level"], r[key]["noise_est"]), key
+    for i in range(len(meta["k_vals"])):
+        src = fresh if i % 2 else nb
+        assert r[f"cmult{i}"]["level"] == src.level
+        assert r[f"cmult{i}"]["noise_est"] == min(params.n_ct * src.noise_est, params.q)
