@@ -192,6 +192,22 @@ int fhegpu_encrypt(fhegpu_ctx *ctx, const uint32_t *pk, const fhegpu_pcg64 *stre
 /* Debug only: timeline probe of the pipelined kernel (64 gates x 16 events, clock64). */
 int fhegpu_debug_ws_trace(uint64_t *host_out);
 
+/* -- Bitsliced cleartext engine (replaces CleartextEngine's evaluation, engine.py:69-121) --
+ * A wire is `lanes` plaintext bits packed 32 per u32 word (bit l of word w = lane 32w + l);
+ * NAND = ~(a & b) on whole words, complement flags as in fhegpu_op.  Used for the
+ * reference's error experiments (harness.py:122-198) at GPU scale.  Slots are wire indices. */
+typedef struct fhegpu_bits fhegpu_bits;
+int fhegpu_bits_create(int device, uint64_t lanes, fhegpu_bits **out);
+void fhegpu_bits_destroy(fhegpu_bits *bits);
+uint32_t fhegpu_bits_words(const fhegpu_bits *bits);       /* u32 words per wire */
+int fhegpu_bits_reserve(fhegpu_bits *bits, uint64_t wires); /* grows, keeps contents */
+int fhegpu_bits_write(fhegpu_bits *bits, const uint64_t *slots, uint64_t count, const uint32_t *words);
+/* One launch per level (levels as in fhegpu_prog_create); synchronous. */
+int fhegpu_bits_run(fhegpu_bits *bits, const fhegpu_op *ops, uint64_t n_ops,
+                    const uint64_t *level_offsets, uint32_t n_levels);
+int fhegpu_bits_read(fhegpu_bits *bits, const uint64_t *slots, const uint8_t *complement,
+                     uint64_t count, uint32_t *words);
+
 #ifdef __cplusplus
 }
 #endif

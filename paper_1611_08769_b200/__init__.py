@@ -11,6 +11,7 @@ declared in ``include/fhegpu.h``.
 from .arith import (FixedFormat, FixedWord, add, bits_to_int, constant_word, decode, encode,
                     encode_int, full_adder, half_adder, input_word, int_to_bits, mul_const,
                     mul_fixed, mul_integer, read_word, sub)
+from .clear import GpuClearEngine
 from .engine import GateStats, GpuBit, GpuEngine
 from .errors import (CapabilityError, DeviceError, FhefftError, NoiseOverflowError,
                      ParameterError, ParseError, RangeError, UsageError)

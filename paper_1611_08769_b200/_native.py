@@ -67,6 +67,13 @@ SIGNATURES = [
     ("fhegpu_prog_destroy", None, [_P]),
     ("fhegpu_nand_batch", ctypes.c_int, [_P, _U32P, _U32P, _U32P, ctypes.c_uint64]),
     ("fhegpu_not_batch", ctypes.c_int, [_P, _U32P, _U32P, ctypes.c_uint64]),
+    ("fhegpu_bits_create", ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
+    ("fhegpu_bits_destroy", None, [_P]),
+    ("fhegpu_bits_words", ctypes.c_uint32, [_P]),
+    ("fhegpu_bits_reserve", ctypes.c_int, [_P, ctypes.c_uint64]),
+    ("fhegpu_bits_write", ctypes.c_int, [_P, _U64P, ctypes.c_uint64, _U32P]),
+    ("fhegpu_bits_run", ctypes.c_int, [_P, _P, ctypes.c_uint64, _U64P, ctypes.c_uint32]),
+    ("fhegpu_bits_read", ctypes.c_int, [_P, _U64P, _P, ctypes.c_uint64, _U32P]),
     ("fhegpu_add_batch", ctypes.c_int, [_P, _U32P, _U32P, _U32P, ctypes.c_uint64]),
     ("fhegpu_mult_batch", ctypes.c_int, [_P, _U32P, _U32P, _U32P, ctypes.c_uint64]),
     ("fhegpu_const_mult_batch", ctypes.c_int, [_P, ctypes.c_uint32, _U32P, _U32P, ctypes.c_uint64]),
@@ -331,3 +338,47 @@ class DeviceContext:
         _check(_lib.fhegpu_not_batch(self.handle, _ptr(v, ctypes.c_uint32), _ptr(out, ctypes.c_uint32),
                                      len(v)), "not_batch")
         return out
+
+
+class BitsContext:
+    """fhegpu_bits: device wire store of the bitsliced cleartext engine (lanes packed 32/word)."""
+
+    def __init__(self, lanes: int, device: int = 0):
+        lib = load_library()
+        h = ctypes.c_void_p()
+        _check(lib.fhegpu_bits_create(int(device), int(lanes), ctypes.byref(h)), "bits_create")
+        self.handle = h.value
+        self.lanes = int(lanes)
+        self.words = int(lib.fhegpu_bits_words(self.handle))
+
+    def reserve(self, wires: int):
+        _check(_lib.fhegpu_bits_reserve(self.handle, int(wires)), "bits_reserve")
+
+    def write(self, slots, words: np.ndarray):
+        slots = np.ascontiguousarray(slots, dtype=np.uint64)
+        words = np.ascontiguousarray(words, dtype=np.uint32)
+        if words.shape != (len(slots), self.words):
+            raise UsageError(f"expected ({len(slots)}, {self.words}) words")
+        _check(_lib.fhegpu_bits_write(self.handle, _ptr(slots, ctypes.c_uint64), len(slots),
+                                      _ptr(words, ctypes.c_uint32)), "bits_write")
+
+    def run(self, ops: np.ndarray, level_offsets):
+        ops = np.ascontiguousarray(ops)
+        offs = np.ascontiguousarray(level_offsets, dtype=np.uint64)
+        _check(_lib.fhegpu_bits_run(self.handle, ops.ctypes.data_as(ctypes.c_void_p), len(ops),
+                                    _ptr(offs, ctypes.c_uint64), len(offs) - 1), "bits_run")
+
+    def read(self, slots, complement=None) -> np.ndarray:
+        slots = np.ascontiguousarray(slots, dtype=np.uint64)
+        out = np.empty((len(slots), self.words), dtype=np.uint32)
+        comp = None if complement is None else np.ascontiguousarray(complement, dtype=np.uint8)
+        _check(_lib.fhegpu_bits_read(self.handle, _ptr(slots, ctypes.c_uint64),
+                                     None if comp is None else comp.ctypes.data_as(ctypes.c_void_p),
+                                     len(slots), _ptr(out, ctypes.c_uint32)), "bits_read")
+        return out
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and _lib is not None:
+            _lib.fhegpu_bits_destroy(h)
+            self.handle = None

@@ -18,6 +18,7 @@
 #include "tc_nand.cuh"
 #include "tc_nand_ws.cuh"
 #include "encrypt.cuh"
+#include "bits.cuh"
 
 using namespace fhegpu;
 
@@ -895,6 +896,157 @@ int fhegpu_encrypt(fhegpu_ctx *c, const uint32_t *pk, const fhegpu_pcg64 *stream
 int fhegpu_debug_ws_trace(uint64_t *host) {
   if (!host) return fail(FHEGPU_EINVAL, "null argument");
   CUDA_TRY(cudaMemcpyFromSymbol(host, tc::g_ws_trace, sizeof(uint64_t) * 64 * 16));
+  return FHEGPU_OK;
+}
+
+// -- bitsliced cleartext engine (CleartextEngine twin, engine.py:69-121) -----------------------
+
+struct fhegpu_bits {
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t lanes = 0;
+  uint32_t words = 0;        // u32 words per wire
+  uint32_t tail_mask = 0;    // valid lane bits of the last word
+  uint32_t *store = nullptr;
+  uint64_t capacity = 0;     // wires
+  OpRec *d_ops = nullptr;
+  size_t ops_cap = 0;
+  uint64_t *d_slots = nullptr;
+  size_t slots_cap = 0;
+  uint32_t *d_io = nullptr;
+  size_t io_cap = 0;
+  uint8_t *d_comp = nullptr;
+  size_t comp_cap = 0;
+};
+
+int fhegpu_bits_create(int device, uint64_t lanes, fhegpu_bits **out) {
+  if (!out) return fail(FHEGPU_EINVAL, "null argument");
+  *out = nullptr;
+  if (lanes == 0 || lanes > (uint64_t(1) << 36)) return fail(FHEGPU_EINVAL, "lanes must be in [1, 2^36]");
+  CUDA_TRY(cudaSetDevice(device));
+  auto *b = new fhegpu_bits();
+  b->device = device;
+  b->lanes = lanes;
+  b->words = (uint32_t)((lanes + 31) / 32);
+  b->tail_mask = (lanes % 32) ? ((1u << (lanes % 32)) - 1u) : 0xFFFFFFFFu;
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete b;
+    return fail(FHEGPU_ECUDA, std::string("bits_create: ") + cudaGetErrorString(e));
+  }
+  b->num_sms = prop.multiProcessorCount;
+  *out = b;
+  return FHEGPU_OK;
+}
+
+void fhegpu_bits_destroy(fhegpu_bits *b) {
+  if (!b) return;
+  cudaSetDevice(b->device);
+  cudaStreamSynchronize(b->stream);
+  cudaFree(b->store);
+  cudaFree(b->d_ops);
+  cudaFree(b->d_slots);
+  cudaFree(b->d_io);
+  cudaFree(b->d_comp);
+  cudaStreamDestroy(b->stream);
+  delete b;
+}
+
+uint32_t fhegpu_bits_words(const fhegpu_bits *b) { return b ? b->words : 0; }
+
+int fhegpu_bits_reserve(fhegpu_bits *b, uint64_t wires) {
+  if (!b) return fail(FHEGPU_EINVAL, "null handle");
+  if (wires <= b->capacity) return FHEGPU_OK;
+  CUDA_TRY(cudaSetDevice(b->device));
+  uint32_t *nw = nullptr;
+  const size_t bytes = (size_t)wires * b->words * 4;
+  if (cudaMalloc(&nw, bytes) != cudaSuccess) return fail(FHEGPU_ENOMEM, "bits_reserve: out of device memory");
+  cudaError_t e = cudaMemsetAsync(nw, 0, bytes, b->stream);
+  if (e == cudaSuccess && b->store)
+    e = cudaMemcpyAsync(nw, b->store, b->capacity * b->words * 4, cudaMemcpyDeviceToDevice, b->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(b->stream);
+  if (e != cudaSuccess) {
+    cudaFree(nw);
+    return fail(FHEGPU_ECUDA, std::string("bits_reserve: ") + cudaGetErrorString(e));
+  }
+  cudaFree(b->store);
+  b->store = nw;
+  b->capacity = wires;
+  return FHEGPU_OK;
+}
+
+static int bits_check_slots(fhegpu_bits *b, const uint64_t *slots, uint64_t count) {
+  for (uint64_t i = 0; i < count; ++i)
+    if (slots[i] >= b->capacity) return fail(FHEGPU_EINVAL, "wire slot beyond capacity");
+  return FHEGPU_OK;
+}
+
+int fhegpu_bits_write(fhegpu_bits *b, const uint64_t *slots, uint64_t count, const uint32_t *words) {
+  if (!b || (count && (!slots || !words))) return fail(FHEGPU_EINVAL, "null argument");
+  if (count == 0) return FHEGPU_OK;
+  if (int rc = bits_check_slots(b, slots, count)) return rc;
+  CUDA_TRY(cudaSetDevice(b->device));
+  const size_t bytes = (size_t)count * b->words * 4;
+  if (int rc = ensure((void **)&b->d_io, &b->io_cap, bytes)) return rc;
+  if (int rc = ensure((void **)&b->d_slots, &b->slots_cap, count * 8)) return rc;
+  CUDA_TRY(cudaMemcpyAsync(b->d_io, words, bytes, cudaMemcpyHostToDevice, b->stream));
+  CUDA_TRY(cudaMemcpyAsync(b->d_slots, slots, count * 8, cudaMemcpyHostToDevice, b->stream));
+  bits_scatter_kernel<<<grid_for(count * b->words, b->num_sms), 256, 0, b->stream>>>(b->store, b->d_slots,
+                                                                                   b->d_io, count, b->words);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(b->stream));
+  return FHEGPU_OK;
+}
+
+int fhegpu_bits_run(fhegpu_bits *b, const fhegpu_op *ops, uint64_t n_ops, const uint64_t *level_offsets,
+                    uint32_t n_levels) {
+  if (!b || (n_ops && !ops) || !level_offsets) return fail(FHEGPU_EINVAL, "null argument");
+  if (level_offsets[0] != 0 || level_offsets[n_levels] != n_ops)
+    return fail(FHEGPU_EINVAL, "level offsets must span [0, n_ops]");
+  for (uint64_t i = 0; i < n_ops; ++i) {
+    const uint64_t mx = std::max(ops[i].left, std::max(ops[i].right, ops[i].out));
+    if (mx >= b->capacity || (ops[i].flags & ~3u)) return fail(FHEGPU_EINVAL, "bad op record " + std::to_string(i));
+  }
+  if (n_ops == 0) return FHEGPU_OK;
+  CUDA_TRY(cudaSetDevice(b->device));
+  if (int rc = ensure((void **)&b->d_ops, &b->ops_cap, n_ops * sizeof(OpRec))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(b->d_ops, ops, n_ops * sizeof(OpRec), cudaMemcpyHostToDevice, b->stream));
+  for (uint32_t l = 0; l < n_levels; ++l) {
+    const uint64_t a = level_offsets[l], e = level_offsets[l + 1];
+    if (e <= a) continue;
+    const uint32_t n = (uint32_t)(e - a);
+    bits_level_kernel<<<grid_for((uint64_t)n * b->words, b->num_sms), 256, 0, b->stream>>>(
+        b->store, b->d_ops + a, n, b->words, b->tail_mask);
+  }
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(b->stream));   // the op table is reused by the next call
+  return FHEGPU_OK;
+}
+
+int fhegpu_bits_read(fhegpu_bits *b, const uint64_t *slots, const uint8_t *comp, uint64_t count,
+                     uint32_t *words) {
+  if (!b || (count && (!slots || !words))) return fail(FHEGPU_EINVAL, "null argument");
+  if (count == 0) return FHEGPU_OK;
+  if (int rc = bits_check_slots(b, slots, count)) return rc;
+  CUDA_TRY(cudaSetDevice(b->device));
+  const size_t bytes = (size_t)count * b->words * 4;
+  if (int rc = ensure((void **)&b->d_io, &b->io_cap, bytes)) return rc;
+  if (int rc = ensure((void **)&b->d_slots, &b->slots_cap, count * 8)) return rc;
+  CUDA_TRY(cudaMemcpyAsync(b->d_slots, slots, count * 8, cudaMemcpyHostToDevice, b->stream));
+  const uint8_t *dcomp = nullptr;
+  if (comp) {
+    if (int rc = ensure((void **)&b->d_comp, &b->comp_cap, count)) return rc;
+    CUDA_TRY(cudaMemcpyAsync(b->d_comp, comp, count, cudaMemcpyHostToDevice, b->stream));
+    dcomp = b->d_comp;
+  }
+  bits_gather_kernel<<<grid_for(count * b->words, b->num_sms), 256, 0, b->stream>>>(
+      b->store, b->d_slots, dcomp, b->d_io, count, b->words, b->tail_mask);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(words, b->d_io, bytes, cudaMemcpyDeviceToHost, b->stream));
+  CUDA_TRY(cudaStreamSynchronize(b->stream));
   return FHEGPU_OK;
 }
 

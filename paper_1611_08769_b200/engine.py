@@ -72,7 +72,114 @@ class GpuBit:
         return None if self.const else self.engine.export_ct(self)
 
 
-class GpuEngine:
+class LevelledNetlist:
+    """Lazy netlist recorder shared by the GPU engines: node tables (level, noise estimate,
+    slot, live-handle refcount), pending gates, and the level sort + liveness slot allocation
+    that turns them into one launch per level."""
+
+    def _init_netlist(self, keep_all: bool = False):
+        self.keep_all = keep_all
+        self._wire = 0
+        self._level: list[int] = []
+        self._est: list[int] = []
+        self._slot: list[int] = []
+        self._refs: list[int] = []
+        self._pending_ops: list[int] = []       # flat: left, lneg, right, rneg, out
+        self._free: list[int] = []
+        self._n_slots = 0
+
+    def _new_wire(self) -> int:
+        w = self._wire
+        self._wire += 1
+        return w
+
+    def _new_node(self, level: int, est: int) -> int:
+        self._level.append(level)
+        self._est.append(est)
+        self._slot.append(-1)
+        self._refs.append(0)
+        return len(self._level) - 1
+
+    def _alloc_slot(self) -> int:
+        if self._free:
+            return self._free.pop()
+        s = self._n_slots
+        self._n_slots += 1
+        return s
+
+    def _compile(self):
+        """Level-sort the pending gates and assign ciphertext slots by liveness.
+
+        A slot read at level L is released before the launch of level L + 1 at
+        the earliest, so no launch ever writes a slot another gate of the same
+        launch reads.  Nodes still referenced by a live handle keep their slot.
+        """
+        ops = np.asarray(self._pending_ops, dtype=np.int64).reshape(-1, 5)
+        level = np.asarray(self._level, dtype=np.int64)
+        slot = np.asarray(self._slot, dtype=np.int64)
+        refs = np.asarray(self._refs, dtype=np.int64)
+        n_nodes = len(level)
+        op_level = level[ops[:, 4]]
+        order = np.argsort(op_level, kind="stable")
+        ops = ops[order]
+        op_level = op_level[order]
+        left, lneg, right, rneg, out = ops.T
+        # last level at which each node is read by a pending gate
+        last_use = np.full(n_nodes, -1, dtype=np.int64)
+        np.maximum.at(last_use, left, op_level)
+        np.maximum.at(last_use, right, op_level)
+        # release point of each slot: the level before whose launch it becomes free
+        never = np.iinfo(np.int64).max
+        free_at = np.full(n_nodes, never, dtype=np.int64)
+        if not self.keep_all:
+            dead = refs <= 0
+            old = (slot >= 0) & dead
+            free_at[old] = np.where(last_use[old] >= 0, last_use[old] + 1, 0)
+            new_dead = np.zeros(n_nodes, dtype=bool)
+            new_dead[out] = True
+            new_dead &= dead
+            free_at[new_dead] = np.maximum(last_use[new_dead], level[new_dead]) + 1
+        cand = np.nonzero(free_at != never)[0]
+        cand = cand[np.argsort(free_at[cand], kind="stable")]
+        cand_at = free_at[cand]
+        lv_vals, lv_start = np.unique(op_level, return_index=True)
+        lv_end = np.append(lv_start[1:], len(op_level))
+        ptr = 0
+        free = self._free
+        for lv, s, e in zip(lv_vals.tolist(), lv_start.tolist(), lv_end.tolist()):
+            hi = int(np.searchsorted(cand_at, lv, side="right"))
+            if hi > ptr:
+                rel = slot[cand[ptr:hi]]
+                free.extend(rel[rel >= 0].tolist())
+                ptr = hi
+            cnt = e - s
+            take = min(cnt, len(free))
+            new_slots = np.empty(cnt, dtype=np.int64)
+            if take:
+                new_slots[:take] = free[len(free) - take:]
+                del free[len(free) - take:]
+            if cnt > take:
+                new_slots[take:] = np.arange(self._n_slots, self._n_slots + cnt - take)
+                self._n_slots += cnt - take
+            slot[out[s:e]] = new_slots
+        table = np.empty(len(out), dtype=[("left", "<u4"), ("right", "<u4"),
+                                          ("out", "<u4"), ("flags", "<u4")])
+        table["left"] = slot[left]
+        table["right"] = slot[right]
+        table["out"] = slot[out]
+        table["flags"] = lneg | (rneg << 1)
+        if ptr < len(cand):                       # released after the last launch
+            rel = slot[cand[ptr:]]
+            free.extend(rel[rel >= 0].tolist())
+        released = cand                            # every released node loses its slot
+        slot[released] = -1
+        self._slot = slot.tolist()
+        offsets = np.append(lv_start, len(out)).astype(np.uint64)
+        return {"ops": table, "offsets": offsets, "levels": lv_vals,
+                "widths": np.diff(offsets).astype(np.int64)}
+
+
+class GpuEngine(LevelledNetlist):
     """Lazy, levelised FHE bit engine on one B200."""
 
     def __init__(self, scheme: GswScheme, keys: KeyPair | None = None, public_key=None,
@@ -98,21 +205,12 @@ class GpuEngine:
         self.max_depth = 0
         self.executed_nands = 0
         self.cse = cse
-        self.keep_all = keep_all
         self.trace = [] if record_trace else None
-        self._wire = 0
-        # node tables (python lists: appended per gate)
-        self._level: list[int] = []
-        self._est: list[int] = []
-        self._slot: list[int] = []
-        self._refs: list[int] = []
-        self._pending_ops: list[int] = []       # flat: left, lneg, right, rneg, out
+        self._init_netlist(keep_all)
         self._pending_in_idx: list[np.ndarray] = []
         self._pending_in_val: list[np.ndarray] = []
         self._pending_in_bytes = 0
         self._cse_map: dict | None = {} if cse else None
-        self._free: list[int] = []
-        self._n_slots = 0
         self.last_program = None
         self.programs_run = 0
         self.launches = 0
@@ -141,25 +239,6 @@ class GpuEngine:
         return self.scheme.ctx
 
     # -- nodes and slots ---------------------------------------------------------------
-
-    def _new_wire(self) -> int:
-        w = self._wire
-        self._wire += 1
-        return w
-
-    def _new_node(self, level: int, est: int) -> int:
-        self._level.append(level)
-        self._est.append(est)
-        self._slot.append(-1)
-        self._refs.append(0)
-        return len(self._level) - 1
-
-    def _alloc_slot(self) -> int:
-        if self._free:
-            return self._free.pop()
-        s = self._n_slots
-        self._n_slots += 1
-        return s
 
     def _lane_idx(self, slot: int) -> np.ndarray:
         return slot * self.batch_size + np.arange(self.batch_size, dtype=np.uint64)
@@ -549,74 +628,3 @@ class GpuEngine:
         if arr.shape[1:] != shape_tail:
             raise UsageError(f"host array shape {arr.shape} is not (lanes,) + {shape_tail}")
         return arr
-
-    def _compile(self):
-        """Level-sort the pending gates and assign ciphertext slots by liveness.
-
-        A slot read at level L is released before the launch of level L + 1 at
-        the earliest, so no launch ever writes a slot another gate of the same
-        launch reads.  Nodes still referenced by a live handle keep their slot.
-        """
-        ops = np.asarray(self._pending_ops, dtype=np.int64).reshape(-1, 5)
-        level = np.asarray(self._level, dtype=np.int64)
-        slot = np.asarray(self._slot, dtype=np.int64)
-        refs = np.asarray(self._refs, dtype=np.int64)
-        n_nodes = len(level)
-        op_level = level[ops[:, 4]]
-        order = np.argsort(op_level, kind="stable")
-        ops = ops[order]
-        op_level = op_level[order]
-        left, lneg, right, rneg, out = ops.T
-        # last level at which each node is read by a pending gate
-        last_use = np.full(n_nodes, -1, dtype=np.int64)
-        np.maximum.at(last_use, left, op_level)
-        np.maximum.at(last_use, right, op_level)
-        # release point of each slot: the level before whose launch it becomes free
-        never = np.iinfo(np.int64).max
-        free_at = np.full(n_nodes, never, dtype=np.int64)
-        if not self.keep_all:
-            dead = refs <= 0
-            old = (slot >= 0) & dead
-            free_at[old] = np.where(last_use[old] >= 0, last_use[old] + 1, 0)
-            new_dead = np.zeros(n_nodes, dtype=bool)
-            new_dead[out] = True
-            new_dead &= dead
-            free_at[new_dead] = np.maximum(last_use[new_dead], level[new_dead]) + 1
-        cand = np.nonzero(free_at != never)[0]
-        cand = cand[np.argsort(free_at[cand], kind="stable")]
-        cand_at = free_at[cand]
-        lv_vals, lv_start = np.unique(op_level, return_index=True)
-        lv_end = np.append(lv_start[1:], len(op_level))
-        ptr = 0
-        free = self._free
-        for lv, s, e in zip(lv_vals.tolist(), lv_start.tolist(), lv_end.tolist()):
-            hi = int(np.searchsorted(cand_at, lv, side="right"))
-            if hi > ptr:
-                rel = slot[cand[ptr:hi]]
-                free.extend(rel[rel >= 0].tolist())
-                ptr = hi
-            cnt = e - s
-            take = min(cnt, len(free))
-            new_slots = np.empty(cnt, dtype=np.int64)
-            if take:
-                new_slots[:take] = free[len(free) - take:]
-                del free[len(free) - take:]
-            if cnt > take:
-                new_slots[take:] = np.arange(self._n_slots, self._n_slots + cnt - take)
-                self._n_slots += cnt - take
-            slot[out[s:e]] = new_slots
-        table = np.empty(len(out), dtype=[("left", "<u4"), ("right", "<u4"),
-                                          ("out", "<u4"), ("flags", "<u4")])
-        table["left"] = slot[left]
-        table["right"] = slot[right]
-        table["out"] = slot[out]
-        table["flags"] = lneg | (rneg << 1)
-        if ptr < len(cand):                       # released after the last launch
-            rel = slot[cand[ptr:]]
-            free.extend(rel[rel >= 0].tolist())
-        released = cand                            # every released node loses its slot
-        slot[released] = -1
-        self._slot = slot.tolist()
-        offsets = np.append(lv_start, len(out)).astype(np.uint64)
-        return {"ops": table, "offsets": offsets, "levels": lv_vals,
-                "widths": np.diff(offsets).astype(np.int64)}

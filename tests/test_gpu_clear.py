@@ -1,0 +1,77 @@
+"""Bitsliced cleartext engine on the GPU (GpuClearEngine) vs the reference CleartextEngine.
+
+Reference: engine.py:69-121 (protocol, fold rules, lane packing); harness.py:122-198 (the
+error experiments it serves).  Goldens: decrypted-output words the reference's own
+CleartextEngine produced (tests/golden/clear_cfg*.npz) and its gate counts (trace_cfg*.json).
+"""
+
+import numpy as np
+import pytest
+
+from paper_1611_08769_b200 import FixedFormat, GpuClearEngine, fft_1d, fft_2d, input_signal
+from paper_1611_08769_b200.errors import UsageError
+from paper_1611_08769_b200.fft import read_signal_ints
+from paper_1611_08769_b200.gates import and_, nor_, not_, or_, xnor_, xor_
+from tests.helpers import FFT_CONFIGS, config_signal, golden_json, golden_npz, model_outputs
+
+pytestmark = pytest.mark.gpu
+
+
+def _fft(eng, cfg, values):
+    _, _, (F, f), dims, _ = FFT_CONFIGS[cfg]
+    sig = input_signal(eng, values, FixedFormat(F, f), dims=dims if isinstance(dims, tuple) else None)
+    return fft_2d(sig) if isinstance(dims, tuple) else fft_1d(sig)
+
+
+@pytest.mark.parametrize("cfg", ["cfg0", "cfg2", "cfg3", "cfg4"])
+def test_fft_configs_equal_reference_cleartext_engine(cfg):
+    lanes = FFT_CONFIGS[cfg][4]
+    vals = np.array([config_signal(cfg, lane)[1] for lane in range(lanes)])
+    eng = GpuClearEngine(batch_size=lanes)
+    out = _fft(eng, cfg, vals if lanes > 1 else vals[0])
+    got = read_signal_ints(eng, out)
+    assert np.array_equal(got, golden_npz(f"clear_{cfg}.npz")["words"])
+    tr = golden_json(f"trace_{cfg}.json")
+    assert (eng.nand_count, eng.max_depth) == (tr["nand_count"], tr["max_depth"])
+    assert eng.launches == tr["max_depth"]                       # one launch per level
+
+
+def test_many_lanes_against_integer_model():
+    """200,003 random 16-point signals (ragged last word) in one pass vs the integer oracle."""
+    lanes = 200_003
+    rng = np.random.default_rng(42)
+    vals = rng.uniform(-1, 1, (lanes, 16)) + 1j * rng.uniform(-1, 1, (lanes, 16))
+    eng = GpuClearEngine(batch_size=lanes)
+    out = _fft(eng, "cfg4", vals)
+    got = read_signal_ints(eng, out)
+    assert np.array_equal(got, model_outputs("cfg4", vals))
+
+
+def test_gates_truth_tables_and_costs():
+    """Every gate on all four input pairs as lanes; NAND costs as gates.py:9-34."""
+    eng = GpuClearEngine(batch_size=4)
+    a, b = eng.input_bit(0b1100), eng.input_bit(0b1010)
+    cases = [(not_, (a,), 0b0011, 1), (and_, (a, b), 0b1000, 2), (or_, (a, b), 0b1110, 3),
+             (xor_, (a, b), 0b0110, 4), (nor_, (a, b), 0b0001, 4), (xnor_, (a, b), 0b1001, 5)]
+    for fn, args, want, cost in cases:
+        before = eng.nand_count
+        h = fn(*args)
+        assert eng.read_back(h) == want, fn.__name__
+        assert eng.nand_count - before == cost, fn.__name__
+
+
+def test_folding_and_constants_like_reference():
+    eng = GpuClearEngine(batch_size=3)
+    x = eng.input_bit(0b101)
+    one, zero = eng.constant(1), eng.constant(0)
+    assert eng.read_back(eng.nand(x, one)) == 0b010          # NOT x, gate-free
+    assert eng.read_back(eng.nand(zero, x)) == 0b111         # constant 1
+    assert eng.read_back(eng.nand(one, one)) == 0
+    assert eng.nand_count == 0 and eng.max_depth == 0
+    with pytest.raises(UsageError):
+        eng.input_bit(0b1000)
+    with pytest.raises(UsageError):
+        eng.constant(2)
+    other = GpuClearEngine(batch_size=3)
+    with pytest.raises(UsageError):
+        eng.nand(x, other.input_bit(1))
