@@ -69,10 +69,23 @@ __device__ __forceinline__ uint32_t prmt_sign(uint32_t x) {
   return r;
 }
 
-// 32 bits of w -> 32 s8 K slots {0, -1}: out[o] byte q = -(bit 8q + o).
+// A operand sign: {0, +1} bytes (default) toggle one bit per byte in the MMA datapath and keep
+// the accumulators positive; {0, -1} (sign-replicating prmt) toggles all eight.  Same
+// instruction count; the tensor pipe's switching power is what the power-capped kernel pays.
+#ifndef FHEGPU_A_POS
+#define FHEGPU_A_POS 1
+#endif
+
+// 32 bits of w -> 32 s8 K slots: out[o] byte q = bit (8q + o) (or its negation).
 __device__ __forceinline__ void spread_word_sr(uint32_t w, uint32_t (&out)[8]) {
 #pragma unroll
-  for (int o = 0; o < 8; ++o) out[o] = prmt_sign(w << (7 - o));
+  for (int o = 0; o < 8; ++o) {
+#if FHEGPU_A_POS
+    out[o] = (w >> o) & 0x01010101u;
+#else
+    out[o] = prmt_sign(w << (7 - o));
+#endif
+  }
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t *v) {
@@ -157,18 +170,24 @@ struct GeoWS {
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
-// Negated-digit epilogue (A = -bits): d[] are -(digit sums).
+// Digit-sum epilogue: d[] are the digit sums S_d (or -S_d when A = -bits).
 template <int ELL, bool PM>
 __device__ __forceinline__ uint32_t finish_neg(const uint32_t *d, uint32_t g, const DevParams &p) {
   uint32_t r;
   if constexpr (PM) {
+#if FHEGPU_A_POS
+    const uint32_t a = d[0] + (d[1] << 8);          // S0 + S1 2^8  (< 2^26)
+    const uint32_t b = d[2] + (d[3] << 8);          // S2 + S3 2^8
+#else
     const uint32_t a = 0u - (d[0] + (d[1] << 8));   // S0 + S1 2^8  (< 2^26)
     const uint32_t b = 0u - (d[2] + (d[3] << 8));   // S2 + S3 2^8
+#endif
     const uint32_t t = a + ((b & ((1u << (ELL - 16)) - 1u)) << 16) + p.pm_c * (b >> (ELL - 16));
     r = min(t, t - p.q);                            // t < 2q
   } else {
-    const int64_t s = -((int64_t)(int32_t)d[0] + ((int64_t)(int32_t)d[1] << 8) +
-                        ((int64_t)(int32_t)d[2] << 16) + ((int64_t)(int32_t)d[3] << 24));
+    const int64_t sum = (int64_t)(int32_t)d[0] + ((int64_t)(int32_t)d[1] << 8) +
+                        ((int64_t)(int32_t)d[2] << 16) + ((int64_t)(int32_t)d[3] << 24);
+    const int64_t s = FHEGPU_A_POS ? sum : -sum;
     r = mod_u64((uint64_t)s, p.q, p.mu);
   }
   const uint32_t x = g - r;
