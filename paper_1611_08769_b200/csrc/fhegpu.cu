@@ -443,7 +443,7 @@ namespace {
 size_t packed_row_bytes(const fhegpu_ctx *c) { return ((size_t)c->p.rows * c->p.rows + 7) / 8; }
 
 int set_pack_smem(fhegpu_ctx *c) {
-  const size_t smem = std::max(packed_row_bytes(c), (size_t)c->p.words * 4);
+  const size_t smem = std::max((packed_row_bytes(c) + 3) / 4 * 4, (size_t)c->p.words * 4);
   if (smem > 48 * 1024) {
     CUDA_TRY(cudaFuncSetAttribute(packed_to_store_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CUDA_TRY(cudaFuncSetAttribute(store_to_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -465,7 +465,7 @@ int fhegpu_store_write_packed(fhegpu_ctx *c, uint64_t first, uint64_t count, con
     const uint64_t n = std::min(chunk, count - s);
     if (int rc = ensure((void **)&c->d_stage, &c->stage_bytes, n * per)) return rc;
     CUDA_TRY(cudaMemcpyAsync(c->d_stage, host + s * per, n * per, cudaMemcpyHostToDevice, c->stream));
-    packed_to_store_kernel<<<(unsigned)std::min<uint64_t>(n, c->num_sms * 8), 256, per, c->stream>>>(
+    packed_to_store_kernel<<<(unsigned)std::min<uint64_t>(n, c->num_sms * 8), 256, (per + 3) / 4 * 4, c->stream>>>(
         c->store + (first + s) * c->p.ct_words, (const uint8_t *)c->d_stage, n, (uint32_t)per, c->p);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(c->stream));  // staging is reused by the next chunk
@@ -663,7 +663,7 @@ int fhegpu_prog_run_host(fhegpu_ctx *c, fhegpu_prog *pr, uint64_t lanes, uint32_
       uint32_t *dst = base + (uint64_t)in_slots[i] * cl * c->p.ct_words;
       const uint8_t *src = stage + (uint64_t)i * chunk * row_bytes;
       if (packed)
-        packed_to_store_kernel<<<g, 256, row_bytes, c->stream>>>(dst, src, cl, (uint32_t)row_bytes, c->p);
+        packed_to_store_kernel<<<g, 256, (row_bytes + 3) / 4 * 4, c->stream>>>(dst, src, cl, (uint32_t)row_bytes, c->p);
       else
         dense_to_store_kernel<<<g, 256, 0, c->stream>>>(dst, (const uint32_t *)src, cl, c->p);
     }

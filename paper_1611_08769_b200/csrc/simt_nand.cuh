@@ -132,27 +132,41 @@ __global__ void store_to_dense_kernel(uint32_t *__restrict__ dense, const uint32
 // Packed matrix bits: the reference's serialised ciphertext (fileio.py:72-79 / EFT1
 // payload): C = decompose(V) row-major, bit j of V[r][i] at stream position
 // r*N + i*ell + j, packed 8 per byte MSB first; ceil(N*N/8) bytes per ciphertext.
+// Since N = k*ell the stream is simply every value v = r*k + i, ell bits each, LSB first.
+//
+// Word view: stream bits [32w, 32w + 32) as a u32 X (bit t = stream bit 32w + t) is the
+// little-endian load of bytes 4w..4w+3 with the bits of each byte reversed:
+//   X = prmt(brev(W), 0x0123)  and  W = prmt(brev(X), 0x0123).
+__device__ __forceinline__ uint32_t stream_word(uint32_t w) { return __byte_perm(__brev(w), 0u, 0x0123); }
+
 __global__ void packed_to_store_kernel(uint32_t *__restrict__ store, const uint8_t *__restrict__ packed,
                                        uint64_t rows, uint32_t row_bytes, DevParams p) {
-  extern __shared__ uint8_t s_bytes[];
+  extern __shared__ uint32_t s_x[];
+  const uint32_t mask = (1u << p.ell) - 1u;
+  const bool wide = (row_bytes & 3u) == 0;
+  const uint32_t n_x = (row_bytes + 3) / 4;
   for (uint64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     const uint8_t *src = packed + r * row_bytes;
-    for (uint32_t b = threadIdx.x; b < row_bytes; b += blockDim.x) s_bytes[b] = src[b];
-    __syncthreads();
-    for (uint32_t w = threadIdx.x; w < p.ct_words; w += blockDim.x) {
-      uint32_t v = 0;
-      if (w < p.words) {
-        const uint32_t rr = w / p.k, i = w - rr * p.k;
-        const uint32_t b0 = rr * p.rows + i * p.ell;           // first stream bit (= bit 0 of v)
-        const uint32_t byte0 = b0 >> 3;
-        uint64_t u = 0;                                         // 5 bytes big-endian >= ell + 7 bits
-#pragma unroll
-        for (int t = 0; t < 5; ++t)
-          u = (u << 8) | (byte0 + t < row_bytes ? s_bytes[byte0 + t] : 0u);
-        const uint32_t x = (uint32_t)(u >> (40 - (b0 & 7) - p.ell)) & ((1u << p.ell) - 1u);
-        v = __brev(x) >> (32 - p.ell);                          // stream order is LSB first
+    if (wide) {                                    // u32 loads (rows 4-byte aligned)
+      const uint32_t *src4 = reinterpret_cast<const uint32_t *>(src);
+      for (uint32_t x = threadIdx.x; x < n_x; x += blockDim.x) s_x[x] = stream_word(src4[x]);
+    } else {
+      for (uint32_t x = threadIdx.x; x < n_x; x += blockDim.x) {
+        uint32_t w = 0;
+        for (uint32_t t = 0; t < 4; ++t)
+          if (4 * x + t < row_bytes) w |= (uint32_t)src[4 * x + t] << (8 * t);
+        s_x[x] = stream_word(w);
       }
-      store[r * p.ct_words + w] = v;
+    }
+    __syncthreads();
+    for (uint32_t v = threadIdx.x; v < p.ct_words; v += blockDim.x) {
+      uint32_t val = 0;
+      if (v < p.words) {
+        const uint32_t bit = v * p.ell, x = bit >> 5;
+        const uint32_t hi = x + 1 < n_x ? s_x[x + 1] : 0u;
+        val = __funnelshift_r(s_x[x], hi, bit & 31u) & mask;
+      }
+      store[r * p.ct_words + v] = val;
     }
     __syncthreads();
   }
@@ -161,24 +175,24 @@ __global__ void packed_to_store_kernel(uint32_t *__restrict__ store, const uint8
 __global__ void store_to_packed_kernel(uint8_t *__restrict__ packed, const uint32_t *__restrict__ store,
                                        uint64_t rows, uint32_t row_bytes, DevParams p) {
   extern __shared__ uint32_t s_vals[];
-  const uint32_t n_bits = p.rows * p.rows;
+  const bool wide = (row_bytes & 3u) == 0;
+  const uint32_t n_x = (row_bytes + 3) / 4;
   for (uint64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     for (uint32_t w = threadIdx.x; w < p.words; w += blockDim.x) s_vals[w] = store[r * p.ct_words + w];
     __syncthreads();
-    for (uint32_t b = threadIdx.x; b < row_bytes; b += blockDim.x) {
-      uint32_t pos = b * 8, rr = pos / p.rows, col = pos - rr * p.rows;
-      uint32_t i = col / p.ell, j = col - i * p.ell;
-      uint32_t byte = 0;
-      for (int t = 0; t < 8; ++t, ++pos) {
-        uint32_t bit = 0;
-        if (pos < n_bits) bit = (s_vals[rr * p.k + i] >> j) & 1u;
-        byte |= bit << (7 - t);
-        if (++j == p.ell) {
-          j = 0;
-          if (++i == p.k) { i = 0; ++rr; }
-        }
+    for (uint32_t x = threadIdx.x; x < n_x; x += blockDim.x) {
+      // stream bits [32x, 32x + 32): value v from bit j on, then v+1, v+2 (ell >= 11)
+      const uint32_t bit = 32 * x, v = bit / p.ell, j = bit - v * p.ell;
+      uint32_t X = v < p.words ? s_vals[v] >> j : 0u;
+      uint32_t got = p.ell - j;
+      for (uint32_t t = 1; got < 32 && v + t < p.words; ++t, got += p.ell) X |= s_vals[v + t] << got;
+      const uint32_t W = stream_word(X);
+      if (wide) {
+        reinterpret_cast<uint32_t *>(packed + r * row_bytes)[x] = W;
+      } else {
+        for (uint32_t t = 0; t < 4; ++t)
+          if (4 * x + t < row_bytes) packed[r * row_bytes + 4 * x + t] = (uint8_t)(W >> (8 * t));
       }
-      packed[r * row_bytes + b] = (uint8_t)byte;
     }
     __syncthreads();
   }
