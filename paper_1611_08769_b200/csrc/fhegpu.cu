@@ -149,9 +149,19 @@ int launch_tc_ws_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t
   const uint64_t grid = std::min<uint64_t>(items, (uint64_t)c->num_sms);
   DevParams p = c->p;
   p.lanes_magic = (uint32_t)(0xFFFFFFFFu / lanes);
-  tc::level_tc_ws_kernel<K, ELL, PM><<<(unsigned)grid, G::THREADS, smem, c->stream>>>(
-      store, ops, n_ops, lanes, p);
-  CUDA_TRY(cudaGetLastError());
+  // programmatic dependent launch (dbg bit 13 disables): consecutive levels overlap the
+  // launch gap and prologue; the kernel's griddepcontrol.wait keeps the data dependence
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(G::THREADS);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (c->p.dbg & 8192u) ? 0 : 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::level_tc_ws_kernel<K, ELL, PM>, store, ops, n_ops, lanes, p));
   return FHEGPU_OK;
 }
 

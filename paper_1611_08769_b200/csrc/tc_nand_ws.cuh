@@ -235,6 +235,9 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
   const int warp = tid >> 5, lane = tid & 31;
   const uint32_t n_items = n_ops * lanes;     // host guarantees < 2^32
 
+  // Programmatic dependent launch: the next level's grid may be scheduled now; its CTAs
+  // take each SM as this grid's CTA leaves it and overlap their prologue with our tail.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (warp == G::WARP_MMA) tmem_alloc<512>(tmem_slot);
   if (tid == 0) {
     for (int i = 0; i < G::S_IN; ++i) {
@@ -262,6 +265,9 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // every global read/write of ciphertexts comes after the previous level has completed
+  // (its outputs are our operands; slots it read may be our outputs); no-op without PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == G::WARP_PROD) {
     // ------------------------------ producer ------------------------------

@@ -6,6 +6,7 @@ from paper_1611_08769_b200 import FixedFormat, GpuEngine, GswScheme, fft_1d, fft
 from tests.helpers import FFT_CONFIGS, config_signal
 from paper_1611_08769_b200 import DEFAULT0_PARAMS, EXACT_PARAMS
 cfg = sys.argv[1]
+dbg = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 pname, seed, (F, f), dims, _ = FFT_CONFIGS[cfg]
 params = {"EXACT": EXACT_PARAMS, "DEFAULT0": DEFAULT0_PARAMS}[pname]
 s = GswScheme(params); keys = s.keygen(seed)
@@ -17,6 +18,7 @@ sig = input_signal(eng, x, FixedFormat(F, f), dims=dims if isinstance(dims, tupl
 out = fft_2d(sig) if isinstance(dims, tuple) else fft_1d(sig)
 build = time.time() - t0
 prog = eng.flush(); torch.cuda.synchronize()
+s.ctx.set_debug(dbg)
 comp = eng.last_compile
 w = comp["widths"]
 print(f"{cfg}: nands={eng.nand_count} levels={len(w)} build_s={build:.2f} slots={eng._n_slots} widths min/med/max={w.min()}/{int(np.median(w))}/{w.max()}")
