@@ -75,3 +75,38 @@ def test_folding_and_constants_like_reference():
     other = GpuClearEngine(batch_size=3)
     with pytest.raises(UsageError):
         eng.nand(x, other.input_bit(1))
+
+
+def test_backend_equivalence_random_circuits_and_lanes():
+    """Random gate circuits agree bit for bit across GpuClearEngine (many lanes), the GPU
+    FHE engine (EXACT) and packed-int cleartext evaluation (tests/test_engine.py:100-123)."""
+    from paper_1611_08769_b200 import EXACT_PARAMS, GpuEngine, GswScheme
+    scheme = GswScheme(EXACT_PARAMS)
+    keys = scheme.keygen(1)
+    rng = np.random.default_rng(123)
+    ops = [not_, and_, or_, xor_, nor_, xnor_]
+    lanes = 77
+    for _ in range(3):
+        clear = GpuClearEngine(batch_size=lanes)
+        fhe = GpuEngine(scheme, keys=keys, rng=np.random.default_rng(5), batch_size=lanes,
+                        device_encrypt=True)
+        masks = [int(m) for m in rng.integers(0, 2, (6, lanes)) @ (1 << np.arange(lanes, dtype=object))]
+        pool_c = [clear.input_bit(m) for m in masks]
+        pool_f = [fhe.input_bit(m) for m in masks]
+        pool_v = list(masks)                                    # packed-int truth
+        full = (1 << lanes) - 1
+        py = {not_: lambda a, b: full ^ a, and_: lambda a, b: a & b, or_: lambda a, b: a | b,
+              xor_: lambda a, b: a ^ b, nor_: lambda a, b: full ^ (a | b), xnor_: lambda a, b: full ^ (a ^ b)}
+        for _ in range(40):
+            op = ops[rng.integers(0, len(ops))]
+            i, j = rng.integers(0, len(pool_c), 2)
+            if op is not_:
+                pool_c.append(op(pool_c[i]))
+                pool_f.append(op(pool_f[i]))
+            else:
+                pool_c.append(op(pool_c[i], pool_c[j]))
+                pool_f.append(op(pool_f[i], pool_f[j]))
+            pool_v.append(py[op](pool_v[i], pool_v[j]))
+        assert clear.nand_count == fhe.nand_count <= 200
+        assert clear.max_depth == fhe.max_depth
+        assert clear.read_back_many(pool_c) == fhe.read_back_many(pool_f) == pool_v
