@@ -154,6 +154,14 @@ int fhegpu_prog_run_host(fhegpu_ctx *ctx, fhegpu_prog *prog, uint64_t lanes, uin
                          int host_format, uint32_t n_in, const uint32_t *in_slots,
                          const void *const *host_in, uint32_t n_out, const uint32_t *out_slots,
                          void *const *host_out);
+/* Dataflow mode: deps[2i], deps[2i+1] = index of the op that produced op i's left / right
+ * operand in this program (-1: written before the run).  Requires SSA slots (no slot
+ * written twice in the program, none overwritten while a reader may still load it) --
+ * the engine's dataflow compile guarantees it.  prog_run then evaluates the whole program
+ * in ONE launch: each operand load waits for its producer through per-CTA progress
+ * counters instead of a kernel boundary per level (narrow, deep netlists such as a single
+ * FFT, fft.py:157-194).  Falls back to level launches where no tcgen05 kernel applies. */
+int fhegpu_prog_set_deps(fhegpu_ctx *ctx, fhegpu_prog *prog, const int32_t *deps);
 uint32_t fhegpu_prog_launches(const fhegpu_prog *prog);       /* launches one run issues */
 void fhegpu_prog_destroy(fhegpu_prog *prog);
 

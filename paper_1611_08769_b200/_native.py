@@ -60,6 +60,7 @@ SIGNATURES = [
     ("fhegpu_prog_run", ctypes.c_int, [_P, _P, ctypes.c_uint32]),
     ("fhegpu_prog_run_range", ctypes.c_int, [_P, _P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]),
     ("fhegpu_prog_launches", ctypes.c_uint32, [_P]),
+    ("fhegpu_prog_set_deps", ctypes.c_int, [_P, _P, _P]),
     ("fhegpu_store_write_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     ("fhegpu_store_read_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     ("fhegpu_prog_run_host", ctypes.c_int, [_P, _P, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int,
@@ -150,6 +151,13 @@ class Program:
         last = self.n_levels if last is None else last
         _check(_lib.fhegpu_prog_run_range(self.ctx.handle, self.handle, lanes, first, last),
                "prog_run")
+
+    def set_deps(self, deps: np.ndarray):
+        """Dataflow mode (fhegpu_prog_set_deps): deps (n_ops, 2) int32 producer op indices."""
+        deps = np.ascontiguousarray(deps, dtype=np.int32)
+        _check(_lib.fhegpu_prog_set_deps(self.ctx.handle, self.handle, deps.ctypes.data_as(ctypes.c_void_p)),
+               "prog_set_deps")
+        self.launches = int(_lib.fhegpu_prog_launches(self.handle))
 
     def run_host(self, lanes: int, chunk_lanes: int, in_slots, in_ptrs, out_slots, out_ptrs,
                  host_format: int = 0):

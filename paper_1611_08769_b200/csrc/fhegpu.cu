@@ -78,6 +78,8 @@ struct fhegpu_prog {
   std::vector<uint64_t> offsets;  // n_levels + 1
   uint64_t n_ops = 0;
   uint64_t n_slots = 0;           // 1 + the largest slot any op names
+  int2 *d_deps = nullptr;         // dataflow mode: producing op of each operand (-1: ready)
+  uint32_t *d_progress = nullptr; // per-CTA completed-item counters
   // CUDA graph of one full run (all level launches), captured on first use per
   // (lanes, stream, kernel choice, debug bits); replayed with a single cudaGraphLaunch
   cudaGraphExec_t graph = nullptr;
@@ -134,7 +136,8 @@ int launch_tc_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_
 }
 
 template <int K, int ELL, bool PM>
-int launch_tc_ws_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes) {
+int launch_tc_ws_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes,
+                      const int2 *deps = nullptr, uint32_t *progress = nullptr) {
   using G = tc::GeoWS<K, ELL, PM>;
   static bool attr_done = false;
   // > half of the SM's shared memory: exactly one CTA (512 TMEM columns) per SM
@@ -161,7 +164,8 @@ int launch_tc_ws_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = (c->p.dbg & 8192u) ? 0 : 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::level_tc_ws_kernel<K, ELL, PM>, store, ops, n_ops, lanes, p));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::level_tc_ws_kernel<K, ELL, PM>, store, ops, n_ops, lanes, p,
+                              deps, progress));
   return FHEGPU_OK;
 }
 
@@ -218,6 +222,20 @@ int launch_level(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_op
     return fail(FHEGPU_EUNSUP, "no tcgen05 instantiation for these params");
   }
   return launch_simt(c, store, ops, n_ops, lanes);
+}
+
+// A whole program in one launch (dataflow over per-CTA progress counters); FHEGPU_EUNSUP when
+// the parameter set / kernel choice has no warp-specialised tcgen05 kernel.
+int launch_dataflow(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes,
+                    const int2 *deps, uint32_t *progress) {
+  if (n_ops == 0 || lanes == 0) return FHEGPU_OK;
+  if (effective_kernel(c) != FHEGPU_KERNEL_TCGEN05 || (c->p.dbg & 4u)) return FHEGPU_EUNSUP;
+  if (!(c->p.k == 9 && c->p.ell == 29)) return FHEGPU_EUNSUP;
+  if ((uint64_t)n_ops * lanes >= (1ull << 32) || c->num_sms > 256) return FHEGPU_EUNSUP;
+  CUDA_TRY(cudaMemsetAsync(progress, 0, (size_t)c->num_sms * sizeof(uint32_t), c->stream));
+  if (pm_ok(c->p.q, c->p.ell) && !(c->p.dbg & 2u))
+    return launch_tc_ws_impl<9, 29, true>(c, store, ops, n_ops, lanes, deps, progress);
+  return launch_tc_ws_impl<9, 29, false>(c, store, ops, n_ops, lanes, deps, progress);
 }
 
 unsigned grid_for(uint64_t work, int num_sms) {
@@ -548,6 +566,11 @@ int fhegpu_prog_run_range(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes, uint32
   const uint32_t n_levels = (uint32_t)pr->offsets.size() - 1;
   last = std::min(last, n_levels);
   CUDA_TRY(cudaSetDevice(c->device));
+  if (pr->d_deps && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
+    const int rc = launch_dataflow(c, c->store, pr->d_ops, (uint32_t)pr->n_ops, lanes, pr->d_deps,
+                                   pr->d_progress);
+    if (rc != FHEGPU_EUNSUP) return rc;            // else: level by level (always valid)
+  }
   for (uint32_t l = first; l < last; ++l) {
     const uint64_t a = pr->offsets[l], b = pr->offsets[l + 1];
     if (int rc = launch_level(c, c->store, pr->d_ops + a, (uint32_t)(b - a), lanes)) return rc;
@@ -704,6 +727,29 @@ int fhegpu_prog_run_host(fhegpu_ctx *c, fhegpu_prog *pr, uint64_t lanes, uint32_
   return FHEGPU_OK;
 }
 
+int fhegpu_prog_set_deps(fhegpu_ctx *c, fhegpu_prog *pr, const int32_t *deps) {
+  if (!c || !pr || (pr->n_ops && !deps)) return fail(FHEGPU_EINVAL, "null argument");
+  if (pr->n_ops >= (1ull << 31)) return fail(FHEGPU_EINVAL, "program too large for dataflow");
+  for (uint64_t i = 0; i < 2 * pr->n_ops; ++i)
+    if (deps[i] < -1 || (int64_t)deps[i] >= (int64_t)(i / 2))
+      return fail(FHEGPU_EINVAL, "dependency " + std::to_string(i) + " is not an earlier op");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaFree(pr->d_deps);
+  cudaFree(pr->d_progress);
+  pr->d_deps = nullptr;
+  pr->d_progress = nullptr;
+  if (pr->n_ops == 0) return FHEGPU_OK;
+  CUDA_TRY(cudaMalloc(&pr->d_deps, pr->n_ops * sizeof(int2)));
+  CUDA_TRY(cudaMalloc(&pr->d_progress, (size_t)std::max(c->num_sms, 1) * sizeof(uint32_t)));
+  CUDA_TRY(cudaMemcpyAsync(pr->d_deps, deps, pr->n_ops * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (pr->graph) {                      // launch structure changed
+    cudaGraphExecDestroy(pr->graph);
+    pr->graph = nullptr;
+  }
+  return FHEGPU_OK;
+}
+
 int fhegpu_ctx_set_graphs(fhegpu_ctx *c, int enable) {
   if (!c) return fail(FHEGPU_EINVAL, "null ctx");
   c->use_graphs = enable != 0;
@@ -712,6 +758,7 @@ int fhegpu_ctx_set_graphs(fhegpu_ctx *c, int enable) {
 
 uint32_t fhegpu_prog_launches(const fhegpu_prog *pr) {
   if (!pr) return 0;
+  if (pr->d_deps) return 1;                     // dataflow: one launch (tcgen05 parameter sets)
   uint32_t n = 0;
   for (size_t l = 0; l + 1 < pr->offsets.size(); ++l) n += pr->offsets[l + 1] > pr->offsets[l];
   return n;
@@ -720,6 +767,8 @@ uint32_t fhegpu_prog_launches(const fhegpu_prog *pr) {
 void fhegpu_prog_destroy(fhegpu_prog *pr) {
   if (!pr) return;
   if (pr->graph) cudaGraphExecDestroy(pr->graph);
+  cudaFree(pr->d_deps);
+  cudaFree(pr->d_progress);
   cudaFree(pr->d_ops);
   delete pr;
 }

@@ -49,6 +49,90 @@ __device__ __forceinline__ void bulk_wait_read_n() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 
+template <int N>
+__device__ __forceinline__ void bulk_wait_n() {                 // writes complete, not just read
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// -- dataflow scheduling (one launch for a whole program) --------------------------------
+// Item i (ops in topological order, lanes inner) runs on CTA i % G as that CTA's local item
+// i / G; progress[c] = number of CTA c's local items whose output ciphertext is globally
+// written.  A consumer waits for progress[producer CTA] > producer's local index.
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Block until the item that produced an operand (op index `dep`, same lane) is written.
+// `seen` caches the last progress value read (acquire) per CTA: counters only grow, so a
+// cached value that already covers the dependency needs no global round trip.
+__device__ __forceinline__ void wait_dep(const uint32_t *progress, uint32_t *seen, int dep, uint32_t lanes,
+                                         uint32_t ln) {
+  if (dep < 0) return;
+  const uint32_t i = (uint32_t)dep * lanes + ln;
+  const uint32_t c = i % gridDim.x, k = i / gridDim.x;
+  if (seen[c] > k) return;
+  uint32_t v;
+  while ((v = ld_acquire_gpu(progress + c)) <= k) __nanosleep(32);
+  seen[c] = v;
+}
+
+// Counters only grow: max-reduction with release semantics, so the two publishers (the
+// epilogue store thread when it is about to block, the tail warp otherwise) never regress.
+__device__ __forceinline__ void red_max_release_gpu(uint32_t *p, uint32_t v) {
+  asm volatile("red.release.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_release_cta_smem(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_cta_smem(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+
+// Make local items [0, n) visible to other CTAs (their bulk stores have completed).  A
+// release on the thread that issued the bulk stores waits for ALL its outstanding stores,
+// so the steady state posts n to shared memory instead (post_local) and the tail warp,
+// which has no global stores in flight, performs the release (relay).
+__device__ __forceinline__ void publish(uint32_t *progress, uint32_t n) {
+  fence_proxy_async_global();
+  red_max_release_gpu(progress + blockIdx.x, n);
+}
+
+__device__ __forceinline__ void post_local(uint32_t *s_pub, uint32_t n) {
+  // the stores being posted have COMPLETED (cp.async.bulk.wait_group returned: their writes
+  // are acknowledged at L2, where consumers' bulk loads read); the proxy fence orders them
+  // before this thread's later generic operations and the shared-memory post only has to
+  // be observed after that point -- a CTA-scope release here would wait for the stores
+  // still in flight, which is the cost this relay exists to avoid
+  fence_proxy_async_global();
+  asm volatile("st.volatile.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(s_pub)), "r"(n) : "memory");
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -72,6 +156,10 @@ __device__ __forceinline__ uint32_t prmt_sign(uint32_t x) {
 // A operand sign: {0, +1} bytes (default) toggle one bit per byte in the MMA datapath and keep
 // the accumulators positive; {0, -1} (sign-replicating prmt) toggles all eight.  Same
 // instruction count; the tensor pipe's switching power is what the power-capped kernel pays.
+#ifndef FHEGPU_PUBLISH_LAG
+#define FHEGPU_PUBLISH_LAG 3   // dataflow: publish outputs this many gates behind the epilogue
+#endif
+
 #ifndef FHEGPU_A_POS
 #define FHEGPU_A_POS 1
 #endif
@@ -162,7 +250,10 @@ struct GeoWS {
   static constexpr int OFF_TA = ((OFF_B + 2 * B_BYTES + 127) / 128) * 128;
   static constexpr int OFF_OUT = ((OFF_TA + (TAIL ? 2 * TA_BYTES : 0) + 127) / 128) * 128;
   static constexpr int OFF_BAR = ((OFF_OUT + N_OUT * CT_BYTES + 127) / 128) * 128;
-  static constexpr int SMEM = OFF_BAR + 256;
+  static constexpr int OFF_SEEN = OFF_BAR + 256;          // dataflow: progress cache, <= 256 CTAs
+  static constexpr int MAX_CTAS = 256;
+  static constexpr int OFF_PUB = OFF_SEEN + 4 * MAX_CTAS;  // dataflow: epilogue -> tail relay
+  static constexpr int SMEM = OFF_PUB + 16;
   static_assert(NDIG == 4 && B::NCOL <= 36, "warp-specialised kernel: 4 digits, <= 36 columns");
   static_assert(MT >= 1 && TAIL <= 8, "two-tile geometry");
   static_assert(B::D_COLS + B::A_COLS <= BUF_COLS, "two TMEM buffers must fit 512 columns");
@@ -213,7 +304,11 @@ __device__ __forceinline__ uint32_t lane_of(uint32_t item, uint32_t lanes, uint3
 template <int K, int ELL, bool PM>
 __global__ void __launch_bounds__(GeoWS<K, ELL, PM>::THREADS, 1)
 level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uint32_t n_ops,
-                   uint32_t lanes, DevParams p) {
+                   uint32_t lanes, DevParams p, const int2 *__restrict__ deps, uint32_t *__restrict__ progress) {
+  // deps == nullptr: one netlist level (the previous level completed before launch).
+  // deps != nullptr: a whole program in dataflow order (ops topologically sorted, SSA slots:
+  // no slot is written twice or overwritten while a reader may still need it); each operand
+  // load waits for its producing item via `progress` (gridDim.x entries, zeroed per run).
   using G = GeoWS<K, ELL, PM>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint32_t *s_in = reinterpret_cast<uint32_t *>(smem + G::OFF_IN);
@@ -230,6 +325,8 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
   uint64_t *out_free = d_free + 2;            // [N_OUT] staging o may take gate t's rows
   uint64_t *tail_ready = out_free + G::N_OUT; // [N_OUT] tail rows of gate t are in staging o
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tail_ready + G::N_OUT);
+  uint32_t *s_seen = reinterpret_cast<uint32_t *>(smem + G::OFF_SEEN);
+  uint32_t *s_pub = reinterpret_cast<uint32_t *>(smem + G::OFF_PUB);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -260,6 +357,8 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
   if constexpr (G::TAIL > 0)
     for (int w = tid; w < 2 * G::TA_BYTES / 4; w += G::THREADS) reinterpret_cast<uint32_t *>(s_ta)[w] = 0u;
   for (int w = tid; w < G::N_OUT * G::CT_WORDS; w += G::THREADS) s_out[w] = 0u;   // padding stays 0
+  for (int w = tid; w < G::MAX_CTAS; w += G::THREADS) s_seen[w] = 0u;
+  if (tid == 0) *s_pub = 0u;
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -274,13 +373,30 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
     if (lane == 0) {
       uint32_t t = 0;
       OpRec op_next = fetch_op(ops, blockIdx.x, n_items, lanes, p.lanes_magic);
+      int2 dep_next = make_int2(-1, -1);
+      if (deps != nullptr && blockIdx.x < n_items) {
+        uint32_t q0, r0;
+        div_lanes(blockIdx.x, lanes, p.lanes_magic, q0, r0);
+        dep_next = deps[q0];
+      }
       for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
         const uint32_t s = t % G::S_IN, k = t / G::S_IN;
         const OpRec op = op_next;
+        const int2 dep = dep_next;
         op_next = fetch_op(ops, item + gridDim.x, n_items, lanes, p.lanes_magic);
+        if (deps != nullptr && item + gridDim.x < n_items) {     // prefetched one item ahead
+          uint32_t q1, r1;
+          div_lanes(item + gridDim.x, lanes, p.lanes_magic, q1, r1);
+          dep_next = deps[q1];
+        }
         mbar_wait(&in_empty[s], (k & 1u) ^ 1u);
         trace_ev(p, t, 0);
         const uint32_t ln = lane_of(item, lanes, p.lanes_magic);
+        if (deps != nullptr) {
+          wait_dep(progress, s_seen, dep.x, lanes, ln);
+          wait_dep(progress, s_seen, dep.y, lanes, ln);
+          fence_proxy_async_global();             // acquired generic flag -> async-proxy loads
+        }
         uint32_t *dst = s_in + s * 2 * G::CT_WORDS;
         if (p.dbg & 256u) {                       // timing experiment: no operand loads
           mbar_arrive(&in_full[s]);
@@ -342,9 +458,19 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
     // folds the 5 rows into the epilogue's staging buffer (the builders build the tail A).
     if constexpr (G::TAIL > 0) {
       uint32_t t = 0;
+      uint32_t relayed = 0;
       for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
         const uint32_t b = t & 1u, u = t >> 1;
         if (lane == 0) trace_ev(p, t, 12);
+        if (progress != nullptr && lane == 0) {     // dataflow: relay the epilogue's count
+          uint32_t v;
+          asm volatile("ld.volatile.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(s_pub)) : "memory");
+          if (v > relayed) {                        // covers completed stores only: relaxed
+            asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(progress + blockIdx.x), "r"(v)
+                         : "memory");
+            relayed = v;
+          }
+        }
         mbar_wait(&main_done[b], u & 1u);
         if (lane == 0) trace_ev(p, t, 13);
         tc_fence_after();
@@ -506,6 +632,17 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
       uint32_t *out_st = s_out + o * G::CT_WORDS;
       // staging o was released by et 0 before the previous gate's barrier (or is fresh)
       if (et == 0) trace_ev(p, t, 8);
+      if (progress != nullptr && et == 0 && t > 0) {
+        // dataflow: publish finished outputs -- all of them before this thread can block
+        // (a later item of this CTA may be waiting for one), else all but the newest
+        if (!mbar_test(&main_done[b], u & 1u)) {
+          bulk_wait_n<0>();
+          publish(progress, t);
+        } else if (t >= FHEGPU_PUBLISH_LAG && !(p.dbg & 65536u)) {
+          bulk_wait_n<FHEGPU_PUBLISH_LAG>();        // stores older than LAG gates are complete
+          post_local(s_pub, t - FHEGPU_PUBLISH_LAG);  // the tail warp relays it
+        }
+      }
       mbar_wait(&main_done[b], u & 1u);
       if (et == 0) trace_ev(p, t, 9);
       tc_fence_after();
@@ -540,7 +677,10 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
         bulk_s2g(store + ((uint64_t)op_cur.out * lanes + ln) * G::CT_WORDS, out_st, G::CT_BYTES);
       }
     }
-    if (et == 0) bulk_wait_all();
+    if (et == 0) {
+      bulk_wait_all();
+      if (progress != nullptr) publish(progress, t);
+    }
   }
 
   tc_fence_before();

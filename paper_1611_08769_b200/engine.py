@@ -107,12 +107,37 @@ class LevelledNetlist:
         self._n_slots += 1
         return s
 
-    def _compile(self):
+    @staticmethod
+    def _dataflow_order(ops, order, sorted_level, n_nodes):
+        """Within each level, order ops by the position of their latest producer.
+
+        A dataflow launch hands item i to CTA i % G in order; an item whose producer is
+        still in flight stalls that CTA's whole pipeline.  Sorting every level by producer
+        position makes the early items of level L+1 consume the early (long finished)
+        items of level L, so dependency distances approach a full level width."""
+        left_n, right_n, out_n = ops[:, 0], ops[:, 2], ops[:, 4]
+        pos = np.full(n_nodes, -1, dtype=np.int64)
+        starts = np.flatnonzero(np.diff(sorted_level, prepend=sorted_level[:1] - 1))
+        ends = np.append(starts[1:], len(order))
+        out = np.empty_like(order)
+        for s, e in zip(starts.tolist(), ends.tolist()):
+            seg = order[s:e]
+            key = np.maximum(pos[left_n[seg]], pos[right_n[seg]])
+            seg = seg[np.argsort(key, kind="stable")]
+            pos[out_n[seg]] = np.arange(s, e)
+            out[s:e] = seg
+        return out
+
+    def _compile(self, ssa: bool = False):
         """Level-sort the pending gates and assign ciphertext slots by liveness.
 
         A slot read at level L is released before the launch of level L + 1 at
         the earliest, so no launch ever writes a slot another gate of the same
         launch reads.  Nodes still referenced by a live handle keep their slot.
+
+        ssa=True (dataflow programs, one launch without level boundaries): no slot is
+        reused within the program -- slots released by it return to the pool only after
+        it -- and ``deps`` gives, per op, the op indices that produced its operands.
         """
         ops = np.asarray(self._pending_ops, dtype=np.int64).reshape(-1, 5)
         level = np.asarray(self._level, dtype=np.int64)
@@ -121,6 +146,8 @@ class LevelledNetlist:
         n_nodes = len(level)
         op_level = level[ops[:, 4]]
         order = np.argsort(op_level, kind="stable")
+        if ssa:
+            order = self._dataflow_order(ops, order, op_level[order], n_nodes)
         ops = ops[order]
         op_level = op_level[order]
         left, lneg, right, rneg, out = ops.T
@@ -146,11 +173,18 @@ class LevelledNetlist:
         lv_end = np.append(lv_start[1:], len(op_level))
         ptr = 0
         free = self._free
+        deferred = []
+        first_lv = int(lv_vals[0]) if len(lv_vals) else 0
         for lv, s, e in zip(lv_vals.tolist(), lv_start.tolist(), lv_end.tolist()):
             hi = int(np.searchsorted(cand_at, lv, side="right"))
             if hi > ptr:
                 rel = slot[cand[ptr:hi]]
-                free.extend(rel[rel >= 0].tolist())
+                if ssa:                            # only slots this program never reads
+                    untouched = free_at[cand[ptr:hi]] <= first_lv
+                    free.extend(rel[(rel >= 0) & untouched].tolist())
+                    deferred.extend(rel[(rel >= 0) & ~untouched].tolist())
+                else:
+                    free.extend(rel[rel >= 0].tolist())
                 ptr = hi
             cnt = e - s
             take = min(cnt, len(free))
@@ -171,12 +205,18 @@ class LevelledNetlist:
         if ptr < len(cand):                       # released after the last launch
             rel = slot[cand[ptr:]]
             free.extend(rel[rel >= 0].tolist())
+        free.extend(deferred)
         released = cand                            # every released node loses its slot
         slot[released] = -1
         self._slot = slot.tolist()
         offsets = np.append(lv_start, len(out)).astype(np.uint64)
-        return {"ops": table, "offsets": offsets, "levels": lv_vals,
+        prog = {"ops": table, "offsets": offsets, "levels": lv_vals,
                 "widths": np.diff(offsets).astype(np.int64)}
+        if ssa:
+            producer = np.full(n_nodes, -1, dtype=np.int64)
+            producer[out] = np.arange(len(out))
+            prog["deps"] = np.stack([producer[left], producer[right]], axis=1).astype(np.int32)
+        return prog
 
 
 class GpuEngine(LevelledNetlist):
@@ -185,11 +225,14 @@ class GpuEngine(LevelledNetlist):
     def __init__(self, scheme: GswScheme, keys: KeyPair | None = None, public_key=None,
                  rng=None, threads: int = 1, batch_size: int = 1, lane_rngs=None,
                  cse: bool = False, keep_all: bool = False, record_trace: bool = False,
-                 dry_run: bool = False, device_encrypt: bool = False):
+                 dry_run: bool = False, device_encrypt: bool = False, schedule: str = "levels"):
         if threads < 1:
             raise UsageError("threads must be >= 1")
         if batch_size < 1:
             raise UsageError("batch_size must be >= 1")
+        if schedule not in ("levels", "dataflow"):
+            raise UsageError(f"schedule must be 'levels' or 'dataflow', got {schedule!r}")
+        self.schedule = schedule
         if lane_rngs is not None and len(lane_rngs) != batch_size:
             raise UsageError("need one rng per lane")
         self.scheme = scheme
@@ -538,7 +581,8 @@ class GpuEngine(LevelledNetlist):
             self._upload_inputs()
         if not self._pending_ops:
             return None
-        prog = self._compile()
+        dataflow = self._use_dataflow()
+        prog = self._compile(ssa=dataflow)
         self._pending_ops = []
         if self._cse_map is not None:
             self._cse_map = {}
@@ -548,12 +592,23 @@ class GpuEngine(LevelledNetlist):
             return prog
         self._ensure_capacity()
         program = self.ctx.program(prog["ops"], prog["offsets"])
+        if dataflow:
+            program.set_deps(prog["deps"])
         program.run(self.batch_size)
         self.last_program = program
         self.last_compile = prog
         self.programs_run += 1
         self.launches += program.launches
         return program
+
+    def _use_dataflow(self) -> bool:
+        """schedule='dataflow': one launch per program with per-operand readiness (per-CTA
+        progress counters) instead of one launch per level; needs SSA slots (no reuse inside
+        the program) and the warp-specialised tcgen05 kernel (k = 9, ell = 29; other
+        parameter sets fall back to level launches).  Measured on B200 it does not beat
+        level launches + PDL for the reference's FFT netlists: a dependency
+        hop costs ~10 us of pipeline latency and the deep netlists are hop-bound."""
+        return self.schedule == "dataflow"
 
     def run_host(self, program, inputs, outputs, chunk_lanes: int = 32768, out=None,
                  sync: bool = True, packed: bool = False):

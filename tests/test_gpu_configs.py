@@ -36,7 +36,7 @@ def gate_digests(eng, lane=0, chunk=16384):
     return digs(ins), digs(gates)
 
 
-def run_fft_config(cfg, device_encrypt, keep_all=True, lanes=1):
+def run_fft_config(cfg, device_encrypt, keep_all=True, lanes=1, schedule="levels"):
     pname, seed, (F, f), dims, _ = FFT_CONFIGS[cfg]
     params = PARAMS[pname]
     scheme = GswScheme(params)
@@ -44,7 +44,7 @@ def run_fft_config(cfg, device_encrypt, keep_all=True, lanes=1):
     if lanes == 1:
         rng, x = config_signal(cfg)
         eng = GpuEngine(scheme, keys=keys, rng=rng, keep_all=keep_all, record_trace=keep_all,
-                        device_encrypt=device_encrypt)
+                        device_encrypt=device_encrypt, schedule=schedule)
         values = x
     else:
         rngs, vals = [], []
@@ -53,7 +53,8 @@ def run_fft_config(cfg, device_encrypt, keep_all=True, lanes=1):
             rngs.append(r)
             vals.append(x)
         eng = GpuEngine(scheme, keys=keys, batch_size=lanes, lane_rngs=rngs,
-                        device_encrypt=device_encrypt, keep_all=keep_all, record_trace=keep_all)
+                        device_encrypt=device_encrypt, keep_all=keep_all, record_trace=keep_all,
+                        schedule=schedule)
         values = np.array(vals)
     sig = input_signal(eng, values, FixedFormat(F, f), dims=dims if isinstance(dims, tuple) else None)
     out = fft_2d(sig) if isinstance(dims, tuple) else fft_1d(sig)
@@ -127,12 +128,17 @@ def test_cfg4_lane0_gate_by_gate():
     assert read_signal_ints(eng, out)[0].tolist() == ref["output_words"]
 
 
-@pytest.mark.parametrize("cfg", ["cfg3", "cfg2"])
-def test_fft_config_gate_by_gate(cfg):
+@pytest.mark.parametrize("cfg,schedule", [("cfg3", "levels"), ("cfg3", "dataflow"), ("cfg2", "levels"),
+                                          ("cfg2", "dataflow")])
+def test_fft_config_gate_by_gate(cfg, schedule):
+    """Every gate's ciphertext equals the reference's; 'dataflow' runs the whole FFT as one
+    launch with per-operand readiness (SSA slots, per-CTA progress counters)."""
     path = os.path.join(GOLDEN, f"cts_{cfg}.json")
     if not os.path.exists(path):
         pytest.skip(f"golden {cfg} ciphertext digests not generated")
-    eng, out, x = run_fft_config(cfg, device_encrypt=True)
+    eng, out, x = run_fft_config(cfg, device_encrypt=True, schedule=schedule)
+    if schedule != "levels":
+        assert eng.launches == 1                      # one launch for the whole FFT
     ref = golden_json(f"cts_{cfg}.json")
     ins, gates = gate_digests(eng)
     assert digest.chain_digest(ins) == ref["inputs_chain"]
@@ -156,3 +162,14 @@ def test_device_encryption_equals_host_encryption():
         assert np.array_equal(dev.transpose(1, 0, 2, 3).reshape(-1, params.n_ct, params.k), host)
         sh, sd = r_host.bit_generator.state, r_dev.bit_generator.state
         assert sh["state"] == sd["state"] and sh["has_uint32"] == sd["has_uint32"] == 0
+
+
+def test_dataflow_many_lanes_equals_levels():
+    """Dataflow with several lanes (items = (op, lane), CTA-strided) vs level launches."""
+    outs = {}
+    for schedule in ("levels", "dataflow"):
+        eng, out, vals = run_fft_config("cfg4", device_encrypt=True, keep_all=False, lanes=5,
+                                        schedule=schedule)
+        outs[schedule] = read_signal_ints(eng, out)
+        assert np.array_equal(outs[schedule], model_outputs("cfg4", vals))
+    assert np.array_equal(outs["levels"], outs["dataflow"])

@@ -15,10 +15,11 @@ from tests.helpers import (FFT_CONFIGS, config_signal, golden_json, golden_npz, 
 PARAMS = {"EXACT": EXACT_PARAMS, "DEFAULT0": DEFAULT0_PARAMS}
 
 
-def _build(cfg, lanes=1, keep_all=False, values=None):
+def _build(cfg, lanes=1, keep_all=False, values=None, schedule="levels"):
     pname, seed, (F, f), dims, _ = FFT_CONFIGS[cfg]
     scheme = GswScheme(PARAMS[pname])
-    eng = GpuEngine(scheme, dry_run=True, record_trace=True, batch_size=lanes, keep_all=keep_all)
+    eng = GpuEngine(scheme, dry_run=True, record_trace=True, batch_size=lanes, keep_all=keep_all,
+                    schedule=schedule)
     if values is None:
         values = config_signal(cfg)[1]
     sig = input_signal(eng, values, FixedFormat(F, f), dims=dims if isinstance(dims, tuple) else None)
@@ -138,3 +139,36 @@ def test_cse_keeps_reference_counts():
     eng.flush()
     store = replay_dry(eng)
     assert read_dry(eng, store, [x, y]) == [0b0110, 0b0001]
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg0"])
+def test_dataflow_compile_is_single_assignment_with_exact_deps(cfg):
+    """schedule='dataflow': no slot written twice, none overwritten after an earlier read in
+    the program, deps name the producing op (< own index); replay still equals the oracle."""
+    eng, out = _build(cfg, schedule="dataflow")
+    eng.flush()
+    comp = eng.dry_programs[0]
+    ops, deps = comp["ops"], comp["deps"]
+    outs = ops["out"].astype(np.int64)
+    assert len(np.unique(outs)) == len(outs)                       # single assignment
+    first_read = {}
+    for i, (l, r) in enumerate(zip(ops["left"].tolist(), ops["right"].tolist())):
+        first_read.setdefault(l, i)
+        first_read.setdefault(r, i)
+    for j, o in enumerate(outs.tolist()):                          # no write-after-read
+        assert first_read.get(o, len(outs)) > j
+    idx = np.arange(len(ops))
+    for side, col in ((0, "left"), (1, "right")):
+        d = deps[:, side]
+        assert ((d >= -1) & (d < idx)).all()
+        has = d >= 0
+        assert np.array_equal(ops[col][has], ops["out"][d[has]])     # operand = producer's slot
+    store = replay_dry(eng)
+    handles = [h for w in signal_words(out) for h in w.bits]
+    bits = read_dry(eng, store, handles)
+    F = FFT_CONFIGS[cfg][2][0]
+    words = []
+    for i in range(0, len(bits), F):
+        u = sum((b & 1) << k for k, b in enumerate(bits[i:i + F]))
+        words.append(u - (1 << F) if u >> (F - 1) else u)
+    assert words == model_outputs(cfg, config_signal(cfg)[1][None])[0].tolist()

@@ -7,12 +7,13 @@ from tests.helpers import FFT_CONFIGS, config_signal
 from paper_1611_08769_b200 import DEFAULT0_PARAMS, EXACT_PARAMS
 cfg = sys.argv[1]
 dbg = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+schedule = sys.argv[3] if len(sys.argv) > 3 else 'levels'
 pname, seed, (F, f), dims, _ = FFT_CONFIGS[cfg]
 params = {"EXACT": EXACT_PARAMS, "DEFAULT0": DEFAULT0_PARAMS}[pname]
 s = GswScheme(params); keys = s.keygen(seed)
 rng, x = config_signal(cfg)
 t0 = time.time()
-eng = GpuEngine(s, keys=keys, rng=rng, device_encrypt=True)
+eng = GpuEngine(s, keys=keys, rng=rng, device_encrypt=True, schedule=schedule)
 stream = torch.cuda.Stream(); torch.cuda.set_stream(stream); s.ctx.use_torch_stream(stream)
 sig = input_signal(eng, x, FixedFormat(F, f), dims=dims if isinstance(dims, tuple) else None)
 out = fft_2d(sig) if isinstance(dims, tuple) else fft_1d(sig)
@@ -21,7 +22,7 @@ prog = eng.flush(); torch.cuda.synchronize()
 s.ctx.set_debug(dbg)
 comp = eng.last_compile
 w = comp["widths"]
-print(f"{cfg}: nands={eng.nand_count} levels={len(w)} build_s={build:.2f} slots={eng._n_slots} widths min/med/max={w.min()}/{int(np.median(w))}/{w.max()}")
+print(f"{cfg} [{schedule}, launches={prog.launches}]: nands={eng.nand_count} levels={len(w)} build_s={build:.2f} slots={eng._n_slots} widths min/med/max={w.min()}/{int(np.median(w))}/{w.max()}")
 for _ in range(2): prog.run(1)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(stream)
