@@ -110,3 +110,27 @@ def read_dry(engine, store, handles):
             v = store[engine._slot[h.node]]
             out.append(v ^ engine.mask if h.neg else v)
     return out
+
+
+def int_word(engine, ints, width):
+    """A word of fresh wires holding one two's-complement integer per lane (lanes packed)."""
+    from paper_1611_08769_b200 import FixedFormat, FixedWord
+    u = [int(v) % (1 << width) for v in ints]
+    wires = [engine.input_bit(sum(((x >> b) & 1) << l for l, x in enumerate(u))) for b in range(width)]
+    return FixedWord(tuple(wires), FixedFormat(width, 1))
+
+
+def word_ints(engine, word, signed=True):
+    """Per-lane integers of a word (one read-back gather)."""
+    masks = engine.read_back_many(list(word.bits))
+    width = len(word.bits)
+    out = []
+    for lane in range(engine.batch_size):
+        u = sum(((m >> lane) & 1) << b for b, m in enumerate(masks))
+        out.append(u - (1 << width) if signed and u >> (width - 1) else u)
+    return out
+
+
+def wrap(v, width):
+    v %= 1 << width
+    return v - (1 << width) if v >> (width - 1) else v
