@@ -143,8 +143,26 @@ class Program:
                                        self.n_levels, ctypes.byref(h)), "prog_create")
         self.handle = h
         self.launches = int(_lib.fhegpu_prog_launches(h))
+        # tiled programs (GpuEngine schedule 'tiled'): ops are replicated per lane chunk, so
+        # every run launches `tile_lanes` lanes whatever the caller's batch; `base` keeps the
+        # untiled level program's (ops, offsets) for level-wise uses (host streaming)
+        self.tile_lanes = None
+        self.base = None
+        self._base_prog = None
+
+    def level_program(self) -> "Program":
+        """The untiled level program (itself unless tiled)."""
+        if self.base is None:
+            return self
+        if self._base_prog is None:
+            self._base_prog = Program(self.ctx, *self.base)
+        return self._base_prog
 
     def run(self, lanes: int = 1, first: int = 0, last: int | None = None):
+        if self.tile_lanes is not None:
+            if (first, last) != (0, None) and (first, last) != (0, self.n_levels):
+                raise UsageError("a tiled program runs whole")
+            lanes = self.tile_lanes
         if first == 0 and last is None:
             _check(_lib.fhegpu_prog_run(self.ctx.handle, self.handle, lanes), "prog_run")
             return

@@ -225,13 +225,13 @@ class GpuEngine(LevelledNetlist):
     def __init__(self, scheme: GswScheme, keys: KeyPair | None = None, public_key=None,
                  rng=None, threads: int = 1, batch_size: int = 1, lane_rngs=None,
                  cse: bool = False, keep_all: bool = False, record_trace: bool = False,
-                 dry_run: bool = False, device_encrypt: bool = False, schedule: str = "levels"):
+                 dry_run: bool = False, device_encrypt: bool = False, schedule: str = "auto"):
         if threads < 1:
             raise UsageError("threads must be >= 1")
         if batch_size < 1:
             raise UsageError("batch_size must be >= 1")
-        if schedule not in ("levels", "dataflow"):
-            raise UsageError(f"schedule must be 'levels' or 'dataflow', got {schedule!r}")
+        if schedule not in ("auto", "levels", "dataflow", "tiled"):
+            raise UsageError(f"schedule must be 'auto', 'levels', 'dataflow' or 'tiled', got {schedule!r}")
         self.schedule = schedule
         if lane_rngs is not None and len(lane_rngs) != batch_size:
             raise UsageError("need one rng per lane")
@@ -581,8 +581,10 @@ class GpuEngine(LevelledNetlist):
             self._upload_inputs()
         if not self._pending_ops:
             return None
-        dataflow = self._use_dataflow()
+        sched = self._pick_schedule()
+        dataflow = sched in ("dataflow", "tiled")
         prog = self._compile(ssa=dataflow)
+        prog["schedule"] = sched
         self._pending_ops = []
         if self._cse_map is not None:
             self._cse_map = {}
@@ -591,24 +593,74 @@ class GpuEngine(LevelledNetlist):
             self.dry_programs.append(prog)
             return prog
         self._ensure_capacity()
-        program = self.ctx.program(prog["ops"], prog["offsets"])
-        if dataflow:
-            program.set_deps(prog["deps"])
-        program.run(self.batch_size)
+        lanes = self.batch_size
+        if sched == "tiled":
+            K = self.batch_size // self.TILE_LANES
+            tops, tdeps = self._tile(prog, K)
+            program = self.ctx.program(tops, np.array([0, len(tops)], dtype=np.uint64))
+            program.set_deps(tdeps)
+            program.tile_lanes = lanes = self.TILE_LANES
+            program.base = (prog["ops"], prog["offsets"])
+        else:
+            program = self.ctx.program(prog["ops"], prog["offsets"])
+            if dataflow:
+                program.set_deps(prog["deps"])
+        program.run(lanes)
         self.last_program = program
         self.last_compile = prog
         self.programs_run += 1
         self.launches += program.launches
         return program
 
-    def _use_dataflow(self) -> bool:
-        """schedule='dataflow': one launch per program with per-operand readiness (per-CTA
-        progress counters) instead of one launch per level; needs SSA slots (no reuse inside
-        the program) and the warp-specialised tcgen05 kernel (k = 9, ell = 29; other
-        parameter sets fall back to level launches).  Measured on B200 it does not beat
-        level launches + PDL for the reference's FFT netlists: a dependency
-        hop costs ~10 us of pipeline latency and the deep netlists are hop-bound."""
-        return self.schedule == "dataflow"
+    # tiled dataflow: lanes per chunk, and the single-assignment store budget it may use
+    TILE_LANES = 256
+    TILED_MAX_BYTES = 100 << 30
+
+    def _pick_schedule(self) -> str:
+        """'levels', 'dataflow' or 'tiled' for the pending program.
+
+        levels    one launch per netlist level over all lanes (PDL between launches).
+        dataflow  the whole program in one launch, operands awaited per item (opt-in: for
+                  the reference's deep single-signal netlists it does not beat levels).
+        tiled     lanes cut into chunks of TILE_LANES; the program is replicated per chunk
+                  and run as ONE dataflow launch in wavefront order (step s = level 0 of chunk
+                  s, level 1 of chunk s-1, ...), so a chunk's intermediates are consumed while
+                  still in L2.  The DRAM traffic it saves is energy under the board power cap:
+                  cfg1 143 -> 154M NAND/s.  'auto' picks it for wide programs
+                  whose single-assignment store fits TILED_MAX_BYTES."""
+        if self.schedule != "auto":
+            return self.schedule
+        if self.dry_run or (self.params.k, self.params.ell) != (9, 29):
+            return "levels"
+        C = self.TILE_LANES
+        if self.batch_size % C or self.batch_size < 8 * C:
+            return "levels"
+        n_ops = len(self._pending_ops) // 5
+        ct_bytes = ((self.params.n_ct * self.params.k + 3) // 4) * 16
+        if (self._n_slots + n_ops) * self.batch_size * ct_bytes > self.TILED_MAX_BYTES:
+            return "levels"
+        return "tiled"
+
+    @staticmethod
+    def _tile(prog, K):
+        """Replicate an SSA program over K lane chunks: op (c, o) uses slot s*K + c (a batch-wide
+        slot s IS chunk-slots s*K + c of batch/K lanes each), wavefront order, remapped deps."""
+        ops, deps, offs = prog["ops"], prog["deps"], prog["offsets"].astype(np.int64)
+        n = len(ops)
+        rank = np.repeat(np.arange(len(offs) - 1), np.diff(offs))          # level index per op
+        cc = np.repeat(np.arange(K, dtype=np.int64), n)
+        oo = np.tile(np.arange(n, dtype=np.int64), K)
+        perm = np.lexsort((cc, oo, rank[oo], cc + rank[oo]))               # step, level, op, chunk
+        pos = np.empty(K * n, dtype=np.int64)
+        pos[perm] = np.arange(K * n)
+        c, o = cc[perm], oo[perm]
+        tiled = np.empty(K * n, dtype=ops.dtype)
+        for f in ("left", "right", "out"):
+            tiled[f] = ops[f][o].astype(np.int64) * K + c
+        tiled["flags"] = ops["flags"][o]
+        d = deps[o]
+        tdeps = np.where(d >= 0, pos[c[:, None] * n + np.maximum(d, 0)], -1).astype(np.int32)
+        return tiled, tdeps
 
     def run_host(self, program, inputs, outputs, chunk_lanes: int = 32768, out=None,
                  sync: bool = True, packed: bool = False):
@@ -663,8 +715,8 @@ class GpuEngine(LevelledNetlist):
         need = regions * n_slots * chunk
         if self.ctx.capacity < need:
             self.ctx.reserve(need)
-        program.run_host(lanes, chunk, in_slots, in_ptrs, out_slots, out_ptrs,
-                         host_format=1 if packed else 0)
+        program.level_program().run_host(lanes, chunk, in_slots, in_ptrs, out_slots, out_ptrs,
+                                         host_format=1 if packed else 0)
         if sync:
             self.ctx.sync()
         return out

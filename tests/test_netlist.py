@@ -172,3 +172,39 @@ def test_dataflow_compile_is_single_assignment_with_exact_deps(cfg):
         u = sum((b & 1) << k for k, b in enumerate(bits[i:i + F]))
         words.append(u - (1 << F) if u >> (F - 1) else u)
     assert words == model_outputs(cfg, config_signal(cfg)[1][None])[0].tolist()
+
+
+@pytest.mark.parametrize("cfg,lanes,K", [("cfg0", 8, 4), ("cfg4", 6, 3)])
+def test_tiled_program_equals_level_program(cfg, lanes, K):
+    """Tiling (schedule 'tiled'): the SSA program replicated over K lane chunks in wavefront
+    order computes the same store as the level program (a batch-wide slot s over B lanes IS
+    chunk-slots s*K + c over B/K lanes), and its deps name earlier ops writing the operand."""
+    vals = np.array([config_signal(cfg, lane)[1] for lane in range(lanes)]) if cfg == "cfg4" \
+        else np.repeat(config_signal(cfg)[1][None], lanes, axis=0)
+    eng, out = _build(cfg, lanes=lanes, values=vals, schedule="dataflow")
+    eng.flush()
+    comp = eng.dry_programs[0]
+    C = lanes // K
+    tops, tdeps = GpuEngine._tile(comp, K)
+    n = len(tops)
+    assert n == K * len(comp["ops"])
+    idx = np.arange(n)
+    for side, col in ((0, "left"), (1, "right")):
+        d = tdeps[:, side]
+        assert ((d >= -1) & (d < idx)).all()
+        assert np.array_equal(tops[col][d >= 0], tops["out"][d[d >= 0]])
+    # replay both on one flat lane-bit store (index = slot * lanes + lane)
+    n_slots = max(int(comp["ops"][f].max()) for f in ("left", "right", "out")) + 1
+    base = np.zeros(n_slots * lanes, dtype=np.uint8)
+    for slot, bits in eng.dry_inputs:
+        base[slot * lanes: (slot + 1) * lanes] = [(bits >> l) & 1 for l in range(lanes)]
+    ref, til = base.copy(), base.copy()
+    lane = np.arange(lanes)
+    for l, r, o, f in comp["ops"].tolist():
+        a, b = ref[l * lanes + lane] ^ (f & 1), ref[r * lanes + lane] ^ ((f >> 1) & 1)
+        ref[o * lanes + lane] = 1 - (a & b)
+    cl = np.arange(C)
+    for l, r, o, f in tops.tolist():
+        a, b = til[l * C + cl] ^ (f & 1), til[r * C + cl] ^ ((f >> 1) & 1)
+        til[o * C + cl] = 1 - (a & b)
+    assert np.array_equal(ref, til)
