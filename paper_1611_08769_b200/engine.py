@@ -26,6 +26,7 @@ randomness from ``lane_rngs[l]`` (or the single ``rng``, lane-major).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -596,7 +597,7 @@ class GpuEngine(LevelledNetlist):
         lanes = self.batch_size
         if sched == "tiled":
             K = self.batch_size // self.TILE_LANES
-            tops, tdeps = self._tile(prog, K)
+            tops, tdeps = self._tile(prog, K, self.TILE_LANES, self.TILE_SKEW, self.TILE_WINDOW)
             program = self.ctx.program(tops, np.array([0, len(tops)], dtype=np.uint64))
             program.set_deps(tdeps)
             program.tile_lanes = lanes = self.TILE_LANES
@@ -613,7 +614,9 @@ class GpuEngine(LevelledNetlist):
         return program
 
     # tiled dataflow: lanes per chunk, and the single-assignment store budget it may use
-    TILE_LANES = 256
+    TILE_LANES = int(os.environ.get("FHEGPU_TILE_LANES", "128"))
+    TILE_SKEW = int(os.environ.get("FHEGPU_TILE_SKEW", "0"))      # 0: pick from the window below
+    TILE_WINDOW = 1536        # items between a level and the next of one chunk (> ~1036 in flight)
     TILED_MAX_BYTES = 100 << 30
 
     def _pick_schedule(self) -> str:
@@ -626,7 +629,7 @@ class GpuEngine(LevelledNetlist):
                   and run as ONE dataflow launch in wavefront order (step s = level 0 of chunk
                   s, level 1 of chunk s-1, ...), so a chunk's intermediates are consumed while
                   still in L2.  The DRAM traffic it saves is energy under the board power cap:
-                  cfg1 143 -> 154M NAND/s.  'auto' picks it for wide programs
+                  cfg1 143 -> 158M NAND/s.  'auto' picks it for wide programs
                   whose single-assignment store fits TILED_MAX_BYTES."""
         if self.schedule != "auto":
             return self.schedule
@@ -642,15 +645,21 @@ class GpuEngine(LevelledNetlist):
         return "tiled"
 
     @staticmethod
-    def _tile(prog, K):
+    def _tile(prog, K, lanes_per_chunk=1, skew=0, window=2048):
         """Replicate an SSA program over K lane chunks: op (c, o) uses slot s*K + c (a batch-wide
-        slot s IS chunk-slots s*K + c of batch/K lanes each), wavefront order, remapped deps."""
+        slot s IS chunk-slots s*K + c of batch/K lanes each), wavefront order, remapped deps.
+
+        Wavefront step of op (c, o) = c + skew * level(o): consecutive levels of one chunk are
+        `skew` steps (~skew * n_ops * lanes_per_chunk items) apart, which must exceed what is in
+        flight on the GPU (~148 CTAs x 7 stages) or consumers stall on their producers."""
         ops, deps, offs = prog["ops"], prog["deps"], prog["offsets"].astype(np.int64)
         n = len(ops)
+        if skew <= 0:
+            skew = max(1, -(-window // max(1, n * lanes_per_chunk)))
         rank = np.repeat(np.arange(len(offs) - 1), np.diff(offs))          # level index per op
         cc = np.repeat(np.arange(K, dtype=np.int64), n)
         oo = np.tile(np.arange(n, dtype=np.int64), K)
-        perm = np.lexsort((cc, oo, rank[oo], cc + rank[oo]))               # step, level, op, chunk
+        perm = np.lexsort((cc, oo, rank[oo], cc + skew * rank[oo]))        # step, level, op, chunk
         pos = np.empty(K * n, dtype=np.int64)
         pos[perm] = np.arange(K * n)
         c, o = cc[perm], oo[perm]

@@ -176,7 +176,7 @@ def test_dataflow_many_lanes_equals_levels():
 
 
 def test_tiled_schedule_equals_levels_bit_exact():
-    """schedule='tiled' (auto for wide programs): 4096 XOR+AND pairs in 16 chunks of 256 lanes,
+    """schedule='tiled' (auto for wide programs): 4096 XOR+AND pairs in 32 chunks of 128 lanes,
     one wavefront dataflow launch -- every output ciphertext equals the level schedule's."""
     scheme = GswScheme(DEFAULT_PARAMS)
     keys = scheme.keygen(1)
@@ -188,7 +188,7 @@ def test_tiled_schedule_equals_levels_bit_exact():
         a, b = eng.input_block(bits)
         x, y = xor_(a, b), and_(a, b)
         prog = eng.flush()
-        assert (prog.tile_lanes == 256) == (schedule == "tiled")
+        assert (prog.tile_lanes == 128) == (schedule == "tiled")
         outs[schedule] = eng.node_values([x, y])
         assert (eng.read_back_bits([x, y]) == np.stack([bits[:, 0] ^ bits[:, 1], bits[:, 0] & bits[:, 1]])).all()
         prog.run(4096)                                     # re-running rewrites identical values
