@@ -13,6 +13,7 @@ FFTs (DEFAULT dims, noise-free), reported as FFTs/s.
   e2e        same metric through the C-ABI with host buffers: pinned H2D of the
              step's input ciphertexts + evaluation + D2H of every output ciphertext
   roofline   level_tc_ws_kernel: algorithmic bytes 3*ceil(N^2/8) per NAND / avg launch time
+             (cfg1 runs as ONE tiled dataflow launch per step: launch time = step time)
   cpu_baseline  the reference algorithm (oracle/gsw.py restates fhe.py:325-341:
              float64 N x N product + flatten) on this box's host cores, time-boxed sample
 
@@ -221,13 +222,14 @@ def level_launch_times(prog, lanes, stream, reps=3):
     return out
 
 
-def _traffic_from_profiles(widths_items, lanes):
-    """dram bytes per launch from the committed ncu capture (profiles/ncu_traffic.json)."""
+def _traffic_from_profiles(widths_items, launches):
+    """dram bytes per launch from the committed ncu capture (profiles/ncu_traffic.json): bytes
+    per gate item of the captured launch x the items one launch of this step processes."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             d = json.load(fh)
         per_item = d["dram_bytes_per_item"]
-        items = sum(widths_items) / max(1, len(widths_items))
+        items = sum(widths_items) / max(1, launches)
         return per_item * items, d
     except Exception:
         return None, None
@@ -270,7 +272,7 @@ def bench_gates(args, world, rank, local):
     peak, peak_kind = _peaks()
     bytes_per_launch = [w * ALG_BYTES_PER_NAND_261 for w in widths_items]
     achieved = sum(bytes_per_launch) / (sum(lv_ms) / 1e3) / 1e9        # GB/s
-    traffic, tinfo = _traffic_from_profiles(widths_items, lanes)
+    traffic, tinfo = _traffic_from_profiles(widths_items, prog.launches)
     res = {
         "ms": ms, "nand_per_step": nand_per_step, "exec_per_step": exec_per_step,
         "launches_per_step": prog.launches, "widths": [int(w) for w in comp["widths"]],
@@ -278,6 +280,8 @@ def bench_gates(args, world, rank, local):
         "traffic": traffic, "traffic_info": tinfo, "ok": ok, "setup_s": setup_s,
         "clocks": sampler.summary(), "kernel": scheme.ctx.kernel,
         "slots": eng._n_slots, "store_gb": eng._n_slots * lanes * scheme.ctx.ct_words * 4 / 1e9,
+        "schedule": comp.get("schedule", "levels") + (f" ({prog.tile_lanes}-lane chunks, one wavefront "
+                                                      f"dataflow launch per step)" if prog.tile_lanes else ""),
     }
     if args.e2e:
         res["e2e"] = e2e_gates(eng, scheme, prog, lanes, (a, b), (x, y), stream, args, world, bits)
@@ -430,7 +434,7 @@ def run_ours(args):
             "levels": len(res["widths"]), "gates_per_level": res["widths"],
             "parallelism": f"replicas x{world} (independent pairs, no collective)",
             "l2": f"inputs {2 * args.pairs * 9408 / 1e9:.1f} GB per step >> 126 MB L2 (no flush needed)",
-            "kernel": res["kernel"], "decrypt_check": res["ok"],
+            "kernel": res["kernel"], "schedule": res["schedule"], "decrypt_check": res["ok"],
             "store_gb": round(res["store_gb"], 1), "setup_s": round(res["setup_s"], 2),
         },
         "roofline": {
