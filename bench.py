@@ -402,6 +402,49 @@ def bench_fft(args, world, rank, local):
             "build_s": build_s, "ok": ok}
 
 
+def bench_fft_single(args, world, rank, local, cfg):
+    """configs[2] (32-pt Q8.24) / configs[3] (8x8 Q9.7 2-D): one signal, FFT/s = 1 / latency.
+    Inputs follow the configs' seeds (DEFAULT dims, noise-free: 'default0'); decrypted outputs
+    are checked against the reference's own words (tests/golden/clear_cfgN.npz)."""
+    import numpy as np
+    import torch
+
+    from paper_1611_08769_b200 import DEFAULT0_PARAMS, FixedFormat, GpuEngine, GswScheme, fft_1d, fft_2d, input_signal
+    from paper_1611_08769_b200.fft import read_signal_ints
+    seed = {"cfg2": 2, "cfg3": 3}[cfg]
+    scheme = GswScheme(DEFAULT0_PARAMS, device=local)
+    keys = scheme.keygen(seed)
+    rng = np.random.default_rng(seed)
+    if cfg == "cfg2":
+        vals = rng.uniform(-1, 1, 32) + 1j * rng.uniform(-1, 1, 32)
+        fmt, dims = FixedFormat(32, 24), None
+    else:
+        vals = (rng.integers(0, 256, (8, 8)) / 255.0).ravel().astype(complex)
+        fmt, dims = FixedFormat(16, 7), (8, 8)
+    eng = GpuEngine(scheme, keys=keys, rng=rng, device_encrypt=True)
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    scheme.ctx.use_torch_stream(stream)
+    sig = input_signal(eng, vals, fmt, dims=dims)
+    out = fft_2d(sig) if dims else fft_1d(sig)
+    prog = eng.flush()
+    torch.cuda.synchronize()
+    got = read_signal_ints(eng, out)[0]
+    ok = None
+    try:
+        want = np.load(os.path.join(ROOT, "tests", "golden", f"clear_{cfg}.npz"))["words"][0]
+        ok = bool(np.array_equal(got, want))
+    except OSError:
+        pass
+    ms = time_program(prog, 1, stream, max(3, args.steps // 2), min(args.warmup, 3), world)
+    return {"metric": f"{'32-pt Q8.24' if cfg == 'cfg2' else '8x8 Q9.7 2-D'} FHE FFTs/s "
+                      f"(configs[{cfg[-1]}], one signal)",
+            "value": world / (ms / 1e3), "unit": "FFT/s", "ms_per_fft": ms,
+            "nand_per_s": eng.nand_count * world / (ms / 1e3), "nand_per_fft": eng.nand_count,
+            "levels": prog.n_levels, "launches_per_fft": prog.launches,
+            "decrypt_check_vs_reference": ok}
+
+
 def run_ours(args):
     world, rank, local = _dist()
     res = bench_gates(args, world, rank, local)
@@ -410,6 +453,12 @@ def run_ours(args):
         import gc
         gc.collect()
         fft = bench_fft(args, world, rank, local)
+    single = {}
+    if args.fft_single:
+        import gc
+        for cfg in ("cfg3", "cfg2"):
+            gc.collect()
+            single[cfg] = bench_fft_single(args, world, rank, local, cfg)
     cpu = None
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
         v, cores, total = cpu_reference(args.cpu_seconds)
@@ -462,6 +511,8 @@ def run_ours(args):
                        "unit": "FFT/s", "nand_per_s": fft["nand_per_s"], "ms_per_step": fft["ms"],
                        "lanes": fft["lanes"], "nand_per_fft": fft["nand_per_fft"],
                        "levels": fft["levels"], "decrypt_check_vs_reference": fft["ok"]}
+    if single:
+        line["fft_single"] = single
     if cpu is not None:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
@@ -512,6 +563,8 @@ def main():
     ap.add_argument("--e2e-format", choices=["packed", "compact"], default="packed",
                     help="host ciphertexts: reference-serialised bits (EFT1 rows) or compact u32")
     ap.add_argument("--no-fft", dest="fft", action="store_false")
+    ap.add_argument("--no-fft-single", dest="fft_single", action="store_false",
+                    help="skip configs[2]/[3] single-signal FFT latency")
     ap.add_argument("--fft-lanes", type=int, default=1024)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--ref-step-seconds", type=float, default=4.0)
