@@ -304,12 +304,21 @@ def e2e_gates(eng, scheme, prog, lanes, inputs, outputs, stream, args, world, bi
     t0 = time.perf_counter()
     # host ciphertexts as a client holds them: the reference's serialised bytes (ceil(N^2/8)
     # per ciphertext, fileio.py / EFT1 payload rows) or dense compact u32 rows
-    if packed:
-        bytes_ct = (p.n_ct * p.n_ct + 7) // 8
-        shape, dt = (lanes, bytes_ct), torch.uint8
-    else:
-        bytes_ct = p.n_ct * p.k * 4
-        shape, dt = (lanes, p.n_ct, p.k), torch.int32
+    bytes_ct = (p.n_ct * p.n_ct + 7) // 8 if packed else p.n_ct * p.k * 4
+    # pinned host buffers for every input and output ciphertext of the step; with several
+    # ranks per node they must share host RAM -- cap at half of what is available (the e2e
+    # figure is a rate; `lanes` in the JSON says how many lanes it streamed)
+    chunk = min(args.e2e_chunk, lanes)
+    total_lanes = lanes
+    try:
+        import psutil
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        per_lane = (len(inputs) + len(outputs)) * bytes_ct
+        cap = int(0.5 * psutil.virtual_memory().available / max(1, local_world) / per_lane)
+        lanes = min(lanes, max(chunk, cap // chunk * chunk))
+    except ImportError:
+        pass
+    shape, dt = ((lanes, bytes_ct), torch.uint8) if packed else ((lanes, p.n_ct, p.k), torch.int32)
     host_in = [torch.empty(shape, dtype=dt, pin_memory=True) for _ in inputs]
     host_out = [torch.empty(shape, dtype=dt, pin_memory=True) for _ in outputs]
     for i, f in enumerate(in_first):
@@ -318,8 +327,6 @@ def e2e_gates(eng, scheme, prog, lanes, inputs, outputs, stream, args, world, bi
         else:
             ctx.read_range(f, lanes, host_in[i].data_ptr())
     pin_s = time.perf_counter() - t0
-
-    chunk = min(args.e2e_chunk, lanes)
 
     def step():
         # fhegpu_prog_run_host: chunks of lanes stream host -> device -> host with copy-in,
@@ -357,6 +364,7 @@ def e2e_gates(eng, scheme, prog, lanes, inputs, outputs, stream, args, world, bi
     return {"ms": ms, "wall_ms": wall_ms, "steps": steps, "pin_s": pin_s,
             "h2d": len(inputs) * lanes * bytes_ct, "d2h": len(outputs) * lanes * bytes_ct,
             "chunk_lanes": chunk, "decrypt_check": ok, "host_format": args.e2e_format,
+            "lanes": lanes, "of_lanes": total_lanes, "nand": eng.nand_count * lanes,
             "bytes_per_ciphertext": bytes_ct,
             }
 
@@ -499,7 +507,7 @@ def run_ours(args):
     }
     if "e2e" in res:
         e = res["e2e"]
-        line["e2e"] = {"value": res["nand_per_step"] * world / (e["ms"] / 1e3), "unit": UNIT,
+        line["e2e"] = {"value": e["nand"] * world / (e["ms"] / 1e3), "unit": UNIT, "lanes": e["lanes"],
                        "h2d_bytes_per_step": e["h2d"], "d2h_bytes_per_step": e["d2h"],
                        "ms_per_step": e["ms"], "steps": e["steps"],
                        "chunk_lanes": e["chunk_lanes"], "decrypt_check": e["decrypt_check"],
