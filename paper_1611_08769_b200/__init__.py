@@ -23,9 +23,10 @@ from .scheme import (DEFAULT0_PARAMS, DEFAULT_PARAMS, EXACT_PARAMS, Ciphertext, 
 
 # reference name for the FHE bit engine
 FheEngine = GpuEngine
+CleartextEngine = GpuClearEngine
 
 __all__ = [
-    "CapabilityError", "Ciphertext", "ComplexFixed", "DEFAULT0_PARAMS", "DEFAULT_PARAMS",
+    "CapabilityError", "Ciphertext", "CleartextEngine", "GpuClearEngine", "ComplexFixed", "DEFAULT0_PARAMS", "DEFAULT_PARAMS",
     "DeviceError", "EXACT_PARAMS", "FheEngine", "FhefftError", "FixedFormat", "FixedWord",
     "GateStats", "GpuBit", "GpuEngine", "GswScheme", "KeyPair", "NoiseOverflowError",
     "ParameterError", "ParseError", "RangeError", "SchemeParams", "SignalBuffer", "TwiddleTable",
