@@ -129,7 +129,7 @@ class LevelledNetlist:
             out[s:e] = seg
         return out
 
-    def _compile(self, ssa: bool = False):
+    def _compile(self, ssa: bool = False, ring_temps: bool = False):
         """Level-sort the pending gates and assign ciphertext slots by liveness.
 
         A slot read at level L is released before the launch of level L + 1 at
@@ -139,6 +139,10 @@ class LevelledNetlist:
         ssa=True (dataflow programs, one launch without level boundaries): no slot is
         reused within the program -- slots released by it return to the pool only after
         it -- and ``deps`` gives, per op, the op indices that produced its operands.
+
+        ring_temps=True (tiled programs): outputs nobody holds after the program
+        ("temporaries") get no batch-wide slot; ``temp`` (per op: left, right, out) carries
+        their index 0..n_temp-1 instead (-1 elsewhere) for _tile to place in an L2-sized ring.
         """
         ops = np.asarray(self._pending_ops, dtype=np.int64).reshape(-1, 5)
         level = np.asarray(self._level, dtype=np.int64)
@@ -167,6 +171,10 @@ class LevelledNetlist:
             new_dead[out] = True
             new_dead &= dead
             free_at[new_dead] = np.maximum(last_use[new_dead], level[new_dead]) + 1
+        temp_id = np.full(n_nodes, -1, dtype=np.int64)
+        if ring_temps and not self.keep_all:
+            tnodes = out[new_dead[out]]
+            temp_id[tnodes] = np.arange(len(tnodes))
         cand = np.nonzero(free_at != never)[0]
         cand = cand[np.argsort(free_at[cand], kind="stable")]
         cand_at = free_at[cand]
@@ -187,7 +195,10 @@ class LevelledNetlist:
                 else:
                     free.extend(rel[rel >= 0].tolist())
                 ptr = hi
-            cnt = e - s
+            outs = out[s:e]
+            if ring_temps:
+                outs = outs[temp_id[outs] < 0]             # temporaries live in the ring
+            cnt = len(outs)
             take = min(cnt, len(free))
             new_slots = np.empty(cnt, dtype=np.int64)
             if take:
@@ -196,12 +207,13 @@ class LevelledNetlist:
             if cnt > take:
                 new_slots[take:] = np.arange(self._n_slots, self._n_slots + cnt - take)
                 self._n_slots += cnt - take
-            slot[out[s:e]] = new_slots
+            slot[outs] = new_slots
         table = np.empty(len(out), dtype=[("left", "<u4"), ("right", "<u4"),
                                           ("out", "<u4"), ("flags", "<u4")])
-        table["left"] = slot[left]
-        table["right"] = slot[right]
-        table["out"] = slot[out]
+        lo = 0 if ring_temps else None              # ring temporaries: placeholder, see _tile
+        table["left"] = np.clip(slot[left], lo, None)
+        table["right"] = np.clip(slot[right], lo, None)
+        table["out"] = np.clip(slot[out], lo, None)
         table["flags"] = lneg | (rneg << 1)
         if ptr < len(cand):                       # released after the last launch
             rel = slot[cand[ptr:]]
@@ -217,6 +229,9 @@ class LevelledNetlist:
             producer = np.full(n_nodes, -1, dtype=np.int64)
             producer[out] = np.arange(len(out))
             prog["deps"] = np.stack([producer[left], producer[right]], axis=1).astype(np.int32)
+        if ring_temps:
+            prog["temp"] = np.stack([temp_id[left], temp_id[right], temp_id[out]], axis=1)
+            prog["n_temp"] = int((temp_id[out] >= 0).sum())
         return prog
 
 
@@ -584,7 +599,8 @@ class GpuEngine(LevelledNetlist):
             return None
         sched = self._pick_schedule()
         dataflow = sched in ("dataflow", "tiled")
-        prog = self._compile(ssa=dataflow)
+        ring = self.TILE_RING if sched == "tiled" and self._ring_ok() else 0
+        prog = self._compile(ssa=dataflow, ring_temps=ring > 0)
         prog["schedule"] = sched
         self._pending_ops = []
         if self._cse_map is not None:
@@ -597,7 +613,15 @@ class GpuEngine(LevelledNetlist):
         lanes = self.batch_size
         if sched == "tiled":
             K = self.batch_size // self.TILE_LANES
-            tops, tdeps = self._tile(prog, K, self.TILE_LANES, self.TILE_SKEW, self.TILE_WINDOW)
+            t_base = self._n_slots * K                       # ring after every batch-wide slot
+            if ring:
+                skew = self.TILE_SKEW or max(1, -(-self.TILE_WINDOW // (len(prog["ops"]) * self.TILE_LANES)))
+                ring = max(ring, skew * (len(prog["offsets"]) - 2) + 1)
+                need = self._n_slots * self.batch_size + ring * prog["n_temp"] * self.TILE_LANES
+                if self.ctx.capacity < need:
+                    self.ctx.reserve(need)
+            tops, tdeps = self._tile(prog, K, self.TILE_LANES, self.TILE_SKEW, self.TILE_WINDOW,
+                                     ring, t_base)
             program = self.ctx.program(tops, np.array([0, len(tops)], dtype=np.uint64))
             program.set_deps(tdeps)
             program.tile_lanes = lanes = self.TILE_LANES
@@ -617,6 +641,17 @@ class GpuEngine(LevelledNetlist):
     TILE_LANES = int(os.environ.get("FHEGPU_TILE_LANES", "128"))
     TILE_SKEW = int(os.environ.get("FHEGPU_TILE_SKEW", "0"))      # 0: pick from the window below
     TILE_WINDOW = 1536        # items between a level and the next of one chunk (> ~1036 in flight)
+    TILE_RING = int(os.environ.get("FHEGPU_TILE_RING", "8"))      # chunks of temporaries kept in L2
+
+    def _ring_ok(self) -> bool:
+        """Ring temporaries need the program to have at most two sinks (see _tile)."""
+        if self.TILE_RING <= 0 or self.keep_all:
+            return False
+        ops = np.asarray(self._pending_ops, dtype=np.int64).reshape(-1, 5)
+        read = np.zeros(len(self._level), dtype=bool)
+        read[ops[:, 0]] = True
+        read[ops[:, 2]] = True
+        return 1 <= int((~read[ops[:, 4]]).sum()) <= 2
     TILED_MAX_BYTES = 100 << 30
 
     def _pick_schedule(self) -> str:
@@ -645,13 +680,20 @@ class GpuEngine(LevelledNetlist):
         return "tiled"
 
     @staticmethod
-    def _tile(prog, K, lanes_per_chunk=1, skew=0, window=2048):
+    def _tile(prog, K, lanes_per_chunk=1, skew=0, window=2048, ring=0, t_base=0):
         """Replicate an SSA program over K lane chunks: op (c, o) uses slot s*K + c (a batch-wide
         slot s IS chunk-slots s*K + c of batch/K lanes each), wavefront order, remapped deps.
 
         Wavefront step of op (c, o) = c + skew * level(o): consecutive levels of one chunk are
         `skew` steps (~skew * n_ops * lanes_per_chunk items) apart, which must exceed what is in
-        flight on the GPU (~148 CTAs x 7 stages) or consumers stall on their producers."""
+        flight on the GPU (~148 CTAs x 7 stages) or consumers stall on their producers.
+
+        ring > 0 (program compiled with ring_temps): temporaries of chunk c live in region
+        c % ring of a small ring at chunk-slot t_base (it stays in L2; no write-back of dead
+        values).  Write-after-read safety through the RAW machinery: the roots of chunk c (ops
+        with no producer in the program; every other op descends from one) also wait for the
+        sinks of chunk c - ring (ops whose output nothing in the program reads), whose
+        completion implies every read of that chunk's temporaries in the lane is done."""
         ops, deps, offs = prog["ops"], prog["deps"], prog["offsets"].astype(np.int64)
         n = len(ops)
         if skew <= 0:
@@ -664,12 +706,30 @@ class GpuEngine(LevelledNetlist):
         pos[perm] = np.arange(K * n)
         c, o = cc[perm], oo[perm]
         tiled = np.empty(K * n, dtype=ops.dtype)
-        for f in ("left", "right", "out"):
-            tiled[f] = ops[f][o].astype(np.int64) * K + c
+        temp = prog.get("temp") if ring else None
+        for i, f in enumerate(("left", "right", "out")):
+            v = ops[f][o].astype(np.int64) * K + c
+            if temp is not None:
+                tid = temp[o, i]
+                v = np.where(tid >= 0, t_base + (c % ring) * prog["n_temp"] + tid, v)
+            tiled[f] = v
         tiled["flags"] = ops["flags"][o]
         d = deps[o]
-        tdeps = np.where(d >= 0, pos[c[:, None] * n + np.maximum(d, 0)], -1).astype(np.int32)
-        return tiled, tdeps
+        tdeps = np.where(d >= 0, pos[c[:, None] * n + np.maximum(d, 0)], -1)
+        if temp is not None:
+            # a root of chunk c (step c) must come after the sinks of chunk c - ring (step
+            # c - ring + skew * level): ring > skew * deepest level keeps the order topological
+            read = np.zeros(n, dtype=bool)
+            read[deps[deps >= 0]] = True
+            sinks = np.flatnonzero(~read)
+            roots = (deps < 0).all(axis=1)
+            assert 1 <= len(sinks) <= 2, "ring temporaries need at most two sinks"
+            assert ring > skew * int(rank[sinks].max()), "ring too short for the wavefront skew"
+            war = roots[o] & (c >= ring)
+            prev = (c[war] - ring) * n
+            tdeps[war, 0] = pos[prev + sinks[0]]
+            tdeps[war, 1] = pos[prev + sinks[-1]]
+        return tiled, tdeps.astype(np.int32)
 
     def run_host(self, program, inputs, outputs, chunk_lanes: int = 32768, out=None,
                  sync: bool = True, packed: bool = False):

@@ -208,3 +208,36 @@ def test_tiled_program_equals_level_program(cfg, lanes, K):
         a, b = til[l * C + cl] ^ (f & 1), til[r * C + cl] ^ ((f >> 1) & 1)
         til[o * C + cl] = 1 - (a & b)
     assert np.array_equal(ref, til)
+
+
+def test_tiled_ring_temporaries_replay_and_war_order():
+    """Ring temporaries (tiled schedule): XOR+AND over 16 lanes in 8 chunks of 2 lanes, a ring
+    of 5 chunk regions; sequential replay in tiled order equals the level program, every
+    dependency (RAW and the roots' write-after-read deps on chunk c-5's sinks) points back."""
+    from paper_1611_08769_b200 import and_, xor_
+    lanes, K, ring = 16, 8, 5
+    eng = GpuEngine(GswScheme(DEFAULT_PARAMS), dry_run=True, batch_size=lanes, schedule="dataflow")
+    rng = np.random.default_rng(3)
+    bits = rng.integers(0, 2, (lanes, 2))
+    a = eng.input_bit(int(sum(int(v) << i for i, v in enumerate(bits[:, 0]))))
+    b = eng.input_bit(int(sum(int(v) << i for i, v in enumerate(bits[:, 1]))))
+    x, y = xor_(a, b), and_(a, b)
+    assert eng._ring_ok()
+    prog = eng._compile(ssa=True, ring_temps=True)
+    assert prog["n_temp"] == 4 and eng._n_slots == 4          # a, b, x, y only
+    C = lanes // K
+    t_base = eng._n_slots * K
+    tops, tdeps = GpuEngine._tile(prog, K, C, skew=2, ring=ring, t_base=t_base)
+    idx = np.arange(len(tops))
+    assert ((tdeps >= -1) & (tdeps < idx[:, None])).all()
+    assert int(tops["out"].max()) < t_base + ring * prog["n_temp"]
+    store = np.zeros((t_base + ring * prog["n_temp"]) * C, dtype=np.uint8)
+    for slot, bmask in eng.dry_inputs:
+        store[slot * lanes:(slot + 1) * lanes] = [(bmask >> l) & 1 for l in range(lanes)]
+    cl = np.arange(C)
+    for l, r, o, f in tops.tolist():
+        u, v = store[l * C + cl] ^ (f & 1), store[r * C + cl] ^ ((f >> 1) & 1)
+        store[o * C + cl] = 1 - (u & v)
+    xs, ys = eng._slot[x.node], eng._slot[y.node]
+    assert (store[xs * lanes:(xs + 1) * lanes] == (bits[:, 0] ^ bits[:, 1])).all()
+    assert (store[ys * lanes:(ys + 1) * lanes] == (bits[:, 0] & bits[:, 1])).all()

@@ -37,11 +37,12 @@ for c in range(K):
     for j, (l, r, out, dl, dr) in enumerate(rows):
         ops[o + j] = (l, r, out, 0)
         deps[o + j] = (dl, dr)
-WAVE = len(sys.argv) > 4 and sys.argv[4] == "wave"
-if WAVE:   # step s: level 0 of chunk s, level 1 of chunk s-1, level 2 of chunk s-2
+WAVE = len(sys.argv) > 4 and sys.argv[4].startswith("wave")
+SKEW = int(sys.argv[4][4:] or 1) if WAVE else 1
+if WAVE:   # step s: level 0 of chunk s, level 1 of chunk s-SKEW, level 2 of chunk s-2*SKEW
     lvl = np.tile(np.array([0, 0, 1, 1, 2, 1]), K)
     chunk = np.repeat(np.arange(K), 6)
-    perm = np.lexsort((np.tile(np.arange(6), K), lvl, chunk + lvl))
+    perm = np.lexsort((np.tile(np.arange(6), K), lvl, chunk + SKEW * lvl))
     pos = np.empty_like(perm); pos[perm] = np.arange(len(perm))
     ops = ops[perm]
     d = deps[perm]
