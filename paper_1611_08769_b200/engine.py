@@ -642,6 +642,7 @@ class GpuEngine(LevelledNetlist):
     TILE_SKEW = int(os.environ.get("FHEGPU_TILE_SKEW", "0"))      # 0: pick from the window below
     TILE_WINDOW = 1536        # items between a level and the next of one chunk (> ~1036 in flight)
     TILE_RING = int(os.environ.get("FHEGPU_TILE_RING", "8"))      # chunks of temporaries kept in L2
+    TILED_MAX_LEVELS = 32
 
     def _ring_ok(self) -> bool:
         """Ring temporaries need the program to have at most two sinks (see _tile)."""
@@ -677,6 +678,9 @@ class GpuEngine(LevelledNetlist):
         ct_bytes = ((self.params.n_ct * self.params.k + 3) // 4) * 16
         if (self._n_slots + n_ops) * self.batch_size * ct_bytes > self.TILED_MAX_BYTES:
             return "levels"
+        outs = np.asarray(self._pending_ops[4::5], dtype=np.int64)
+        if len(np.unique(np.asarray(self._level, dtype=np.int64)[outs])) > self.TILED_MAX_LEVELS:
+            return "levels"                    # deep programs are dependency-hop bound (4.8)
         return "tiled"
 
     @staticmethod

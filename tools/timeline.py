@@ -7,7 +7,7 @@ lanes = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 extra = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 s = GswScheme(DEFAULT_PARAMS); keys = s.keygen(1)
 rng = np.random.default_rng(1)
-eng = GpuEngine(s, keys=keys, rng=rng, batch_size=lanes, device_encrypt=True)
+eng = GpuEngine(s, keys=keys, rng=rng, batch_size=lanes, device_encrypt=True, schedule="levels")
 a, b = eng.input_block(rng.integers(0, 2, (lanes, 2)))
 x = xor_(a, b); y = and_(a, b)
 prog = eng.flush(); s.ctx.sync()
