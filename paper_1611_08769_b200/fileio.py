@@ -72,14 +72,16 @@ def unpack_compact(packed: np.ndarray, params: SchemeParams) -> np.ndarray:
     """Inverse of pack_compact; entries of C are 0/1 so V = sum_j C[r, i ell + j] 2^j exactly.
 
     (fhe.py:181-185 with no mod: a stored flattened matrix is already reduced.)"""
-    n = params.n_ct
+    n, ell = params.n_ct, params.ell
     bits = np.unpackbits(np.asarray(packed, dtype=np.uint8), axis=1)[:, :n * n]
-    bits = bits.reshape(len(packed), n, params.k, params.ell).astype(np.uint64)
-    w = np.uint64(1) << np.arange(params.ell, dtype=np.uint64)
-    vals = (bits * w).sum(axis=3)
+    bits = bits.reshape(len(packed), n, params.k, ell)
+    # bit j of V[r, i] is C[r, i*ell + j]: repack each ell-bit group LSB first into a u32
+    pad = np.zeros(bits.shape[:3] + (32 - ell,), dtype=np.uint8)
+    vals = np.packbits(np.concatenate([bits, pad], axis=3), axis=3, bitorder="little")
+    vals = vals.view("<u4")[..., 0]
     if (vals >= params.q).any():
         raise ParseError("container holds a matrix that is not a flattened ciphertext")
-    return vals.astype(np.uint32)
+    return np.ascontiguousarray(vals, dtype=np.uint32)
 
 
 def encode_container(params: SchemeParams, fmt: FixedFormat, dims, n_points: int,
