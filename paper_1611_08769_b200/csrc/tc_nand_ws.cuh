@@ -34,10 +34,17 @@
 namespace fhegpu {
 namespace tc {
 
-// Pipeline timeline probe (dbg bit 14): CTA 0 records clock64 per (gate, event).
+// Pipeline timeline probe (dbg bit 14, builds with -DFHEGPU_TRACE=1 only -- tools/timeline.py):
+// CTA 0 records clock64 per (gate, event).  Compiled out by default: even predicated off, the
+// probes cost the issue-bound roles a few instructions per gate.
+#ifndef FHEGPU_TRACE
+#define FHEGPU_TRACE 0
+#endif
 __device__ uint64_t g_ws_trace[64 * 16];
 __device__ __forceinline__ void trace_ev(const DevParams &p, uint32_t t, int ev) {
+#if FHEGPU_TRACE
   if ((p.dbg & 16384u) && blockIdx.x == 0 && t < 64) g_ws_trace[t * 16 + ev] = clock64();
+#endif
 }
 
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
@@ -253,7 +260,8 @@ struct GeoWS {
   static constexpr int OFF_SEEN = OFF_BAR + 256;          // dataflow: progress cache, <= 256 CTAs
   static constexpr int MAX_CTAS = 256;
   static constexpr int OFF_PUB = OFF_SEEN + 4 * MAX_CTAS;  // dataflow: epilogue -> tail relay
-  static constexpr int SMEM = OFF_PUB + 16;
+  static constexpr int OFF_FLAGS = OFF_PUB + 16;            // op flags of each input stage
+  static constexpr int SMEM = OFF_FLAGS + 4 * ((S_IN + 3) / 4 * 4);
   static_assert(NDIG == 4 && B::NCOL <= 36, "warp-specialised kernel: 4 digits, <= 36 columns");
   static_assert(MT >= 1 && TAIL <= 8, "two-tile geometry");
   static_assert(B::D_COLS + B::A_COLS <= BUF_COLS, "two TMEM buffers must fit 512 columns");
@@ -327,6 +335,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tail_ready + G::N_OUT);
   uint32_t *s_seen = reinterpret_cast<uint32_t *>(smem + G::OFF_SEEN);
   uint32_t *s_pub = reinterpret_cast<uint32_t *>(smem + G::OFF_PUB);
+  uint32_t *s_flags = reinterpret_cast<uint32_t *>(smem + G::OFF_FLAGS);  // written by the producer
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -398,6 +407,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
           fence_proxy_async_global();             // acquired generic flag -> async-proxy loads
         }
         uint32_t *dst = s_in + s * 2 * G::CT_WORDS;
+        s_flags[s] = op.flags;                    // published to the builders by in_full's arrive
         if (p.dbg & 256u) {                       // timing experiment: no operand loads
           mbar_arrive(&in_full[s]);
           continue;
@@ -514,14 +524,27 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
     const int row = 128 * tile + 32 * quad + lane;
     const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
     const int row_blk = row / ELL, row_bit = row - row_blk * ELL;
+    // B copy addressing is the same every gate: K row kr <-> bit j = 8q + o of word w with
+    // kk = 4o + q (matches spread_word_sr); this thread copies rows bt and bt + 128*MT
+    constexpr int B_ROWS = (G::KB + 128 * G::MT - 1) / (128 * G::MT);
+    int b_src[B_ROWS], b_dst[B_ROWS], b_w[B_ROWS], b_j[B_ROWS];
+#pragma unroll
+    for (int x = 0; x < B_ROWS; ++x) {
+      const int kr = bt + x * 128 * G::MT;
+      const int w = kr >> 5, kk = kr & 31;
+      const int j = 8 * (kk & 3) + (kk >> 2);
+      const bool ok = kr < G::KB && j < ELL && !(p.dbg & 32u);   // padding rows stay zero
+      b_src[x] = ok ? (w * ELL + j) * K : -1;
+      b_dst[x] = (kr >> 3) * G::LBO + (kr & 7) * 16;
+      b_w[x] = w;
+      b_j[x] = j;
+    }
     uint32_t t = 0;
-    uint32_t flags_next = fetch_op(ops, blockIdx.x, n_items, lanes, p.lanes_magic).flags;
     for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
       const uint32_t s = t % G::S_IN, k = t / G::S_IN, b = t & 1u, u = t >> 1;
-      const uint32_t flags = flags_next;
-      flags_next = fetch_op(ops, item + gridDim.x, n_items, lanes, p.lanes_magic).flags;
-      const bool comp1 = flags & 1u, comp2 = flags & 2u;
       mbar_wait(&in_full[s], k & 1u);
+      const uint32_t flags = s_flags[s];
+      const bool comp1 = flags & 1u, comp2 = flags & 2u;
       if (bt == 0) trace_ev(p, t, 5);
       mbar_wait(&a_free[b], (u & 1u) ^ 1u);            // gate t-2: MMAs done, tail read out
       if (bt == 0) trace_ev(p, t, 6);
@@ -575,20 +598,18 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
           *reinterpret_cast<uint4 *>(dst + G::TA_LBO) = make_uint4(sp[4], sp[5], sp[6], sp[7]);
         }
       }
-      // B: K row kr <-> bit j = 8q + o of word w, kk = 4o + q (matches spread_word_sr)
-      for (int kr = (p.dbg & 32u) ? G::KB : bt; kr < G::KB; kr += 128 * G::MT) {
-        const int w = kr >> 5, kk = kr & 31;
-        const int j = 8 * (kk & 3) + (kk >> 2);
-        if (j >= ELL) continue;                         // padding rows stay zero
-        const int c = w * ELL + j;
+      // B: V2 rows copied into the MN-major canonical layout (digits = the value's bytes)
+#pragma unroll
+      for (int x = 0; x < B_ROWS; ++x) {
+        if (b_src[x] < 0) continue;
         uint32_t vals[K];
 #pragma unroll
-        for (int i = 0; i < K; ++i) vals[i] = v2[c * K + i];
+        for (int i = 0; i < K; ++i) vals[i] = v2[b_src[x] + i];
         if (comp2) {
 #pragma unroll
-          for (int i = 0; i < K; ++i) vals[i] = sub_mod(i == w ? (1u << j) : 0u, vals[i], p.q);
+          for (int i = 0; i < K; ++i) vals[i] = sub_mod(i == b_w[x] ? (1u << b_j[x]) : 0u, vals[i], p.q);
         }
-        uint8_t *dst = bb + (kr >> 3) * G::LBO + (kr & 7) * 16;
+        uint8_t *dst = bb + b_dst[x];
 #pragma unroll
         for (int ch = 0; ch < G::NCH; ++ch) {
           uint4 val;
