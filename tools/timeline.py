@@ -1,4 +1,7 @@
-"""Timeline probe of the pipelined kernel on CTA 0 (clock64 per gate and event)."""
+"""Timeline probe of the pipelined kernel on CTA 0 (clock64 per gate and event).
+
+Needs a library built with the probes compiled in:
+  nvcc ... -DFHEGPU_TRACE=1 -o paper_1611_08769_b200/libfhegpu.so paper_1611_08769_b200/csrc/fhegpu.cu"""
 import sys, ctypes
 import numpy as np, torch
 sys.path.insert(0, '/root/repo')
