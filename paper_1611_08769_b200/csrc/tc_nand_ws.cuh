@@ -275,13 +275,18 @@ __device__ __forceinline__ uint32_t finish_neg(const uint32_t *d, uint32_t g, co
   uint32_t r;
   if constexpr (PM) {
 #if FHEGPU_A_POS
-    const uint32_t a = d[0] + (d[1] << 8);          // S0 + S1 2^8  (< 2^26)
-    const uint32_t b = d[2] + (d[3] << 8);          // S2 + S3 2^8
+    // S = a + b 2^16 with a = S0 + S1 2^8, b = S2 + S3 2^8 (both < 2^26).  Folding b's bits
+    // above 2^(ELL-16) with 2^ELL = c (mod q) gives t = a + bl 2^16 + c bh < 2q (host-checked,
+    // pm_ok) -- and t = a + b 2^16 - q bh exactly, so t can be formed modulo 2^32 from the
+    // wrapped S32 = S0 + S1 2^8 + S2 2^16 + S3 2^24: five instructions instead of eight
+    const uint32_t b = d[2] + (d[3] << 8);
+    const uint32_t s32 = d[0] + (d[1] << 8) + (b << 16);
+    const uint32_t t = s32 - p.q * (b >> (ELL - 16));
 #else
     const uint32_t a = 0u - (d[0] + (d[1] << 8));   // S0 + S1 2^8  (< 2^26)
     const uint32_t b = 0u - (d[2] + (d[3] << 8));   // S2 + S3 2^8
-#endif
     const uint32_t t = a + ((b & ((1u << (ELL - 16)) - 1u)) << 16) + p.pm_c * (b >> (ELL - 16));
+#endif
     r = min(t, t - p.q);                            // t < 2q
   } else {
     const int64_t sum = (int64_t)(int32_t)d[0] + ((int64_t)(int32_t)d[1] << 8) +
