@@ -194,3 +194,27 @@ def test_tiled_schedule_equals_levels_bit_exact():
         prog.run(4096)                                     # re-running rewrites identical values
         assert np.array_equal(eng.node_values([x, y]), outs[schedule])
     assert np.array_equal(outs["levels"], outs["tiled"])
+
+
+def test_tiled_incremental_flushes_equal_levels():
+    """Two chained tiled programs (the second consumes the first's outputs, with its own ring
+    of temporaries above every live slot) equal the level schedule bit for bit."""
+    scheme = GswScheme(DEFAULT0_PARAMS)                # depth 5 > DEFAULT's budget of 3
+    keys = scheme.keygen(2)
+    bits = np.random.default_rng(4).integers(0, 2, (2048, 3))
+    res = {}
+    for schedule in ("levels", "auto"):
+        eng = GpuEngine(scheme, keys=keys, rng=np.random.default_rng(2), batch_size=2048,
+                        device_encrypt=True, schedule=schedule)
+        a, b, c = eng.input_block(bits)
+        x, y = xor_(a, b), and_(a, b)
+        p1 = eng.flush()
+        z, w = xor_(x, c), and_(y, c)                 # second program on the first's outputs
+        p2 = eng.flush()
+        if schedule == "auto":
+            assert p1.tile_lanes == 128 and p2.tile_lanes == 128
+        res[schedule] = eng.node_values([x, y, z, w])
+        got = eng.read_back_bits([z, w])
+        assert (got[0] == (bits[:, 0] ^ bits[:, 1] ^ bits[:, 2])).all()
+        assert (got[1] == (bits[:, 0] & bits[:, 1] & bits[:, 2])).all()
+    assert np.array_equal(res["levels"], res["auto"])

@@ -241,3 +241,24 @@ def test_tiled_ring_temporaries_replay_and_war_order():
     xs, ys = eng._slot[x.node], eng._slot[y.node]
     assert (store[xs * lanes:(xs + 1) * lanes] == (bits[:, 0] ^ bits[:, 1])).all()
     assert (store[ys * lanes:(ys + 1) * lanes] == (bits[:, 0] & bits[:, 1])).all()
+
+
+def test_auto_schedule_policy():
+    """'auto': tiled only for wide (batch % 128 == 0, >= 1024 lanes), shallow (<= 32 levels)
+    programs on the tcgen05 geometry whose store fits; levels otherwise."""
+    from paper_1611_08769_b200 import and_, xor_
+
+    def pick(lanes, params=DEFAULT_PARAMS, depth=1):
+        eng = GpuEngine(GswScheme(params), dry_run=True, batch_size=lanes)
+        a, b = eng.input_bit(0), eng.input_bit(0)
+        for _ in range(depth):
+            a, b = xor_(a, b), and_(a, b)
+        eng.dry_run = False                       # policy only; nothing is flushed
+        return eng._pick_schedule()
+
+    assert pick(4096) == "tiled"
+    assert pick(1024) == "tiled"
+    assert pick(512) == "levels"                  # too narrow to fill chunks
+    assert pick(4000) == "levels"                 # not a multiple of the chunk
+    assert pick(4096, EXACT_PARAMS) == "levels"   # no warp-specialised kernel for N = 51
+    assert pick(4096, DEFAULT0_PARAMS, depth=12) == "levels"   # 36 levels: hop bound
