@@ -218,3 +218,21 @@ def test_tiled_incremental_flushes_equal_levels():
         assert (got[0] == (bits[:, 0] ^ bits[:, 1] ^ bits[:, 2])).all()
         assert (got[1] == (bits[:, 0] & bits[:, 1] & bits[:, 2])).all()
     assert np.array_equal(res["levels"], res["auto"])
+
+
+def test_cfg1_full_size_every_lane_decrypts():
+    """configs[1] at full size (2^20 pairs, default tiled schedule, device encryption with the
+    cfg1 seeds): every one of the 2^21 output ciphertexts decrypts to the right bit."""
+    scheme = GswScheme(DEFAULT_PARAMS)
+    keys = scheme.keygen(1)
+    rng = np.random.default_rng(1)
+    bits = rng.integers(0, 2, (1 << 20, 2))
+    eng = GpuEngine(scheme, keys=keys, rng=rng, batch_size=1 << 20, device_encrypt=True)
+    a, b = eng.input_block(bits)
+    x, y = xor_(a, b), and_(a, b)
+    prog = eng.flush()
+    assert prog.tile_lanes == 128 and prog.launches == 1
+    got = eng.read_back_bits([x, y])
+    assert (got[0] == (bits[:, 0] ^ bits[:, 1])).all()
+    assert (got[1] == (bits[:, 0] & bits[:, 1])).all()
+    assert eng.nand_count == 6 and eng.max_depth == 3
