@@ -43,7 +43,9 @@ namespace tc {
 __device__ uint64_t g_ws_trace[64 * 16];
 __device__ __forceinline__ void trace_ev(const DevParams &p, uint32_t t, int ev) {
 #if FHEGPU_TRACE
-  if ((p.dbg & 16384u) && blockIdx.x == 0 && t < 64) g_ws_trace[t * 16 + ev] = clock64();
+  // window of 64 gates starting at gate 64 * (dbg >> 20) of CTA 0
+  const uint32_t t0 = 64u * (p.dbg >> 20);
+  if ((p.dbg & 16384u) && blockIdx.x == 0 && t >= t0 && t < t0 + 64) g_ws_trace[(t - t0) * 16 + ev] = clock64();
 #endif
 }
 

@@ -8,14 +8,20 @@ sys.path.insert(0, '/root/repo')
 from paper_1611_08769_b200 import DEFAULT_PARAMS, GswScheme, GpuEngine, and_, xor_, _native
 lanes = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 extra = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+schedule = sys.argv[3] if len(sys.argv) > 3 else "levels"     # "tiled": whole program, window
+window = int(sys.argv[4]) if len(sys.argv) > 4 else 0          # trace gates [64w, 64w + 64)
 s = GswScheme(DEFAULT_PARAMS); keys = s.keygen(1)
 rng = np.random.default_rng(1)
-eng = GpuEngine(s, keys=keys, rng=rng, batch_size=lanes, device_encrypt=True, schedule="levels")
+eng = GpuEngine(s, keys=keys, rng=rng, batch_size=lanes, device_encrypt=True, schedule=schedule)
 a, b = eng.input_block(rng.integers(0, 2, (lanes, 2)))
 x = xor_(a, b); y = and_(a, b)
 prog = eng.flush(); s.ctx.sync()
-s.ctx.set_debug(16384 | extra)
-prog.run(lanes, 1, 2); s.ctx.sync()
+s.ctx.set_debug(16384 | extra | (window << 20))
+if schedule == "levels":
+    prog.run(lanes, 1, 2)
+else:
+    prog.run(lanes)
+s.ctx.sync()
 buf = np.zeros(64 * 16, dtype=np.uint64)
 _native._lib.fhegpu_debug_ws_trace(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
 tr = buf.reshape(64, 16).astype(np.int64)
