@@ -166,7 +166,7 @@ __device__ __forceinline__ uint32_t prmt_sign(uint32_t x) {
 // the accumulators positive; {0, -1} (sign-replicating prmt) toggles all eight.  Same
 // instruction count; the tensor pipe's switching power is what the power-capped kernel pays.
 #ifndef FHEGPU_PUBLISH_LAG
-#define FHEGPU_PUBLISH_LAG 3   // dataflow: publish outputs this many gates behind the epilogue
+#define FHEGPU_PUBLISH_LAG 1   // dataflow: publish outputs this many gates behind the epilogue
 #endif
 
 #ifndef FHEGPU_A_POS
