@@ -615,8 +615,12 @@ class GpuEngine(LevelledNetlist):
             K = self.batch_size // self.TILE_LANES
             t_base = self._n_slots * K                       # ring after every batch-wide slot
             if ring:
-                skew = self.TILE_SKEW or max(1, -(-self.TILE_WINDOW // (len(prog["ops"]) * self.TILE_LANES)))
-                ring = max(ring, skew * (len(prog["offsets"]) - 2) + 1)
+                step_items = len(prog["ops"]) * self.TILE_LANES
+                slack = max(1, -(-self.TILE_WINDOW // step_items))   # steps covering the window
+                skew = self.TILE_SKEW or slack
+                # the roots of chunk c wait for the sinks of chunk c - ring (at step c - ring +
+                # skew * depth): keep those a window's worth of steps back, out of flight
+                ring = max(ring, skew * (len(prog["offsets"]) - 2) + 1 + slack)
                 need = self._n_slots * self.batch_size + ring * prog["n_temp"] * self.TILE_LANES
                 if self.ctx.capacity < need:
                     self.ctx.reserve(need)

@@ -11,12 +11,13 @@ from paper_1611_08769_b200 import DEFAULT_PARAMS, GswScheme, GpuEngine, and_, xo
 
 lanes = int(sys.argv[1]); seconds = float(sys.argv[2]) if len(sys.argv) > 2 else 3.0
 dbg = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+schedule = sys.argv[4] if len(sys.argv) > 4 else "auto"
 s = GswScheme(DEFAULT_PARAMS)
 keys = s.keygen(1)
 rng = np.random.default_rng(1)
 base = s.encrypt_many(keys.public_key, rng.integers(0, 2, 2048), rng)
 reps = (lanes + 1023) // 1024
-eng = GpuEngine(s, keys=keys, batch_size=lanes)
+eng = GpuEngine(s, keys=keys, batch_size=lanes, schedule=schedule)
 a = eng.input_values(np.tile(base[0::2], (reps, 1, 1))[:lanes], noise_est=64)
 b = eng.input_values(np.tile(base[1::2], (reps, 1, 1))[:lanes], noise_est=64)
 x = xor_(a, b); y = and_(a, b)
@@ -50,6 +51,6 @@ stop.set(); t.join()
 ms = e0.elapsed_time(e1) / steps
 n = 6 * lanes
 half = len(clk) // 2
-print(f"dbg={dbg:5d} lanes={lanes:8d} ws={eng._n_slots * lanes * 9408 / 1e6:8.1f}MB steps={steps:5d} "
+print(f"{schedule} dbg={dbg:5d} lanes={lanes:8d} ws={eng._n_slots * lanes * 9408 / 1e6:8.1f}MB steps={steps:5d} "
       f"NAND/s={n / ms * 1e3 / 1e6:7.1f}M clk(med,2nd half)={statistics.median(clk[half:]):.0f} "
       f"power(med,2nd half)={statistics.median(pw[half:]):.0f}W limit={pynvml.nvmlDeviceGetEnforcedPowerLimit(h)/1000:.0f}W")
