@@ -110,3 +110,20 @@ def test_backend_equivalence_random_circuits_and_lanes():
         assert clear.nand_count == fhe.nand_count <= 200
         assert clear.max_depth == fhe.max_depth
         assert clear.read_back_many(pool_c) == fhe.read_back_many(pool_f) == pool_v
+
+
+def test_mul_const_matches_mul_fixed_bit_for_bit():
+    """tests/test_arith.py:214-223 at scale: a plaintext-constant multiply equals the
+    ciphertext-word multiply bit for bit (4096 lanes per constant, bitsliced engine)."""
+    from paper_1611_08769_b200 import mul_const, mul_fixed
+    from paper_1611_08769_b200.arith import input_word
+    rng = np.random.default_rng(7)
+    fmt = FixedFormat(32, 16)
+    for _ in range(6):
+        c = float(rng.uniform(-1, 1))
+        xs = list(rng.uniform(-1, 1, 4096))
+        eng = GpuClearEngine(batch_size=4096)
+        x = input_word(eng, xs, fmt)
+        via_const = mul_const(x, c)
+        via_ct = mul_fixed(x, input_word(eng, [c] * 4096, fmt))
+        assert eng.read_back_many(list(via_const.bits)) == eng.read_back_many(list(via_ct.bits))

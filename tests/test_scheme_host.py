@@ -92,3 +92,18 @@ def test_ring_op_levels_and_noise_like_reference(name):
         src = fresh if i % 2 else nb
         assert r[f"cmult{i}"]["level"] == src.level
         assert r[f"cmult{i}"]["noise_est"] == min(params.n_ct * src.noise_est, params.q)
+
+
+def test_wrong_key_raises_noise_overflow():
+    """tests/test_fhe.py:175-184: decrypting with another key trips the noise check."""
+    s = GswScheme(DEFAULT_PARAMS)
+    keys, other = s.keygen(seed=1), s.keygen(seed=999)
+    rng = np.random.default_rng(7)
+    observed = 0
+    for _ in range(16):
+        ct = s.encrypt_bit(keys.public_key, 1, rng)
+        try:
+            s.decrypt_bit(other.secret_key, ct)
+        except NoiseOverflowError:
+            observed += 1
+    assert observed >= 8
