@@ -235,3 +235,16 @@ def test_ring_ops_match_ring_oracle_like_reference_tests():
     outs = s.hom_mult_many([(s.encrypt_value(pk, int(a), rng), s.encrypt_value(pk, int(b), rng))
                             for a, b in zip(m1, m2)])
     assert [s.decrypt_value(sk, c) for c in outs] == [int((a * b) % q) for a, b in zip(m1, m2)]
+
+
+def test_plain_c_abi_reproduces_reference_nand():
+    """C program over the C ABI (no Python in the loop): hom_nand of two reference
+    ciphertexts equals the reference's output; hom_not twice is the identity."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([os.path.join(root, "tests", "c", "abi_kat"),
+                          os.path.join(root, "tests", "golden", "kat_default_nand.bin")],
+                         capture_output=True, text=True, timeout=120)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "== reference" in res.stdout

@@ -84,3 +84,13 @@ def test_python_layer_fails_loudly_without_a_device():
     x = eng.input_bit(0b1010)
     with pytest.raises(DeviceError):
         eng.read_back(eng.nand(x, x))
+
+
+def test_plain_c_consumer_links_against_the_abi():
+    """tests/c/abi_kat (built by __graft_entry__.build with gcc) resolves every symbol it uses
+    from the in-tree libfhegpu.so -- no Python, no torch."""
+    import subprocess
+    kat = os.path.join(ROOT, "tests", "c", "abi_kat")
+    assert os.path.exists(kat)
+    out = subprocess.run(["ldd", kat], capture_output=True, text=True).stdout
+    assert "libfhegpu.so" in out and "not found" not in out
