@@ -160,7 +160,9 @@ int fhegpu_prog_run_host(fhegpu_ctx *ctx, fhegpu_prog *prog, uint64_t lanes, uin
  * the engine's dataflow compile guarantees it.  prog_run then evaluates the whole program
  * in ONE launch: each operand load waits for its producer through per-CTA progress
  * counters instead of a kernel boundary per level (narrow, deep netlists such as a single
- * FFT, fft.py:157-194).  Falls back to level launches where no tcgen05 kernel applies. */
+ * FFT, fft.py:157-194).  Where no tcgen05 kernel applies it falls back to level launches if
+ * the level offsets are a valid schedule (no op depends on an op of its own level), and
+ * otherwise fails with FHEGPU_EUNSUP instead of running it wrongly. */
 int fhegpu_prog_set_deps(fhegpu_ctx *ctx, fhegpu_prog *prog, const int32_t *deps);
 uint32_t fhegpu_prog_launches(const fhegpu_prog *prog);       /* launches one run issues */
 void fhegpu_prog_destroy(fhegpu_prog *prog);

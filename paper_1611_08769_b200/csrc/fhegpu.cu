@@ -79,6 +79,8 @@ struct fhegpu_prog {
   uint64_t n_ops = 0;
   uint64_t n_slots = 0;           // 1 + the largest slot any op names
   int2 *d_deps = nullptr;         // dataflow mode: producing op of each operand (-1: ready)
+  bool levels_valid = true;       // level launches are a valid fallback (no op depends on an op
+                                  // of its own level); false for tiled programs
   uint32_t *d_progress = nullptr; // per-CTA completed-item counters
   // CUDA graph of one full run (all level launches), captured on first use per
   // (lanes, stream, kernel choice, debug bits); replayed with a single cudaGraphLaunch
@@ -569,7 +571,13 @@ int fhegpu_prog_run_range(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes, uint32
   if (pr->d_deps && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
     const int rc = launch_dataflow(c, c->store, pr->d_ops, (uint32_t)pr->n_ops, lanes, pr->d_deps,
                                    pr->d_progress);
-    if (rc != FHEGPU_EUNSUP) return rc;            // else: level by level (always valid)
+    if (rc != FHEGPU_EUNSUP) return rc;
+    if (!pr->levels_valid)
+      return fail(FHEGPU_EUNSUP, "program needs the dataflow kernel (tcgen05, k = 9, ell = 29, "
+                                 "< 2^32 items), which does not apply here");
+    // else: level by level (valid: no op depends on an op of its own level)
+  } else if (pr->d_deps && !pr->levels_valid) {
+    return fail(FHEGPU_EINVAL, "a program without level structure runs whole (dataflow) only");
   }
   for (uint32_t l = first; l < last; ++l) {
     const uint64_t a = pr->offsets[l], b = pr->offsets[l + 1];
@@ -733,6 +741,15 @@ int fhegpu_prog_set_deps(fhegpu_ctx *c, fhegpu_prog *pr, const int32_t *deps) {
   for (uint64_t i = 0; i < 2 * pr->n_ops; ++i)
     if (deps[i] < -1 || (int64_t)deps[i] >= (int64_t)(i / 2))
       return fail(FHEGPU_EINVAL, "dependency " + std::to_string(i) + " is not an earlier op");
+  // level launches stay a valid fallback only if no op depends on an op of its own level
+  pr->levels_valid = true;
+  for (size_t l = 0; l + 1 < pr->offsets.size() && pr->levels_valid; ++l)
+    for (uint64_t i = pr->offsets[l]; i < pr->offsets[l + 1]; ++i)
+      if ((deps[2 * i] >= 0 && (uint64_t)deps[2 * i] >= pr->offsets[l]) ||
+          (deps[2 * i + 1] >= 0 && (uint64_t)deps[2 * i + 1] >= pr->offsets[l])) {
+        pr->levels_valid = false;
+        break;
+      }
   CUDA_TRY(cudaSetDevice(c->device));
   cudaFree(pr->d_deps);
   cudaFree(pr->d_progress);

@@ -678,10 +678,14 @@ class GpuEngine(LevelledNetlist):
         C = self.TILE_LANES
         if self.batch_size % C or self.batch_size < 8 * C:
             return "levels"
+        if self.ctx.kernel != "tcgen05":              # the dataflow launch needs the tcgen05 kernel
+            return "levels"
         n_ops = len(self._pending_ops) // 5
         ct_bytes = ((self.params.n_ct * self.params.k + 3) // 4) * 16
         if (self._n_slots + n_ops) * self.batch_size * ct_bytes > self.TILED_MAX_BYTES:
             return "levels"
+        if n_ops * self.batch_size >= 1 << 31 or n_ops * (self.batch_size // C) > 1 << 24:
+            return "levels"                   # item index range / host-side tiling cost
         outs = np.asarray(self._pending_ops[4::5], dtype=np.int64)
         if len(np.unique(np.asarray(self._level, dtype=np.int64)[outs])) > self.TILED_MAX_LEVELS:
             return "levels"                    # deep programs are dependency-hop bound (4.8)

@@ -236,3 +236,20 @@ def test_cfg1_full_size_every_lane_decrypts():
     assert (got[0] == (bits[:, 0] ^ bits[:, 1])).all()
     assert (got[1] == (bits[:, 0] & bits[:, 1])).all()
     assert eng.nand_count == 6 and eng.max_depth == 3
+
+
+def test_tiled_program_refuses_level_fallback():
+    """A tiled program has no level structure: if the dataflow kernel cannot run (SIMT kernel
+    forced) it must fail loudly rather than run its dependent ops as one level."""
+    from paper_1611_08769_b200 import DeviceError, _native
+    scheme = GswScheme(DEFAULT_PARAMS)
+    keys = scheme.keygen(1)
+    eng = GpuEngine(scheme, keys=keys, rng=np.random.default_rng(1), batch_size=2048,
+                    device_encrypt=True, schedule="tiled")
+    a, b = eng.input_block(np.random.default_rng(2).integers(0, 2, (2048, 2)))
+    x = xor_(a, b)
+    prog = eng.flush()
+    scheme.ctx.set_kernel(_native.KERNEL_SIMT)
+    with pytest.raises(DeviceError, match="dataflow"):
+        prog.run(2048)
+    scheme.ctx.set_kernel(_native.KERNEL_AUTO)

@@ -248,12 +248,13 @@ def test_auto_schedule_policy():
     programs on the tcgen05 geometry whose store fits; levels otherwise."""
     from paper_1611_08769_b200 import and_, xor_
 
-    def pick(lanes, params=DEFAULT_PARAMS, depth=1):
+    def pick(lanes, params=DEFAULT_PARAMS, depth=1, kernel="tcgen05"):
         eng = GpuEngine(GswScheme(params), dry_run=True, batch_size=lanes)
         a, b = eng.input_bit(0), eng.input_bit(0)
         for _ in range(depth):
             a, b = xor_(a, b), and_(a, b)
         eng.dry_run = False                       # policy only; nothing is flushed
+        eng.scheme._ctx = type("Ctx", (), {"kernel": kernel})()   # stand-in device context
         return eng._pick_schedule()
 
     assert pick(4096) == "tiled"
@@ -262,3 +263,4 @@ def test_auto_schedule_policy():
     assert pick(4000) == "levels"                 # not a multiple of the chunk
     assert pick(4096, EXACT_PARAMS) == "levels"   # no warp-specialised kernel for N = 51
     assert pick(4096, DEFAULT0_PARAMS, depth=12) == "levels"   # 36 levels: hop bound
+    assert pick(4096, kernel="simt") == "levels"  # dataflow launches need the tcgen05 kernel
