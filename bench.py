@@ -411,19 +411,24 @@ def bench_fft(args, world, rank, local):
 
 
 def bench_fft_single(args, world, rank, local, cfg):
-    """configs[2] (32-pt Q8.24) / configs[3] (8x8 Q9.7 2-D): one signal, FFT/s = 1 / latency.
-    Inputs follow the configs' seeds (DEFAULT dims, noise-free: 'default0'); decrypted outputs
-    are checked against the reference's own words (tests/golden/clear_cfgN.npz)."""
+    """configs[0] (8-pt Q4.12, EXACT) / [2] (32-pt Q8.24) / [3] (8x8 Q9.7 2-D): one signal, FFT/s =
+    1 / latency.  Inputs follow the configs' seeds (configs 2-3: DEFAULT dims, noise-free
+    'default0'); decrypted outputs are checked against the reference's own words
+    (tests/golden/clear_cfgN.npz)."""
     import numpy as np
     import torch
 
-    from paper_1611_08769_b200 import DEFAULT0_PARAMS, FixedFormat, GpuEngine, GswScheme, fft_1d, fft_2d, input_signal
+    from paper_1611_08769_b200 import (DEFAULT0_PARAMS, EXACT_PARAMS, FixedFormat, GpuEngine, GswScheme,
+                                       fft_1d, fft_2d, input_signal)
     from paper_1611_08769_b200.fft import read_signal_ints
-    seed = {"cfg2": 2, "cfg3": 3}[cfg]
-    scheme = GswScheme(DEFAULT0_PARAMS, device=local)
+    seed = {"cfg0": 0, "cfg2": 2, "cfg3": 3}[cfg]
+    scheme = GswScheme(EXACT_PARAMS if cfg == "cfg0" else DEFAULT0_PARAMS, device=local)
     keys = scheme.keygen(seed)
     rng = np.random.default_rng(seed)
-    if cfg == "cfg2":
+    if cfg == "cfg0":
+        vals = rng.uniform(-1, 1, 8).astype(complex)
+        fmt, dims = FixedFormat(16, 12), None
+    elif cfg == "cfg2":
         vals = rng.uniform(-1, 1, 32) + 1j * rng.uniform(-1, 1, 32)
         fmt, dims = FixedFormat(32, 24), None
     else:
@@ -445,8 +450,8 @@ def bench_fft_single(args, world, rank, local, cfg):
     except OSError:
         pass
     ms = time_program(prog, 1, stream, max(3, args.steps // 2), min(args.warmup, 3), world)
-    return {"metric": f"{'32-pt Q8.24' if cfg == 'cfg2' else '8x8 Q9.7 2-D'} FHE FFTs/s "
-                      f"(configs[{cfg[-1]}], one signal)",
+    name = {"cfg0": "8-pt Q4.12 (EXACT params)", "cfg2": "32-pt Q8.24", "cfg3": "8x8 Q9.7 2-D"}[cfg]
+    return {"metric": f"{name} FHE FFTs/s (configs[{cfg[-1]}], one signal)",
             "value": world / (ms / 1e3), "unit": "FFT/s", "ms_per_fft": ms,
             "nand_per_s": eng.nand_count * world / (ms / 1e3), "nand_per_fft": eng.nand_count,
             "levels": prog.n_levels, "launches_per_fft": prog.launches,
@@ -464,7 +469,7 @@ def run_ours(args):
     single = {}
     if args.fft_single:
         import gc
-        for cfg in ("cfg3", "cfg2"):
+        for cfg in ("cfg0", "cfg3", "cfg2"):
             gc.collect()
             single[cfg] = bench_fft_single(args, world, rank, local, cfg)
     cpu = None
@@ -572,7 +577,7 @@ def main():
                     help="host ciphertexts: reference-serialised bits (EFT1 rows) or compact u32")
     ap.add_argument("--no-fft", dest="fft", action="store_false")
     ap.add_argument("--no-fft-single", dest="fft_single", action="store_false",
-                    help="skip configs[2]/[3] single-signal FFT latency")
+                    help="skip configs[0]/[2]/[3] single-signal FFT latency")
     ap.add_argument("--fft-lanes", type=int, default=1024)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--ref-step-seconds", type=float, default=4.0)
