@@ -254,6 +254,12 @@ struct GeoWS {
   // idesc: S32 accumulator, A s8 (bits 7-9 = 1), B u8, A K-major, B MN-major, N>>3, M>>4
   static constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 16) |
                                     ((uint32_t)(NPAD >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  // tail MMA (5 live rows, A aliased over the M extent): M = TAIL_M halves the datapath work of
+  // the duplicate rows when 64 -- same issue cost (the floor is max(M, 128)), less energy
+#ifndef FHEGPU_TAIL_M
+#define FHEGPU_TAIL_M 64
+#endif
+  static constexpr uint32_t IDESC_TAIL = (IDESC & ~(0x1fu << 24)) | ((uint32_t)(FHEGPU_TAIL_M >> 4) << 24);
   static constexpr int OFF_IN = 0;
   static constexpr int OFF_B = OFF_IN + S_IN * 2 * CT_BYTES;
   static constexpr int OFF_TA = ((OFF_B + 2 * B_BYTES + 127) / 128) * 128;
@@ -457,7 +463,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
 #pragma unroll
             for (int s = 0; s < K; ++s)
               mma_i8_ss(tb + G::D_COLS, td_b + ((s * 2 * G::TA_LBO) >> 4),
-                        bd_b + ((s * 4 * G::LBO) >> 4), idesc, s > 0 ? 1u : 0u);
+                        bd_b + ((s * 4 * G::LBO) >> 4), G::IDESC_TAIL, s > 0 ? 1u : 0u);
           }
         }
         __syncwarp();
