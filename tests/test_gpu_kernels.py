@@ -248,3 +248,25 @@ def test_plain_c_abi_reproduces_reference_nand():
                          capture_output=True, text=True, timeout=120)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "== reference" in res.stdout
+
+
+@pytest.mark.parametrize("n,q", [(3, 2 ** 13 - 1), (5, 2 ** 20 + 7), (8, 2 ** 31 - 1)])
+def test_engine_fft_on_other_parameter_sets(n, q):
+    """Any valid SchemeParams runs through the engine (the CUDA-core kernel where no tcgen05
+    instance exists: N = 12, 126, 279 here): a noise-free 4-point Q8.8 FFT over 8 lanes
+    decrypts to the integer model's words."""
+    from paper_1611_08769_b200 import FixedFormat, GpuEngine, fft_1d, input_signal
+    from paper_1611_08769_b200.fft import read_signal_ints
+    from oracle import fixedfft
+    p = SchemeParams(n=n, q=q, m=8, noise_bound=0, depth_budget=10 ** 9)
+    s = GswScheme(p)
+    keys = s.keygen(2)
+    rng = np.random.default_rng(9)
+    vals = rng.uniform(-1, 1, (8, 4)) + 1j * rng.uniform(-1, 1, (8, 4))
+    eng = GpuEngine(s, keys=keys, rng=rng, batch_size=8, device_encrypt=(p.n_ct * p.m) % 2 == 0)
+    out = fft_1d(input_signal(eng, vals, FixedFormat(16, 8)))
+    got = read_signal_ints(eng, out)
+    re = fixedfft.encode_lanes(vals.real, 16, 8)
+    im = fixedfft.encode_lanes(vals.imag, 16, 8)
+    want = fixedfft.interleave(*fixedfft.fft_1d(re, im, 16, 8))
+    assert np.array_equal(got, want)
