@@ -137,15 +137,15 @@ int launch_tc_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_
   return FHEGPU_OK;
 }
 
-template <int K, int ELL, bool PM>
-int launch_tc_ws_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes,
-                      const int2 *deps = nullptr, uint32_t *progress = nullptr) {
-  using G = tc::GeoWS<K, ELL, PM>;
+template <int K, int ELL, bool PM, int ENC>
+int launch_tc_ws_enc(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes,
+                      const int2 *deps, uint32_t *progress) {
+  using G = tc::GeoWS<K, ELL, PM, ENC>;
   static bool attr_done = false;
   // > half of the SM's shared memory: exactly one CTA (512 TMEM columns) per SM
   const int smem = std::max(G::SMEM, 120 * 1024);
   if (!attr_done) {
-    CUDA_TRY(cudaFuncSetAttribute(tc::level_tc_ws_kernel<K, ELL, PM>,
+    CUDA_TRY(cudaFuncSetAttribute(tc::level_tc_ws_kernel<K, ELL, PM, ENC>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_done = true;
   }
@@ -166,9 +166,18 @@ int launch_tc_ws_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = (c->p.dbg & 8192u) ? 0 : 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::level_tc_ws_kernel<K, ELL, PM>, store, ops, n_ops, lanes, p,
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::level_tc_ws_kernel<K, ELL, PM, ENC>, store, ops, n_ops, lanes, p,
                               deps, progress));
   return FHEGPU_OK;
+}
+
+// Level launches and dataflow launches use different A encodings (tc_nand_ws.cuh, AEnc).
+template <int K, int ELL, bool PM>
+int launch_tc_ws_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes,
+                      const int2 *deps = nullptr, uint32_t *progress = nullptr) {
+  if (deps == nullptr)
+    return launch_tc_ws_enc<K, ELL, PM, FHEGPU_ENC_LEVELS>(c, store, ops, n_ops, lanes, deps, progress);
+  return launch_tc_ws_enc<K, ELL, PM, FHEGPU_ENC_FLOW>(c, store, ops, n_ops, lanes, deps, progress);
 }
 
 template <int K, int ELL>

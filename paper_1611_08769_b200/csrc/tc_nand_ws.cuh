@@ -162,26 +162,40 @@ __device__ __forceinline__ uint32_t prmt_sign(uint32_t x) {
   return r;
 }
 
-// A operand sign: {0, +1} bytes (default) toggle one bit per byte in the MMA datapath and keep
-// the accumulators positive; {0, -1} (sign-replicating prmt) toggles all eight.  Same
-// instruction count; the tensor pipe's switching power is what the power-capped kernel pays.
 #ifndef FHEGPU_PUBLISH_LAG
 #define FHEGPU_PUBLISH_LAG 1   // dataflow: publish outputs this many gates behind the epilogue
 #endif
 
-#ifndef FHEGPU_A_POS
-#define FHEGPU_A_POS 1
+// A operand encoding (kernel template parameter ENC), both toggling one bit per byte in the
+// MMA datapath ({0, -1} bytes, all eight bits, cost 2.6% under the power cap):
+//   1: s8 {0, +1} = (w >> o) & 0x01010101 -- two ALU-pipe ops per output register;
+//      D = digit sums.  Used by dataflow (tiled) launches.
+//   2: u8 {0, 128} = (w << (7 - o)) & 0x80808080 -- ptxas issues the left shift on the FMA
+//      pipe (IMAD.SHL), halving the ALU work of the spread, which saturates that pipe
+//      (tools/micro/tmem_st_bench.cu); D = 128 x digit sums.  Level launches: +1.7%
+//      (load-bound there, the builders finish early); in dataflow launches the larger
+//      accumulators and the epilogue's extra shift cost more than the builders gain (-6%).
+#ifndef FHEGPU_ENC_LEVELS
+#define FHEGPU_ENC_LEVELS 2
+#endif
+#ifndef FHEGPU_ENC_FLOW
+#define FHEGPU_ENC_FLOW 1
 #endif
 
-// 32 bits of w -> 32 s8 K slots: out[o] byte q = bit (8q + o) (or its negation).
+template <int ENC>
+struct AEnc {
+  static_assert(ENC == 1 || ENC == 2, "A operand encoding");
+  static constexpr int SHIFT = ENC == 2 ? 7 : 0;        // log2 of the accumulator scale
+  static constexpr uint32_t A_FMT = ENC == 2 ? 0u : 1u;  // idesc a_format: u8 / s8
+};
+
+// 32 bits of w -> 32 K slots: out[o] byte q = bit (8q + o) (scaled per encoding).
+template <int ENC>
 __device__ __forceinline__ void spread_word_sr(uint32_t w, uint32_t (&out)[8]) {
 #pragma unroll
   for (int o = 0; o < 8; ++o) {
-#if FHEGPU_A_POS
-    out[o] = (w >> o) & 0x01010101u;
-#else
-    out[o] = prmt_sign(w << (7 - o));
-#endif
+    if constexpr (ENC == 2) out[o] = (w * (1u << (7 - o))) & 0x80808080u;
+    else out[o] = (w >> o) & 0x01010101u;
   }
 }
 
@@ -229,7 +243,7 @@ __device__ __forceinline__ void load_acc36(uint32_t taddr, uint32_t (&d)[36], bo
   tmem_ld4(taddr + 32, d + 32);
 }
 
-template <int K, int ELL, bool PM>
+template <int K, int ELL, bool PM, int ENC>
 struct GeoWS {
   using B = Geo<K, ELL>;
   static constexpr int ROWS = B::ROWS;
@@ -251,8 +265,9 @@ struct GeoWS {
   static constexpr int S_IN = 7;                            // ~2.5 us load latency x bandwidth
   static constexpr int N_OUT = 3;                           // output staging buffers
   static constexpr uint32_t OP_ARRIVALS = NB_WARPS;
-  // idesc: S32 accumulator, A s8 (bits 7-9 = 1), B u8, A K-major, B MN-major, N>>3, M>>4
-  static constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 16) |
+  // idesc: S32 accumulator, A s8 (bits 7-9 = 1) or u8 (encoding 2), B u8, A K-major,
+  // B MN-major, N>>3, M>>4
+  static constexpr uint32_t IDESC = (2u << 4) | (AEnc<ENC>::A_FMT << 7) | (1u << 16) |
                                     ((uint32_t)(NPAD >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   // tail MMA (5 live rows, A aliased over the M extent): M = TAIL_M halves the datapath work of
   // the duplicate rows when 64 -- same issue cost (the floor is max(M, 128)), less energy
@@ -272,34 +287,33 @@ struct GeoWS {
   static constexpr int SMEM = OFF_FLAGS + 4 * ((S_IN + 3) / 4 * 4);
   static_assert(NDIG == 4 && B::NCOL <= 36, "warp-specialised kernel: 4 digits, <= 36 columns");
   static_assert(MT >= 1 && TAIL <= 8, "two-tile geometry");
+  static_assert((uint64_t)ROWS * 255u * 257u << AEnc<ENC>::SHIFT < (1ull << 32), "scaled digit sums fit u32");
   static_assert(B::D_COLS + B::A_COLS <= BUF_COLS, "two TMEM buffers must fit 512 columns");
   static_assert(MAIN_BYTES % 16 == 0, "bulk store size");
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
-// Digit-sum epilogue: d[] are the digit sums S_d (or -S_d when A = -bits).
-template <int ELL, bool PM>
+// Digit-sum epilogue: d[] are the digit sums S_d scaled by 2^SHIFT.
+template <int ELL, bool PM, int ENC>
 __device__ __forceinline__ uint32_t finish_neg(const uint32_t *d, uint32_t g, const DevParams &p) {
   uint32_t r;
   if constexpr (PM) {
-#if FHEGPU_A_POS
     // S = a + b 2^16 with a = S0 + S1 2^8, b = S2 + S3 2^8 (both < 2^26).  Folding b's bits
     // above 2^(ELL-16) with 2^ELL = c (mod q) gives t = a + bl 2^16 + c bh < 2q (host-checked,
     // pm_ok) -- and t = a + b 2^16 - q bh exactly, so t can be formed modulo 2^32 from the
-    // wrapped S32 = S0 + S1 2^8 + S2 2^16 + S3 2^24: five instructions instead of eight
+    // wrapped S32 = S0 + S1 2^8 + S2 2^16 + S3 2^24.  Encoding 2 carries every digit sum
+    // scaled by 2^7: a' = 2^7 a < 2^32 and b' = 2^7 b < 2^29 (top digits < 2^(ELL-24)) stay
+    // exact, a = a' >> 7 and b 2^16 = b' << 9 (mod 2^32).
+    constexpr int SH = AEnc<ENC>::SHIFT;
     const uint32_t b = d[2] + (d[3] << 8);
-    const uint32_t s32 = d[0] + (d[1] << 8) + (b << 16);
-    const uint32_t t = s32 - p.q * (b >> (ELL - 16));
-#else
-    const uint32_t a = 0u - (d[0] + (d[1] << 8));   // S0 + S1 2^8  (< 2^26)
-    const uint32_t b = 0u - (d[2] + (d[3] << 8));   // S2 + S3 2^8
-    const uint32_t t = a + ((b & ((1u << (ELL - 16)) - 1u)) << 16) + p.pm_c * (b >> (ELL - 16));
-#endif
+    const uint32_t a = d[0] + (d[1] << 8);
+    const uint32_t s32 = (a >> SH) + (b << (16 - SH));
+    const uint32_t t = s32 - p.q * (b >> (ELL - 16 + SH));
     r = min(t, t - p.q);                            // t < 2q
   } else {
     const int64_t sum = (int64_t)(int32_t)d[0] + ((int64_t)(int32_t)d[1] << 8) +
                         ((int64_t)(int32_t)d[2] << 16) + ((int64_t)(int32_t)d[3] << 24);
-    const int64_t s = FHEGPU_A_POS ? sum : -sum;
+    const int64_t s = sum >> AEnc<ENC>::SHIFT;
     r = mod_u64((uint64_t)s, p.q, p.mu);
   }
   const uint32_t x = g - r;
@@ -322,15 +336,15 @@ __device__ __forceinline__ uint32_t lane_of(uint32_t item, uint32_t lanes, uint3
   return r;
 }
 
-template <int K, int ELL, bool PM>
-__global__ void __launch_bounds__(GeoWS<K, ELL, PM>::THREADS, 1)
+template <int K, int ELL, bool PM, int ENC>
+__global__ void __launch_bounds__(GeoWS<K, ELL, PM, ENC>::THREADS, 1)
 level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uint32_t n_ops,
                    uint32_t lanes, DevParams p, const int2 *__restrict__ deps, uint32_t *__restrict__ progress) {
   // deps == nullptr: one netlist level (the previous level completed before launch).
   // deps != nullptr: a whole program in dataflow order (ops topologically sorted, SSA slots:
   // no slot is written twice or overwritten while a reader may still need it); each operand
   // load waits for its producing item via `progress` (gridDim.x entries, zeroed per run).
-  using G = GeoWS<K, ELL, PM>;
+  using G = GeoWS<K, ELL, PM, ENC>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint32_t *s_in = reinterpret_cast<uint32_t *>(smem + G::OFF_IN);
   uint8_t *s_b = smem + G::OFF_B;
@@ -520,7 +534,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
 #pragma unroll
           for (int i = 0; i < K; ++i) {
             const uint32_t g = (i == rb) ? (1u << rbit) : 0u;
-            out_st[r * K + i] = finish_neg<ELL, PM>(&d[i * 4], g, p);
+            out_st[r * K + i] = finish_neg<ELL, PM, ENC>(&d[i * 4], g, p);
           }
         }
         if (lane == 0) trace_ev(p, t, 1);
@@ -586,7 +600,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               uint32_t one[8];
-              spread_word_sr(words[w0 + j], one);
+              spread_word_sr<ENC>(words[w0 + j], one);
 #pragma unroll
               for (int x = 0; x < 8; ++x) sp[8 * j + x] = one[x];
             }
@@ -595,7 +609,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
 #pragma unroll
             for (int w = w0; w < K; ++w) {
               uint32_t sp[8];
-              spread_word_sr(words[w], sp);
+              spread_word_sr<ENC>(words[w], sp);
               tmem_st8(a_addr + 8 * w, sp);
             }
           }
@@ -609,7 +623,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
           uint32_t v = v1[r * K + w];
           if (comp1) v = sub_mod(w == r / ELL ? (1u << (r % ELL)) : 0u, v, p.q);
           uint32_t sp[8];
-          spread_word_sr(v, sp);
+          spread_word_sr<ENC>(v, sp);
           uint8_t *dst = s_ta + b * G::TA_BYTES + (2 * w) * G::TA_LBO + m * 16;
           *reinterpret_cast<uint4 *>(dst) = make_uint4(sp[0], sp[1], sp[2], sp[3]);
           *reinterpret_cast<uint4 *>(dst + G::TA_LBO) = make_uint4(sp[4], sp[5], sp[6], sp[7]);
@@ -694,7 +708,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
 #pragma unroll
         for (int i = 0; i < K; ++i) {
           const uint32_t g = (i == row_blk) ? (1u << row_bit) : 0u;
-          out_st[row * K + i] = finish_neg<ELL, PM>(&d[i * 4], g, p);
+          out_st[row * K + i] = finish_neg<ELL, PM, ENC>(&d[i * 4], g, p);
         }
       }
       fence_proxy_async_smem();

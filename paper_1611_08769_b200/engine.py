@@ -644,7 +644,8 @@ class GpuEngine(LevelledNetlist):
     # tiled dataflow: lanes per chunk, and the single-assignment store budget it may use
     TILE_LANES = int(os.environ.get("FHEGPU_TILE_LANES", "128"))
     TILE_SKEW = int(os.environ.get("FHEGPU_TILE_SKEW", "0"))      # 0: pick from the window below
-    TILE_WINDOW = 1536        # items between a level and the next of one chunk (> ~1036 in flight)
+    TILE_WINDOW = 2304        # items between a level and the next of one chunk: more than a CTA
+    #                           pipeline holds (148 x ~12 items, ring + buffers + staging)
     TILE_RING = int(os.environ.get("FHEGPU_TILE_RING", "8"))      # chunks of temporaries kept in L2
     TILED_MAX_LEVELS = 32
 
