@@ -131,9 +131,18 @@ int launch_tc_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_
   }
   const uint64_t items = (uint64_t)n_ops * lanes;
   const uint64_t grid = std::min<uint64_t>(items, (uint64_t)c->num_sms * 2);
-  tc::level_tc_kernel<K, ELL, PM><<<(unsigned)grid, G::THREADS, smem, c->stream>>>(
-      store, ops, n_ops, lanes, c->p);
-  CUDA_TRY(cudaGetLastError());
+  // programmatic dependent launch as for the warp-specialised kernel (dbg bit 13 disables)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(G::THREADS);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (c->p.dbg & 8192u) ? 0 : 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::level_tc_kernel<K, ELL, PM>, store, ops, n_ops, lanes, c->p));
   return FHEGPU_OK;
 }
 

@@ -311,6 +311,9 @@ level_tc_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uin
   const int warp = tid >> 5;
   const uint64_t n_items = (uint64_t)n_ops * lanes;
 
+  // programmatic dependent launch: the next level's CTAs may take SMs as ours leave and
+  // run their prologue (TMEM alloc, barrier init, smem zeroing) under our tail
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (warp == 0) tmem_alloc<G::TMEM_COLS>(tmem_slot);
   if (tid == 0) {
 #pragma unroll
@@ -330,6 +333,8 @@ level_tc_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uin
   const int tile = warp >> 2;                                      // MMA tile of this thread's row
   const int row = tid;                                             // ciphertext row of this thread
   const int row_blk = row / ELL, row_bit = row - row_blk * ELL;
+  // every ciphertext access comes after the previous level completed (no-op without PDL)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   auto item_ptrs = [&](uint64_t item, const uint32_t *&a, const uint32_t *&b, uint32_t *&o,
                        uint32_t &flags) {
