@@ -484,6 +484,7 @@ def run_ours(args):
         return
     ms = res["ms"]
     value = res["nand_per_step"] * world / (ms / 1e3)
+    tiled = res["schedule"].startswith("tiled")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -499,10 +500,10 @@ def run_ours(args):
             "kernel": res["kernel"], "schedule": res["schedule"], "decrypt_check": res["ok"],
             "store_gb": round(res["store_gb"], 1), "setup_s": round(res["setup_s"], 2),
         },
-        "roofline": {
+        "roofline": {   # A-operand encoding template arg: 1 in dataflow launches, 2 in levels
             "bound": "hbm", "achieved": res["achieved"], "peak": res["peak"], "unit": "GB/s",
             "frac": res["achieved"] / res["peak"], "traffic": res["traffic"],
-            "kernel": "fhegpu::tc::level_tc_ws_kernel<9,29,true>",
+            "kernel": "fhegpu::tc::level_tc_ws_kernel<9,29,true,%d>" % (1 if tiled else 2),
             "algorithmic_bytes_per_nand": ALG_BYTES_PER_NAND_261,
             "level_launch_ms": [round(x, 4) for x in res["level_ms"]],
             "peak_source": res["peak_kind"],
