@@ -243,6 +243,15 @@ __device__ __forceinline__ void load_acc36(uint32_t taddr, uint32_t (&d)[36], bo
   tmem_ld4(taddr + 32, d + 32);
 }
 
+// tail MMA (5 live rows): M = FHEGPU_TAIL_M; FHEGPU_TAIL_ZERO backs the rows past the live
+// 8-row group with zeros (see GeoWS::TA_GROUPS)
+#ifndef FHEGPU_TAIL_M
+#define FHEGPU_TAIL_M 64
+#endif
+#ifndef FHEGPU_TAIL_ZERO
+#define FHEGPU_TAIL_ZERO 1
+#endif
+
 template <int K, int ELL, bool PM, int ENC>
 struct GeoWS {
   using B = Geo<K, ELL>;
@@ -252,7 +261,13 @@ struct GeoWS {
   static constexpr int MMA_ROWS = B::MMA_ROWS;
   static constexpr int NPAD = B::NPAD, NCH = B::NCH, KB = B::KB, NDIG = B::NDIG;
   static constexpr uint32_t SBO = B::SBO, LBO = B::LBO, TA_LBO = B::TA_LBO;
-  static constexpr int B_BYTES = B::B_BYTES, TA_BYTES = B::TA_BYTES;
+  static constexpr int B_BYTES = B::B_BYTES;
+  // tail A: the live 8-row core-matrix group (rows MMA_ROWS.., K-major) followed by
+  // TAIL_M/8 - 1 all-zero groups, so the M = TAIL_M tail MMA multiplies B by zero rows
+  // (no datapath toggles) instead of by copies of the live rows (SBO = 0 aliasing)
+  static constexpr int TA_GROUPS = FHEGPU_TAIL_ZERO ? FHEGPU_TAIL_M / 8 : 1;
+  static constexpr uint32_t TA_SBO = FHEGPU_TAIL_ZERO ? (uint32_t)B::TA_BYTES : 0u;
+  static constexpr int TA_BYTES = B::TA_BYTES * TA_GROUPS;
   static constexpr int WORDS = B::WORDS;
   static constexpr int CT_WORDS = B::CT_WORDS, CT_BYTES = B::CT_BYTES;
   static constexpr int MAIN_BYTES = MMA_ROWS * K * 4;       // rows stored by the bulk copy
@@ -269,11 +284,8 @@ struct GeoWS {
   // B MN-major, N>>3, M>>4
   static constexpr uint32_t IDESC = (2u << 4) | (AEnc<ENC>::A_FMT << 7) | (1u << 16) |
                                     ((uint32_t)(NPAD >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  // tail MMA (5 live rows, A aliased over the M extent): M = TAIL_M halves the datapath work of
-  // the duplicate rows when 64 -- same issue cost (the floor is max(M, 128)), less energy
-#ifndef FHEGPU_TAIL_M
-#define FHEGPU_TAIL_M 64
-#endif
+  // tail MMA (5 live rows): M = 64 has the issue cost of M = 128 (the floor is max(M, 128))
+  // and half the datapath work
   static constexpr uint32_t IDESC_TAIL = (IDESC & ~(0x1fu << 24)) | ((uint32_t)(FHEGPU_TAIL_M >> 4) << 24);
   static constexpr int OFF_IN = 0;
   static constexpr int OFF_B = OFF_IN + S_IN * 2 * CT_BYTES;
@@ -456,7 +468,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
     uint32_t t = 0;
     const uint32_t idesc = G::IDESC;
     const uint64_t bdesc0 = smem_desc(smem_u32(s_b), G::LBO, G::SBO);
-    const uint64_t tdesc0 = smem_desc(smem_u32(s_ta), G::TA_LBO, 0u);
+    const uint64_t tdesc0 = smem_desc(smem_u32(s_ta), G::TA_LBO, G::TA_SBO);
     for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
       const uint32_t b = t & 1u, u = t >> 1;
       mbar_wait(&op_full[b], u & 1u);
