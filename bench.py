@@ -42,6 +42,14 @@ PAIRS_FULL = 1 << 20
 ALG_BYTES_PER_NAND_261 = 3 * math.ceil(261 * 261 / 8)   # 25,548 B
 
 
+def _fft_roofline(nand_per_s: float, n_ct: int) -> dict:
+    """HBM-roofline fraction of an FFT line: reference-counted NAND/s x 3*ceil(N^2/8) bytes."""
+    peak, kind = _peaks()
+    achieved = nand_per_s * 3 * math.ceil(n_ct * n_ct / 8) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "algorithmic_bytes_per_nand": 3 * math.ceil(n_ct * n_ct / 8), "peak_source": kind}
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -407,7 +415,8 @@ def bench_fft(args, world, rank, local):
     return {"ms": ms, "ffts_per_s": lanes * world / (ms / 1e3),
             "nand_per_s": eng.nand_count * lanes * world / (ms / 1e3),
             "nand_per_fft": eng.nand_count, "levels": prog.n_levels, "lanes": lanes,
-            "build_s": build_s, "ok": ok}
+            "build_s": build_s, "ok": ok,
+            "roofline": _fft_roofline(eng.nand_count * lanes * world / (ms / 1e3), scheme.params.n_ct)}
 
 
 def bench_fft_single(args, world, rank, local, cfg):
@@ -455,6 +464,7 @@ def bench_fft_single(args, world, rank, local, cfg):
             "value": world / (ms / 1e3), "unit": "FFT/s", "ms_per_fft": ms,
             "nand_per_s": eng.nand_count * world / (ms / 1e3), "nand_per_fft": eng.nand_count,
             "levels": prog.n_levels, "launches_per_fft": prog.launches,
+            "roofline": _fft_roofline(eng.nand_count * world / (ms / 1e3), scheme.params.n_ct),
             "decrypt_check_vs_reference": ok}
 
 
@@ -524,7 +534,8 @@ def run_ours(args):
         line["fft"] = {"metric": "16-pt Q4.12 FHE FFTs/s (configs[4])", "value": fft["ffts_per_s"],
                        "unit": "FFT/s", "nand_per_s": fft["nand_per_s"], "ms_per_step": fft["ms"],
                        "lanes": fft["lanes"], "nand_per_fft": fft["nand_per_fft"],
-                       "levels": fft["levels"], "decrypt_check_vs_reference": fft["ok"]}
+                       "levels": fft["levels"], "roofline": fft["roofline"],
+                       "decrypt_check_vs_reference": fft["ok"]}
     if single:
         line["fft_single"] = single
     if cpu is not None:
