@@ -53,7 +53,10 @@ typedef struct {
 /* One netlist gate.  `left` is the operand the reference multiplies on the
  * left AFTER its noise swap (fhe.py:336-337).  Flags bit 0 / bit 1 complement
  * the left / right operand on load: that is how NOT gates (hom_not, produced
- * only by folding NAND(x, 1), engine.py:180-187) are evaluated for free. */
+ * only by folding NAND(x, 1), engine.py:180-187) are evaluated for free.
+ * Flags bit 3 (FHEGPU_OP_STREAM_OUT, a hint): nothing later in the same program reads `out`;
+ * its store is marked L2 evict-first so it does not displace the program's temporaries. */
+#define FHEGPU_OP_STREAM_OUT 8u
 typedef struct {
   uint32_t left;
   uint32_t right;

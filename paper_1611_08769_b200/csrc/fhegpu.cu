@@ -553,7 +553,7 @@ int fhegpu_prog_create(fhegpu_ctx *c, const fhegpu_op *ops, uint64_t n_ops,
   uint64_t n_slots = 0;
   for (uint64_t i = 0; i < n_ops; ++i) {
     const uint32_t mx = std::max(ops[i].left, std::max(ops[i].right, ops[i].out));
-    if (mx >= (1u << 31) || (ops[i].flags & ~3u))
+    if (mx >= (1u << 31) || (ops[i].flags & ~(3u | FHEGPU_OP_STREAM_OUT)))
       return fail(FHEGPU_EINVAL, "bad op record " + std::to_string(i));
     n_slots = std::max<uint64_t>(n_slots, uint64_t(mx) + 1);
   }

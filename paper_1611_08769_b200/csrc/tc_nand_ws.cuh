@@ -142,6 +142,20 @@ __device__ __forceinline__ void post_local(uint32_t *s_pub, uint32_t n) {
   asm volatile("st.volatile.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(s_pub)), "r"(n) : "memory");
 }
 
+// L2 evict-first policy for stores of streamed outputs (op flag FHEGPU_OP_STREAM_OUT)
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ void bulk_s2g_hint(void *dst, const void *src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes), "l"(pol)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -688,6 +702,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
     }
     uint32_t t = 0;
     OpRec op_next = fetch_op(ops, blockIdx.x, n_items, lanes, p.lanes_magic);
+    const uint64_t pol_stream = policy_evict_first();
     for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
       const uint32_t b = t & 1u, u = t >> 1;
       const OpRec op_cur = op_next;
@@ -738,7 +753,9 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
       }
       if (et == 0 && !(p.dbg & 512u)) {
         const uint32_t ln = lane_of(item, lanes, p.lanes_magic);
-        bulk_s2g(store + ((uint64_t)op_cur.out * lanes + ln) * G::CT_WORDS, out_st, G::CT_BYTES);
+        uint32_t *dst = store + ((uint64_t)op_cur.out * lanes + ln) * G::CT_WORDS;
+        if (op_cur.flags & 8u) bulk_s2g_hint(dst, out_st, G::CT_BYTES, pol_stream);
+        else bulk_s2g(dst, out_st, G::CT_BYTES);
       }
     }
     if (et == 0) {

@@ -35,6 +35,7 @@ from .errors import CapabilityError, NoiseOverflowError, UsageError
 from .scheme import Ciphertext, GswScheme, KeyPair
 
 _UPLOAD_BATCH_BYTES = 256 << 20
+STREAM_OUT = 8          # fhegpu_op flag (include/fhegpu.h): output not read later in the program
 
 
 @dataclass(frozen=True)
@@ -726,14 +727,16 @@ class GpuEngine(LevelledNetlist):
                 tid = temp[o, i]
                 v = np.where(tid >= 0, t_base + (c % ring) * prog["n_temp"] + tid, v)
             tiled[f] = v
-        tiled["flags"] = ops["flags"][o]
+        # outputs no op of the program reads (sinks) are stored L2 evict-first: they stream out
+        # and should not push the chunks' temporaries out of L2
+        read = np.zeros(n, dtype=bool)
+        read[deps[deps >= 0]] = True
+        tiled["flags"] = ops["flags"][o] | np.where(read[o], 0, STREAM_OUT).astype(ops["flags"].dtype)
         d = deps[o]
         tdeps = np.where(d >= 0, pos[c[:, None] * n + np.maximum(d, 0)], -1)
         if temp is not None:
             # a root of chunk c (step c) must come after the sinks of chunk c - ring (step
             # c - ring + skew * level): ring > skew * deepest level keeps the order topological
-            read = np.zeros(n, dtype=bool)
-            read[deps[deps >= 0]] = True
             sinks = np.flatnonzero(~read)
             roots = (deps < 0).all(axis=1)
             assert 1 <= len(sinks) <= 2, "ring temporaries need at most two sinks"
