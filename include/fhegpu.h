@@ -167,6 +167,15 @@ int fhegpu_prog_run_host(fhegpu_ctx *ctx, fhegpu_prog *prog, uint64_t lanes, uin
  * the level offsets are a valid schedule (no op depends on an op of its own level), and
  * otherwise fails with FHEGPU_EUNSUP instead of running it wrongly. */
 int fhegpu_prog_set_deps(fhegpu_ctx *ctx, fhegpu_prog *prog, const int32_t *deps);
+
+/* Opt-in ready-queue execution of a program whose dependencies are set (fhegpu_prog_set_deps):
+ * one launch in which CTAs pop only items whose producing items have completed and retire
+ * their own items to the consumers' pending counts (pushing consumers that become ready).
+ * No static item -> CTA assignment, so no CTA waits on an operand while other work is ready.
+ * Same results as level launches (SSA slots required, as for dataflow).  enable = 0 reverts
+ * to the static dataflow order.  Replaces the reference's sequential gate loop
+ * (engine.py:168-178 driving fhe.py:325-341) like fhegpu_prog_run. */
+int fhegpu_prog_set_queue(fhegpu_ctx *ctx, fhegpu_prog *prog, int enable);
 uint32_t fhegpu_prog_launches(const fhegpu_prog *prog);       /* launches one run issues */
 void fhegpu_prog_destroy(fhegpu_prog *prog);
 

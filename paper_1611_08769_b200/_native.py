@@ -61,6 +61,7 @@ SIGNATURES = [
     ("fhegpu_prog_run_range", ctypes.c_int, [_P, _P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]),
     ("fhegpu_prog_launches", ctypes.c_uint32, [_P]),
     ("fhegpu_prog_set_deps", ctypes.c_int, [_P, _P, _P]),
+    ("fhegpu_prog_set_queue", ctypes.c_int, [_P, _P, ctypes.c_int]),
     ("fhegpu_store_write_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     ("fhegpu_store_read_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     ("fhegpu_prog_run_host", ctypes.c_int, [_P, _P, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int,
@@ -175,6 +176,12 @@ class Program:
         deps = np.ascontiguousarray(deps, dtype=np.int32)
         _check(_lib.fhegpu_prog_set_deps(self.ctx.handle, self.handle, deps.ctypes.data_as(ctypes.c_void_p)),
                "prog_set_deps")
+        self.launches = int(_lib.fhegpu_prog_launches(self.handle))
+
+    def set_queue(self, enable: bool = True):
+        """Ready-queue mode (fhegpu_prog_set_queue): one launch in which CTAs pop only items
+        whose producers have completed (needs set_deps first)."""
+        _check(_lib.fhegpu_prog_set_queue(self.ctx.handle, self.handle, int(bool(enable))), "prog_set_queue")
         self.launches = int(_lib.fhegpu_prog_launches(self.handle))
 
     def run_host(self, lanes: int, chunk_lanes: int, in_slots, in_ptrs, out_slots, out_ptrs,

@@ -82,6 +82,14 @@ struct fhegpu_prog {
   bool levels_valid = true;       // level launches are a valid fallback (no op depends on an op
                                   // of its own level); false for tiled programs
   uint32_t *d_progress = nullptr; // per-CTA completed-item counters
+  // ready-queue launches (fhegpu_prog_set_queue): per-op pending counts, consumer lists, roots
+  std::vector<int32_t> deps_host;
+  bool use_queue = false;
+  uint32_t *d_qmeta = nullptr;    // pend0[n_ops] | cons_off[n_ops + 1] | cons[n_edges] | roots[n_roots]
+  uint64_t n_edges = 0;
+  uint32_t n_roots = 0;
+  uint32_t *d_qrun = nullptr;     // per run: counters[4] | pending[n_items] | queue[n_items]
+  size_t qrun_cap = 0;
   // CUDA graph of one full run (all level launches), captured on first use per
   // (lanes, stream, kernel choice, debug bits); replayed with a single cudaGraphLaunch
   cudaGraphExec_t graph = nullptr;
@@ -146,15 +154,15 @@ int launch_tc_impl(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_
   return FHEGPU_OK;
 }
 
-template <int K, int ELL, bool PM, int ENC>
+template <int K, int ELL, bool PM, int ENC, bool Q = false>
 int launch_tc_ws_enc(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t n_ops, uint32_t lanes,
-                      const int2 *deps, uint32_t *progress) {
-  using G = tc::GeoWS<K, ELL, PM, ENC>;
+                      const int2 *deps, uint32_t *progress, const tc::QueueArgs &qa = tc::QueueArgs{}) {
+  using G = tc::GeoWS<K, ELL, PM, ENC, Q>;
   static bool attr_done = false;
   // > half of the SM's shared memory: exactly one CTA (512 TMEM columns) per SM
   const int smem = std::max(G::SMEM, 120 * 1024);
   if (!attr_done) {
-    CUDA_TRY(cudaFuncSetAttribute(tc::level_tc_ws_kernel<K, ELL, PM, ENC>,
+    CUDA_TRY(cudaFuncSetAttribute(tc::level_tc_ws_kernel<K, ELL, PM, ENC, Q>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_done = true;
   }
@@ -175,8 +183,8 @@ int launch_tc_ws_enc(fhegpu_ctx *c, uint32_t *store, const OpRec *ops, uint32_t 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = (c->p.dbg & 8192u) ? 0 : 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::level_tc_ws_kernel<K, ELL, PM, ENC>, store, ops, n_ops, lanes, p,
-                              deps, progress));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, tc::level_tc_ws_kernel<K, ELL, PM, ENC, Q>, store, ops, n_ops, lanes, p,
+                              deps, progress, qa));
   return FHEGPU_OK;
 }
 
@@ -262,6 +270,49 @@ unsigned grid_for(uint64_t work, int num_sms) {
   uint64_t g = (work + 255) / 256;
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, (uint64_t)num_sms * 16));
 }
+
+// Ready-queue state before a run: every item's pending count from its op, the queue holding
+// the root items (ops with no producer in the program) and EMPTY elsewhere, cursors reset.
+__global__ void queue_init_kernel(uint32_t *counters, uint32_t *pending, uint32_t *queue, const uint32_t *pend0,
+                                  const uint32_t *roots, uint32_t n_roots, uint32_t lanes, uint32_t n_items) {
+  const uint32_t n_root_items = n_roots * lanes;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_items; i += gridDim.x * blockDim.x) {
+    const uint32_t op = i / lanes, ln = i - op * lanes;
+    pending[i] = pend0[op];
+    queue[i] = i < n_root_items ? roots[op] * lanes + ln : tc::Q_EMPTY;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    counters[0] = 0u;
+    counters[1] = n_root_items;
+  }
+}
+
+#ifndef FHEGPU_ENC_QUEUE
+#define FHEGPU_ENC_QUEUE 1     // A encoding of ready-queue launches (cfg2/cfg3: 1 is ~1% faster)
+#endif
+
+// A whole program in one launch over a ready queue (after queue_init_kernel).
+int launch_queue(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
+  if (pr->n_ops == 0 || lanes == 0) return FHEGPU_OK;
+  if (effective_kernel(c) != FHEGPU_KERNEL_TCGEN05 || (c->p.dbg & 4u)) return FHEGPU_EUNSUP;
+  if (!(c->p.k == 9 && c->p.ell == 29)) return FHEGPU_EUNSUP;
+  const uint64_t n_items = pr->n_ops * lanes;
+  if (n_items >= (1ull << 31)) return FHEGPU_EUNSUP;
+  if (int rc = ensure((void **)&pr->d_qrun, &pr->qrun_cap, (4 + 2 * n_items) * sizeof(uint32_t))) return rc;
+  uint32_t *counters = pr->d_qrun, *pending = counters + 4, *queue = pending + n_items;
+  const uint32_t *pend0 = pr->d_qmeta, *cons_off = pend0 + pr->n_ops, *cons = cons_off + pr->n_ops + 1;
+  const uint32_t *roots = cons + pr->n_edges;
+  queue_init_kernel<<<grid_for(n_items, c->num_sms), 256, 0, c->stream>>>(
+      counters, pending, queue, pend0, roots, pr->n_roots, lanes, (uint32_t)n_items);
+  CUDA_TRY(cudaGetLastError());
+  const tc::QueueArgs qa{queue, counters, pending, cons_off, cons};
+  if (pm_ok(c->p.q, c->p.ell) && !(c->p.dbg & 2u))
+    return launch_tc_ws_enc<9, 29, true, FHEGPU_ENC_QUEUE, true>(c, c->store, pr->d_ops, (uint32_t)pr->n_ops,
+                                                                 lanes, nullptr, nullptr, qa);
+  return launch_tc_ws_enc<9, 29, false, FHEGPU_ENC_QUEUE, true>(c, c->store, pr->d_ops, (uint32_t)pr->n_ops,
+                                                                lanes, nullptr, nullptr, qa);
+}
+
 
 }  // namespace
 
@@ -586,7 +637,11 @@ int fhegpu_prog_run_range(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes, uint32
   const uint32_t n_levels = (uint32_t)pr->offsets.size() - 1;
   last = std::min(last, n_levels);
   CUDA_TRY(cudaSetDevice(c->device));
-  if (pr->d_deps && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
+  if (pr->use_queue && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
+    const int rc = launch_queue(c, pr, lanes);
+    if (rc != FHEGPU_EUNSUP) return rc;
+    // else: level by level (queue programs keep their level structure)
+  } else if (pr->d_deps && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
     const int rc = launch_dataflow(c, c->store, pr->d_ops, (uint32_t)pr->n_ops, lanes, pr->d_deps,
                                    pr->d_progress);
     if (rc != FHEGPU_EUNSUP) return rc;
@@ -778,10 +833,58 @@ int fhegpu_prog_set_deps(fhegpu_ctx *c, fhegpu_prog *pr, const int32_t *deps) {
   CUDA_TRY(cudaMalloc(&pr->d_progress, (size_t)std::max(c->num_sms, 1) * sizeof(uint32_t)));
   CUDA_TRY(cudaMemcpyAsync(pr->d_deps, deps, pr->n_ops * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  pr->deps_host.assign(deps, deps + 2 * pr->n_ops);
+  pr->use_queue = false;                 // (re)enable with fhegpu_prog_set_queue
   if (pr->graph) {                      // launch structure changed
     cudaGraphExecDestroy(pr->graph);
     pr->graph = nullptr;
   }
+  return FHEGPU_OK;
+}
+
+int fhegpu_prog_set_queue(fhegpu_ctx *c, fhegpu_prog *pr, int enable) {
+  if (!c || !pr) return fail(FHEGPU_EINVAL, "null argument");
+  if (pr->graph) {                      // launch structure changes
+    cudaGraphExecDestroy(pr->graph);
+    pr->graph = nullptr;
+  }
+  if (!enable) {
+    pr->use_queue = false;
+    return FHEGPU_OK;
+  }
+  const uint64_t n = pr->n_ops;
+  if (pr->deps_host.size() != 2 * n) return fail(FHEGPU_EINVAL, "set the program's dependencies first");
+  if (!pr->levels_valid) return fail(FHEGPU_EINVAL, "ready-queue programs need a level structure");
+  // pending count = distinct producing ops; consumer lists (CSR) per producing op
+  std::vector<uint32_t> pend0(n), cons_off(n + 1, 0);
+  for (uint64_t i = 0; i < n; ++i) {
+    const int32_t a = pr->deps_host[2 * i], b = pr->deps_host[2 * i + 1];
+    pend0[i] = (a >= 0) + (b >= 0 && b != a);
+    if (a >= 0) ++cons_off[a + 1];
+    if (b >= 0 && b != a) ++cons_off[b + 1];
+  }
+  for (uint64_t i = 0; i < n; ++i) cons_off[i + 1] += cons_off[i];
+  std::vector<uint32_t> cons(cons_off[n]), fill(cons_off.begin(), cons_off.end() - 1), roots;
+  for (uint64_t i = 0; i < n; ++i) {
+    const int32_t a = pr->deps_host[2 * i], b = pr->deps_host[2 * i + 1];
+    if (a >= 0) cons[fill[a]++] = (uint32_t)i;
+    if (b >= 0 && b != a) cons[fill[b]++] = (uint32_t)i;
+    if (pend0[i] == 0) roots.push_back((uint32_t)i);
+  }
+  std::vector<uint32_t> meta;
+  meta.reserve(2 * n + 1 + cons.size() + roots.size());
+  meta.insert(meta.end(), pend0.begin(), pend0.end());
+  meta.insert(meta.end(), cons_off.begin(), cons_off.end());
+  meta.insert(meta.end(), cons.begin(), cons.end());
+  meta.insert(meta.end(), roots.begin(), roots.end());
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaFree(pr->d_qmeta);
+  pr->d_qmeta = nullptr;
+  CUDA_TRY(cudaMalloc(&pr->d_qmeta, meta.size() * sizeof(uint32_t)));
+  CUDA_TRY(cudaMemcpy(pr->d_qmeta, meta.data(), meta.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  pr->n_edges = cons.size();
+  pr->n_roots = (uint32_t)roots.size();
+  pr->use_queue = true;
   return FHEGPU_OK;
 }
 
@@ -793,6 +896,7 @@ int fhegpu_ctx_set_graphs(fhegpu_ctx *c, int enable) {
 
 uint32_t fhegpu_prog_launches(const fhegpu_prog *pr) {
   if (!pr) return 0;
+  if (pr->use_queue) return 2;                  // ready queue: state reset + one launch
   if (pr->d_deps) return 1;                     // dataflow: one launch (tcgen05 parameter sets)
   uint32_t n = 0;
   for (size_t l = 0; l + 1 < pr->offsets.size(); ++l) n += pr->offsets[l + 1] > pr->offsets[l];
@@ -804,6 +908,8 @@ void fhegpu_prog_destroy(fhegpu_prog *pr) {
   if (pr->graph) cudaGraphExecDestroy(pr->graph);
   cudaFree(pr->d_deps);
   cudaFree(pr->d_progress);
+  cudaFree(pr->d_qmeta);
+  cudaFree(pr->d_qrun);
   cudaFree(pr->d_ops);
   delete pr;
 }

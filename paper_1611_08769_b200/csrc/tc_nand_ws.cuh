@@ -266,7 +266,7 @@ __device__ __forceinline__ void load_acc36(uint32_t taddr, uint32_t (&d)[36], bo
 #define FHEGPU_TAIL_ZERO 1
 #endif
 
-template <int K, int ELL, bool PM, int ENC>
+template <int K, int ELL, bool PM, int ENC, bool Q = false>
 struct GeoWS {
   using B = Geo<K, ELL>;
   static constexpr int ROWS = B::ROWS;
@@ -290,8 +290,25 @@ struct GeoWS {
   static constexpr int NB_WARPS = 4 * MT, NE_WARPS = 4 * MT;
   static constexpr int WARP_TAIL = 0, WARP_PROD = 1, WARP_MMA = 2;
   static constexpr int WARP_BUILD0 = 3, WARP_EPI0 = 3 + NB_WARPS;
-  static constexpr int THREADS = 32 * (3 + NB_WARPS + NE_WARPS);
-  static constexpr int S_IN = 7;                            // ~2.5 us load latency x bandwidth
+  // ready-queue launches (Q): a fetcher warp (pops ready items) and a signaler warp (retires
+  // completed items to their consumers) after the epilogue warps
+  static constexpr int WARP_FETCH = 3 + NB_WARPS + NE_WARPS, WARP_SIG = WARP_FETCH + 1;
+  static constexpr int THREADS = 32 * (3 + NB_WARPS + NE_WARPS + (Q ? 2 : 0));
+// ready-queue launches: operand stages, fetch-ring entries, queue pops per fetch batch
+// (swept on cfg2/cfg3: 5/4/2; one pop per batch leaves the fetcher latency-bound, deeper
+// rings put more items ahead of each dependency hop)
+#ifndef FHEGPU_Q_STAGES
+#define FHEGPU_Q_STAGES 5
+#endif
+#ifndef FHEGPU_Q_FQ
+#define FHEGPU_Q_FQ 4
+#endif
+#ifndef FHEGPU_Q_FD
+#define FHEGPU_Q_FD 2
+#endif
+  // operand stages: ~2.5 us load latency x bandwidth (ready-queue launches: every stage is
+  // also latency on the dependency chain; their operands are mostly L2 hits)
+  static constexpr int S_IN = Q ? FHEGPU_Q_STAGES : 7;
   static constexpr int N_OUT = 3;                           // output staging buffers
   static constexpr uint32_t OP_ARRIVALS = NB_WARPS;
   // idesc: S32 accumulator, A s8 (bits 7-9 = 1) or u8 (encoding 2), B u8, A K-major,
@@ -310,7 +327,16 @@ struct GeoWS {
   static constexpr int MAX_CTAS = 256;
   static constexpr int OFF_PUB = OFF_SEEN + 4 * MAX_CTAS;  // dataflow: epilogue -> tail relay
   static constexpr int OFF_FLAGS = OFF_PUB + 16;            // op flags of each input stage
-  static constexpr int SMEM = OFF_FLAGS + 4 * ((S_IN + 3) / 4 * 4);
+  // ready queue (Q): fetched-entry ring, per-slot item / output rings, counters
+  static constexpr int FQ = FHEGPU_Q_FQ, FD = FHEGPU_Q_FD;  // fetch ring entries, pops per batch
+  static constexpr int QR = 64;                             // slot ring (item, output ciphertext)
+  static constexpr int OFF_Q = OFF_FLAGS + 4 * ((S_IN + 3) / 4 * 4);
+  static constexpr int OFF_FQ = OFF_Q;                      // FQ x uint4 {left, right, out, flags}
+  static constexpr int OFF_FQI = OFF_FQ + 16 * FQ;          // FQ x {item, seq}
+  static constexpr int OFF_QITEM = OFF_FQI + 8 * FQ;        // QR items
+  static constexpr int OFF_QOUT = OFF_QITEM + 4 * QR;       // QR output ciphertext indices
+  static constexpr int OFF_QCNT = OFF_QOUT + 4 * QR;        // fq_used, signaled, epi_end, pad
+  static constexpr int SMEM = Q ? OFF_QCNT + 16 : OFF_Q;
   static_assert(NDIG == 4 && B::NCOL <= 36, "warp-specialised kernel: 4 digits, <= 36 columns");
   static_assert(MT >= 1 && TAIL <= 8, "two-tile geometry");
   static_assert((uint64_t)ROWS * 255u * 257u << AEnc<ENC>::SHIFT < (1ull << 32), "scaled digit sums fit u32");
@@ -346,6 +372,32 @@ __device__ __forceinline__ uint32_t finish_neg(const uint32_t *d, uint32_t g, co
   return min(x, x + p.q);                           // (g - r) mod q for g, r < q
 }
 
+// Ready-queue state of one run (fhegpu.cu launch_queue resets it before every launch).
+struct QueueArgs {
+  uint32_t *queue;            // n_items entries: ready items in push order, EMPTY until pushed
+  uint32_t *counters;         // [0] pop cursor, [1] push cursor
+  uint32_t *pending;          // per item: producing items not yet retired
+  const uint32_t *cons_off;   // per op: consumer list offsets (n_ops + 1)
+  const uint32_t *cons;       // consumer ops (distinct per producer)
+};
+constexpr uint32_t Q_EMPTY = 0xFFFFFFFFu, Q_END = 0xFFFFFFFEu;
+
+__device__ __forceinline__ uint32_t ld_volatile_smem(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.volatile.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_volatile_smem(uint32_t *p, uint32_t v) {
+  asm volatile("st.volatile.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_dec_acq_rel_gpu(uint32_t *p) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(0xFFFFFFFFu) : "memory");
+  return old;
+}
+// bounded spin (a protocol error traps instead of hanging the GPU)
+#define FHEGPU_SPIN_LIMIT (1u << 26)
+
 // Op record of gate item `item` (or a dummy past the end): issued one gate ahead so the
 // global-load latency never sits on a role's critical loop.
 __device__ __forceinline__ OpRec fetch_op(const OpRec *ops, uint32_t item, uint32_t n_items,
@@ -362,15 +414,20 @@ __device__ __forceinline__ uint32_t lane_of(uint32_t item, uint32_t lanes, uint3
   return r;
 }
 
-template <int K, int ELL, bool PM, int ENC>
-__global__ void __launch_bounds__(GeoWS<K, ELL, PM, ENC>::THREADS, 1)
+template <int K, int ELL, bool PM, int ENC, bool Q>
+__global__ void __launch_bounds__(GeoWS<K, ELL, PM, ENC, Q>::THREADS, 1)
 level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, uint32_t n_ops,
-                   uint32_t lanes, DevParams p, const int2 *__restrict__ deps, uint32_t *__restrict__ progress) {
+                   uint32_t lanes, DevParams p, const int2 *__restrict__ deps, uint32_t *__restrict__ progress,
+                   QueueArgs qa) {
   // deps == nullptr: one netlist level (the previous level completed before launch).
   // deps != nullptr: a whole program in dataflow order (ops topologically sorted, SSA slots:
   // no slot is written twice or overwritten while a reader may still need it); each operand
   // load waits for its producing item via `progress` (gridDim.x entries, zeroed per run).
-  using G = GeoWS<K, ELL, PM, ENC>;
+  // Q: a whole program over a ready queue (SSA slots): CTAs pop items whose producers have
+  // retired (fetcher warp), and retire their own completed items to the consumers' pending
+  // counters, pushing each consumer whose count reaches zero (signaler warp).  Every role
+  // then runs slot by slot until the END slot; the per-slot item lives in a smem ring.
+  using G = GeoWS<K, ELL, PM, ENC, Q>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint32_t *s_in = reinterpret_cast<uint32_t *>(smem + G::OFF_IN);
   uint8_t *s_b = smem + G::OFF_B;
@@ -389,6 +446,11 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
   uint32_t *s_seen = reinterpret_cast<uint32_t *>(smem + G::OFF_SEEN);
   uint32_t *s_pub = reinterpret_cast<uint32_t *>(smem + G::OFF_PUB);
   uint32_t *s_flags = reinterpret_cast<uint32_t *>(smem + G::OFF_FLAGS);  // written by the producer
+  uint4 *s_fq = reinterpret_cast<uint4 *>(smem + G::OFF_FQ);               // Q: fetched ops
+  uint32_t *s_fqi = reinterpret_cast<uint32_t *>(smem + G::OFF_FQI);       // Q: {item, seq}
+  uint32_t *s_qitem = reinterpret_cast<uint32_t *>(smem + G::OFF_QITEM);   // Q: item of slot t
+  uint32_t *s_qout = reinterpret_cast<uint32_t *>(smem + G::OFF_QOUT);     // Q: output ct of slot t
+  uint32_t *s_qcnt = reinterpret_cast<uint32_t *>(smem + G::OFF_QCNT);     // Q: fq_used, signaled, epi_end
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -421,6 +483,10 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
   for (int w = tid; w < G::N_OUT * G::CT_WORDS; w += G::THREADS) s_out[w] = 0u;   // padding stays 0
   for (int w = tid; w < G::MAX_CTAS; w += G::THREADS) s_seen[w] = 0u;
   if (tid == 0) *s_pub = 0u;
+  if constexpr (Q) {
+    for (int w = tid; w < 2 * G::FQ; w += G::THREADS) s_fqi[w] = 0u;
+    if (tid < 4) s_qcnt[tid] = 0u;
+  }
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -432,7 +498,39 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
 
   if (warp == G::WARP_PROD) {
     // ------------------------------ producer ------------------------------
-    if (lane == 0) {
+    if (Q && lane == 0) {
+      // ready-queue launch: slot t takes fetched entry t (its operands are already written)
+      for (uint32_t t = 0;; ++t) {
+        const uint32_t s = t % G::S_IN, k = t / G::S_IN, e = t % G::FQ;
+        uint32_t spins = 0;
+        while (ld_acquire_cta_smem(&s_fqi[2 * e + 1]) != t + 1)
+          if (++spins > FHEGPU_SPIN_LIMIT) __trap();
+        const uint4 ent = s_fq[e];
+        const uint32_t item = s_fqi[2 * e];
+        st_release_cta_smem(&s_qcnt[0], t + 1);     // entry consumed: the fetcher may refill it
+        // slot-ring entry t % QR is reused once the signaler has retired slot t - QR
+        spins = 0;
+        while (t >= (uint32_t)G::QR && ld_volatile_smem(&s_qcnt[1]) + G::QR <= t) {
+          __nanosleep(32);
+          if (++spins > FHEGPU_SPIN_LIMIT) __trap();
+        }
+        mbar_wait(&in_empty[s], (k & 1u) ^ 1u);
+        s_qitem[t % G::QR] = item;
+        s_qout[t % G::QR] = ent.z;
+        if (item == Q_END) {                       // every role leaves at this slot
+          s_flags[s] = 0u;
+          mbar_arrive(&in_full[s]);
+          break;
+        }
+        fence_proxy_async_global();                 // acquired ready item -> async-proxy loads
+        const bool same = ent.x == ent.y;
+        s_flags[s] = ent.w | (same ? 4u : 0u);
+        uint32_t *dst = s_in + s * 2 * G::CT_WORDS;
+        mbar_expect_tx(&in_full[s], (same ? 1 : 2) * G::CT_BYTES);
+        bulk_g2s(dst, store + (uint64_t)ent.x * G::CT_WORDS, G::CT_BYTES, &in_full[s]);
+        if (!same) bulk_g2s(dst + G::CT_WORDS, store + (uint64_t)ent.y * G::CT_WORDS, G::CT_BYTES, &in_full[s]);
+      }
+    } else if (!Q && lane == 0) {
       uint32_t t = 0;
       OpRec op_next = fetch_op(ops, blockIdx.x, n_items, lanes, p.lanes_magic);
       int2 dep_next = make_int2(-1, -1);
@@ -483,9 +581,14 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
     const uint32_t idesc = G::IDESC;
     const uint64_t bdesc0 = smem_desc(smem_u32(s_b), G::LBO, G::SBO);
     const uint64_t tdesc0 = smem_desc(smem_u32(s_ta), G::TA_LBO, G::TA_SBO);
-    for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
+    for (uint32_t item = blockIdx.x; Q || item < n_items; item += gridDim.x, ++t) {
       const uint32_t b = t & 1u, u = t >> 1;
       mbar_wait(&op_full[b], u & 1u);
+      if (Q && s_qitem[t % G::QR] == Q_END) {       // release the tail / epilogue and leave
+        if (elect_one()) mma_commit(&main_done[b]);
+        __syncwarp();
+        break;
+      }
       if (lane == 0) trace_ev(p, t, 2);
       mbar_wait(&d_free[b], (u & 1u) ^ 1u);       // epilogue of gate t-2 has read D(b)
       if (lane == 0) trace_ev(p, t, 3);
@@ -526,7 +629,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
     if constexpr (G::TAIL > 0) {
       uint32_t t = 0;
       uint32_t relayed = 0;
-      for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
+      for (uint32_t item = blockIdx.x; Q || item < n_items; item += gridDim.x, ++t) {
         const uint32_t b = t & 1u, u = t >> 1;
         if (lane == 0) trace_ev(p, t, 12);
         if (progress != nullptr && lane == 0) {     // dataflow: relay the epilogue's count
@@ -539,6 +642,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
           }
         }
         mbar_wait(&main_done[b], u & 1u);
+        if (Q && s_qitem[t % G::QR] == Q_END) break;
         if (lane == 0) trace_ev(p, t, 13);
         tc_fence_after();
         uint32_t d[36];
@@ -572,6 +676,110 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
         }
       }
     }
+  } else if (warp == G::WARP_FETCH || warp == G::WARP_SIG) {
+    if constexpr (Q) {
+      if (warp == G::WARP_FETCH) {
+        // ------------------------------ fetcher (Q) ------------------------------
+        // Pops FD queue positions at a time; lane j waits until position base + j holds a
+        // pushed (ready) item, resolves its op to ciphertext indices and publishes the entry
+        // on its own (a later position may depend on an earlier one: no batch-wide wait)
+        uint32_t next = 0;
+        for (;;) {
+          if (lane == 0) {
+            uint32_t spins = 0;
+            while (next + G::FD - ld_acquire_cta_smem(&s_qcnt[0]) > (uint32_t)G::FQ) {
+              __nanosleep(20);
+              if (++spins > FHEGPU_SPIN_LIMIT) __trap();
+            }
+          }
+          __syncwarp();
+          uint32_t base = 0;
+          if (lane == 0) base = atomicAdd(qa.counters, (uint32_t)G::FD);
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (lane < G::FD) {
+            const uint32_t pos = base + lane, e = (next + lane) % G::FQ;
+            uint32_t item = Q_END;
+            uint4 ent = make_uint4(0u, 0u, 0u, 0u);
+            if (pos < n_items) {
+              uint32_t spins = 0;
+              while ((item = ld_acquire_gpu(qa.queue + pos)) == Q_EMPTY) {
+                __nanosleep(64);
+                if (++spins > FHEGPU_SPIN_LIMIT) __trap();
+              }
+              uint32_t q, ln;
+              div_lanes(item, lanes, p.lanes_magic, q, ln);
+              const OpRec op = ops[q];
+              ent = make_uint4(op.left * lanes + ln, op.right * lanes + ln, op.out * lanes + ln, op.flags);
+            }
+            s_fq[e] = ent;
+            s_fqi[2 * e] = item;
+            st_release_cta_smem(&s_fqi[2 * e + 1], next + lane + 1);
+          }
+          __syncwarp();
+          next += G::FD;
+          if (base + G::FD > n_items) break;      // an END entry has been published
+        }
+      } else {
+        // ------------------------------ signaler (Q) ------------------------------
+        // Retires slots whose output stores completed (posted by the epilogue): decrements
+        // each consumer's pending count; consumers reaching zero are pushed (release) onto
+        // the queue.  (slot, consumer) pairs of a batch of slots are spread over the lanes.
+        const uint32_t FULL = 0xffffffffu;
+        uint32_t done = 0;
+        for (;;) {
+          const uint32_t fin = ld_volatile_smem(&s_qcnt[2]);
+          __threadfence_block();
+          const uint32_t pub = ld_volatile_smem(s_pub);
+          if (pub <= done) {
+            if (fin != 0u && done + 1u >= fin) break;
+            __nanosleep(64);
+            continue;
+          }
+          const uint32_t n = min(pub - done, 32u);
+          uint32_t c0 = 0, cnt = 0, ln = 0;
+          if (lane < n) {
+            const uint32_t item = s_qitem[(done + lane) % G::QR];
+            uint32_t q;
+            div_lanes(item, lanes, p.lanes_magic, q, ln);
+            c0 = qa.cons_off[q];
+            cnt = qa.cons_off[q + 1] - c0;
+          }
+          uint32_t incl = cnt;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t v = __shfl_up_sync(FULL, incl, off);
+            if (lane >= off) incl += v;
+          }
+          const uint32_t total = __shfl_sync(FULL, incl, 31), excl = incl - cnt;
+          for (uint32_t base = 0; base < total; base += 32) {
+            const uint32_t idx = base + lane;
+            uint32_t owner = 0;
+            for (uint32_t jj = 0; jj < n; ++jj) {
+              const uint32_t ej = __shfl_sync(FULL, excl, jj), cj = __shfl_sync(FULL, cnt, jj);
+              if (idx >= ej && idx < ej + cj) owner = jj;
+            }
+            const uint32_t oc0 = __shfl_sync(FULL, c0, owner), oex = __shfl_sync(FULL, excl, owner);
+            const uint32_t oln = __shfl_sync(FULL, ln, owner);
+            uint32_t ci = 0;
+            bool ready = false;
+            if (idx < total) {
+              ci = qa.cons[oc0 + idx - oex] * lanes + oln;
+              ready = atom_dec_acq_rel_gpu(qa.pending + ci) == 1u;
+            }
+            const uint32_t m = __ballot_sync(FULL, ready);
+            if (m) {
+              const int leader = __ffs(m) - 1;
+              uint32_t tb = 0;
+              if (lane == leader) tb = atomicAdd(qa.counters + 1, (uint32_t)__popc(m));
+              tb = __shfl_sync(FULL, tb, leader);
+              if (ready) st_release_gpu(qa.queue + tb + __popc(m & ((1u << lane) - 1u)), ci);
+            }
+          }
+          done += n;
+          st_volatile_smem(&s_qcnt[1], done);     // producer flow control (slot ring)
+        }
+      }
+    }
   } else if (warp < G::WARP_EPI0) {
     // ------------------------------ operand builders ------------------------------
     const int bt = tid - 32 * G::WARP_BUILD0;           // 0 .. 128*MT-1
@@ -597,9 +805,14 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
       b_j[x] = j;
     }
     uint32_t t = 0;
-    for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
+    for (uint32_t item = blockIdx.x; Q || item < n_items; item += gridDim.x, ++t) {
       const uint32_t s = t % G::S_IN, k = t / G::S_IN, b = t & 1u, u = t >> 1;
       mbar_wait(&in_full[s], k & 1u);
+      if (Q && s_qitem[t % G::QR] == Q_END) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&op_full[b]);
+        break;
+      }
       const uint32_t flags = s_flags[s];
       const bool comp1 = flags & 1u, comp2 = flags & 2u;
       if (bt == 0) trace_ev(p, t, 5);
@@ -701,16 +914,27 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
       if (et == 0) mbar_arrive(&out_free[0]);          // staging 0 is free for gate 0
     }
     uint32_t t = 0;
-    OpRec op_next = fetch_op(ops, blockIdx.x, n_items, lanes, p.lanes_magic);
+    OpRec op_next = Q ? OpRec{} : fetch_op(ops, blockIdx.x, n_items, lanes, p.lanes_magic);
     const uint64_t pol_stream = policy_evict_first();
-    for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
+    for (uint32_t item = blockIdx.x; Q || item < n_items; item += gridDim.x, ++t) {
       const uint32_t b = t & 1u, u = t >> 1;
       const OpRec op_cur = op_next;
-      if (et == 0) op_next = fetch_op(ops, item + gridDim.x, n_items, lanes, p.lanes_magic);
+      if (!Q && et == 0) op_next = fetch_op(ops, item + gridDim.x, n_items, lanes, p.lanes_magic);
       const uint32_t o = t % G::N_OUT, ou = t / G::N_OUT;
       uint32_t *out_st = s_out + o * G::CT_WORDS;
       // staging o was released by et 0 before the previous gate's barrier (or is fresh)
       if (et == 0) trace_ev(p, t, 8);
+      if (Q && et == 0 && t > 0) {
+        // ready queue: post completed stores for the signaler -- all of them before this
+        // thread can block (a popped item elsewhere may wait for one), else all but the newest
+        if (!mbar_test(&main_done[b], u & 1u)) {
+          bulk_wait_n<0>();
+          post_local(s_pub, t);
+        } else if (t >= FHEGPU_PUBLISH_LAG) {
+          bulk_wait_n<FHEGPU_PUBLISH_LAG>();
+          post_local(s_pub, t - FHEGPU_PUBLISH_LAG);
+        }
+      }
       if (progress != nullptr && et == 0 && t > 0) {
         // dataflow: publish finished outputs -- all of them before this thread can block
         // (a later item of this CTA may be waiting for one), else all but the newest
@@ -723,6 +947,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
         }
       }
       mbar_wait(&main_done[b], u & 1u);
+      if (Q && s_qitem[t % G::QR] == Q_END) break;
       if (et == 0) trace_ev(p, t, 9);
       tc_fence_after();
       uint32_t d[36];
@@ -751,7 +976,9 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
       if (et == 0) {
         if constexpr (G::TAIL > 0) mbar_wait(&tail_ready[o], ou & 1u);
       }
-      if (et == 0 && !(p.dbg & 512u)) {
+      if (Q && et == 0) {
+        bulk_s2g(store + (uint64_t)s_qout[t % G::QR] * G::CT_WORDS, out_st, G::CT_BYTES);
+      } else if (et == 0 && !(p.dbg & 512u)) {
         const uint32_t ln = lane_of(item, lanes, p.lanes_magic);
         uint32_t *dst = store + ((uint64_t)op_cur.out * lanes + ln) * G::CT_WORDS;
         if (op_cur.flags & 8u) bulk_s2g_hint(dst, out_st, G::CT_BYTES, pol_stream);
@@ -761,6 +988,11 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
     if (et == 0) {
       bulk_wait_all();
       if (progress != nullptr) publish(progress, t);
+      if constexpr (Q) {                  // t = slots stored; the signaler retires them and leaves
+        post_local(s_pub, t);
+        __threadfence_block();
+        st_volatile_smem(&s_qcnt[2], t + 1);
+      }
     }
   }
 

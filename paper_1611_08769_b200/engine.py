@@ -247,8 +247,9 @@ class GpuEngine(LevelledNetlist):
             raise UsageError("threads must be >= 1")
         if batch_size < 1:
             raise UsageError("batch_size must be >= 1")
-        if schedule not in ("auto", "levels", "dataflow", "tiled"):
-            raise UsageError(f"schedule must be 'auto', 'levels', 'dataflow' or 'tiled', got {schedule!r}")
+        if schedule not in ("auto", "levels", "dataflow", "queue", "tiled"):
+            raise UsageError(f"schedule must be 'auto', 'levels', 'dataflow', 'queue' or 'tiled', "
+                             f"got {schedule!r}")
         self.schedule = schedule
         if lane_rngs is not None and len(lane_rngs) != batch_size:
             raise UsageError("need one rng per lane")
@@ -599,7 +600,7 @@ class GpuEngine(LevelledNetlist):
         if not self._pending_ops:
             return None
         sched = self._pick_schedule()
-        dataflow = sched in ("dataflow", "tiled")
+        dataflow = sched in ("dataflow", "queue", "tiled")
         ring = self.TILE_RING if sched == "tiled" and self._ring_ok() else 0
         prog = self._compile(ssa=dataflow, ring_temps=ring > 0)
         prog["schedule"] = sched
@@ -635,6 +636,8 @@ class GpuEngine(LevelledNetlist):
             program = self.ctx.program(prog["ops"], prog["offsets"])
             if dataflow:
                 program.set_deps(prog["deps"])
+            if sched == "queue":
+                program.set_queue(True)
         program.run(lanes)
         self.last_program = program
         self.last_compile = prog
@@ -662,11 +665,15 @@ class GpuEngine(LevelledNetlist):
     TILED_MAX_BYTES = 100 << 30
 
     def _pick_schedule(self) -> str:
-        """'levels', 'dataflow' or 'tiled' for the pending program.
+        """'levels', 'dataflow', 'queue' or 'tiled' for the pending program.
 
         levels    one launch per netlist level over all lanes (PDL between launches).
         dataflow  the whole program in one launch, operands awaited per item (opt-in: for
                   the reference's deep single-signal netlists it does not beat levels).
+        queue     the whole program in one launch over a ready queue: CTAs pop only items
+                  whose producers have completed.  'auto' picks it for deep programs over
+                  few lanes whose single-assignment store fits QUEUE_MAX_BYTES (configs[2]
+                  and [3]: +8% over levels).
         tiled     lanes cut into chunks of TILE_LANES; the program is replicated per chunk
                   and run as ONE dataflow launch in wavefront order (step s = level 0 of chunk
                   s, level 1 of chunk s-1, ...), so a chunk's intermediates are consumed while
@@ -679,7 +686,7 @@ class GpuEngine(LevelledNetlist):
             return "levels"
         C = self.TILE_LANES
         if self.batch_size % C or self.batch_size < 8 * C:
-            return "levels"
+            return "queue" if self._pick_queue() else "levels"
         if self.ctx.kernel != "tcgen05":              # the dataflow launch needs the tcgen05 kernel
             return "levels"
         n_ops = len(self._pending_ops) // 5
@@ -692,6 +699,23 @@ class GpuEngine(LevelledNetlist):
         if len(np.unique(np.asarray(self._level, dtype=np.int64)[outs])) > self.TILED_MAX_LEVELS:
             return "levels"                    # deep programs are dependency-hop bound (4.8)
         return "tiled"
+
+    QUEUE_MIN_LEVELS = 64          # 'auto' runs deeper single-signal programs over the ready queue
+    QUEUE_MAX_BYTES = 40 << 30     # ... when their single-assignment store fits this
+
+    def _pick_queue(self) -> bool:
+        """Deep programs over few lanes (single-signal FFTs, configs[2]/[3]): one ready-queue
+        launch instead of a launch per level when its SSA store fits."""
+        if self.dry_run or (self.params.k, self.params.ell) != (9, 29) or self.ctx.kernel != "tcgen05":
+            return False
+        n_ops = len(self._pending_ops) // 5
+        ct_bytes = ((self.params.n_ct * self.params.k + 3) // 4) * 16
+        if (self._n_slots + n_ops) * self.batch_size * ct_bytes > self.QUEUE_MAX_BYTES:
+            return False
+        if n_ops * self.batch_size >= 1 << 31:
+            return False
+        outs = np.asarray(self._pending_ops[4::5], dtype=np.int64)
+        return len(np.unique(np.asarray(self._level, dtype=np.int64)[outs])) >= self.QUEUE_MIN_LEVELS
 
     @staticmethod
     def _tile(prog, K, lanes_per_chunk=1, skew=0, window=2048, ring=0, t_base=0):

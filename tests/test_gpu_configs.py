@@ -128,17 +128,20 @@ def test_cfg4_lane0_gate_by_gate():
     assert read_signal_ints(eng, out)[0].tolist() == ref["output_words"]
 
 
-@pytest.mark.parametrize("cfg,schedule", [("cfg3", "levels"), ("cfg3", "dataflow"), ("cfg2", "levels"),
-                                          ("cfg2", "dataflow")])
+@pytest.mark.parametrize("cfg,schedule", [("cfg3", "levels"), ("cfg3", "dataflow"), ("cfg3", "queue"),
+                                          ("cfg2", "levels"), ("cfg2", "dataflow"), ("cfg2", "queue")])
 def test_fft_config_gate_by_gate(cfg, schedule):
     """Every gate's ciphertext equals the reference's; 'dataflow' runs the whole FFT as one
-    launch with per-operand readiness (SSA slots, per-CTA progress counters)."""
+    launch with per-operand readiness (SSA slots, per-CTA progress counters), 'queue' as one
+    launch over a ready queue (CTAs pop items whose producers have completed)."""
     path = os.path.join(GOLDEN, f"cts_{cfg}.json")
     if not os.path.exists(path):
         pytest.skip(f"golden {cfg} ciphertext digests not generated")
     eng, out, x = run_fft_config(cfg, device_encrypt=True, schedule=schedule)
-    if schedule != "levels":
+    if schedule == "dataflow":
         assert eng.launches == 1                      # one launch for the whole FFT
+    elif schedule == "queue":
+        assert eng.launches == 2                      # queue reset + one launch for the whole FFT
     ref = golden_json(f"cts_{cfg}.json")
     ins, gates = gate_digests(eng)
     assert digest.chain_digest(ins) == ref["inputs_chain"]
@@ -165,14 +168,16 @@ def test_device_encryption_equals_host_encryption():
 
 
 def test_dataflow_many_lanes_equals_levels():
-    """Dataflow with several lanes (items = (op, lane), CTA-strided) vs level launches."""
+    """Dataflow (items = (op, lane), CTA-strided) and ready-queue launches with several lanes
+    vs level launches."""
     outs = {}
-    for schedule in ("levels", "dataflow"):
+    for schedule in ("levels", "dataflow", "queue"):
         eng, out, vals = run_fft_config("cfg4", device_encrypt=True, keep_all=False, lanes=5,
                                         schedule=schedule)
         outs[schedule] = read_signal_ints(eng, out)
         assert np.array_equal(outs[schedule], model_outputs("cfg4", vals))
     assert np.array_equal(outs["levels"], outs["dataflow"])
+    assert np.array_equal(outs["levels"], outs["queue"])
 
 
 def test_tiled_schedule_equals_levels_bit_exact():
