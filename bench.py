@@ -464,6 +464,7 @@ def bench_fft_single(args, world, rank, local, cfg):
             "value": world / (ms / 1e3), "unit": "FFT/s", "ms_per_fft": ms,
             "nand_per_s": eng.nand_count * world / (ms / 1e3), "nand_per_fft": eng.nand_count,
             "levels": prog.n_levels, "launches_per_fft": prog.launches,
+            "schedule": eng.last_compile.get("schedule", "levels"),
             "roofline": _fft_roofline(eng.nand_count * world / (ms / 1e3), scheme.params.n_ct),
             "decrypt_check_vs_reference": ok}
 

@@ -98,6 +98,7 @@ class GpuClearEngine(LevelledNetlist):
         pad = np.zeros((self.words * 32, bits.shape[1]), dtype=np.uint8)
         pad[: self.batch_size] = bits
         packed = np.packbits(pad.T.reshape(bits.shape[1], self.words, 32), axis=2, bitorder="little")
+        packed = np.ascontiguousarray(packed)          # view as u32 needs a contiguous last axis
         return self.input_words(packed.view("<u4").reshape(bits.shape[1], self.words))
 
     def _input(self, words: np.ndarray) -> GpuBit:

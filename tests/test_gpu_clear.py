@@ -164,3 +164,43 @@ def test_random_circuits_tiled_equals_levels_and_clear():
             results[name + "_ct"] = eng.node_values([h for h in keep if not h.const])
     assert results["levels"] == results["tiled"] == results["clear"]
     assert np.array_equal(results["levels_ct"], results["tiled_ct"])
+
+
+@pytest.mark.gpu
+def test_random_deep_circuit_queue_equals_levels():
+    """A random deep circuit (600 gates of every type, operands drawn with a bias to the
+    newest wires -> long dependency chains, plus high-fan-out early wires) over 7 lanes: the
+    ready-queue launch, the static dataflow launch and level launches give identical
+    ciphertexts and the bitsliced cleartext engine's bits."""
+    from paper_1611_08769_b200 import DEFAULT0_PARAMS, GpuEngine, GswScheme
+    scheme = GswScheme(DEFAULT0_PARAMS)
+    keys = scheme.keygen(5)
+    lanes = 7
+    rng = np.random.default_rng(23)
+    ops = [not_, and_, or_, xor_, nor_, xnor_]
+    plan = []
+    for n in range(600):
+        k = int(rng.integers(0, len(ops)))
+        pick = lambda: int(rng.integers(0, 6)) if rng.random() < 0.15 else -1 - int(rng.integers(0, 4))
+        plan.append((k, pick(), pick()))
+    bits = rng.integers(0, 2, (lanes, 6))
+    results = {}
+    for name in ("levels", "queue", "dataflow", "clear"):
+        if name == "clear":
+            eng = GpuClearEngine(batch_size=lanes)
+        else:
+            eng = GpuEngine(scheme, keys=keys, rng=np.random.default_rng(2), batch_size=lanes,
+                            device_encrypt=True, schedule=name)
+        pool = eng.input_block(bits)
+        for k, i, j in plan:
+            a, b = pool[i], pool[j]
+            pool.append(ops[k](a) if ops[k] is not_ else ops[k](a, b))
+        keep = pool[-8:] + pool[6:10]
+        del pool, a, b
+        results[name] = eng.read_back_many(keep)
+        if name != "clear":
+            assert eng.max_depth > 64                       # deep enough for 'auto' to pick the queue
+            results[name + "_ct"] = eng.node_values([h for h in keep if not h.const])
+    assert results["levels"] == results["queue"] == results["dataflow"] == results["clear"]
+    assert np.array_equal(results["levels_ct"], results["queue_ct"])
+    assert np.array_equal(results["levels_ct"], results["dataflow_ct"])
