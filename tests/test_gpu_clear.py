@@ -204,3 +204,19 @@ def test_random_deep_circuit_queue_equals_levels():
     assert results["levels"] == results["queue"] == results["dataflow"] == results["clear"]
     assert np.array_equal(results["levels_ct"], results["queue_ct"])
     assert np.array_equal(results["levels_ct"], results["dataflow_ct"])
+
+
+@pytest.mark.gpu
+def test_queue_tiny_programs_and_fallback():
+    """Queue launches with fewer items than SMs (a 3-gate program, one lane) and a queue
+    request on a parameter set without the warp-specialised kernel (EXACT: level launches)."""
+    from paper_1611_08769_b200 import DEFAULT0_PARAMS, EXACT_PARAMS, GpuEngine, GswScheme
+    for params in (DEFAULT0_PARAMS, EXACT_PARAMS):
+        scheme = GswScheme(params)
+        keys = scheme.keygen(7)
+        for bits in ((0, 1), (1, 1)):
+            eng = GpuEngine(scheme, keys=keys, rng=np.random.default_rng(3), schedule="queue",
+                            device_encrypt=True)
+            a, b = eng.input_bit(bits[0]), eng.input_bit(bits[1])
+            y = xor_(and_(a, b), b)
+            assert eng.read_back(y) == ((bits[0] & bits[1]) ^ bits[1])
