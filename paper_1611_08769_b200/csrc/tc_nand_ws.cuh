@@ -297,6 +297,9 @@ struct GeoWS {
 // ready-queue launches: operand stages, fetch-ring entries, queue pops per fetch batch
 // (swept on cfg2/cfg3: 5/4/2; one pop per batch leaves the fetcher latency-bound, deeper
 // rings put more items ahead of each dependency hop)
+#ifndef FHEGPU_STAGES
+#define FHEGPU_STAGES 7        // operand stages of level / dataflow launches
+#endif
 #ifndef FHEGPU_Q_STAGES
 #define FHEGPU_Q_STAGES 5
 #endif
@@ -308,7 +311,7 @@ struct GeoWS {
 #endif
   // operand stages: ~2.5 us load latency x bandwidth (ready-queue launches: every stage is
   // also latency on the dependency chain; their operands are mostly L2 hits)
-  static constexpr int S_IN = Q ? FHEGPU_Q_STAGES : 7;
+  static constexpr int S_IN = Q ? FHEGPU_Q_STAGES : FHEGPU_STAGES;
   static constexpr int N_OUT = 3;                           // output staging buffers
   static constexpr uint32_t OP_ARRIVALS = NB_WARPS;
   // idesc: S32 accumulator, A s8 (bits 7-9 = 1) or u8 (encoding 2), B u8, A K-major,
