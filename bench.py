@@ -111,7 +111,7 @@ def cpu_reference(seconds: float, workers: int | None = None):
 class ClockSampler:
     def __init__(self, device: int, period: float = 0.02):
         self.device, self.period = device, period
-        self.samples, self.reasons, self.power = [], set(), []
+        self.samples, self.reasons = [], set()
         self._stop = threading.Event()
         self.max_mhz = None
         self.ok = True
@@ -121,10 +121,6 @@ class ClockSampler:
             self._nv = pynvml
             self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
-            try:
-                self.power_limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self._h) / 1000
-            except Exception:
-                self.power_limit_w = None
         except Exception:
             self.ok = False
 
@@ -136,10 +132,6 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
-                try:
-                    self.power.append(nv.nvmlDeviceGetPowerUsage(self._h) / 1000)
-                except Exception:
-                    pass
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
                 for bit, name in self._BITS.items():
                     if r & bit:
@@ -162,12 +154,8 @@ class ClockSampler:
     def summary(self):
         if not self.ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
-        out = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-               "reasons": sorted(self.reasons), "samples": len(self.samples)}
-        if self.power:       # board power: the gate kernels run at the board limit
-            out["power_w"] = round(statistics.median(self.power), 1)
-            out["power_limit_w"] = self.power_limit_w
-        return out
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
 # ----------------------------------------------------------------------------------------
