@@ -8,6 +8,7 @@ import pytest
 
 from paper_1611_08769_b200 import (DEFAULT0_PARAMS, DEFAULT_PARAMS, EXACT_PARAMS, FixedFormat,
                                    GpuEngine, GswScheme, and_, fft_1d, fft_2d, input_signal, xor_)
+from oracle import fixedfft
 from paper_1611_08769_b200.fft import signal_words
 from tests.helpers import (FFT_CONFIGS, config_signal, golden_json, golden_npz, model_outputs,
                            read_dry, replay_dry)
@@ -264,3 +265,38 @@ def test_auto_schedule_policy():
     assert pick(4096, EXACT_PARAMS) == "levels"   # no warp-specialised kernel for N = 51
     assert pick(4096, DEFAULT0_PARAMS, depth=12) == "levels"   # 36 levels: hop bound
     assert pick(4096, kernel="simt") == "levels"  # dataflow launches need the tcgen05 kernel
+
+
+@pytest.mark.parametrize("normalize", [False, True])
+def test_ifft_replay_matches_swap_model(normalize):
+    """ifft_1d = swap(fft(swap(x))) (+ floor shift by log2 M): the replayed netlist equals the
+    integer model on 8 lanes of random 8-point Q4.12 signals, costs exactly the fft's NANDs,
+    and fft -> ifft returns the input within the fixed-point rounding of the two passes."""
+    from paper_1611_08769_b200.fft import ifft_1d
+    lanes, M, F, f = 8, 8, 16, 12
+    rng = np.random.default_rng(31)
+    vals = rng.uniform(-0.5, 0.5, (lanes, M)) + 1j * rng.uniform(-0.5, 0.5, (lanes, M))
+    scheme = GswScheme(EXACT_PARAMS)
+    eng = GpuEngine(scheme, dry_run=True, batch_size=lanes)
+    sig = input_signal(eng, vals, FixedFormat(F, f))
+    out = ifft_1d(sig, normalize=normalize)
+    eng.flush()
+    store = replay_dry(eng)
+    bits = read_dry(eng, store, [h for w in signal_words(out) for h in w.bits])
+    got = np.zeros((lanes, 2 * M), dtype=np.int64)
+    for wi in range(2 * M):
+        u = [sum(((bits[wi * F + k] >> l) & 1) << k for k in range(F)) for l in range(lanes)]
+        got[:, wi] = [x - (1 << F) if x >> (F - 1) else x for x in u]
+    re = fixedfft.encode_lanes(vals.real, F, f)
+    im = fixedfft.encode_lanes(vals.imag, F, f)
+    o_im, o_re = fixedfft.fft_1d(im, re, F, f)           # swap in, fft, swap out
+    if normalize:
+        o_re, o_im = o_re >> 3, o_im >> 3                 # floor division by M = 8
+    assert np.array_equal(got, fixedfft.interleave(o_re, o_im))
+    ref_eng = GpuEngine(scheme, dry_run=True, batch_size=lanes)
+    fft_1d(input_signal(ref_eng, vals, FixedFormat(F, f)))
+    assert eng.nand_count == ref_eng.nand_count           # the swaps and the shift are wiring
+    if normalize:                                         # round trip through the integer model
+        f_re, f_im = fixedfft.fft_1d(re, im, F, f)
+        b_im, b_re = fixedfft.fft_1d(f_im, f_re, F, f)
+        assert np.abs((b_re >> 3) - re).max() <= 8 and np.abs((b_im >> 3) - im).max() <= 8
