@@ -604,12 +604,13 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
         if (elect_one()) {
 #pragma unroll
           for (int mt = 0; mt < G::MT; ++mt) {
+            if (p.dbg & (1u << 18)) break;             // ablation: no tile MMAs (results invalid)
 #pragma unroll
             for (int s = 0; s < K; ++s)
               mma_i8_ts(tb + mt * G::NPAD, tb + G::D_COLS + mt * 8 * K + 8 * s,
                         bd_b + ((s * 4 * G::LBO) >> 4), idesc, s > 0 ? 1u : 0u);
           }
-          if constexpr (G::TAIL > 0) {
+          if (G::TAIL > 0 && !(p.dbg & (1u << 17))) {  // ablation bit 17: no tail MMAs
 #pragma unroll
             for (int s = 0; s < K; ++s)
               mma_i8_ss(tb + G::D_COLS, td_b + ((s * 2 * G::TA_LBO) >> 4),
