@@ -176,6 +176,30 @@ int fhegpu_prog_set_deps(fhegpu_ctx *ctx, fhegpu_prog *prog, const int32_t *deps
  * to the static dataflow order.  Replaces the reference's sequential gate loop
  * (engine.py:168-178 driving fhe.py:325-341) like fhegpu_prog_run. */
 int fhegpu_prog_set_queue(fhegpu_ctx *ctx, fhegpu_prog *prog, int enable);
+
+/* One gate of a lane-resident program (fhegpu_prog_set_resident), 16 bytes. */
+typedef struct {
+  uint8_t lkind, lidx;   /* left operand: kind 0 = program input lidx, 1 = local buffer lidx */
+  uint8_t rkind, ridx;   /* right operand, same encoding */
+  uint8_t dest;          /* local buffer the gate writes */
+  uint8_t is_out;        /* 1: the gate's output is also stored to slot out_slot */
+  uint8_t flags;         /* bit 0 / 1: complement the left / right operand (as fhegpu_op) */
+  uint8_t pad;
+  int16_t lprod, rprod;  /* plan index of the gate that produced a local operand (-1: input) */
+  uint32_t out_slot;
+} fhegpu_res_op;
+
+/* Opt-in lane-resident execution of a small per-lane program (<= 8 gates, <= 4 inputs, <= 8
+ * local buffers; the gates in topological order): one launch in which every CTA runs the whole
+ * program for 2 lanes at a time, loading the program inputs (store slots in_slots[]) once and
+ * keeping every gate output in a shared-memory buffer of its lane; only is_out gates are stored.
+ * A local buffer may be reused once every reader of its previous value precedes the writer in
+ * the plan; output gates need buffers of their own.  Same results as fhegpu_prog_run's level
+ * launches (which remain the fallback where no tcgen05 kernel applies); n_ops = 0 disables.
+ * Replaces the reference's gate-by-gate evaluation (engine.py:168-178 -> fhe.py:325-341) for
+ * independent lanes, e.g. the gate benchmark's XOR + AND (gates.py:9-34). */
+int fhegpu_prog_set_resident(fhegpu_ctx *ctx, fhegpu_prog *prog, const fhegpu_res_op *plan, uint32_t n_ops,
+                             const uint32_t *in_slots, uint32_t n_in, uint32_t n_local);
 uint32_t fhegpu_prog_launches(const fhegpu_prog *prog);       /* launches one run issues */
 void fhegpu_prog_destroy(fhegpu_prog *prog);
 

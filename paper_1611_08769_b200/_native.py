@@ -21,6 +21,9 @@ HOST_COMPACT, HOST_PACKED = 0, 1      # fhegpu_prog_run_host host formats
 KERNEL_NAMES = {KERNEL_AUTO: "auto", KERNEL_SIMT: "simt", KERNEL_TCGEN05: "tcgen05"}
 
 OP_DTYPE = np.dtype([("left", "<u4"), ("right", "<u4"), ("out", "<u4"), ("flags", "<u4")])
+RES_OP_DTYPE = np.dtype([("lkind", "u1"), ("lidx", "u1"), ("rkind", "u1"), ("ridx", "u1"),
+                         ("dest", "u1"), ("is_out", "u1"), ("flags", "u1"), ("pad", "u1"),
+                         ("lprod", "<i2"), ("rprod", "<i2"), ("out_slot", "<u4")])   # fhegpu_res_op
 
 
 class _Params(ctypes.Structure):
@@ -62,6 +65,8 @@ SIGNATURES = [
     ("fhegpu_prog_launches", ctypes.c_uint32, [_P]),
     ("fhegpu_prog_set_deps", ctypes.c_int, [_P, _P, _P]),
     ("fhegpu_prog_set_queue", ctypes.c_int, [_P, _P, ctypes.c_int]),
+    ("fhegpu_prog_set_resident", ctypes.c_int, [_P, _P, _P, ctypes.c_uint32, _P, ctypes.c_uint32,
+                                                ctypes.c_uint32]),
     ("fhegpu_store_write_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     ("fhegpu_store_read_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     ("fhegpu_prog_run_host", ctypes.c_int, [_P, _P, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int,
@@ -182,6 +187,16 @@ class Program:
         """Ready-queue mode (fhegpu_prog_set_queue): one launch in which CTAs pop only items
         whose producers have completed (needs set_deps first)."""
         _check(_lib.fhegpu_prog_set_queue(self.ctx.handle, self.handle, int(bool(enable))), "prog_set_queue")
+        self.launches = int(_lib.fhegpu_prog_launches(self.handle))
+
+    def set_resident(self, plan: np.ndarray, in_slots, n_local: int):
+        """Lane-resident mode (fhegpu_prog_set_resident): plan = RES_OP_DTYPE records of the
+        per-lane program, in_slots = store slots of its inputs.  An empty plan disables."""
+        plan = np.ascontiguousarray(plan, dtype=RES_OP_DTYPE)
+        ins = np.ascontiguousarray(np.asarray(in_slots, dtype=np.uint32).reshape(-1))
+        _check(_lib.fhegpu_prog_set_resident(self.ctx.handle, self.handle, plan.ctypes.data_as(ctypes.c_void_p),
+                                             len(plan), ins.ctypes.data_as(ctypes.c_void_p), len(ins),
+                                             int(n_local)), "prog_set_resident")
         self.launches = int(_lib.fhegpu_prog_launches(self.handle))
 
     def run_host(self, lanes: int, chunk_lanes: int, in_slots, in_ptrs, out_slots, out_ptrs,

@@ -17,6 +17,7 @@
 #include "simt_nand.cuh"
 #include "tc_nand.cuh"
 #include "tc_nand_ws.cuh"
+#include "tc_nand_resident.cuh"
 #include "encrypt.cuh"
 #include "bits.cuh"
 
@@ -90,6 +91,11 @@ struct fhegpu_prog {
   uint32_t n_roots = 0;
   uint32_t *d_qrun = nullptr;     // per run: counters[4] | pending[n_items] | queue[n_items]
   size_t qrun_cap = 0;
+  // lane-resident launches (fhegpu_prog_set_resident): per-lane gate plan + program inputs
+  bool use_resident = false;
+  tc::ResOp *d_rplan = nullptr;
+  uint32_t *d_rin = nullptr;
+  uint32_t r_ops = 0, r_in = 0, r_local = 0, r_out = 0;
   // CUDA graph of one full run (all level launches), captured on first use per
   // (lanes, stream, kernel choice, debug bits); replayed with a single cudaGraphLaunch
   cudaGraphExec_t graph = nullptr;
@@ -313,6 +319,31 @@ int launch_queue(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
                                                                 lanes, nullptr, nullptr, qa);
 }
 
+
+#ifndef FHEGPU_ENC_RESIDENT
+#define FHEGPU_ENC_RESIDENT 1
+#endif
+
+// A whole small per-lane program in one lane-resident launch (tc_nand_resident.cuh).
+int launch_resident(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
+  if (lanes == 0 || pr->r_ops == 0) return FHEGPU_OK;
+  if (effective_kernel(c) != FHEGPU_KERNEL_TCGEN05 || (c->p.dbg & 4u)) return FHEGPU_EUNSUP;
+  if (!(c->p.k == 9 && c->p.ell == 29) || lanes % tc::RES_W) return FHEGPU_EUNSUP;
+  using R = tc::GeoRes<9, 29>;
+  const uint32_t smem = R::smem_bytes(pr->r_in, pr->r_local);
+  if (smem > 227u * 1024u) return FHEGPU_EUNSUP;
+  const uint32_t n_groups = lanes / tc::RES_W;
+  const unsigned grid = (unsigned)std::min<uint64_t>(n_groups, (uint64_t)c->num_sms);
+  DevParams p = c->p;
+  const bool pm = pm_ok(c->p.q, c->p.ell) && !(c->p.dbg & 2u);
+  auto kern = pm ? tc::resident_tc_kernel<9, 29, true, FHEGPU_ENC_RESIDENT>
+                 : tc::resident_tc_kernel<9, 29, false, FHEGPU_ENC_RESIDENT>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, R::THREADS, smem, c->stream>>>(c->store, pr->d_rplan, pr->d_rin, pr->r_ops, pr->r_in, pr->r_local,
+                                               pr->r_out, lanes, n_groups, p);
+  CUDA_TRY(cudaGetLastError());
+  return FHEGPU_OK;
+}
 
 }  // namespace
 
@@ -637,7 +668,11 @@ int fhegpu_prog_run_range(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes, uint32
   const uint32_t n_levels = (uint32_t)pr->offsets.size() - 1;
   last = std::min(last, n_levels);
   CUDA_TRY(cudaSetDevice(c->device));
-  if (pr->use_queue && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
+  if (pr->use_resident && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
+    const int rc = launch_resident(c, pr, lanes);
+    if (rc != FHEGPU_EUNSUP) return rc;
+    // else: level by level (resident programs keep their level structure)
+  } else if (pr->use_queue && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
     const int rc = launch_queue(c, pr, lanes);
     if (rc != FHEGPU_EUNSUP) return rc;
     // else: level by level (queue programs keep their level structure)
@@ -888,6 +923,50 @@ int fhegpu_prog_set_queue(fhegpu_ctx *c, fhegpu_prog *pr, int enable) {
   return FHEGPU_OK;
 }
 
+int fhegpu_prog_set_resident(fhegpu_ctx *c, fhegpu_prog *pr, const fhegpu_res_op *plan, uint32_t n_ops,
+                             const uint32_t *in_slots, uint32_t n_in, uint32_t n_local) {
+  if (!c || !pr) return fail(FHEGPU_EINVAL, "null argument");
+  if (pr->graph) {
+    cudaGraphExecDestroy(pr->graph);
+    pr->graph = nullptr;
+  }
+  if (n_ops == 0) {
+    pr->use_resident = false;
+    return FHEGPU_OK;
+  }
+  if (!plan || (n_in && !in_slots)) return fail(FHEGPU_EINVAL, "null argument");
+  if (n_ops > (uint32_t)tc::RES_MAX_OPS || n_in > (uint32_t)tc::RES_MAX_IN || n_local > (uint32_t)tc::RES_MAX_LOCAL)
+    return fail(FHEGPU_EINVAL, "resident program too large");
+  static_assert(sizeof(fhegpu_res_op) == sizeof(tc::ResOp), "fhegpu_res_op layout");
+  uint32_t n_out = 0;
+  for (uint32_t i = 0; i < n_ops; ++i) {
+    const fhegpu_res_op &o = plan[i];
+    auto bad_src = [&](uint32_t kind, uint32_t idx, int32_t prod) {
+      if (kind == 0) return idx >= n_in || prod != -1;
+      return kind != 1 || idx >= n_local || prod < 0 || (uint32_t)prod >= i || plan[prod].dest != idx;
+    };
+    if (bad_src(o.lkind, o.lidx, o.lprod) || bad_src(o.rkind, o.ridx, o.rprod) || o.dest >= n_local ||
+        o.is_out > 1 || (o.flags & ~3u))
+      return fail(FHEGPU_EINVAL, "bad resident op " + std::to_string(i));
+    n_out += o.is_out;
+  }
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaFree(pr->d_rplan);
+  cudaFree(pr->d_rin);
+  pr->d_rplan = nullptr;
+  pr->d_rin = nullptr;
+  CUDA_TRY(cudaMalloc(&pr->d_rplan, n_ops * sizeof(tc::ResOp)));
+  CUDA_TRY(cudaMalloc(&pr->d_rin, std::max(n_in, 1u) * sizeof(uint32_t)));
+  CUDA_TRY(cudaMemcpy(pr->d_rplan, plan, n_ops * sizeof(tc::ResOp), cudaMemcpyHostToDevice));
+  if (n_in) CUDA_TRY(cudaMemcpy(pr->d_rin, in_slots, n_in * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  pr->r_ops = n_ops;
+  pr->r_in = n_in;
+  pr->r_local = n_local;
+  pr->r_out = n_out;
+  pr->use_resident = true;
+  return FHEGPU_OK;
+}
+
 int fhegpu_ctx_set_graphs(fhegpu_ctx *c, int enable) {
   if (!c) return fail(FHEGPU_EINVAL, "null ctx");
   c->use_graphs = enable != 0;
@@ -896,6 +975,7 @@ int fhegpu_ctx_set_graphs(fhegpu_ctx *c, int enable) {
 
 uint32_t fhegpu_prog_launches(const fhegpu_prog *pr) {
   if (!pr) return 0;
+  if (pr->use_resident) return 1;               // lane-resident: one launch
   if (pr->use_queue) return 2;                  // ready queue: state reset + one launch
   if (pr->d_deps) return 1;                     // dataflow: one launch (tcgen05 parameter sets)
   uint32_t n = 0;
@@ -910,6 +990,8 @@ void fhegpu_prog_destroy(fhegpu_prog *pr) {
   cudaFree(pr->d_progress);
   cudaFree(pr->d_qmeta);
   cudaFree(pr->d_qrun);
+  cudaFree(pr->d_rplan);
+  cudaFree(pr->d_rin);
   cudaFree(pr->d_ops);
   delete pr;
 }

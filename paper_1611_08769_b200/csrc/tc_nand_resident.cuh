@@ -1,0 +1,493 @@
+// tc_nand_resident.cuh -- lane-resident launches of small per-lane programs (the gate benchmark's
+// XOR + AND, or any netlist of <= RES_MAX_OPS gates per lane whose outputs are its sinks).
+//
+// The level / dataflow launches move every operand through L2 (2 x 9.4 KB per gate) and every
+// output back (9.4 KB): measured 1.55 uJ of the 4.6 uJ a gate costs above idle, at the board
+// power limit that sets the throughput.  Here a CTA takes W lanes at a time and
+// runs the whole per-lane program on them: the program's inputs are bulk-loaded once into a
+// double-buffered input set, every gate's output is written by the epilogue straight into a
+// shared-memory buffer of that lane (the operand of later gates), and only the program's
+// outputs are stored.  cfg1: 2 loads + 2 stores per 6 gates instead of 11 + 6.
+//
+// Pipeline roles, TMEM double buffers, MMA sequence, A/B operand construction and the fold are
+// those of level_tc_ws_kernel (tc_nand_ws.cuh).  Slot t of a CTA is (group g, op o, lane w)
+// with t = g * S + o * W + w, S = n_ops * W: gates of one op for the W lanes back to back, ops
+// in the host's topological order, so a gate's producer is >= W slots earlier.  A builder
+// reading a gate output waits until the epilogue has published that slot (epi_done).
+#pragma once
+
+#include "tc_nand_ws.cuh"
+
+namespace fhegpu {
+namespace tc {
+
+constexpr int RES_W = 2;          // lanes per group
+constexpr int RES_MAX_OPS = 8;    // gates per lane program
+constexpr int RES_MAX_IN = 4;     // program inputs
+constexpr int RES_MAX_LOCAL = 8;  // per-lane shared-memory ciphertext buffers
+
+// One gate of the per-lane program (16 bytes, same layout as fhegpu_res_op).
+struct ResOp {
+  uint8_t lkind, lidx, rkind, ridx;  // operand source: kind 0 = program input idx, 1 = local buffer idx
+  uint8_t dest, is_out, flags, pad;  // local buffer written; 1: also stored to out_slot; complements
+  int16_t lprod, rprod;              // plan index of the gate producing a local operand (-1: input)
+  uint32_t out_slot;                 // store slot of a program output
+};
+
+template <int K, int ELL>
+struct GeoRes {
+  using W = GeoWS<K, ELL, true, 1, false>;
+  using B = Geo<K, ELL>;
+  static constexpr int CT_BYTES = B::CT_BYTES, CT_WORDS = B::CT_WORDS;
+  static constexpr int B_BYTES = B::B_BYTES;
+  static constexpr int TA_BYTES = B::TA_BYTES;   // one 8-row tail group, aliased over M (SBO 0)
+  static constexpr int N_OUT = 3;
+#ifndef FHEGPU_RES_EPI_SPLIT
+#define FHEGPU_RES_EPI_SPLIT 1   // 2: 16 epilogue warps (72 registers: slower, measured)
+#endif
+  // epilogue warps: 8 x SPLIT (SPLIT = 2: two threads per row, values 0-4 and 5-8)
+  static constexpr int EPI_SPLIT = FHEGPU_RES_EPI_SPLIT;
+  static constexpr int NE_WARPS = 8 * EPI_SPLIT;
+  static constexpr int THREADS = 32 * (3 + W::NB_WARPS + NE_WARPS);
+  static constexpr int OFF_BAR_SIZE = 64 * 8;
+  // runtime layout (host computes the same): inputs | locals | B x 2 | TA x 2 | barriers | plan
+  __host__ __device__ static uint32_t off_local(uint32_t n_in) { return 2u * RES_W * n_in * CT_BYTES; }
+  __host__ __device__ static uint32_t off_b(uint32_t n_in, uint32_t n_local) {
+    return ((off_local(n_in) + RES_W * n_local * CT_BYTES + 127u) / 128u) * 128u;
+  }
+  __host__ __device__ static uint32_t off_ta(uint32_t n_in, uint32_t n_local) {
+    return off_b(n_in, n_local) + 2u * B_BYTES;
+  }
+  __host__ __device__ static uint32_t off_bar(uint32_t n_in, uint32_t n_local) {
+    return ((off_ta(n_in, n_local) + 2u * TA_BYTES + 127u) / 128u) * 128u;
+  }
+  __host__ __device__ static uint32_t smem_bytes(uint32_t n_in, uint32_t n_local) {
+    return off_bar(n_in, n_local) + OFF_BAR_SIZE + RES_MAX_OPS * sizeof(ResOp) +
+           RES_MAX_OPS * RES_W * 16u + 32u;
+  }
+};
+
+// Position of slot t in its group, advanced incrementally (no runtime divisions per slot).
+struct SlotPos {
+  uint32_t g = 0, r = 0, o = 0, w = 0, gS = 0;   // group, slot in group, gate, lane, group's first slot
+  __device__ __forceinline__ void next(uint32_t S, uint32_t W) {
+    if (++w == W) {
+      w = 0;
+      ++o;
+    }
+    if (++r == S) {
+      r = 0;
+      o = 0;
+      ++g;
+      gS += S;
+    }
+  }
+};
+
+// Per slot of a group (r = o * W + w), precomputed once per CTA: operand / destination buffer
+// indices (ciphertext units; inputs relative to their set), flags, and the RAW dependency.
+struct __align__(16) SlotInfo {
+  uint32_t v1, v2;         // left / right operand buffer (ciphertext words offset)
+  uint32_t dest;           // destination local buffer (ciphertext words offset)
+  uint16_t need;           // 1 + the latest in-group slot producing an operand (0: none)
+  uint8_t bits;            // 1, 2: complement left / right; 4: output gate; 8 / 16: left / right local
+  uint8_t pad;
+};
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t *v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t *v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_read_dyn(uint32_t n) {
+  switch (n) {   // cp.async.bulk.wait_group.read takes an immediate
+    case 0: bulk_wait_read_n<0>(); break;
+    case 1: bulk_wait_read_n<1>(); break;
+    case 2: bulk_wait_read_n<2>(); break;
+    case 3: bulk_wait_read_n<3>(); break;
+    case 4: bulk_wait_read_n<4>(); break;
+    case 5: bulk_wait_read_n<5>(); break;
+    case 6: bulk_wait_read_n<6>(); break;
+    default: bulk_wait_read_n<7>(); break;
+  }
+}
+
+template <int K, int ELL, bool PM, int ENC>
+__global__ void __launch_bounds__(GeoRes<K, ELL>::THREADS, 1)
+resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan, const uint32_t *__restrict__ in_slots,
+                   uint32_t n_ops, uint32_t n_in, uint32_t n_local, uint32_t n_out, uint32_t lanes,
+                   uint32_t n_groups, DevParams p) {
+  using R = GeoRes<K, ELL>;
+  using G = GeoWS<K, ELL, PM, ENC, false>;       // roles, TMEM columns, MMA descriptors
+  constexpr int W = RES_W;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint32_t *s_inb = reinterpret_cast<uint32_t *>(smem);
+  uint32_t *s_loc = reinterpret_cast<uint32_t *>(smem + R::off_local(n_in));
+  uint8_t *s_b = smem + R::off_b(n_in, n_local);
+  uint8_t *s_ta = smem + R::off_ta(n_in, n_local);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + R::off_bar(n_in, n_local));
+  uint64_t *in_full = bar;                  // [2] input set loaded
+  uint64_t *in_empty = bar + 2;             // [2] input set read by every gate of its group
+  uint64_t *op_full = bar + 4;              // [2]
+  uint64_t *main_done = bar + 6;            // [2]
+  uint64_t *a_free = bar + 8;               // [2]
+  uint64_t *d_free = bar + 10;              // [2]
+  uint64_t *out_free = bar + 12;            // [N_OUT] tail rows of slot t may be written
+  uint64_t *tail_ready = bar + 12 + R::N_OUT;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 12 + 2 * R::N_OUT);
+  uint32_t *epi_done = tmem_slot + 1;       // slots whose output is in its local buffer
+  ResOp *s_plan = reinterpret_cast<ResOp *>(smem + R::off_bar(n_in, n_local) + R::OFF_BAR_SIZE);
+  SlotInfo *s_slot = reinterpret_cast<SlotInfo *>(s_plan + RES_MAX_OPS);   // 16-byte aligned
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const uint32_t S = n_ops * W;                                     // slots per group
+  const uint32_t my_groups = blockIdx.x < n_groups ? (n_groups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const uint32_t n_slots = my_groups * S;
+  auto lane_of_group = [&](uint32_t g, uint32_t w) { return (g * gridDim.x + blockIdx.x) * W + w; };
+  auto in_ptr = [&](uint32_t set, uint32_t w, uint32_t i) {
+    return s_inb + ((set * W + w) * n_in + i) * R::CT_WORDS;
+  };
+
+  if (warp == G::WARP_MMA) tmem_alloc<512>(tmem_slot);
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&in_full[i], 1);
+      mbar_init(&in_empty[i], G::NB_WARPS);
+      mbar_init(&op_full[i], G::NB_WARPS);
+      mbar_init(&main_done[i], 1);
+      mbar_init(&a_free[i], 1);
+      mbar_init(&d_free[i], R::NE_WARPS);
+    }
+    for (int i = 0; i < R::N_OUT; ++i) {
+      mbar_init(&out_free[i], 1);
+      mbar_init(&tail_ready[i], 1);
+    }
+    *epi_done = 0u;
+    fence_mbar_init();
+  }
+  for (uint32_t i = tid; i < n_ops * (sizeof(ResOp) / 4); i += R::THREADS)
+    reinterpret_cast<uint32_t *>(s_plan)[i] = reinterpret_cast<const uint32_t *>(plan)[i];
+  if (tid < n_ops * W) {
+    const ResOp op = plan[tid / W];
+    const uint32_t w = tid % W;
+    SlotInfo si;
+    si.v1 = (op.lkind ? w * n_local + op.lidx : w * n_in + op.lidx) * R::CT_WORDS;
+    si.v2 = (op.rkind ? w * n_local + op.ridx : w * n_in + op.ridx) * R::CT_WORDS;
+    si.dest = (w * n_local + op.dest) * R::CT_WORDS;
+    si.bits = (op.flags & 3u) | (op.is_out ? 4u : 0u) | (op.lkind ? 8u : 0u) | (op.rkind ? 16u : 0u);
+    si.pad = 0;
+    si.need = max(op.lkind ? op.lprod * W + w + 1 : 0, op.rkind ? op.rprod * W + w + 1 : 0);
+    s_slot[tid] = si;
+  }
+  for (uint32_t w = tid; w < 2 * R::B_BYTES / 4; w += R::THREADS) reinterpret_cast<uint32_t *>(s_b)[w] = 0u;
+  for (uint32_t w = tid; w < 2 * R::TA_BYTES / 4; w += R::THREADS) reinterpret_cast<uint32_t *>(s_ta)[w] = 0u;
+  // ciphertext padding words of every local buffer stay zero (the epilogue writes N * K words)
+  for (uint32_t w = tid; w < W * n_local * R::CT_WORDS; w += R::THREADS) s_loc[w] = 0u;
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp == G::WARP_PROD) {
+    // ------------------------------ producer: program inputs, one group ahead ------------------------------
+    if (lane == 0) {
+      for (uint32_t g = 0; g < my_groups; ++g) {
+        const uint32_t set = g & 1u;
+        mbar_wait(&in_empty[set], ((g >> 1) & 1u) ^ 1u);
+        mbar_expect_tx(&in_full[set], W * n_in * R::CT_BYTES);
+        for (uint32_t w = 0; w < W; ++w) {
+          const uint32_t ln = lane_of_group(g, w);
+          for (uint32_t i = 0; i < n_in; ++i)
+            bulk_g2s(in_ptr(set, w, i), store + ((uint64_t)in_slots[i] * lanes + ln) * R::CT_WORDS, R::CT_BYTES,
+                     &in_full[set]);
+        }
+      }
+    }
+  } else if (warp == G::WARP_MMA) {
+    // ------------------------------ MMA issuer (as level_tc_ws_kernel) ------------------------------
+    const uint64_t bdesc0 = smem_desc(smem_u32(s_b), G::LBO, G::SBO);
+    const uint64_t tdesc0 = smem_desc(smem_u32(s_ta), G::TA_LBO, 0u);
+    for (uint32_t t = 0; t < n_slots; ++t) {
+      const uint32_t b = t & 1u, u = t >> 1;
+      mbar_wait(&op_full[b], u & 1u);
+      mbar_wait(&d_free[b], (u & 1u) ^ 1u);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + b * G::BUF_COLS;
+      const uint64_t bd_b = bdesc0 + ((b * R::B_BYTES) >> 4);
+      const uint64_t td_b = tdesc0 + ((b * R::TA_BYTES) >> 4);
+      if (elect_one()) {
+#pragma unroll
+        for (int mt = 0; mt < G::MT; ++mt) {
+#pragma unroll
+          for (int s = 0; s < K; ++s)
+            mma_i8_ts(tb + mt * G::NPAD, tb + G::D_COLS + mt * 8 * K + 8 * s, bd_b + ((s * 4 * G::LBO) >> 4),
+                      G::IDESC, s > 0 ? 1u : 0u);
+        }
+        if constexpr (G::TAIL > 0) {
+#pragma unroll
+          for (int s = 0; s < K; ++s)
+            mma_i8_ss(tb + G::D_COLS, td_b + ((s * 2 * G::TA_LBO) >> 4), bd_b + ((s * 4 * G::LBO) >> 4),
+                      G::IDESC_TAIL, s > 0 ? 1u : 0u);
+        }
+      }
+      __syncwarp();
+      if (elect_one()) mma_commit(&main_done[b]);
+      __syncwarp();
+    }
+  } else if (warp == G::WARP_TAIL) {
+    // ------------------------------ tail rows, into the gate's local buffer ------------------------------
+    if constexpr (G::TAIL > 0) {
+      SlotPos pos;
+      for (uint32_t t = 0; t < n_slots; ++t, pos.next(S, W)) {
+        const uint32_t b = t & 1u, u = t >> 1;
+        mbar_wait(&main_done[b], u & 1u);
+        tc_fence_after();
+        uint32_t d[36];
+        load_acc36(tmem_base + b * G::BUF_COLS + G::D_COLS, d, false);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_free[b]);
+        const uint32_t ob = t % R::N_OUT, ou = t / R::N_OUT;
+        mbar_wait(&out_free[ob], ou & 1u);
+        uint32_t *out_st = s_loc + s_slot[pos.r].dest;
+        if (lane < G::TAIL) {
+          const int row = G::MMA_ROWS + lane;
+          const int rb = row / ELL, rbit = row - rb * ELL;
+#pragma unroll
+          for (int i = 0; i < K; ++i) out_st[row * K + i] = finish_neg<ELL, PM, ENC>(&d[i * 4], i == rb ? (1u << rbit) : 0u, p);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tail_ready[ob]);
+      }
+    }
+  } else if (warp < G::WARP_EPI0) {
+    // ------------------------------ operand builders ------------------------------
+    const int bt = tid - 32 * G::WARP_BUILD0;
+    const int bw = bt >> 5;
+    const int quad = warp & 3;
+    const int tile = bw >> 2;
+    const int row = 128 * tile + 32 * quad + lane;
+    const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
+    const int row_blk = row / ELL, row_bit = row - row_blk * ELL;
+    constexpr int B_ROWS = (G::KB + 128 * G::MT - 1) / (128 * G::MT);
+    int b_src[B_ROWS], b_dst[B_ROWS], b_w[B_ROWS], b_j[B_ROWS];
+#pragma unroll
+    for (int x = 0; x < B_ROWS; ++x) {
+      const int kr = bt + x * 128 * G::MT;
+      const int ww = kr >> 5, kk = kr & 31;
+      const int j = 8 * (kk & 3) + (kk >> 2);
+      const bool ok = kr < G::KB && j < ELL;
+      b_src[x] = ok ? (ww * ELL + j) * K : -1;
+      b_dst[x] = (kr >> 3) * G::LBO + (kr & 7) * 16;
+      b_w[x] = ww;
+      b_j[x] = j;
+    }
+    SlotPos pos;
+    const uint32_t in_set_words = W * n_in * R::CT_WORDS;
+    for (uint32_t t = 0; t < n_slots; ++t, pos.next(S, W)) {
+      const uint32_t g = pos.g, r = pos.r;
+      const uint32_t set = g & 1u, b = t & 1u, u = t >> 1;
+      if (r == 0) mbar_wait(&in_full[set], (g >> 1) & 1u);
+      const SlotInfo si = s_slot[r];
+      // operands produced in this group: wait until the epilogue has published their slots
+      if (si.need > 0 && lane == 0 && !(p.dbg & (1u << 19))) {   // dbg bit 19: no RAW waits (timing only)
+        const uint32_t need = pos.gS + si.need;
+        uint32_t spins = 0;
+        while (ld_acquire_cta_smem(epi_done) < need)
+          if (++spins > FHEGPU_SPIN_LIMIT) __trap();
+      }
+      __syncwarp();
+      mbar_wait(&a_free[b], (u & 1u) ^ 1u);
+      tc_fence_after();
+      const uint32_t *in_b = s_inb + set * in_set_words;
+      const uint32_t *v1 = ((si.bits & 8u) ? s_loc : in_b) + si.v1;
+      const uint32_t *v2 = ((si.bits & 16u) ? s_loc : in_b) + si.v2;
+      const bool comp1 = si.bits & 1u, comp2 = si.bits & 2u;
+      uint8_t *bb = s_b + b * R::B_BYTES;
+      {
+        uint32_t words[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) words[i] = v1[row * K + i];
+        if (comp1) {
+#pragma unroll
+          for (int i = 0; i < K; ++i) words[i] = sub_mod(i == row_blk ? (1u << row_bit) : 0u, words[i], p.q);
+        }
+        const uint32_t a_addr = tmem_base + b * G::BUF_COLS + lane_off + G::D_COLS + tile * 8 * K;
+#pragma unroll
+        for (int w0 = 0; w0 < K; w0 += 4) {
+          if (w0 + 4 <= K) {
+            uint32_t sp[32];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint32_t one[8];
+              spread_word_sr<ENC>(words[w0 + j], one);
+#pragma unroll
+              for (int x = 0; x < 8; ++x) sp[8 * j + x] = one[x];
+            }
+            tmem_st32(a_addr + 8 * w0, sp);
+          } else {
+#pragma unroll
+            for (int ww = w0; ww < K; ++ww) {
+              uint32_t sp[8];
+              spread_word_sr<ENC>(words[ww], sp);
+              tmem_st8(a_addr + 8 * ww, sp);
+            }
+          }
+        }
+      }
+      if constexpr (G::TAIL > 0) {
+        if (bt < G::TAIL * K) {
+          const int m = bt / K, ww = bt - m * K;
+          const int rr = G::MMA_ROWS + m;
+          uint32_t v = v1[rr * K + ww];
+          if (comp1) v = sub_mod(ww == rr / ELL ? (1u << (rr % ELL)) : 0u, v, p.q);
+          uint32_t sp[8];
+          spread_word_sr<ENC>(v, sp);
+          uint8_t *dst = s_ta + b * R::TA_BYTES + (2 * ww) * G::TA_LBO + m * 16;
+          *reinterpret_cast<uint4 *>(dst) = make_uint4(sp[0], sp[1], sp[2], sp[3]);
+          *reinterpret_cast<uint4 *>(dst + G::TA_LBO) = make_uint4(sp[4], sp[5], sp[6], sp[7]);
+        }
+      }
+#pragma unroll
+      for (int x = 0; x < B_ROWS; ++x) {
+        if (b_src[x] < 0) continue;
+        uint32_t vals[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) vals[i] = v2[b_src[x] + i];
+        if (comp2) {
+#pragma unroll
+          for (int i = 0; i < K; ++i) vals[i] = sub_mod(i == b_w[x] ? (1u << b_j[x]) : 0u, vals[i], p.q);
+        }
+        uint8_t *dst = bb + b_dst[x];
+#pragma unroll
+        for (int ch = 0; ch < G::NCH; ++ch) {
+          uint4 val;
+          val.x = 4 * ch + 0 < K ? vals[4 * ch + 0] : 0u;
+          val.y = 4 * ch + 1 < K ? vals[4 * ch + 1] : 0u;
+          val.z = 4 * ch + 2 < K ? vals[4 * ch + 2] : 0u;
+          val.w = 4 * ch + 3 < K ? vals[4 * ch + 3] : 0u;
+          *reinterpret_cast<uint4 *>(dst + ch * G::SBO) = val;
+        }
+      }
+      tmem_wait_st();
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&op_full[b]);
+        if (r == S - 1) mbar_arrive(&in_empty[set]);   // every gate of the group has read its inputs
+      }
+    }
+  } else {
+    // ------------------------------ epilogue, into the gate's local buffer ------------------------------
+    const int et = tid - 32 * G::WARP_EPI0;
+    const int ew = et >> 5;
+    const int quad = warp & 3;
+    const int tile = (ew >> 2) & 1;
+    const int part = ew >> 3;                      // value range of this thread (EPI_SPLIT = 2)
+    const int row = 128 * tile + 32 * quad + lane;
+    const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
+    const int row_blk = row / ELL, row_bit = row - row_blk * ELL;
+    constexpr uint32_t NE_THREADS = 32 * R::NE_WARPS;
+    // stores outstanding when a gate writes an output buffer: the same buffer's store of the
+    // previous group is at most n_out * W - 1 stores back
+    const uint32_t out_lag = n_out * W > 0 ? n_out * W - 1 : 0;
+    if (et == 0) {
+      if (s_plan[0].is_out) bulk_wait_read_dyn(out_lag);
+      mbar_arrive(&out_free[0]);
+    }
+    SlotPos pos;
+    for (uint32_t t = 0; t < n_slots; ++t, pos.next(S, W)) {
+      const uint32_t b = t & 1u, u = t >> 1;
+      const uint32_t g = pos.g, r = pos.r, o = pos.o, w = pos.w;
+      const SlotInfo si = s_slot[r];
+      uint32_t *out_st = s_loc + si.dest;
+      mbar_wait(&main_done[b], u & 1u);
+      tc_fence_after();
+      const uint32_t dcol = tmem_base + b * G::BUF_COLS + lane_off + tile * G::NPAD;
+      if constexpr (R::EPI_SPLIT == 1) {
+        uint32_t d[36];
+        load_acc36(dcol, d, false);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&d_free[b]);
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+          out_st[row * K + i] = finish_neg<ELL, PM, ENC>(&d[i * 4], i == row_blk ? (1u << row_bit) : 0u, p);
+      } else {
+        static_assert(K == 9, "split epilogue: values 0-4 and 5-8");
+        uint32_t d[20];
+        if (part == 0) {                           // values 0-4: columns 0-19
+          tmem_ld16(dcol, d);
+          tmem_ld4(dcol + 16, d + 16);
+        } else {                                   // values 5-8: columns 20-35 (naturally aligned pieces)
+          tmem_ld4(dcol + 20, d);
+          tmem_ld8(dcol + 24, d + 4);
+          tmem_ld4(dcol + 32, d + 12);
+        }
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&d_free[b]);
+        if (part == 0) {
+#pragma unroll
+          for (int i = 0; i < 5; ++i)
+            out_st[row * K + i] = finish_neg<ELL, PM, ENC>(&d[i * 4], i == row_blk ? (1u << row_bit) : 0u, p);
+        } else {
+#pragma unroll
+          for (int i = 5; i < 9; ++i)
+            out_st[row * K + i] =
+                finish_neg<ELL, PM, ENC>(&d[(i - 5) * 4], i == row_blk ? (1u << row_bit) : 0u, p);
+        }
+      }
+      fence_proxy_async_smem();
+      if (et == 0 && t + 1 < n_slots) {
+        // the next gate's buffer: if it is an output buffer, its previous store must have read it
+        if (s_slot[r + 1 == S ? 0u : r + 1].bits & 4u) bulk_wait_read_dyn(out_lag);   // next slot
+        mbar_arrive(&out_free[(t + 1) % R::N_OUT]);
+      }
+      named_bar(1, NE_THREADS);
+      if (et == 0) {
+        const uint32_t ob = t % R::N_OUT, ou = t / R::N_OUT;
+        mbar_wait(&tail_ready[ob], ou & 1u);
+        if (si.bits & 4u) {
+          const uint32_t ln = lane_of_group(g, w);
+          bulk_s2g(store + ((uint64_t)s_plan[o].out_slot * lanes + ln) * R::CT_WORDS, out_st, R::CT_BYTES);
+        }
+      } else if (et == 32) {
+        // the gate's output is readable in its buffer: published by a thread without bulk
+        // stores in flight (a release on the storing thread would wait for its stores)
+        const uint32_t ob = t % R::N_OUT, ou = t / R::N_OUT;
+        mbar_wait(&tail_ready[ob], ou & 1u);
+        st_release_cta_smem(epi_done, t + 1);
+      }
+    }
+    if (et == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == G::WARP_MMA) tmem_dealloc<512>(tmem_base);
+}
+
+}  // namespace tc
+}  // namespace fhegpu

@@ -32,6 +32,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .errors import CapabilityError, NoiseOverflowError, UsageError
+from ._native import RES_OP_DTYPE
 from .scheme import Ciphertext, GswScheme, KeyPair
 
 _UPLOAD_BATCH_BYTES = 256 << 20
@@ -225,7 +226,9 @@ class LevelledNetlist:
         self._slot = slot.tolist()
         offsets = np.append(lv_start, len(out)).astype(np.uint64)
         prog = {"ops": table, "offsets": offsets, "levels": lv_vals,
-                "widths": np.diff(offsets).astype(np.int64)}
+                "widths": np.diff(offsets).astype(np.int64),
+                "nodes": np.stack([left, right, out], axis=1),
+                "held": np.ones(len(out), dtype=bool) if self.keep_all else ~new_dead[out]}
         if ssa:
             producer = np.full(n_nodes, -1, dtype=np.int64)
             producer[out] = np.arange(len(out))
@@ -247,9 +250,9 @@ class GpuEngine(LevelledNetlist):
             raise UsageError("threads must be >= 1")
         if batch_size < 1:
             raise UsageError("batch_size must be >= 1")
-        if schedule not in ("auto", "levels", "dataflow", "queue", "tiled"):
-            raise UsageError(f"schedule must be 'auto', 'levels', 'dataflow', 'queue' or 'tiled', "
-                             f"got {schedule!r}")
+        if schedule not in ("auto", "levels", "dataflow", "queue", "tiled", "resident"):
+            raise UsageError(f"schedule must be 'auto', 'levels', 'dataflow', 'queue', 'tiled' or "
+                             f"'resident', got {schedule!r}")
         self.schedule = schedule
         if lane_rngs is not None and len(lane_rngs) != batch_size:
             raise UsageError("need one rng per lane")
@@ -638,6 +641,10 @@ class GpuEngine(LevelledNetlist):
                 program.set_deps(prog["deps"])
             if sched == "queue":
                 program.set_queue(True)
+            if sched == "resident" and self.batch_size % 2 == 0:   # lanes run in pairs
+                plan = self._resident_plan(prog)
+                if plan is not None:                 # else: the level launches of `program`
+                    program.set_resident(*plan)
         program.run(lanes)
         self.last_program = program
         self.last_compile = prog
@@ -716,6 +723,55 @@ class GpuEngine(LevelledNetlist):
             return False
         outs = np.asarray(self._pending_ops[4::5], dtype=np.int64)
         return len(np.unique(np.asarray(self._level, dtype=np.int64)[outs])) >= self.QUEUE_MIN_LEVELS
+
+    RES_MAX_OPS, RES_MAX_IN, RES_MAX_LOCAL = 8, 4, 8       # tc_nand_resident.cuh limits
+    RES_SMEM_LIMIT = 227 * 1024
+
+    @classmethod
+    def _resident_plan(cls, prog):
+        """Per-lane plan of a small level-compiled program for fhegpu_prog_set_resident, or None.
+
+        Gates keep the level order; an operand produced in the program is read from the local
+        buffer its producer wrote, other operands are program inputs (their store slots).
+        Outputs (nodes still held after the program) get buffers of their own and are stored;
+        a temporary's buffer is reused once every reader of its value precedes the writer."""
+        table, nodes, held = prog["ops"], prog["nodes"], prog["held"]
+        n = len(table)
+        if n == 0 or n > cls.RES_MAX_OPS:
+            return None
+        producer = {int(nd): i for i, nd in enumerate(nodes[:, 2])}
+        last_read = np.full(n, -1)
+        for i in range(n):
+            for nd in nodes[i, :2]:
+                if int(nd) in producer:
+                    last_read[producer[int(nd)]] = i
+        plan = np.zeros(n, dtype=RES_OP_DTYPE)
+        inputs, dest, holder, n_local = [], [0] * n, {}, 0     # holder: buffer -> gate whose value it has
+        for i in range(n):
+            for side, (kind, idx, prod) in enumerate((("lkind", "lidx", "lprod"), ("rkind", "ridx", "rprod"))):
+                nd, slot = int(nodes[i, side]), int(table[i]["left" if side == 0 else "right"])
+                if nd in producer:
+                    plan[i][kind], plan[i][idx], plan[i][prod] = 1, dest[producer[nd]], producer[nd]
+                else:
+                    if slot not in inputs:
+                        inputs.append(slot)
+                    plan[i][kind], plan[i][idx], plan[i][prod] = 0, inputs.index(slot), -1
+            free = [b for b, j in holder.items() if not held[j] and last_read[j] < i]
+            if held[i] or not free:
+                dest[i], n_local = n_local, n_local + 1
+            else:
+                dest[i] = min(free)
+            holder[dest[i]] = i
+            plan[i]["dest"], plan[i]["is_out"] = dest[i], int(held[i])
+            plan[i]["flags"] = int(table[i]["flags"]) & 3
+            plan[i]["out_slot"] = int(table[i]["out"]) if held[i] else 0
+        if len(inputs) > cls.RES_MAX_IN or n_local > cls.RES_MAX_LOCAL:
+            return None
+        ct = 9408                                     # 9 x 29-bit rows of 261 values, padded
+        smem = (2 * 2 * len(inputs) + 2 * n_local) * ct + 2 * 13824 + 2 * 2304 + 1024
+        if smem > cls.RES_SMEM_LIMIT:
+            return None
+        return plan, np.asarray(inputs, dtype=np.uint32), n_local
 
     @staticmethod
     def _tile(prog, K, lanes_per_chunk=1, skew=0, window=2048, ring=0, t_base=0):

@@ -300,3 +300,72 @@ def test_ifft_replay_matches_swap_model(normalize):
         f_re, f_im = fixedfft.fft_1d(re, im, F, f)
         b_im, b_re = fixedfft.fft_1d(f_im, f_re, F, f)
         assert np.abs((b_re >> 3) - re).max() <= 8 and np.abs((b_im >> 3) - im).max() <= 8
+
+
+def _replay_resident(eng, prog, plan, inputs, n_local):
+    """Cleartext model of the lane-resident kernel (tc_nand_resident.cuh) on packed lane bits:
+    inputs from the dry-run store, every gate into its local buffer, outputs to their slots."""
+    store = replay_dry(eng)          # the level replay's final store: the reference results
+    before = {slot: bits for slot, bits in eng.dry_inputs}   # input slots may be reused by outputs
+    mask = eng.mask
+    loc = [None] * n_local
+    ins = [before[int(s)] for s in inputs]
+    outs = {}
+    for rec in plan:
+        x = loc[rec["lidx"]] if rec["lkind"] else ins[rec["lidx"]]
+        y = loc[rec["ridx"]] if rec["rkind"] else ins[rec["ridx"]]
+        if rec["flags"] & 1:
+            x ^= mask
+        if rec["flags"] & 2:
+            y ^= mask
+        loc[rec["dest"]] = mask ^ (x & y)
+        if rec["is_out"]:
+            outs[int(rec["out_slot"])] = loc[rec["dest"]]
+    return store, outs
+
+
+def test_resident_plan_cfg1_and_random_programs():
+    """Lane-resident plans (GpuEngine._resident_plan): the gate benchmark's XOR + AND uses 2
+    inputs and 6 local buffers (4 temporaries, 2 outputs) and reproduces the level replay;
+    random small programs (temporaries reused, complemented operands, outputs also read
+    later) agree too or are refused when they exceed the kernel's limits."""
+    from paper_1611_08769_b200.gates import nor_, not_, or_, xnor_
+    scheme = GswScheme(DEFAULT_PARAMS)
+    eng = GpuEngine(scheme, dry_run=True, batch_size=64)
+    rng = np.random.default_rng(4)
+    a, b = (eng.input_bit(int(rng.integers(0, 1 << 62))) for _ in range(2))
+    x, y = xor_(a, b), and_(a, b)
+    eng.flush()
+    prog = eng.dry_programs[-1]
+    plan, inputs, n_local = GpuEngine._resident_plan(prog)
+    assert (len(plan), len(inputs), n_local) == (6, 2, 6)
+    assert plan["is_out"].sum() == 2
+    store, outs = _replay_resident(eng, prog, plan, inputs, n_local)
+    for h in (x, y):
+        assert outs[eng._slot[h.node]] == store[eng._slot[h.node]]
+    gates = [not_, and_, or_, xor_, nor_, xnor_]
+    done = 0
+    scheme0 = GswScheme(DEFAULT0_PARAMS)                   # no depth budget for random programs
+    for trial in range(40):
+        eng = GpuEngine(scheme0, dry_run=True, batch_size=32)
+        pool = [eng.input_bit(int(rng.integers(0, 1 << 31))) for _ in range(int(rng.integers(1, 4)))]
+        for _ in range(int(rng.integers(1, 4))):
+            g = gates[int(rng.integers(0, len(gates)))]
+            p1, p2 = pool[int(rng.integers(0, len(pool)))], pool[int(rng.integers(0, len(pool)))]
+            pool.append(g(p1) if g is not_ else g(p1, p2))
+        keep = pool[-2:] + [pool[int(rng.integers(0, len(pool)))]]
+        del pool
+        eng.flush()
+        if not eng.dry_programs:
+            continue
+        prog = eng.dry_programs[-1]
+        res = GpuEngine._resident_plan(prog)
+        if res is None:                     # over the kernel's gate / input / buffer limits
+            continue
+        plan, inputs, n_local = res
+        store, outs = _replay_resident(eng, prog, plan, inputs, n_local)
+        for h in keep:
+            if not h.const and eng._slot[h.node] in outs:
+                assert outs[eng._slot[h.node]] == store[eng._slot[h.node]]
+        done += 1
+    assert done >= 10
