@@ -14,6 +14,7 @@
 // with t = g * S + o * W + w, S = n_ops * W: gates of one op for the W lanes back to back, ops
 // in the host's topological order, so a gate's producer is >= W slots earlier.  A builder
 // reading a gate output waits until the epilogue has published that slot (epi_done).
+// Timeline probes (trace_ev, -DFHEGPU_TRACE=1 builds only): tools/timeline_resident.py.
 #pragma once
 
 #include "tc_nand_ws.cuh"
@@ -225,7 +226,9 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
     for (uint32_t t = 0; t < n_slots; ++t) {
       const uint32_t b = t & 1u, u = t >> 1;
       mbar_wait(&op_full[b], u & 1u);
+      if (lane == 0) trace_ev(p, t, 2);
       mbar_wait(&d_free[b], (u & 1u) ^ 1u);
+      if (lane == 0) trace_ev(p, t, 3);
       tc_fence_after();
       const uint32_t tb = tmem_base + b * G::BUF_COLS;
       const uint64_t bd_b = bdesc0 + ((b * R::B_BYTES) >> 4);
@@ -248,6 +251,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       __syncwarp();
       if (elect_one()) mma_commit(&main_done[b]);
       __syncwarp();
+      if (lane == 0) trace_ev(p, t, 4);
     }
   } else if (warp == G::WARP_TAIL) {
     // ------------------------------ tail rows, into the gate's local buffer ------------------------------
@@ -256,6 +260,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       for (uint32_t t = 0; t < n_slots; ++t, pos.next(S, W)) {
         const uint32_t b = t & 1u, u = t >> 1;
         mbar_wait(&main_done[b], u & 1u);
+        if (lane == 0) trace_ev(p, t, 12);
         tc_fence_after();
         uint32_t d[36];
         load_acc36(tmem_base + b * G::BUF_COLS + G::D_COLS, d, false);
@@ -265,6 +270,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
         if (lane == 0) mbar_arrive(&a_free[b]);
         const uint32_t ob = t % R::N_OUT, ou = t / R::N_OUT;
         mbar_wait(&out_free[ob], ou & 1u);
+        if (lane == 0) trace_ev(p, t, 13);
         uint32_t *out_st = s_loc + s_slot[pos.r].dest;
         if (lane < G::TAIL) {
           const int row = G::MMA_ROWS + lane;
@@ -275,6 +281,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tail_ready[ob]);
+        if (lane == 0) trace_ev(p, t, 14);
       }
     }
   } else if (warp < G::WARP_EPI0) {
@@ -305,6 +312,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       const uint32_t g = pos.g, r = pos.r;
       const uint32_t set = g & 1u, b = t & 1u, u = t >> 1;
       if (r == 0) mbar_wait(&in_full[set], (g >> 1) & 1u);
+      if (bt == 0) trace_ev(p, t, 5);
       const SlotInfo si = s_slot[r];
       // operands produced in this group: wait until the epilogue has published their slots
       if (si.need > 0 && lane == 0 && !(p.dbg & (1u << 19))) {   // dbg bit 19: no RAW waits (timing only)
@@ -314,7 +322,9 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
           if (++spins > FHEGPU_SPIN_LIMIT) __trap();
       }
       __syncwarp();
+      if (bt == 0) trace_ev(p, t, 6);
       mbar_wait(&a_free[b], (u & 1u) ^ 1u);
+      if (bt == 0) trace_ev(p, t, 7);
       tc_fence_after();
       const uint32_t *in_b = s_inb + set * in_set_words;
       const uint32_t *v1 = ((si.bits & 8u) ? s_loc : in_b) + si.v1;
@@ -394,6 +404,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
         mbar_arrive(&op_full[b]);
         if (r == S - 1) mbar_arrive(&in_empty[set]);   // every gate of the group has read its inputs
       }
+      if (bt == 0) trace_ev(p, t, 8);
     }
   } else {
     // ------------------------------ epilogue, into the gate's local buffer ------------------------------
@@ -420,6 +431,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       const SlotInfo si = s_slot[r];
       uint32_t *out_st = s_loc + si.dest;
       mbar_wait(&main_done[b], u & 1u);
+      if (et == 0) trace_ev(p, t, 9);
       tc_fence_after();
       const uint32_t dcol = tmem_base + b * G::BUF_COLS + lane_off + tile * G::NPAD;
       if constexpr (R::EPI_SPLIT == 1) {
@@ -465,6 +477,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
         mbar_arrive(&out_free[(t + 1) % R::N_OUT]);
       }
       named_bar(1, NE_THREADS);
+      if (et == 0) trace_ev(p, t, 10);
       if (et == 0) {
         const uint32_t ob = t % R::N_OUT, ou = t / R::N_OUT;
         mbar_wait(&tail_ready[ob], ou & 1u);
@@ -478,6 +491,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
         const uint32_t ob = t % R::N_OUT, ou = t / R::N_OUT;
         mbar_wait(&tail_ready[ob], ou & 1u);
         st_release_cta_smem(epi_done, t + 1);
+        trace_ev(p, t, 11);
       }
     }
     if (et == 0) bulk_wait_all();
