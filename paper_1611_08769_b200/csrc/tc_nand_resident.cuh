@@ -13,7 +13,8 @@
 // those of level_tc_ws_kernel (tc_nand_ws.cuh).  Slot t of a CTA is (group g, op o, lane w)
 // with t = g * S + o * W + w, S = n_ops * W: gates of one op for the W lanes back to back, ops
 // in the host's topological order, so a gate's producer is >= W slots earlier.  A builder
-// reading a gate output waits until the epilogue has published that slot (epi_done).
+// reading a gate output waits on that gate's mbarrier (out_ready), which the epilogue arrives on
+// once the output sits in its local buffer (one phase per lane group).
 // Timeline probes (trace_ev, -DFHEGPU_TRACE=1 builds only): tools/timeline_resident.py.
 #pragma once
 
@@ -90,7 +91,7 @@ struct SlotPos {
 struct __align__(16) SlotInfo {
   uint32_t v1, v2;         // left / right operand buffer (ciphertext words offset)
   uint32_t dest;           // destination local buffer (ciphertext words offset)
-  uint16_t need;           // 1 + the latest in-group slot producing an operand (0: none)
+  uint16_t need;           // unused (operand readiness: out_ready mbarriers)
   uint8_t bits;            // 1, 2: complement left / right; 4: output gate; 8 / 16: left / right local
   uint8_t pad;
 };
@@ -147,8 +148,8 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
   uint64_t *d_free = bar + 10;              // [2]
   uint64_t *out_free = bar + 12;            // [N_OUT] tail rows of slot t may be written
   uint64_t *tail_ready = bar + 12 + R::N_OUT;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 12 + 2 * R::N_OUT);
-  uint32_t *epi_done = tmem_slot + 1;       // slots whose output is in its local buffer
+  uint64_t *out_ready = bar + 12 + 2 * R::N_OUT;           // [RES_MAX_OPS * W] gate output in its buffer
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(out_ready + RES_MAX_OPS * RES_W);
   ResOp *s_plan = reinterpret_cast<ResOp *>(smem + R::off_bar(n_in, n_local) + R::OFF_BAR_SIZE);
   SlotInfo *s_slot = reinterpret_cast<SlotInfo *>(s_plan + RES_MAX_OPS);   // 16-byte aligned
 
@@ -176,7 +177,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       mbar_init(&out_free[i], 1);
       mbar_init(&tail_ready[i], 1);
     }
-    *epi_done = 0u;
+    for (int i = 0; i < RES_MAX_OPS * W; ++i) mbar_init(&out_ready[i], 1);
     fence_mbar_init();
   }
   for (uint32_t i = tid; i < n_ops * (sizeof(ResOp) / 4); i += R::THREADS)
@@ -190,7 +191,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
     si.dest = (w * n_local + op.dest) * R::CT_WORDS;
     si.bits = (op.flags & 3u) | (op.is_out ? 4u : 0u) | (op.lkind ? 8u : 0u) | (op.rkind ? 16u : 0u);
     si.pad = 0;
-    si.need = max(op.lkind ? op.lprod * W + w + 1 : 0, op.rkind ? op.rprod * W + w + 1 : 0);
+    si.need = 0;
     s_slot[tid] = si;
   }
   for (uint32_t w = tid; w < 2 * R::B_BYTES / 4; w += R::THREADS) reinterpret_cast<uint32_t *>(s_b)[w] = 0u;
@@ -314,14 +315,13 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       if (r == 0) mbar_wait(&in_full[set], (g >> 1) & 1u);
       if (bt == 0) trace_ev(p, t, 5);
       const SlotInfo si = s_slot[r];
-      // operands produced in this group: wait until the epilogue has published their slots
-      if (si.need > 0 && lane == 0 && !(p.dbg & (1u << 19))) {   // dbg bit 19: no RAW waits (timing only)
-        const uint32_t need = pos.gS + si.need;
-        uint32_t spins = 0;
-        while (ld_acquire_cta_smem(epi_done) < need)
-          if (++spins > FHEGPU_SPIN_LIMIT) __trap();
+      // operands produced in this group: wait until the epilogue has put them in their buffers
+      // (one mbarrier phase per group; the producer of the next group runs after this slot)
+      if (!(p.dbg & (1u << 19))) {                 // dbg bit 19: no waits (timing only)
+        const ResOp op = s_plan[pos.o];
+        if (op.lkind) mbar_wait(&out_ready[op.lprod * W + pos.w], g & 1u);
+        if (op.rkind) mbar_wait(&out_ready[op.rprod * W + pos.w], g & 1u);
       }
-      __syncwarp();
       if (bt == 0) trace_ev(p, t, 6);
       mbar_wait(&a_free[b], (u & 1u) ^ 1u);
       if (bt == 0) trace_ev(p, t, 7);
@@ -490,7 +490,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
         // stores in flight (a release on the storing thread would wait for its stores)
         const uint32_t ob = t % R::N_OUT, ou = t / R::N_OUT;
         mbar_wait(&tail_ready[ob], ou & 1u);
-        st_release_cta_smem(epi_done, t + 1);
+        mbar_arrive(&out_ready[r]);               // r = o * W + w
         trace_ev(p, t, 11);
       }
     }
