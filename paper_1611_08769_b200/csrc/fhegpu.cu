@@ -328,11 +328,11 @@ int launch_queue(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
 int launch_resident(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
   if (lanes == 0 || pr->r_ops == 0) return FHEGPU_OK;
   if (effective_kernel(c) != FHEGPU_KERNEL_TCGEN05 || (c->p.dbg & 4u)) return FHEGPU_EUNSUP;
-  if (!(c->p.k == 9 && c->p.ell == 29) || lanes % tc::RES_W) return FHEGPU_EUNSUP;
+  if (!(c->p.k == 9 && c->p.ell == 29)) return FHEGPU_EUNSUP;
   using R = tc::GeoRes<9, 29>;
   const uint32_t smem = R::smem_bytes(pr->r_in, pr->r_local);
   if (smem > 227u * 1024u) return FHEGPU_EUNSUP;
-  const uint32_t n_groups = lanes / tc::RES_W;
+  const uint32_t n_groups = (lanes + tc::RES_W - 1) / tc::RES_W;    // the last group may be partial
   const unsigned grid = (unsigned)std::min<uint64_t>(n_groups, (uint64_t)c->num_sms);
   DevParams p = c->p;
   const bool pm = pm_ok(c->p.q, c->p.ell) && !(c->p.dbg & 2u);

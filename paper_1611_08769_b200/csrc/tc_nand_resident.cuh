@@ -23,7 +23,15 @@
 namespace fhegpu {
 namespace tc {
 
-constexpr int RES_W = 2;          // lanes per group
+#ifndef FHEGPU_RES_W
+#define FHEGPU_RES_W 3
+#endif
+#ifndef FHEGPU_RES_NSETS
+#define FHEGPU_RES_NSETS 1
+#endif
+constexpr int RES_W = FHEGPU_RES_W;          // lanes per group (3: producers >= 6 slots ahead)
+constexpr int RES_NSETS = FHEGPU_RES_NSETS;  // input sets (1: the next group's inputs load after
+                                             // the group's last input reader)
 constexpr int RES_MAX_OPS = 8;    // gates per lane program
 constexpr int RES_MAX_IN = 4;     // program inputs
 constexpr int RES_MAX_LOCAL = 8;  // per-lane shared-memory ciphertext buffers
@@ -53,7 +61,7 @@ struct GeoRes {
   static constexpr int THREADS = 32 * (3 + W::NB_WARPS + NE_WARPS);
   static constexpr int OFF_BAR_SIZE = 64 * 8;
   // runtime layout (host computes the same): inputs | locals | B x 2 | TA x 2 | barriers | plan
-  __host__ __device__ static uint32_t off_local(uint32_t n_in) { return 2u * RES_W * n_in * CT_BYTES; }
+  __host__ __device__ static uint32_t off_local(uint32_t n_in) { return RES_NSETS * RES_W * n_in * CT_BYTES; }
   __host__ __device__ static uint32_t off_b(uint32_t n_in, uint32_t n_local) {
     return ((off_local(n_in) + RES_W * n_local * CT_BYTES + 127u) / 128u) * 128u;
   }
@@ -91,8 +99,9 @@ struct SlotPos {
 struct __align__(16) SlotInfo {
   uint32_t v1, v2;         // left / right operand buffer (ciphertext words offset)
   uint32_t dest;           // destination local buffer (ciphertext words offset)
-  uint16_t need;           // unused (operand readiness: out_ready mbarriers)
-  uint8_t bits;            // 1, 2: complement left / right; 4: output gate; 8 / 16: left / right local
+  uint8_t dep_l, dep_r;    // out_ready index (o * W + w) of a local operand's producer (0xFF: input)
+  uint8_t bits;            // 1, 2: complement left / right; 4: output gate; 8 / 16: left / right local;
+                           // 32: the group's last input-reading slot
   uint8_t pad;
 };
 
@@ -182,6 +191,9 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
   }
   for (uint32_t i = tid; i < n_ops * (sizeof(ResOp) / 4); i += R::THREADS)
     reinterpret_cast<uint32_t *>(s_plan)[i] = reinterpret_cast<const uint32_t *>(plan)[i];
+  uint32_t in_last = 0;                        // last gate reading a program input
+  for (uint32_t i = 0; i < n_ops; ++i)
+    if (plan[i].lkind == 0 || plan[i].rkind == 0) in_last = i;
   if (tid < n_ops * W) {
     const ResOp op = plan[tid / W];
     const uint32_t w = tid % W;
@@ -189,9 +201,15 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
     si.v1 = (op.lkind ? w * n_local + op.lidx : w * n_in + op.lidx) * R::CT_WORDS;
     si.v2 = (op.rkind ? w * n_local + op.ridx : w * n_in + op.ridx) * R::CT_WORDS;
     si.dest = (w * n_local + op.dest) * R::CT_WORDS;
-    si.bits = (op.flags & 3u) | (op.is_out ? 4u : 0u) | (op.lkind ? 8u : 0u) | (op.rkind ? 16u : 0u);
+    si.bits = (op.flags & 3u) | (op.is_out ? 4u : 0u) | (op.lkind ? 8u : 0u) | (op.rkind ? 16u : 0u) |
+              (tid / W == in_last && w == W - 1 ? 32u : 0u);
     si.pad = 0;
-    si.need = 0;
+    // A producer >= 5 slots back needs no wait: the builder's a_free wait for slot t implies
+    // main_done(t-2), hence the MMA of t-2 was issued after d_free(t-4), which every epilogue
+    // warp arrives on only after finishing slot t-5 (outputs written, out_ready published).
+    const uint32_t o = tid / W;
+    si.dep_l = op.lkind && (o - op.lprod) * W < 5 ? (uint8_t)(op.lprod * W + w) : (uint8_t)0xFF;
+    si.dep_r = op.rkind && (o - op.rprod) * W < 5 ? (uint8_t)(op.rprod * W + w) : (uint8_t)0xFF;
     s_slot[tid] = si;
   }
   for (uint32_t w = tid; w < 2 * R::B_BYTES / 4; w += R::THREADS) reinterpret_cast<uint32_t *>(s_b)[w] = 0u;
@@ -209,11 +227,13 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
     // ------------------------------ producer: program inputs, one group ahead ------------------------------
     if (lane == 0) {
       for (uint32_t g = 0; g < my_groups; ++g) {
-        const uint32_t set = g & 1u;
-        mbar_wait(&in_empty[set], ((g >> 1) & 1u) ^ 1u);
-        mbar_expect_tx(&in_full[set], W * n_in * R::CT_BYTES);
-        for (uint32_t w = 0; w < W; ++w) {
-          const uint32_t ln = lane_of_group(g, w);
+        const uint32_t set = RES_NSETS == 2 ? g & 1u : 0u, ph = RES_NSETS == 2 ? g >> 1 : g;
+        mbar_wait(&in_empty[set], (ph & 1u) ^ 1u);
+        const uint32_t ln0 = lane_of_group(g, 0);
+        const uint32_t valid = min((uint32_t)W, lanes - ln0);      // the last group may be partial
+        mbar_expect_tx(&in_full[set], valid * n_in * R::CT_BYTES);
+        for (uint32_t w = 0; w < valid; ++w) {
+          const uint32_t ln = ln0 + w;
           for (uint32_t i = 0; i < n_in; ++i)
             bulk_g2s(in_ptr(set, w, i), store + ((uint64_t)in_slots[i] * lanes + ln) * R::CT_WORDS, R::CT_BYTES,
                      &in_full[set]);
@@ -311,19 +331,19 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
     const uint32_t in_set_words = W * n_in * R::CT_WORDS;
     for (uint32_t t = 0; t < n_slots; ++t, pos.next(S, W)) {
       const uint32_t g = pos.g, r = pos.r;
-      const uint32_t set = g & 1u, b = t & 1u, u = t >> 1;
-      if (r == 0) mbar_wait(&in_full[set], (g >> 1) & 1u);
+      const uint32_t set = RES_NSETS == 2 ? g & 1u : 0u, ph = RES_NSETS == 2 ? g >> 1 : g;
+      const uint32_t b = t & 1u, u = t >> 1;
+      if (r == 0) mbar_wait(&in_full[set], ph & 1u);
       if (bt == 0) trace_ev(p, t, 5);
       const SlotInfo si = s_slot[r];
-      // operands produced in this group: wait until the epilogue has put them in their buffers
-      // (one mbarrier phase per group; the producer of the next group runs after this slot)
-      if (!(p.dbg & (1u << 19))) {                 // dbg bit 19: no waits (timing only)
-        const ResOp op = s_plan[pos.o];
-        if (op.lkind) mbar_wait(&out_ready[op.lprod * W + pos.w], g & 1u);
-        if (op.rkind) mbar_wait(&out_ready[op.rprod * W + pos.w], g & 1u);
-      }
       if (bt == 0) trace_ev(p, t, 6);
       mbar_wait(&a_free[b], (u & 1u) ^ 1u);
+      // operands produced in this group: wait until the epilogue has put them in their buffers
+      // (one mbarrier phase per lane group; the producer's next group runs after this slot)
+      if (!(p.dbg & (1u << 19))) {                 // dbg bit 19: no waits (timing only)
+        if (si.dep_l != 0xFF) mbar_wait(&out_ready[si.dep_l], g & 1u);
+        if (si.dep_r != 0xFF) mbar_wait(&out_ready[si.dep_r], g & 1u);
+      }
       if (bt == 0) trace_ev(p, t, 7);
       tc_fence_after();
       const uint32_t *in_b = s_inb + set * in_set_words;
@@ -402,7 +422,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&op_full[b]);
-        if (r == S - 1) mbar_arrive(&in_empty[set]);   // every gate of the group has read its inputs
+        if (si.bits & 32u) mbar_arrive(&in_empty[set]);   // every input reader of the group is built
       }
       if (bt == 0) trace_ev(p, t, 8);
     }
@@ -417,13 +437,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
     const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
     const int row_blk = row / ELL, row_bit = row - row_blk * ELL;
     constexpr uint32_t NE_THREADS = 32 * R::NE_WARPS;
-    // stores outstanding when a gate writes an output buffer: the same buffer's store of the
-    // previous group is at most n_out * W - 1 stores back
-    const uint32_t out_lag = n_out * W > 0 ? n_out * W - 1 : 0;
-    if (et == 0) {
-      if (s_plan[0].is_out) bulk_wait_read_dyn(out_lag);
-      mbar_arrive(&out_free[0]);
-    }
+    if (et == 0) mbar_arrive(&out_free[0]);
     SlotPos pos;
     for (uint32_t t = 0; t < n_slots; ++t, pos.next(S, W)) {
       const uint32_t b = t & 1u, u = t >> 1;
@@ -472,8 +486,9 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       }
       fence_proxy_async_smem();
       if (et == 0 && t + 1 < n_slots) {
-        // the next gate's buffer: if it is an output buffer, its previous store must have read it
-        if (s_slot[r + 1 == S ? 0u : r + 1].bits & 4u) bulk_wait_read_dyn(out_lag);   // next slot
+        // the next gate writes an output buffer: every earlier store (outputs of one group may
+        // share a buffer) must have read its source
+        if (s_slot[r + 1 == S ? 0u : r + 1].bits & 4u) bulk_wait_read_n<0>();
         mbar_arrive(&out_free[(t + 1) % R::N_OUT]);
       }
       named_bar(1, NE_THREADS);
@@ -481,10 +496,9 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       if (et == 0) {
         const uint32_t ob = t % R::N_OUT, ou = t / R::N_OUT;
         mbar_wait(&tail_ready[ob], ou & 1u);
-        if (si.bits & 4u) {
-          const uint32_t ln = lane_of_group(g, w);
+        const uint32_t ln = lane_of_group(g, w);
+        if ((si.bits & 4u) && ln < lanes)                 // partial last group: no store
           bulk_s2g(store + ((uint64_t)s_plan[o].out_slot * lanes + ln) * R::CT_WORDS, out_st, R::CT_BYTES);
-        }
       } else if (et == 32) {
         // the gate's output is readable in its buffer: published by a thread without bulk
         // stores in flight (a release on the storing thread would wait for its stores)

@@ -641,7 +641,7 @@ class GpuEngine(LevelledNetlist):
                 program.set_deps(prog["deps"])
             if sched == "queue":
                 program.set_queue(True)
-            if sched == "resident" and self.batch_size % 2 == 0:   # lanes run in pairs
+            if sched == "resident":
                 plan = self._resident_plan(prog)
                 if plan is not None:                 # else: the level launches of `program`
                     program.set_resident(*plan)
@@ -756,8 +756,11 @@ class GpuEngine(LevelledNetlist):
                     if slot not in inputs:
                         inputs.append(slot)
                     plan[i][kind], plan[i][idx], plan[i][prod] = 0, inputs.index(slot), -1
-            free = [b for b, j in holder.items() if not held[j] and last_read[j] < i]
-            if held[i] or not free:
+            # a buffer is free for gate i once every reader of its value is gate i or earlier (a
+            # gate's builders read before its epilogue writes); outputs and temporaries keep to
+            # buffers of their own kind (the kernel orders output writes after earlier stores)
+            free = [b for b, j in holder.items() if bool(held[j]) == bool(held[i]) and last_read[j] <= i]
+            if not free:
                 dest[i], n_local = n_local, n_local + 1
             else:
                 dest[i] = min(free)
@@ -767,8 +770,8 @@ class GpuEngine(LevelledNetlist):
             plan[i]["out_slot"] = int(table[i]["out"]) if held[i] else 0
         if len(inputs) > cls.RES_MAX_IN or n_local > cls.RES_MAX_LOCAL:
             return None
-        ct = 9408                                     # 9 x 29-bit rows of 261 values, padded
-        smem = (2 * 2 * len(inputs) + 2 * n_local) * ct + 2 * 13824 + 2 * 2304 + 1024
+        ct, W = 9408, 3                               # ciphertext bytes; lanes per group (RES_W)
+        smem = (W * len(inputs) + W * n_local) * ct + 2 * 13824 + 2 * 2304 + 1024
         if smem > cls.RES_SMEM_LIMIT:
             return None
         return plan, np.asarray(inputs, dtype=np.uint32), n_local

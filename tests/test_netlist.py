@@ -326,7 +326,8 @@ def _replay_resident(eng, prog, plan, inputs, n_local):
 
 def test_resident_plan_cfg1_and_random_programs():
     """Lane-resident plans (GpuEngine._resident_plan): the gate benchmark's XOR + AND uses 2
-    inputs and 6 local buffers (4 temporaries, 2 outputs) and reproduces the level replay;
+    inputs and 4 local buffers (3 for temporaries, 1 shared by the 2 outputs) and reproduces
+    the level replay;
     random small programs (temporaries reused, complemented operands, outputs also read
     later) agree too or are refused when they exceed the kernel's limits."""
     from paper_1611_08769_b200.gates import nor_, not_, or_, xnor_
@@ -338,7 +339,7 @@ def test_resident_plan_cfg1_and_random_programs():
     eng.flush()
     prog = eng.dry_programs[-1]
     plan, inputs, n_local = GpuEngine._resident_plan(prog)
-    assert (len(plan), len(inputs), n_local) == (6, 2, 6)
+    assert (len(plan), len(inputs), n_local) == (6, 2, 4)     # v into t1's buffer, x into y's
     assert plan["is_out"].sum() == 2
     store, outs = _replay_resident(eng, prog, plan, inputs, n_local)
     for h in (x, y):
