@@ -215,8 +215,18 @@ def time_program(prog, lanes, stream, steps, warmup, world, sampler=None):
 
 
 def level_launch_times(prog, lanes, stream, reps=3):
-    """Average duration (ms) of each level's single kernel launch (CUDA events)."""
+    """Average duration (ms) of each kernel launch of one run (CUDA events): one entry per level,
+    or a single entry for programs that run as one launch (resident, tiled, dataflow)."""
     import torch
+    if prog.launches == 1:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        prog.run(lanes)
+        e0.record(stream)
+        for _ in range(reps):
+            prog.run(lanes)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return [e0.elapsed_time(e1) / reps]
     out = []
     for lv in range(prog.n_levels):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -288,8 +298,10 @@ def bench_gates(args, world, rank, local):
         "traffic": traffic, "traffic_info": tinfo, "ok": ok, "setup_s": setup_s,
         "clocks": sampler.summary(), "kernel": scheme.ctx.kernel,
         "slots": eng._n_slots, "store_gb": eng._n_slots * lanes * scheme.ctx.ct_words * 4 / 1e9,
-        "schedule": comp.get("schedule", "levels") + (f" ({prog.tile_lanes}-lane chunks, one wavefront "
-                                                      f"dataflow launch per step)" if prog.tile_lanes else ""),
+        "schedule": comp.get("schedule", "levels") + (
+            f" ({prog.tile_lanes}-lane chunks, one wavefront dataflow launch per step)" if prog.tile_lanes
+            else " (one lane-resident launch per step: 3 lanes per CTA group, intermediates in shared memory)"
+            if comp.get("schedule") == "resident" else ""),
     }
     if args.e2e:
         res["e2e"] = e2e_gates(eng, scheme, prog, lanes, (a, b), (x, y), stream, args, world, bits)
@@ -495,7 +507,10 @@ def run_ours(args):
         return
     ms = res["ms"]
     value = res["nand_per_step"] * world / (ms / 1e3)
-    tiled = res["schedule"].startswith("tiled")
+    sched = res["schedule"].split()[0]
+    kernel = {"resident": "fhegpu::tc::resident_tc_kernel<9,29,true,1>",
+              "tiled": "fhegpu::tc::level_tc_ws_kernel<9,29,true,1>"}.get(
+                  sched, "fhegpu::tc::level_tc_ws_kernel<9,29,true,2>")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -511,10 +526,10 @@ def run_ours(args):
             "kernel": res["kernel"], "schedule": res["schedule"], "decrypt_check": res["ok"],
             "store_gb": round(res["store_gb"], 1), "setup_s": round(res["setup_s"], 2),
         },
-        "roofline": {   # A-operand encoding template arg: 1 in dataflow launches, 2 in levels
+        "roofline": {   # the step's kernel (A-operand encoding: 1 resident / dataflow, 2 levels)
             "bound": "hbm", "achieved": res["achieved"], "peak": res["peak"], "unit": "GB/s",
             "frac": res["achieved"] / res["peak"], "traffic": res["traffic"],
-            "kernel": "fhegpu::tc::level_tc_ws_kernel<9,29,true,%d>" % (1 if tiled else 2),
+            "kernel": kernel,
             "algorithmic_bytes_per_nand": ALG_BYTES_PER_NAND_261,
             "level_launch_ms": [round(x, 4) for x in res["level_ms"]],
             "peak_source": res["peak_kind"],

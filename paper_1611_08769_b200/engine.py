@@ -691,6 +691,8 @@ class GpuEngine(LevelledNetlist):
             return self.schedule
         if self.dry_run or (self.params.k, self.params.ell) != (9, 29):
             return "levels"
+        if self.batch_size >= self.RESIDENT_MIN_LANES and self.ctx.kernel == "tcgen05" and self._resident_ok():
+            return "resident"
         C = self.TILE_LANES
         if self.batch_size % C or self.batch_size < 8 * C:
             return "queue" if self._pick_queue() else "levels"
@@ -725,56 +727,91 @@ class GpuEngine(LevelledNetlist):
         return len(np.unique(np.asarray(self._level, dtype=np.int64)[outs])) >= self.QUEUE_MIN_LEVELS
 
     RES_MAX_OPS, RES_MAX_IN, RES_MAX_LOCAL = 8, 4, 8       # tc_nand_resident.cuh limits
+    RESIDENT_MIN_LANES = 1024      # 'auto' runs small per-lane programs over this many lanes resident
     RES_SMEM_LIMIT = 227 * 1024
 
     @classmethod
-    def _resident_plan(cls, prog):
-        """Per-lane plan of a small level-compiled program for fhegpu_prog_set_resident, or None.
-
-        Gates keep the level order; an operand produced in the program is read from the local
-        buffer its producer wrote, other operands are program inputs (their store slots).
-        Outputs (nodes still held after the program) get buffers of their own and are stored;
-        a temporary's buffer is reused once every reader of its value precedes the writer."""
-        table, nodes, held = prog["ops"], prog["nodes"], prog["held"]
-        n = len(table)
-        if n == 0 or n > cls.RES_MAX_OPS:
-            return None
+    def _resident_layout(cls, nodes, held):
+        """Buffer layout of a per-lane program (gates in level order; nodes (n, 3) = left,
+        right, out node ids; held: outputs still referenced after the program): per gate the
+        producer of each operand (-1: program input), its destination buffer, the input nodes
+        in first-use order and the number of buffers.  A buffer is free for gate i once every
+        reader of its value is gate i or earlier (a gate's builders read before its epilogue
+        writes); outputs and temporaries keep to buffers of their own kind (the kernel orders
+        output writes after earlier stores)."""
+        n = len(nodes)
         producer = {int(nd): i for i, nd in enumerate(nodes[:, 2])}
         last_read = np.full(n, -1)
         for i in range(n):
             for nd in nodes[i, :2]:
                 if int(nd) in producer:
                     last_read[producer[int(nd)]] = i
+        prods, dest, inputs, holder, n_local = [], [0] * n, [], {}, 0
+        for i in range(n):
+            pr = []
+            for nd in (int(nodes[i, 0]), int(nodes[i, 1])):
+                if nd in producer:
+                    pr.append(producer[nd])
+                else:
+                    pr.append(-1)
+                    if nd not in inputs:
+                        inputs.append(nd)
+            prods.append(pr)
+            free = [b for b, j in holder.items() if bool(held[j]) == bool(held[i]) and last_read[j] <= i]
+            dest[i] = min(free) if free else n_local
+            n_local += 0 if free else 1
+            holder[dest[i]] = i
+        return prods, dest, inputs, n_local
+
+    @classmethod
+    def _resident_fits(cls, n_ops, n_in, n_local) -> bool:
+        ct, W = 9408, 3                               # ciphertext bytes; lanes per group (RES_W)
+        smem = (W * n_in + W * n_local) * ct + 2 * 13824 + 2 * 2304 + 1024
+        return (0 < n_ops <= cls.RES_MAX_OPS and n_in <= cls.RES_MAX_IN and n_local <= cls.RES_MAX_LOCAL
+                and smem <= cls.RES_SMEM_LIMIT)
+
+    @classmethod
+    def _resident_plan(cls, prog):
+        """Per-lane plan of a small level-compiled program for fhegpu_prog_set_resident, or None.
+
+        Gates keep the level order; an operand produced in the program is read from the local
+        buffer its producer wrote, other operands are program inputs (their store slots);
+        outputs (nodes still held after the program) are stored (`_resident_layout`)."""
+        table, nodes, held = prog["ops"], prog["nodes"], prog["held"]
+        n = len(table)
+        if n == 0 or n > cls.RES_MAX_OPS:
+            return None
+        prods, dest, in_nodes, n_local = cls._resident_layout(nodes, held)
+        if not cls._resident_fits(n, len(in_nodes), n_local):
+            return None
         plan = np.zeros(n, dtype=RES_OP_DTYPE)
-        inputs, dest, holder, n_local = [], [0] * n, {}, 0     # holder: buffer -> gate whose value it has
+        in_slots = [0] * len(in_nodes)
         for i in range(n):
             for side, (kind, idx, prod) in enumerate((("lkind", "lidx", "lprod"), ("rkind", "ridx", "rprod"))):
-                nd, slot = int(nodes[i, side]), int(table[i]["left" if side == 0 else "right"])
-                if nd in producer:
-                    plan[i][kind], plan[i][idx], plan[i][prod] = 1, dest[producer[nd]], producer[nd]
+                p = prods[i][side]
+                if p >= 0:
+                    plan[i][kind], plan[i][idx], plan[i][prod] = 1, dest[p], p
                 else:
-                    if slot not in inputs:
-                        inputs.append(slot)
-                    plan[i][kind], plan[i][idx], plan[i][prod] = 0, inputs.index(slot), -1
-            # a buffer is free for gate i once every reader of its value is gate i or earlier (a
-            # gate's builders read before its epilogue writes); outputs and temporaries keep to
-            # buffers of their own kind (the kernel orders output writes after earlier stores)
-            free = [b for b, j in holder.items() if bool(held[j]) == bool(held[i]) and last_read[j] <= i]
-            if not free:
-                dest[i], n_local = n_local, n_local + 1
-            else:
-                dest[i] = min(free)
-            holder[dest[i]] = i
+                    k = in_nodes.index(int(nodes[i, side]))
+                    in_slots[k] = int(table[i]["left" if side == 0 else "right"])
+                    plan[i][kind], plan[i][idx], plan[i][prod] = 0, k, -1
             plan[i]["dest"], plan[i]["is_out"] = dest[i], int(held[i])
             plan[i]["flags"] = int(table[i]["flags"]) & 3
             plan[i]["out_slot"] = int(table[i]["out"]) if held[i] else 0
-        if len(inputs) > cls.RES_MAX_IN or n_local > cls.RES_MAX_LOCAL:
-            return None
-        ct, W = 9408, 3                               # ciphertext bytes; lanes per group (RES_W)
-        smem = (W * len(inputs) + W * n_local) * ct + 2 * 13824 + 2 * 2304 + 1024
-        if smem > cls.RES_SMEM_LIMIT:
-            return None
-        return plan, np.asarray(inputs, dtype=np.uint32), n_local
+        return plan, np.asarray(in_slots, dtype=np.uint32), n_local
+
+    def _resident_ok(self) -> bool:
+        """The pending program as a lane-resident launch fits the kernel's limits (checked on
+        the node structure before slots are assigned)."""
+        n = len(self._pending_ops) // 5
+        if n == 0 or n > self.RES_MAX_OPS or self.keep_all:
+            return False
+        ops = np.asarray(self._pending_ops, dtype=np.int64).reshape(-1, 5)
+        order = np.argsort(np.asarray(self._level, dtype=np.int64)[ops[:, 4]], kind="stable")
+        ops = ops[order]
+        held = np.asarray(self._refs, dtype=np.int64)[ops[:, 4]] > 0
+        _, _, in_nodes, n_local = self._resident_layout(ops[:, [0, 2, 4]], held)
+        return self._resident_fits(n, len(in_nodes), n_local)
 
     @staticmethod
     def _tile(prog, K, lanes_per_chunk=1, skew=0, window=2048, ring=0, t_base=0):

@@ -245,8 +245,9 @@ def test_tiled_ring_temporaries_replay_and_war_order():
 
 
 def test_auto_schedule_policy():
-    """'auto': tiled only for wide (batch % 128 == 0, >= 1024 lanes), shallow (<= 32 levels)
-    programs on the tcgen05 geometry whose store fits; levels otherwise."""
+    """'auto' on the tcgen05 geometry: resident for small per-lane programs (<= 8 gates) over
+    >= 1024 lanes; tiled for wide (batch % 128 == 0, >= 1024 lanes), shallow (<= 32 levels)
+    programs whose store fits; levels otherwise."""
     from paper_1611_08769_b200 import and_, xor_
 
     def pick(lanes, params=DEFAULT_PARAMS, depth=1, kernel="tcgen05"):
@@ -258,10 +259,13 @@ def test_auto_schedule_policy():
         eng.scheme._ctx = type("Ctx", (), {"kernel": kernel})()   # stand-in device context
         return eng._pick_schedule()
 
-    assert pick(4096) == "tiled"
-    assert pick(1024) == "tiled"
-    assert pick(512) == "levels"                  # too narrow to fill chunks
-    assert pick(4000) == "levels"                 # not a multiple of the chunk
+    assert pick(4096) == "resident"               # one XOR + AND per lane: 6 gates
+    assert pick(1024) == "resident"
+    assert pick(4000) == "resident"               # a partial last lane group is fine
+    assert pick(4096, DEFAULT0_PARAMS, depth=2) == "tiled"   # 12 gates per lane
+    assert pick(1024, DEFAULT0_PARAMS, depth=2) == "tiled"
+    assert pick(512) == "levels"                  # too narrow to fill the SMs
+    assert pick(4000, DEFAULT0_PARAMS, depth=2) == "levels"  # not a multiple of the tiled chunk
     assert pick(4096, EXACT_PARAMS) == "levels"   # no warp-specialised kernel for N = 51
     assert pick(4096, DEFAULT0_PARAMS, depth=12) == "levels"   # 36 levels: hop bound
     assert pick(4096, kernel="simt") == "levels"  # dataflow launches need the tcgen05 kernel

@@ -5,4 +5,4 @@ python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tai
 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo bench rc=$?
 cat gpurun_out/bench_default.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv python bench.py > gpurun_out/ncu_launch.log 2>&1; echo launches rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:level_tc_ws --launch-skip 1 --launch-count 1 -o gpurun_out/ws_full python tools/ncu_probe.py 131072 > gpurun_out/ncu_full.log 2>&1; echo full rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'resident_tc|level_tc_ws' --launch-skip 1 --launch-count 1 -o gpurun_out/ws_full python tools/ncu_probe.py 131072 > gpurun_out/ncu_full.log 2>&1; echo full rc=$?
