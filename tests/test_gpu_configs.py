@@ -201,33 +201,38 @@ def test_tiled_schedule_equals_levels_bit_exact():
     assert np.array_equal(outs["levels"], outs["tiled"])
 
 
-def test_tiled_incremental_flushes_equal_levels():
-    """Two chained tiled programs (the second consumes the first's outputs, with its own ring
-    of temporaries above every live slot) equal the level schedule bit for bit."""
+@pytest.mark.parametrize("schedule", ["tiled", "resident"])
+def test_chained_flushes_equal_levels(schedule):
+    """Two chained programs (the second consumes the first's outputs; tiled: its own ring of
+    temporaries above every live slot; resident: its own per-lane plan) equal the level
+    schedule bit for bit."""
     scheme = GswScheme(DEFAULT0_PARAMS)                # depth 5 > DEFAULT's budget of 3
     keys = scheme.keygen(2)
     bits = np.random.default_rng(4).integers(0, 2, (2048, 3))
     res = {}
-    for schedule in ("levels", "auto"):
+    for sched in ("levels", schedule):
         eng = GpuEngine(scheme, keys=keys, rng=np.random.default_rng(2), batch_size=2048,
-                        device_encrypt=True, schedule=schedule)
+                        device_encrypt=True, schedule=sched)
         a, b, c = eng.input_block(bits)
         x, y = xor_(a, b), and_(a, b)
         p1 = eng.flush()
         z, w = xor_(x, c), and_(y, c)                 # second program on the first's outputs
         p2 = eng.flush()
-        if schedule == "auto":
+        if sched == "tiled":
             assert p1.tile_lanes == 128 and p2.tile_lanes == 128
-        res[schedule] = eng.node_values([x, y, z, w])
+        elif sched == "resident":
+            assert p1.launches == 1 and p2.launches == 1
+        res[sched] = eng.node_values([x, y, z, w])
         got = eng.read_back_bits([z, w])
         assert (got[0] == (bits[:, 0] ^ bits[:, 1] ^ bits[:, 2])).all()
         assert (got[1] == (bits[:, 0] & bits[:, 1] & bits[:, 2])).all()
-    assert np.array_equal(res["levels"], res["auto"])
+    assert np.array_equal(res["levels"], res[schedule])
 
 
 def test_cfg1_full_size_every_lane_decrypts():
-    """configs[1] at full size (2^20 pairs, default tiled schedule, device encryption with the
-    cfg1 seeds): every one of the 2^21 output ciphertexts decrypts to the right bit."""
+    """configs[1] at full size (2^20 pairs, the default lane-resident schedule with a partial
+    last 3-lane group, device encryption with the cfg1 seeds): every one of the 2^21 output
+    ciphertexts decrypts to the right bit."""
     scheme = GswScheme(DEFAULT_PARAMS)
     keys = scheme.keygen(1)
     rng = np.random.default_rng(1)
@@ -236,7 +241,7 @@ def test_cfg1_full_size_every_lane_decrypts():
     a, b = eng.input_block(bits)
     x, y = xor_(a, b), and_(a, b)
     prog = eng.flush()
-    assert prog.tile_lanes == 128 and prog.launches == 1
+    assert eng.last_compile["schedule"] == "resident" and prog.launches == 1
     got = eng.read_back_bits([x, y])
     assert (got[0] == (bits[:, 0] ^ bits[:, 1])).all()
     assert (got[1] == (bits[:, 0] & bits[:, 1])).all()
