@@ -26,7 +26,7 @@ order = [5, 6, 7, 8, 2, 3, 4, 12, 13, 14, 9, 10, 11]
 print("slot(gate,lane) " + " ".join(f"{names[e]:>9s}" for e in order))
 gates = ["t1", "t2", "u", "v", "y", "x"]
 for i in range(16, 40):
-    print(f"{i:3d} {gates[(i % 12) // 2]:>2s}{i % 2}     " + " ".join(f"{tr[i, e] - t0:9d}" for e in order))
+    print(f"{i:3d} {gates[(i % 18) // 3]:>2s}{i % 3}     " + " ".join(f"{tr[i, e] - t0:9d}" for e in order))
 for e, nm in ((8, "builder done"), (4, "MMA commit"), (10, "epilogue barrier"), (11, "epi_done publish")):
     print(f"{nm} period (median cycles): {np.median(np.diff(tr[8:56, e]))}")
 raw = tr[8:56, 6] - tr[8:56, 5]
