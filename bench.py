@@ -40,6 +40,8 @@ METRIC = "encrypted gates/s (homomorphic NAND, reference-counted) on B200"
 UNIT = "NAND/s"
 PAIRS_FULL = 1 << 20
 ALG_BYTES_PER_NAND_261 = 3 * math.ceil(261 * 261 / 8)   # 25,548 B
+MMA_MAC_SLOTS_PER_NAND = 2 * 9 * 128 * 48 * 32 + 9 * 64 * 48 * 32   # 4,423,680 (tc_nand_ws.cuh)
+I8_DENSE_TOPS = 4500.0                                   # B200 dense int8 spec
 
 
 def _fft_roofline(nand_per_s: float, n_ct: int) -> dict:
@@ -534,6 +536,16 @@ def run_ours(args):
             "level_launch_ms": [round(x, 4) for x in res["level_ms"]],
             "peak_source": res["peak_kind"],
         },
+        # fused multi-gate launches (resident) move fewer bytes than the per-gate model: report
+        # the tensor pipe too -- executed i8 MAC slots of a gate's 27 MMAs (2 tiles x 9 K-steps
+        # of 128 x 48 x 32, 9 tail K-steps of 64 x 48 x 32) against the dense i8 spec peak
+        "roofline_compute": {
+            "bound": "tensor", "unit": "TOPS",
+            "achieved": 2 * MMA_MAC_SLOTS_PER_NAND * value / world / 1e12,
+            "peak": I8_DENSE_TOPS, "frac": 2 * MMA_MAC_SLOTS_PER_NAND * value / world / 1e12 / I8_DENSE_TOPS,
+            "peak_source": "spec (B200 dense int8, not measured here)",
+            "note": "per NAND 4,423,680 executed MAC slots (N padded 36 -> 48, tail M = 64 for 5 rows); "
+                    "a kind::i8 MMA with N <= 64 issues no faster than every ~46 cycles (DESIGN.md 4.1)"},
         "gpu_launches": res["launches_per_step"] * args.steps,
         "clocks": res["clocks"],
     }
