@@ -44,6 +44,41 @@ struct ResOp {
   uint32_t out_slot;                 // store slot of a program output
 };
 
+// A operand of one row, words [W0, W1): bits -> K slots, tcgen05.st into TMEM (4 words = one
+// 32-column store, a remainder word = one 8-column store).
+template <int K, int W0, int W1, int ENC>
+__device__ __forceinline__ void build_a_words(const uint32_t *v1, int row, int row_blk, int row_bit, bool comp,
+                                              uint32_t q, uint32_t a_addr) {
+  uint32_t words[W1 - W0];
+#pragma unroll
+  for (int i = W0; i < W1; ++i) words[i - W0] = v1[row * K + i];
+  if (comp) {
+#pragma unroll
+    for (int i = W0; i < W1; ++i) words[i - W0] = sub_mod(i == row_blk ? (1u << row_bit) : 0u, words[i - W0], q);
+  }
+#pragma unroll
+  for (int w0 = W0; w0 < W1; w0 += 4) {
+    if (w0 + 4 <= W1) {
+      uint32_t sp[32];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t one[8];
+        spread_word_sr<ENC>(words[w0 + j - W0], one);
+#pragma unroll
+        for (int x = 0; x < 8; ++x) sp[8 * j + x] = one[x];
+      }
+      tmem_st32(a_addr + 8 * w0, sp);
+    } else {
+#pragma unroll
+      for (int w = w0; w < W1; ++w) {
+        uint32_t sp[8];
+        spread_word_sr<ENC>(words[w - W0], sp);
+        tmem_st8(a_addr + 8 * w, sp);
+      }
+    }
+  }
+}
+
 template <int K, int ELL>
 struct GeoRes {
   using W = GeoWS<K, ELL, true, 1, false>;
@@ -56,9 +91,15 @@ struct GeoRes {
 #define FHEGPU_RES_EPI_SPLIT 1   // 2: 16 epilogue warps (72 registers: slower, measured)
 #endif
   // epilogue warps: 8 x SPLIT (SPLIT = 2: two threads per row, values 0-4 and 5-8)
+#ifndef FHEGPU_RES_BSPLIT
+#define FHEGPU_RES_BSPLIT 1    // 2: two builder threads per A row (words 0-3 / 4-8)
+#endif
   static constexpr int EPI_SPLIT = FHEGPU_RES_EPI_SPLIT;
+  static constexpr int BSPLIT = FHEGPU_RES_BSPLIT;
   static constexpr int NE_WARPS = 8 * EPI_SPLIT;
-  static constexpr int THREADS = 32 * (3 + W::NB_WARPS + NE_WARPS);
+  static constexpr int NB_WARPS = 4 * W::MT * BSPLIT;
+  static constexpr int WARP_EPI0 = 3 + NB_WARPS;
+  static constexpr int THREADS = 32 * (3 + NB_WARPS + NE_WARPS);
   static constexpr int OFF_BAR_SIZE = 64 * 8;
   // runtime layout (host computes the same): inputs | locals | B x 2 | TA x 2 | barriers | plan
   __host__ __device__ static uint32_t off_local(uint32_t n_in) { return RES_NSETS * RES_W * n_in * CT_BYTES; }
@@ -176,8 +217,8 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&in_full[i], 1);
-      mbar_init(&in_empty[i], G::NB_WARPS);
-      mbar_init(&op_full[i], G::NB_WARPS);
+      mbar_init(&in_empty[i], R::NB_WARPS);
+      mbar_init(&op_full[i], R::NB_WARPS);
       mbar_init(&main_done[i], 1);
       mbar_init(&a_free[i], 1);
       mbar_init(&d_free[i], R::NE_WARPS);
@@ -305,20 +346,23 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
         if (lane == 0) trace_ev(p, t, 14);
       }
     }
-  } else if (warp < G::WARP_EPI0) {
+  } else if (warp < R::WARP_EPI0) {
     // ------------------------------ operand builders ------------------------------
     const int bt = tid - 32 * G::WARP_BUILD0;
     const int bw = bt >> 5;
     const int quad = warp & 3;
-    const int tile = bw >> 2;
+    const int tile = (bw >> 2) % G::MT;
+    const int part = (bw >> 2) / G::MT;          // BSPLIT = 2: words 0-3 (part 0) or 4-8 (part 1)
     const int row = 128 * tile + 32 * quad + lane;
     const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
     const int row_blk = row / ELL, row_bit = row - row_blk * ELL;
-    constexpr int B_ROWS = (G::KB + 128 * G::MT - 1) / (128 * G::MT);
+    constexpr int NBT = 128 * G::MT * R::BSPLIT;
+    const int tb = R::BSPLIT == 1 ? bt : bt - 128 * G::MT;   // tail-A thread index (part 1)
+    constexpr int B_ROWS = (G::KB + NBT - 1) / NBT;
     int b_src[B_ROWS], b_dst[B_ROWS], b_w[B_ROWS], b_j[B_ROWS];
 #pragma unroll
     for (int x = 0; x < B_ROWS; ++x) {
-      const int kr = bt + x * 128 * G::MT;
+      const int kr = bt + x * NBT;
       const int ww = kr >> 5, kk = kr & 31;
       const int j = 8 * (kk & 3) + (kk >> 2);
       const bool ok = kr < G::KB && j < ELL;
@@ -352,39 +396,17 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       const bool comp1 = si.bits & 1u, comp2 = si.bits & 2u;
       uint8_t *bb = s_b + b * R::B_BYTES;
       {
-        uint32_t words[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) words[i] = v1[row * K + i];
-        if (comp1) {
-#pragma unroll
-          for (int i = 0; i < K; ++i) words[i] = sub_mod(i == row_blk ? (1u << row_bit) : 0u, words[i], p.q);
-        }
         const uint32_t a_addr = tmem_base + b * G::BUF_COLS + lane_off + G::D_COLS + tile * 8 * K;
-#pragma unroll
-        for (int w0 = 0; w0 < K; w0 += 4) {
-          if (w0 + 4 <= K) {
-            uint32_t sp[32];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint32_t one[8];
-              spread_word_sr<ENC>(words[w0 + j], one);
-#pragma unroll
-              for (int x = 0; x < 8; ++x) sp[8 * j + x] = one[x];
-            }
-            tmem_st32(a_addr + 8 * w0, sp);
-          } else {
-#pragma unroll
-            for (int ww = w0; ww < K; ++ww) {
-              uint32_t sp[8];
-              spread_word_sr<ENC>(words[ww], sp);
-              tmem_st8(a_addr + 8 * ww, sp);
-            }
-          }
+        if constexpr (R::BSPLIT == 1) {
+          build_a_words<K, 0, K, ENC>(v1, row, row_blk, row_bit, comp1, p.q, a_addr);
+        } else {
+          if (part == 0) build_a_words<K, 0, 4, ENC>(v1, row, row_blk, row_bit, comp1, p.q, a_addr);
+          else build_a_words<K, 4, K, ENC>(v1, row, row_blk, row_bit, comp1, p.q, a_addr);
         }
       }
       if constexpr (G::TAIL > 0) {
-        if (bt < G::TAIL * K) {
-          const int m = bt / K, ww = bt - m * K;
+        if (tb >= 0 && tb < G::TAIL * K) {
+          const int m = tb / K, ww = tb - m * K;
           const int rr = G::MMA_ROWS + m;
           uint32_t v = v1[rr * K + ww];
           if (comp1) v = sub_mod(ww == rr / ELL ? (1u << (rr % ELL)) : 0u, v, p.q);
@@ -428,7 +450,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
     }
   } else {
     // ------------------------------ epilogue, into the gate's local buffer ------------------------------
-    const int et = tid - 32 * G::WARP_EPI0;
+    const int et = tid - 32 * R::WARP_EPI0;
     const int ew = et >> 5;
     const int quad = warp & 3;
     const int tile = (ew >> 2) & 1;
