@@ -105,6 +105,26 @@ def test_cfg1_sample_pairs_bit_exact():
     assert eng.nand_count == 6 and eng.max_depth == 3
 
 
+@pytest.mark.parametrize("schedule", ["auto", "tiled"])
+def test_cfg1_sample_outputs_default_schedules(schedule):
+    """The same 4096 pairs on the schedules the benchmark uses ('auto' = lane-resident for the
+    XOR + AND program, and tiled): every output ciphertext equals the reference's."""
+    ref = golden_json("cts_cfg1.json")
+    pairs = ref["pairs"]
+    scheme = GswScheme(DEFAULT_PARAMS)
+    keys = scheme.keygen(1)
+    rng = np.random.default_rng(1)
+    bits = rng.integers(0, 2, (1 << 20, 2))
+    eng = GpuEngine(scheme, keys=keys, rng=rng, batch_size=pairs, device_encrypt=True, schedule=schedule)
+    a, b = eng.input_block(bits[:pairs])
+    x, y = xor_(a, b), and_(a, b)
+    eng.flush()
+    assert eng.last_compile["schedule"] == ("resident" if schedule == "auto" else "tiled")
+    vx, vy = eng.node_values([x, y])
+    assert [digest.digest_compact(v) for v in vx] == ref["xor_digests"]
+    assert [digest.digest_compact(v) for v in vy] == ref["and_digests"]
+
+
 def test_cfg4_all_lanes_outputs():
     """1024 signals as lanes (device encryption, per-lane generators): all outputs bit-exact."""
     eng, out, vals = run_fft_config("cfg4", device_encrypt=True, keep_all=False, lanes=1024)
