@@ -207,6 +207,24 @@ def test_random_deep_circuit_queue_equals_levels():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("lanes", [1, 2, 5])
+def test_resident_tiny_batches(lanes):
+    """Lane-resident launches with fewer lanes than one 3-lane group or a partial last group."""
+    from paper_1611_08769_b200 import DEFAULT_PARAMS, GpuEngine, GswScheme
+    scheme = GswScheme(DEFAULT_PARAMS)
+    keys = scheme.keygen(7)
+    bits = np.random.default_rng(lanes).integers(0, 2, (lanes, 2))
+    eng = GpuEngine(scheme, keys=keys, rng=np.random.default_rng(3), batch_size=lanes, schedule="resident",
+                    device_encrypt=True)
+    a, b = eng.input_block(bits)
+    x, y = xor_(a, b), and_(a, b)
+    prog = eng.flush()
+    assert prog.launches == 1
+    got = eng.read_back_bits([x, y])
+    assert (got[0] == (bits[:, 0] ^ bits[:, 1])).all() and (got[1] == (bits[:, 0] & bits[:, 1])).all()
+
+
+@pytest.mark.gpu
 def test_queue_tiny_programs_and_fallback():
     """Queue launches with fewer items than SMs (a 3-gate program, one lane) and a queue
     request on a parameter set without the warp-specialised kernel (EXACT: level launches)."""
