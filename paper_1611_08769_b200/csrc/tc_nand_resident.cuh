@@ -97,9 +97,14 @@ struct GeoRes {
   static constexpr int EPI_SPLIT = FHEGPU_RES_EPI_SPLIT;
   static constexpr int BSPLIT = FHEGPU_RES_BSPLIT;
   static constexpr int NE_WARPS = 8 * EPI_SPLIT;
+#ifndef FHEGPU_RES_BCOPY_WARPS
+#define FHEGPU_RES_BCOPY_WARPS 4   // warps that copy the B operand (0: the A builders do it too)
+#endif
   static constexpr int NB_WARPS = 4 * W::MT * BSPLIT;
-  static constexpr int WARP_EPI0 = 3 + NB_WARPS;
-  static constexpr int THREADS = 32 * (3 + NB_WARPS + NE_WARPS);
+  static constexpr int NBC_WARPS = FHEGPU_RES_BCOPY_WARPS;
+  static constexpr int WARP_BC0 = 3 + NB_WARPS;
+  static constexpr int WARP_EPI0 = WARP_BC0 + NBC_WARPS;
+  static constexpr int THREADS = 32 * (3 + NB_WARPS + NBC_WARPS + NE_WARPS);
   static constexpr int OFF_BAR_SIZE = 64 * 8;
   // runtime layout (host computes the same): inputs | locals | B x 2 | TA x 2 | barriers | plan
   __host__ __device__ static uint32_t off_local(uint32_t n_in) { return RES_NSETS * RES_W * n_in * CT_BYTES; }
@@ -217,8 +222,8 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&in_full[i], 1);
-      mbar_init(&in_empty[i], R::NB_WARPS);
-      mbar_init(&op_full[i], R::NB_WARPS);
+      mbar_init(&in_empty[i], R::NB_WARPS + R::NBC_WARPS);
+      mbar_init(&op_full[i], R::NB_WARPS + R::NBC_WARPS);
       mbar_init(&main_done[i], 1);
       mbar_init(&a_free[i], 1);
       mbar_init(&d_free[i], R::NE_WARPS);
@@ -346,6 +351,65 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
         if (lane == 0) trace_ev(p, t, 14);
       }
     }
+  } else if (warp >= R::WARP_BC0 && warp < R::WARP_EPI0) {
+    // ------------------------------ B operand copiers ------------------------------
+    // V2 rows into the MN-major canonical layout (digits = the value's bytes), off the A
+    // builders' critical path (measured: the builders pace the resident pipeline)
+    const int bc = tid - 32 * R::WARP_BC0;
+    constexpr int NBT = 32 * (R::NBC_WARPS > 0 ? R::NBC_WARPS : 1);
+    constexpr int B_ROWS = (G::KB + NBT - 1) / NBT;
+    int b_src[B_ROWS], b_dst[B_ROWS], b_w[B_ROWS], b_j[B_ROWS];
+#pragma unroll
+    for (int x = 0; x < B_ROWS; ++x) {
+      const int kr = bc + x * NBT;
+      const int ww = kr >> 5, kk = kr & 31;
+      const int j = 8 * (kk & 3) + (kk >> 2);
+      b_src[x] = kr < G::KB && j < ELL ? (ww * ELL + j) * K : -1;
+      b_dst[x] = (kr >> 3) * G::LBO + (kr & 7) * 16;
+      b_w[x] = ww;
+      b_j[x] = j;
+    }
+    SlotPos pos;
+    const uint32_t in_set_words = W * n_in * R::CT_WORDS;
+    for (uint32_t t = 0; t < n_slots; ++t, pos.next(S, W)) {
+      const uint32_t g = pos.g, r = pos.r;
+      const uint32_t set = RES_NSETS == 2 ? g & 1u : 0u, ph = RES_NSETS == 2 ? g >> 1 : g;
+      const uint32_t b = t & 1u, u = t >> 1;
+      if (r == 0) mbar_wait(&in_full[set], ph & 1u);
+      const SlotInfo si = s_slot[r];
+      mbar_wait(&a_free[b], (u & 1u) ^ 1u);        // B(b) was last read by the MMAs of slot t - 2
+      if (si.dep_r != 0xFF) mbar_wait(&out_ready[si.dep_r], g & 1u);
+      const uint32_t *v2 = ((si.bits & 16u) ? s_loc : s_inb + set * in_set_words) + si.v2;
+      const bool comp2 = si.bits & 2u;
+      uint8_t *bb = s_b + b * R::B_BYTES;
+#pragma unroll
+      for (int x = 0; x < B_ROWS; ++x) {
+        if (b_src[x] < 0) continue;
+        uint32_t vals[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) vals[i] = v2[b_src[x] + i];
+        if (comp2) {
+#pragma unroll
+          for (int i = 0; i < K; ++i) vals[i] = sub_mod(i == b_w[x] ? (1u << b_j[x]) : 0u, vals[i], p.q);
+        }
+        uint8_t *dst = bb + b_dst[x];
+#pragma unroll
+        for (int ch = 0; ch < G::NCH; ++ch) {
+          uint4 val;
+          val.x = 4 * ch + 0 < K ? vals[4 * ch + 0] : 0u;
+          val.y = 4 * ch + 1 < K ? vals[4 * ch + 1] : 0u;
+          val.z = 4 * ch + 2 < K ? vals[4 * ch + 2] : 0u;
+          val.w = 4 * ch + 3 < K ? vals[4 * ch + 3] : 0u;
+          *reinterpret_cast<uint4 *>(dst + ch * G::SBO) = val;
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&op_full[b]);
+        if (si.bits & 32u) mbar_arrive(&in_empty[set]);
+      }
+    }
   } else if (warp < R::WARP_EPI0) {
     // ------------------------------ operand builders ------------------------------
     const int bt = tid - 32 * G::WARP_BUILD0;
@@ -419,7 +483,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       }
 #pragma unroll
       for (int x = 0; x < B_ROWS; ++x) {
-        if (b_src[x] < 0) continue;
+        if (R::NBC_WARPS > 0 || b_src[x] < 0) continue;   // the B copiers do it
         uint32_t vals[K];
 #pragma unroll
         for (int i = 0; i < K; ++i) vals[i] = v2[b_src[x] + i];
