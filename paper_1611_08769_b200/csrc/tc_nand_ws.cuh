@@ -287,13 +287,16 @@ struct GeoWS {
   static constexpr int MAIN_BYTES = MMA_ROWS * K * 4;       // rows stored by the bulk copy
   static constexpr int D_COLS = B::D_COLS;                 // per buffer
   static constexpr int BUF_COLS = 256;                      // buffer stride in TMEM columns
-  static constexpr int NB_WARPS = 4 * MT, NE_WARPS = 4 * MT;
+#ifndef FHEGPU_WS_BCOPY
+#define FHEGPU_WS_BCOPY 4      // ready-queue launches: warps dedicated to the B copy (cfg2/cfg3
+#endif                         // +4%; level and tiled launches keep the builders' copy: -6% / -1%)
+  static constexpr int NB_WARPS = 4 * MT, NE_WARPS = 4 * MT, NBC_WARPS = Q ? FHEGPU_WS_BCOPY : 0;
   static constexpr int WARP_TAIL = 0, WARP_PROD = 1, WARP_MMA = 2;
-  static constexpr int WARP_BUILD0 = 3, WARP_EPI0 = 3 + NB_WARPS;
+  static constexpr int WARP_BUILD0 = 3, WARP_BC0 = 3 + NB_WARPS, WARP_EPI0 = WARP_BC0 + NBC_WARPS;
   // ready-queue launches (Q): a fetcher warp (pops ready items) and a signaler warp (retires
   // completed items to their consumers) after the epilogue warps
-  static constexpr int WARP_FETCH = 3 + NB_WARPS + NE_WARPS, WARP_SIG = WARP_FETCH + 1;
-  static constexpr int THREADS = 32 * (3 + NB_WARPS + NE_WARPS + (Q ? 2 : 0));
+  static constexpr int WARP_FETCH = WARP_EPI0 + NE_WARPS, WARP_SIG = WARP_FETCH + 1;
+  static constexpr int THREADS = 32 * (3 + NB_WARPS + NBC_WARPS + NE_WARPS + (Q ? 2 : 0));
 // ready-queue launches: operand stages, fetch-ring entries, queue pops per fetch batch
 // (swept on cfg2/cfg3: 5/4/2; one pop per batch leaves the fetcher latency-bound, deeper
 // rings put more items ahead of each dependency hop)
@@ -313,7 +316,7 @@ struct GeoWS {
   // also latency on the dependency chain; their operands are mostly L2 hits)
   static constexpr int S_IN = Q ? FHEGPU_Q_STAGES : FHEGPU_STAGES;
   static constexpr int N_OUT = 3;                           // output staging buffers
-  static constexpr uint32_t OP_ARRIVALS = NB_WARPS;
+  static constexpr uint32_t OP_ARRIVALS = NB_WARPS + NBC_WARPS;
   // idesc: S32 accumulator, A s8 (bits 7-9 = 1) or u8 (encoding 2), B u8, A K-major,
   // B MN-major, N>>3, M>>4
   static constexpr uint32_t IDESC = (2u << 4) | (AEnc<ENC>::A_FMT << 7) | (1u << 16) |
@@ -784,6 +787,64 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
         }
       }
     }
+  } else if (warp >= G::WARP_BC0 && warp < G::WARP_EPI0) {
+    // ------------------------------ B operand copiers (FHEGPU_WS_BCOPY) ------------------------------
+    const int bc = tid - 32 * G::WARP_BC0;
+    constexpr int NBT = 32 * (G::NBC_WARPS > 0 ? G::NBC_WARPS : 1);
+    constexpr int B_ROWS = (G::KB + NBT - 1) / NBT;
+    int b_src[B_ROWS], b_dst[B_ROWS], b_w[B_ROWS], b_j[B_ROWS];
+#pragma unroll
+    for (int x = 0; x < B_ROWS; ++x) {
+      const int kr = bc + x * NBT;
+      const int w = kr >> 5, kk = kr & 31;
+      const int j = 8 * (kk & 3) + (kk >> 2);
+      b_src[x] = kr < G::KB && j < ELL ? (w * ELL + j) * K : -1;
+      b_dst[x] = (kr >> 3) * G::LBO + (kr & 7) * 16;
+      b_w[x] = w;
+      b_j[x] = j;
+    }
+    uint32_t t = 0;
+    for (uint32_t item = blockIdx.x; Q || item < n_items; item += gridDim.x, ++t) {
+      const uint32_t s = t % G::S_IN, k = t / G::S_IN, b = t & 1u, u = t >> 1;
+      mbar_wait(&in_full[s], k & 1u);
+      if (Q && s_qitem[t % G::QR] == Q_END) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&op_full[b]);
+        break;
+      }
+      const uint32_t flags = s_flags[s];
+      mbar_wait(&a_free[b], (u & 1u) ^ 1u);            // B(b) was last read by the MMAs of t - 2
+      const uint32_t *v1 = s_in + s * 2 * G::CT_WORDS;
+      const uint32_t *v2 = (flags & 4u) ? v1 : v1 + G::CT_WORDS;
+      uint8_t *bb = s_b + b * G::B_BYTES;
+#pragma unroll
+      for (int x = 0; x < B_ROWS; ++x) {
+        if (b_src[x] < 0) continue;
+        uint32_t vals[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) vals[i] = v2[b_src[x] + i];
+        if (flags & 2u) {
+#pragma unroll
+          for (int i = 0; i < K; ++i) vals[i] = sub_mod(i == b_w[x] ? (1u << b_j[x]) : 0u, vals[i], p.q);
+        }
+        uint8_t *dst = bb + b_dst[x];
+#pragma unroll
+        for (int ch = 0; ch < G::NCH; ++ch) {
+          uint4 val;
+          val.x = 4 * ch + 0 < K ? vals[4 * ch + 0] : 0u;
+          val.y = 4 * ch + 1 < K ? vals[4 * ch + 1] : 0u;
+          val.z = 4 * ch + 2 < K ? vals[4 * ch + 2] : 0u;
+          val.w = 4 * ch + 3 < K ? vals[4 * ch + 3] : 0u;
+          *reinterpret_cast<uint4 *>(dst + ch * G::SBO) = val;
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&op_full[b]);
+        mbar_arrive(&in_empty[s]);
+      }
+    }
   } else if (warp < G::WARP_EPI0) {
     // ------------------------------ operand builders ------------------------------
     const int bt = tid - 32 * G::WARP_BUILD0;           // 0 .. 128*MT-1
@@ -875,7 +936,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
       // B: V2 rows copied into the MN-major canonical layout (digits = the value's bytes)
 #pragma unroll
       for (int x = 0; x < B_ROWS; ++x) {
-        if (b_src[x] < 0) continue;
+        if (G::NBC_WARPS > 0 || b_src[x] < 0) continue;   // FHEGPU_WS_BCOPY: the copy warps do it
         uint32_t vals[K];
 #pragma unroll
         for (int i = 0; i < K; ++i) vals[i] = v2[b_src[x] + i];
