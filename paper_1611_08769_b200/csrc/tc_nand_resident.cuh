@@ -482,8 +482,8 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
         }
       }
 #pragma unroll
-      for (int x = 0; x < B_ROWS; ++x) {
-        if (R::NBC_WARPS > 0 || b_src[x] < 0) continue;   // the B copiers do it
+      for (int x = 0; x < (R::NBC_WARPS > 0 ? 0 : B_ROWS); ++x) {   // else the B copiers do it
+        if (b_src[x] < 0) continue;
         uint32_t vals[K];
 #pragma unroll
         for (int i = 0; i < K; ++i) vals[i] = v2[b_src[x] + i];

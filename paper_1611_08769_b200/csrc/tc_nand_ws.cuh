@@ -935,8 +935,8 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
       }
       // B: V2 rows copied into the MN-major canonical layout (digits = the value's bytes)
 #pragma unroll
-      for (int x = 0; x < B_ROWS; ++x) {
-        if (G::NBC_WARPS > 0 || b_src[x] < 0) continue;   // FHEGPU_WS_BCOPY: the copy warps do it
+      for (int x = 0; x < (G::NBC_WARPS > 0 ? 0 : B_ROWS); ++x) {   // FHEGPU_WS_BCOPY: the copy warps do it
+        if (b_src[x] < 0) continue;
         uint32_t vals[K];
 #pragma unroll
         for (int i = 0; i < K; ++i) vals[i] = v2[b_src[x] + i];
