@@ -191,10 +191,10 @@ typedef struct {
 
 /* Opt-in lane-resident execution of a small per-lane program (<= 8 gates, <= 4 inputs, <= 8
  * local buffers; the gates in topological order): one launch in which every CTA runs the whole
- * program for 2 lanes at a time, loading the program inputs (store slots in_slots[]) once and
+ * program for 3 lanes at a time, loading the program inputs (store slots in_slots[]) once and
  * keeping every gate output in a shared-memory buffer of its lane; only is_out gates are stored.
- * A local buffer may be reused once every reader of its previous value precedes the writer in
- * the plan; output gates need buffers of their own.  Same results as fhegpu_prog_run's level
+ * A local buffer may be reused once every reader of its previous value is the writer or
+ * precedes it in the plan; output gates use buffers only outputs use.  Same results as fhegpu_prog_run's level
  * launches (which remain the fallback where no tcgen05 kernel applies); n_ops = 0 disables.
  * Replaces the reference's gate-by-gate evaluation (engine.py:168-178 -> fhe.py:325-341) for
  * independent lanes, e.g. the gate benchmark's XOR + AND (gates.py:9-34). */

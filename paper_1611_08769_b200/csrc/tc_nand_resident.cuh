@@ -4,17 +4,20 @@
 // The level / dataflow launches move every operand through L2 (2 x 9.4 KB per gate) and every
 // output back (9.4 KB): measured 1.55 uJ of the 4.6 uJ a gate costs above idle, at the board
 // power limit that sets the throughput.  Here a CTA takes W lanes at a time and
-// runs the whole per-lane program on them: the program's inputs are bulk-loaded once into a
-// double-buffered input set, every gate's output is written by the epilogue straight into a
+// runs the whole per-lane program on them: the program's inputs are bulk-loaded once into an
+// input set (released after the group's last input reader, so the next group's loads overlap
+// the rest of this one), every gate's output is written by the epilogue straight into a
 // shared-memory buffer of that lane (the operand of later gates), and only the program's
-// outputs are stored.  cfg1: 2 loads + 2 stores per 6 gates instead of 11 + 6.
+// outputs are stored.  cfg1: 2 loads + 2 stores per 6 gates instead of 11 + 6.  Four warps copy
+// the B operands so the A builders, the pipeline's pacer, only build A.
 //
 // Pipeline roles, TMEM double buffers, MMA sequence, A/B operand construction and the fold are
 // those of level_tc_ws_kernel (tc_nand_ws.cuh).  Slot t of a CTA is (group g, op o, lane w)
 // with t = g * S + o * W + w, S = n_ops * W: gates of one op for the W lanes back to back, ops
 // in the host's topological order, so a gate's producer is >= W slots earlier.  A builder
 // reading a gate output waits on that gate's mbarrier (out_ready), which the epilogue arrives on
-// once the output sits in its local buffer (one phase per lane group).
+// once the output sits in its local buffer (one phase per lane group) -- unless the producer is
+// >= 5 slots back, which the A-buffer handshake already implies (see the slot table setup).
 // Timeline probes (trace_ev, -DFHEGPU_TRACE=1 builds only): tools/timeline_resident.py.
 #pragma once
 
