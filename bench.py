@@ -510,7 +510,7 @@ def run_ours(args):
     ms = res["ms"]
     value = res["nand_per_step"] * world / (ms / 1e3)
     sched = res["schedule"].split()[0]
-    kernel = {"resident": "fhegpu::tc::resident_tc_kernel<9,29,true,2>",
+    kernel = {"resident": "fhegpu::tc::resident_tc_kernel<9,29,true,2,false>",
               "tiled": "fhegpu::tc::level_tc_ws_kernel<9,29,true,1>"}.get(
                   sched, "fhegpu::tc::level_tc_ws_kernel<9,29,true,2>")
     line = {

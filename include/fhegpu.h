@@ -193,6 +193,8 @@ typedef struct {
  * local buffers; the gates in topological order): one launch in which every CTA runs the whole
  * program for 3 lanes at a time, loading the program inputs (store slots in_slots[]) once and
  * keeping every gate output in a shared-memory buffer of its lane; only is_out gates are stored.
+ * The gates of a lane group run in the order of fhegpu_res_slot_order (a gate whose operand
+ * equals its lane's previous gate's reuses that operand's tensor-core staging).
  * A local buffer may be reused once every reader of its previous value is the writer or
  * precedes it in the plan; output gates use buffers only outputs use.  Same results as fhegpu_prog_run's level
  * launches (which remain the fallback where no tcgen05 kernel applies); n_ops = 0 disables.
@@ -200,6 +202,11 @@ typedef struct {
  * independent lanes, e.g. the gate benchmark's XOR + AND (gates.py:9-34). */
 int fhegpu_prog_set_resident(fhegpu_ctx *ctx, fhegpu_prog *prog, const fhegpu_res_op *plan, uint32_t n_ops,
                              const uint32_t *in_slots, uint32_t n_in, uint32_t n_local);
+/* The order in which a lane-resident launch runs the lanes x n_ops gates of one lane group
+ * (host only, no GPU): order[t] = gate | lane << 3 | 32 (left operand reused from slot t - 2) |
+ * 64 (right operand reused).  fhegpu_prog_set_resident uses it with lanes = 3; exposed for
+ * tests and tools.  lanes <= 4, lanes * n_ops <= 32. */
+int fhegpu_res_slot_order(const fhegpu_res_op *plan, uint32_t n_ops, uint32_t lanes, uint8_t *order);
 uint32_t fhegpu_prog_launches(const fhegpu_prog *prog);       /* launches one run issues */
 void fhegpu_prog_destroy(fhegpu_prog *prog);
 

@@ -67,6 +67,7 @@ SIGNATURES = [
     ("fhegpu_prog_set_queue", ctypes.c_int, [_P, _P, ctypes.c_int]),
     ("fhegpu_prog_set_resident", ctypes.c_int, [_P, _P, _P, ctypes.c_uint32, _P, ctypes.c_uint32,
                                                 ctypes.c_uint32]),
+    ("fhegpu_res_slot_order", ctypes.c_int, [_P, ctypes.c_uint32, ctypes.c_uint32, _P]),
     ("fhegpu_store_write_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     ("fhegpu_store_read_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     ("fhegpu_prog_run_host", ctypes.c_int, [_P, _P, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int,
@@ -128,6 +129,18 @@ def _check(rc: int, what: str):
     if rc != 0:
         msg = _lib.fhegpu_last_error().decode(errors="replace")
         raise DeviceError(f"{what} failed (code {rc}): {msg}")
+
+
+def res_slot_order(plan: np.ndarray, lanes: int = 3) -> np.ndarray:
+    """Slot order of a lane-resident group (fhegpu_res_slot_order; host only): one byte per slot,
+    gate | lane << 3 | 32 (left operand reused) | 64 (right operand reused)."""
+    if _lib is None:
+        load_library()
+    plan = np.ascontiguousarray(plan, dtype=RES_OP_DTYPE)
+    order = np.zeros(len(plan) * lanes, dtype=np.uint8)
+    _check(_lib.fhegpu_res_slot_order(plan.ctypes.data_as(ctypes.c_void_p), len(plan), int(lanes),
+                                      order.ctypes.data_as(ctypes.c_void_p)), "res_slot_order")
+    return order
 
 
 def _ptr(arr, ctype):

@@ -96,6 +96,7 @@ struct fhegpu_prog {
   tc::ResOp *d_rplan = nullptr;
   uint32_t *d_rin = nullptr;
   uint32_t r_ops = 0, r_in = 0, r_local = 0, r_out = 0;
+  bool r_deps = true;             // the slot order has operands produced < 5 slots back
   // CUDA graph of one full run (all level launches), captured on first use per
   // (lanes, stream, kernel choice, debug bits); replayed with a single cudaGraphLaunch
   cudaGraphExec_t graph = nullptr;
@@ -336,8 +337,11 @@ int launch_resident(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
   const unsigned grid = (unsigned)std::min<uint64_t>(n_groups, (uint64_t)c->num_sms);
   DevParams p = c->p;
   const bool pm = pm_ok(c->p.q, c->p.ell) && !(c->p.dbg & 2u);
-  auto kern = pm ? tc::resident_tc_kernel<9, 29, true, FHEGPU_ENC_RESIDENT>
-                 : tc::resident_tc_kernel<9, 29, false, FHEGPU_ENC_RESIDENT>;
+  // plans whose slot order has no operand produced < 5 slots back compile the RAW waits out
+  auto kern = pm ? (pr->r_deps ? tc::resident_tc_kernel<9, 29, true, FHEGPU_ENC_RESIDENT, true>
+                               : tc::resident_tc_kernel<9, 29, true, FHEGPU_ENC_RESIDENT, false>)
+                 : (pr->r_deps ? tc::resident_tc_kernel<9, 29, false, FHEGPU_ENC_RESIDENT, true>
+                               : tc::resident_tc_kernel<9, 29, false, FHEGPU_ENC_RESIDENT, false>);
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<grid, R::THREADS, smem, c->stream>>>(c->store, pr->d_rplan, pr->d_rin, pr->r_ops, pr->r_in, pr->r_local,
                                                pr->r_out, lanes, n_groups, p);
@@ -955,15 +959,36 @@ int fhegpu_prog_set_resident(fhegpu_ctx *c, fhegpu_prog *pr, const fhegpu_res_op
   cudaFree(pr->d_rin);
   pr->d_rplan = nullptr;
   pr->d_rin = nullptr;
-  CUDA_TRY(cudaMalloc(&pr->d_rplan, n_ops * sizeof(tc::ResOp)));
+  // the plan, then the group's slot order (operand reuse, RAW distances)
+  std::vector<uint8_t> buf(n_ops * sizeof(tc::ResOp) + n_ops * tc::RES_W);
+  std::memcpy(buf.data(), plan, n_ops * sizeof(tc::ResOp));
+  tc::ResSlotOrder sched;
+  const uint8_t *order = buf.data() + n_ops * sizeof(tc::ResOp);
+  sched.run(reinterpret_cast<const tc::ResOp *>(plan), (int)n_ops, tc::RES_W, buf.data() + n_ops * sizeof(tc::ResOp));
+  pr->r_deps = tc::ResSlotOrder::near_deps(reinterpret_cast<const tc::ResOp *>(plan), (int)n_ops, tc::RES_W, order);
+  CUDA_TRY(cudaMalloc(&pr->d_rplan, buf.size()));
   CUDA_TRY(cudaMalloc(&pr->d_rin, std::max(n_in, 1u) * sizeof(uint32_t)));
-  CUDA_TRY(cudaMemcpy(pr->d_rplan, plan, n_ops * sizeof(tc::ResOp), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(pr->d_rplan, buf.data(), buf.size(), cudaMemcpyHostToDevice));
   if (n_in) CUDA_TRY(cudaMemcpy(pr->d_rin, in_slots, n_in * sizeof(uint32_t), cudaMemcpyHostToDevice));
   pr->r_ops = n_ops;
   pr->r_in = n_in;
   pr->r_local = n_local;
   pr->r_out = n_out;
   pr->use_resident = true;
+  return FHEGPU_OK;
+}
+
+int fhegpu_res_slot_order(const fhegpu_res_op *plan, uint32_t n_ops, uint32_t lanes, uint8_t *order) {
+  if (!plan || !order) return fail(FHEGPU_EINVAL, "null argument");
+  if (lanes < 1 || lanes > 4 || n_ops > (uint32_t)tc::RES_MAX_OPS || lanes * n_ops > 32)
+    return fail(FHEGPU_EINVAL, "slot order: lanes <= 4, n_ops <= 8");
+  for (uint32_t i = 0; i < n_ops; ++i) {
+    const fhegpu_res_op &o = plan[i];
+    if ((o.lkind && (o.lprod < 0 || (uint32_t)o.lprod >= i)) || (o.rkind && (o.rprod < 0 || (uint32_t)o.rprod >= i)))
+      return fail(FHEGPU_EINVAL, "bad resident op " + std::to_string(i));
+  }
+  tc::ResSlotOrder sched;
+  sched.run(reinterpret_cast<const tc::ResOp *>(plan), (int)n_ops, (int)lanes, order);
   return FHEGPU_OK;
 }
 

@@ -21,6 +21,10 @@
 // Timeline probes (trace_ev, -DFHEGPU_TRACE=1 builds only): tools/timeline_resident.py.
 #pragma once
 
+#include <climits>
+#include <unordered_map>
+#include <utility>
+
 #include "tc_nand_ws.cuh"
 
 namespace fhegpu {
@@ -32,7 +36,7 @@ namespace tc {
 #ifndef FHEGPU_RES_NSETS
 #define FHEGPU_RES_NSETS 1
 #endif
-constexpr int RES_W = FHEGPU_RES_W;          // lanes per group (3: producers >= 6 slots ahead)
+constexpr int RES_W = FHEGPU_RES_W;          // lanes per group
 constexpr int RES_NSETS = FHEGPU_RES_NSETS;  // input sets (1: the next group's inputs load after
                                              // the group's last input reader)
 constexpr int RES_MAX_OPS = 8;    // gates per lane program
@@ -45,6 +49,109 @@ struct ResOp {
   uint8_t dest, is_out, flags, pad;  // local buffer written; 1: also stored to out_slot; complements
   int16_t lprod, rprod;              // plan index of the gate producing a local operand (-1: input)
   uint32_t out_slot;                 // store slot of a program output
+};
+
+// Slot order of a group (host side, fhegpu_prog_set_resident): the W * n_ops slots (gate o of
+// lane w) in the order the CTA runs them, one byte each: o | w << 3 | 32 (left operand reused) |
+// 64 (right operand reused).  Slot t runs in TMEM / B buffer t & 1, so a gate placed two slots
+// after its lane's previous gate finds that gate's A (TMEM) and B (shared memory) operands still
+// in its buffers: an identical left operand (same source, same complement) rebuilds only the
+// A columns the tail accumulator overwrote, an identical right operand skips the B copy.  A
+// local operand produced fewer than 5 slots back costs a wait on its producer's epilogue, an
+// output gate right after its lane's output gate into the same buffer an epilogue barrier.  The
+// order maximises reuse (left 3, right 1) minus 4 per such wait (2 per barrier) over all orders
+// that keep each lane's gates in plan order: exhaustive search over (per-lane progress, last 4
+// slots), memoised (W * n_ops <= 24 slots).
+struct ResSlotOrder {
+  const ResOp *plan;
+  int n, W;
+  int same_l[RES_MAX_OPS], same_r[RES_MAX_OPS];
+  std::unordered_map<uint64_t, std::pair<int, int>> memo;   // state -> (best score, lane taken)
+
+  static bool same_src(const ResOp &a, const ResOp &b, bool left) {
+    const uint8_t ka = left ? a.lkind : a.rkind, kb = left ? b.lkind : b.rkind;
+    const uint32_t ia = ka ? (uint32_t)(left ? a.lprod : a.rprod) : (left ? a.lidx : a.ridx);
+    const uint32_t ib = kb ? (uint32_t)(left ? b.lprod : b.rprod) : (left ? b.lidx : b.ridx);
+    const uint32_t m = left ? 1u : 2u;
+    return ka == kb && ia == ib && (a.flags & m) == (b.flags & m);
+  }
+  // state: progress of each lane (4 bits) | last 4 slots (6 bits each: 0 none, else 1 + o + 8 w)
+  static uint64_t key(const int *prog, int W, const int *last) {
+    uint64_t k = 0;
+    for (int w = 0; w < W; ++w) k = (k << 4) | (uint64_t)prog[w];
+    for (int i = 0; i < 4; ++i) k = (k << 6) | (uint64_t)last[i];
+    return k;
+  }
+  int gain(int o, int w, const int *last, bool *ra, bool *rb) const {
+    int s = 0;
+    *ra = *rb = false;
+    if (o > 0 && last[1] == 1 + (o - 1) + 8 * w) {
+      *ra = same_l[o];
+      *rb = same_r[o];
+      s += 3 * same_l[o] + same_r[o];
+    }
+    const ResOp &op = plan[o];
+    if (last[0] > 0) {                             // store hazard (an epilogue barrier): avoid
+      const int po = (last[0] - 1) & 7, pw = (last[0] - 1) >> 3;
+      if (pw == w && op.is_out && plan[po].is_out && plan[po].dest == op.dest) s -= 2;
+    }
+    for (int side = 0; side < 2; ++side) {
+      const int kind = side ? op.rkind : op.lkind, prod = side ? op.rprod : op.lprod;
+      if (!kind) continue;
+      for (int i = 0; i < 4; ++i)
+        if (last[i] == 1 + prod + 8 * w) s -= 4;
+    }
+    return s;
+  }
+  int best(int *prog, int *last, int left) {
+    if (left == 0) return 0;
+    const uint64_t k = key(prog, W, last);
+    auto it = memo.find(k);
+    if (it != memo.end()) return it->second.first;
+    int bs = INT32_MIN, bw = -1;
+    for (int w = 0; w < W; ++w) {
+      const int o = prog[w];
+      if (o >= n) continue;
+      bool ra, rb;
+      const int g = gain(o, w, last, &ra, &rb);
+      int nl[4] = {1 + o + 8 * w, last[0], last[1], last[2]};
+      ++prog[w];
+      const int sc = g + best(prog, nl, left - 1);
+      --prog[w];
+      if (sc > bs) bs = sc, bw = w;
+    }
+    memo.emplace(k, std::make_pair(bs, bw));
+    return bs;
+  }
+  // any local operand produced fewer than 5 slots back (else the kernel compiles its waits out)
+  static bool near_deps(const ResOp *p, int n_ops, int lanes, const uint8_t *order) {
+    int pos[RES_MAX_OPS][4];
+    for (int t = 0; t < n_ops * lanes; ++t) pos[order[t] & 7][(order[t] >> 3) & 3] = t;
+    for (int t = 0; t < n_ops * lanes; ++t) {
+      const ResOp &op = p[order[t] & 7];
+      const int w = (order[t] >> 3) & 3;
+      if ((op.lkind && t - pos[op.lprod][w] < 5) || (op.rkind && t - pos[op.rprod][w] < 5)) return true;
+    }
+    return false;
+  }
+  void run(const ResOp *p, int n_ops, int lanes, uint8_t *order) {
+    plan = p, n = n_ops, W = lanes;
+    for (int o = 0; o < n; ++o) {
+      same_l[o] = o > 0 && same_src(p[o], p[o - 1], true);
+      same_r[o] = o > 0 && same_src(p[o], p[o - 1], false);
+    }
+    int prog[4] = {0, 0, 0, 0}, last[4] = {0, 0, 0, 0};
+    best(prog, last, n * W);
+    for (int t = 0; t < n * W; ++t) {
+      const int w = memo.at(key(prog, W, last)).second, o = prog[w];
+      bool ra, rb;
+      gain(o, w, last, &ra, &rb);
+      order[t] = (uint8_t)(o | (w << 3) | (ra ? 32 : 0) | (rb ? 64 : 0));
+      ++prog[w];
+      for (int i = 3; i > 0; --i) last[i] = last[i - 1];
+      last[0] = 1 + o + 8 * w;
+    }
+  }
 };
 
 // A operand of one row, words [W0, W1): bits -> K slots, tcgen05.st into TMEM (4 words = one
@@ -150,8 +257,9 @@ struct __align__(16) SlotInfo {
   uint32_t dest;           // destination local buffer (ciphertext words offset)
   uint8_t dep_l, dep_r;    // out_ready index (o * W + w) of a local operand's producer (0xFF: input)
   uint8_t bits;            // 1, 2: complement left / right; 4: output gate; 8 / 16: left / right local;
-                           // 32: the group's last input-reading slot
-  uint8_t pad;
+                           // 32: the group's last input-reading slot; 64 / 128: left / right
+                           // operand reused from slot t - 2 (ResSlotOrder)
+  uint8_t ow;              // gate | lane << 3 | 32 (store hazard on the previous slot)
 };
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t *v) {
@@ -184,7 +292,7 @@ __device__ __forceinline__ void bulk_wait_read_dyn(uint32_t n) {
   }
 }
 
-template <int K, int ELL, bool PM, int ENC>
+template <int K, int ELL, bool PM, int ENC, bool DEPS>
 __global__ void __launch_bounds__(GeoRes<K, ELL>::THREADS, 1)
 resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan, const uint32_t *__restrict__ in_slots,
                    uint32_t n_ops, uint32_t n_in, uint32_t n_local, uint32_t n_out, uint32_t lanes,
@@ -240,25 +348,38 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
   }
   for (uint32_t i = tid; i < n_ops * (sizeof(ResOp) / 4); i += R::THREADS)
     reinterpret_cast<uint32_t *>(s_plan)[i] = reinterpret_cast<const uint32_t *>(plan)[i];
-  uint32_t in_last = 0;                        // last gate reading a program input
-  for (uint32_t i = 0; i < n_ops; ++i)
-    if (plan[i].lkind == 0 || plan[i].rkind == 0) in_last = i;
-  if (tid < n_ops * W) {
-    const ResOp op = plan[tid / W];
-    const uint32_t w = tid % W;
+  // slot order (ResSlotOrder), stored after the plan
+  const uint8_t *order = reinterpret_cast<const uint8_t *>(plan + n_ops);
+  if (tid < S) {
+    const uint32_t code = order[tid];
+    const uint32_t o = code & 7u, w = (code >> 3) & 3u;
+    const ResOp op = plan[o];
     SlotInfo si;
     si.v1 = (op.lkind ? w * n_local + op.lidx : w * n_in + op.lidx) * R::CT_WORDS;
     si.v2 = (op.rkind ? w * n_local + op.ridx : w * n_in + op.ridx) * R::CT_WORDS;
     si.dest = (w * n_local + op.dest) * R::CT_WORDS;
+    uint32_t in_last = 0, slot_l = 0, slot_r = 0;  // last input-reading slot; producers' slots
+    for (uint32_t r = 0; r < S; ++r) {
+      const uint32_t c = order[r] & 31u;
+      if (plan[c & 7u].lkind == 0 || plan[c & 7u].rkind == 0) in_last = r;
+      if (op.lkind && c == ((uint32_t)op.lprod | w << 3)) slot_l = r;
+      if (op.rkind && c == ((uint32_t)op.rprod | w << 3)) slot_r = r;
+    }
+    const bool reuse = !(p.dbg & (1u << 20));       // dbg bit 20: no operand reuse
     si.bits = (op.flags & 3u) | (op.is_out ? 4u : 0u) | (op.lkind ? 8u : 0u) | (op.rkind ? 16u : 0u) |
-              (tid / W == in_last && w == W - 1 ? 32u : 0u);
-    si.pad = 0;
+              (tid == in_last ? 32u : 0u) | (reuse && (code & 32u) ? 64u : 0u) |
+              (reuse && (code & 64u) ? 128u : 0u);
+    // store hazard: the previous slot is an output gate of the same lane writing the same buffer,
+    // so this gate's writes must wait for that slot's store to have read it (epilogue, below)
+    const uint32_t prev = order[(tid + S - 1) % S];
+    const bool hazard = op.is_out && plan[prev & 7u].is_out && ((prev >> 3) & 3u) == w &&
+                        plan[prev & 7u].dest == op.dest;
+    si.ow = (uint8_t)((code & 31u) | (hazard ? 32u : 0u));
     // A producer >= 5 slots back needs no wait: the builder's a_free wait for slot t implies
     // main_done(t-2), hence the MMA of t-2 was issued after d_free(t-4), which every epilogue
     // warp arrives on only after finishing slot t-5 (outputs written, out_ready published).
-    const uint32_t o = tid / W;
-    si.dep_l = op.lkind && (o - op.lprod) * W < 5 ? (uint8_t)(op.lprod * W + w) : (uint8_t)0xFF;
-    si.dep_r = op.rkind && (o - op.rprod) * W < 5 ? (uint8_t)(op.rprod * W + w) : (uint8_t)0xFF;
+    si.dep_l = op.lkind && tid - slot_l < 5 ? (uint8_t)slot_l : (uint8_t)0xFF;
+    si.dep_r = op.rkind && tid - slot_r < 5 ? (uint8_t)slot_r : (uint8_t)0xFF;
     s_slot[tid] = si;
   }
   for (uint32_t w = tid; w < 2 * R::B_BYTES / 4; w += R::THREADS) reinterpret_cast<uint32_t *>(s_b)[w] = 0u;
@@ -381,12 +502,12 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       if (r == 0) mbar_wait(&in_full[set], ph & 1u);
       const SlotInfo si = s_slot[r];
       mbar_wait(&a_free[b], (u & 1u) ^ 1u);        // B(b) was last read by the MMAs of slot t - 2
-      if (si.dep_r != 0xFF) mbar_wait(&out_ready[si.dep_r], g & 1u);
+      if (DEPS && si.dep_r != 0xFF) mbar_wait(&out_ready[si.dep_r], g & 1u);
       const uint32_t *v2 = ((si.bits & 16u) ? s_loc : s_inb + set * in_set_words) + si.v2;
       const bool comp2 = si.bits & 2u;
       uint8_t *bb = s_b + b * R::B_BYTES;
 #pragma unroll
-      for (int x = 0; x < B_ROWS; ++x) {
+      for (int x = 0; x < ((si.bits & 128u) ? 0 : B_ROWS); ++x) {   // reuse: B(b) holds this B
         if (b_src[x] < 0) continue;
         uint32_t vals[K];
 #pragma unroll
@@ -451,7 +572,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       mbar_wait(&a_free[b], (u & 1u) ^ 1u);
       // operands produced in this group: wait until the epilogue has put them in their buffers
       // (one mbarrier phase per lane group; the producer's next group runs after this slot)
-      if (!(p.dbg & (1u << 19))) {                 // dbg bit 19: no waits (timing only)
+      if (DEPS && !(p.dbg & (1u << 19))) {         // dbg bit 19: no waits (timing only)
         if (si.dep_l != 0xFF) mbar_wait(&out_ready[si.dep_l], g & 1u);
         if (si.dep_r != 0xFF) mbar_wait(&out_ready[si.dep_r], g & 1u);
       }
@@ -464,7 +585,9 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       uint8_t *bb = s_b + b * R::B_BYTES;
       {
         const uint32_t a_addr = tmem_base + b * G::BUF_COLS + lane_off + G::D_COLS + tile * 8 * K;
-        if constexpr (R::BSPLIT == 1) {
+        if (si.bits & 64u) {                       // reuse: only the columns the tail MMA overwrote
+          if (tile == 0) build_a_words<K, 0, 6, ENC>(v1, row, row_blk, row_bit, comp1, p.q, a_addr);
+        } else if constexpr (R::BSPLIT == 1) {
           build_a_words<K, 0, K, ENC>(v1, row, row_blk, row_bit, comp1, p.q, a_addr);
         } else {
           if (part == 0) build_a_words<K, 0, 4, ENC>(v1, row, row_blk, row_bit, comp1, p.q, a_addr);
@@ -472,7 +595,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
         }
       }
       if constexpr (G::TAIL > 0) {
-        if (tb >= 0 && tb < G::TAIL * K) {
+        if (tb >= 0 && tb < G::TAIL * K && !(si.bits & 64u)) {   // reuse: TA(b) holds this tail A
           const int m = tb / K, ww = tb - m * K;
           const int rr = G::MMA_ROWS + m;
           uint32_t v = v1[rr * K + ww];
@@ -530,10 +653,12 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
     SlotPos pos;
     for (uint32_t t = 0; t < n_slots; ++t, pos.next(S, W)) {
       const uint32_t b = t & 1u, u = t >> 1;
-      const uint32_t g = pos.g, r = pos.r, o = pos.o, w = pos.w;
+      const uint32_t g = pos.g, r = pos.r;
       const SlotInfo si = s_slot[r];
+      const uint32_t o = si.ow & 7u, w = (si.ow >> 3) & 3u;
       uint32_t *out_st = s_loc + si.dest;
       mbar_wait(&main_done[b], u & 1u);
+      if (si.ow & 32u) named_bar(2, NE_THREADS);   // store hazard: slot t-1's store has read the buffer
       if (et == 0) trace_ev(p, t, 9);
       tc_fence_after();
       const uint32_t dcol = tmem_base + b * G::BUF_COLS + lane_off + tile * G::NPAD;
@@ -574,11 +699,13 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
         }
       }
       fence_proxy_async_smem();
+      const SlotInfo sn = s_slot[r + 1 == S ? 0u : r + 1];
+      const bool next_hazard = (sn.ow & 32u) && t + 1 < n_slots;
       if (et == 0 && t + 1 < n_slots) {
         // the next gate writes an output buffer: every earlier store (outputs of one group may
         // share a buffer) must have read its source
-        if (s_slot[r + 1 == S ? 0u : r + 1].bits & 4u) bulk_wait_read_n<0>();
-        mbar_arrive(&out_free[(t + 1) % R::N_OUT]);
+        if (sn.bits & 4u) bulk_wait_read_n<0>();
+        if (!next_hazard) mbar_arrive(&out_free[(t + 1) % R::N_OUT]);
       }
       named_bar(1, NE_THREADS);
       if (et == 0) trace_ev(p, t, 10);
@@ -588,12 +715,16 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
         const uint32_t ln = lane_of_group(g, w);
         if ((si.bits & 4u) && ln < lanes)                 // partial last group: no store
           bulk_s2g(store + ((uint64_t)s_plan[o].out_slot * lanes + ln) * R::CT_WORDS, out_st, R::CT_BYTES);
+        if (next_hazard) {                         // the next gate rewrites this buffer
+          bulk_wait_read_n<0>();
+          mbar_arrive(&out_free[(t + 1) % R::N_OUT]);
+        }
       } else if (et == 32) {
         // the gate's output is readable in its buffer: published by a thread without bulk
         // stores in flight (a release on the storing thread would wait for its stores)
         const uint32_t ob = t % R::N_OUT, ou = t / R::N_OUT;
         mbar_wait(&tail_ready[ob], ou & 1u);
-        mbar_arrive(&out_ready[r]);               // r = o * W + w
+        mbar_arrive(&out_ready[r]);
         trace_ev(p, t, 11);
       }
     }

@@ -94,3 +94,63 @@ def test_plain_c_consumer_links_against_the_abi():
     assert os.path.exists(kat)
     out = subprocess.run(["ldd", kat], capture_output=True, text=True).stdout
     assert "libfhegpu.so" in out and "not found" not in out
+
+
+def test_resident_slot_order():
+    """fhegpu_res_slot_order (host only): every (gate, lane) slot once, each lane's gates in plan
+    order, reuse flags only where slot t - 2 is the lane's previous gate with an identical operand;
+    the gate benchmark's XOR + AND reuses both operands of its second NAND and the left operand
+    of its fourth in every lane, with no operand produced fewer than 5 slots back."""
+    import numpy as np
+
+    from paper_1611_08769_b200 import DEFAULT0_PARAMS, DEFAULT_PARAMS, GswScheme
+    from paper_1611_08769_b200.engine import GpuEngine
+    from paper_1611_08769_b200.gates import and_, nor_, not_, or_, xnor_, xor_
+
+    def check(plan, lanes):
+        order = _native.res_slot_order(plan, lanes)
+        ow = [(int(c) & 7, (int(c) >> 3) & 3) for c in order]
+        assert sorted(ow) == sorted((o, w) for o in range(len(plan)) for w in range(lanes))
+        for w in range(lanes):
+            assert [o for o, ww in ow if ww == w] == list(range(len(plan)))
+        for t, c in enumerate(order):
+            o, w = ow[t]
+            if c & 96:
+                assert t >= 2 and ow[t - 2] == (o - 1, w)
+                for bit, kind, idx, prod, m in ((32, "lkind", "lidx", "lprod", 1), (64, "rkind", "ridx", "rprod", 2)):
+                    if c & bit:
+                        a, b = plan[o], plan[o - 1]
+                        assert a[kind] == b[kind] and (a["flags"] & m) == (b["flags"] & m)
+                        assert (a[prod] == b[prod]) if a[kind] else (a[idx] == b[idx])
+        return order, ow
+
+    eng = GpuEngine(GswScheme(DEFAULT_PARAMS), dry_run=True, batch_size=64)
+    a, b = eng.input_bit(1), eng.input_bit(0)
+    xor_(a, b), and_(a, b)
+    eng.flush()
+    plan = GpuEngine._resident_plan(eng.dry_programs[-1])[0]
+    order, ow = check(plan, 3)
+    assert sum(bool(c & 32) for c in order) == 6 and sum(bool(c & 64) for c in order) == 3
+    pos = {s: t for t, s in enumerate(ow)}
+    for (o, w), t in pos.items():
+        for kind, prod in (("lkind", "lprod"), ("rkind", "rprod")):
+            if plan[o][kind]:
+                assert t - pos[(int(plan[o][prod]), w)] >= 5
+    rng = np.random.default_rng(5)
+    gates = [not_, and_, or_, xor_, nor_, xnor_]
+    done = 0
+    for trial in range(30):
+        eng = GpuEngine(GswScheme(DEFAULT0_PARAMS), dry_run=True, batch_size=32)
+        pool = [eng.input_bit(int(rng.integers(0, 1 << 31))) for _ in range(int(rng.integers(1, 4)))]
+        for _ in range(int(rng.integers(1, 4))):
+            g = gates[int(rng.integers(0, len(gates)))]
+            p1, p2 = pool[int(rng.integers(0, len(pool)))], pool[int(rng.integers(0, len(pool)))]
+            pool.append(g(p1) if g is not_ else g(p1, p2))
+        eng.flush()
+        res = GpuEngine._resident_plan(eng.dry_programs[-1]) if eng.dry_programs else None
+        if res is None:
+            continue
+        for lanes in (1, 2, 3, 4):
+            check(res[0], lanes)
+        done += 1
+    assert done >= 10

@@ -9,7 +9,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G, P = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles")
 items = int(sys.argv[1])
 label = sys.argv[2] if len(sys.argv) > 2 else "resident"
-KERNEL = {"resident": "resident_tc_kernel<9,29,true,2>", "tiled": "level_tc_ws_kernel<9,29,true,1>"}.get(
+KERNEL = {"resident": "resident_tc_kernel<9,29,true,2,false>", "tiled": "level_tc_ws_kernel<9,29,true,1>"}.get(
     label, "level_tc_ws_kernel<9,29,true,2>")
 FNAME = "r1_ncu_full_resident" if label == "resident" else f"r1_ncu_full_level_tc_ws_{label}"
 shutil.copy(os.path.join(G, "bench_default.json"), os.path.join(P, "r1_bench_default_final.json"))
