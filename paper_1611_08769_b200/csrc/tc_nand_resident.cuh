@@ -51,6 +51,19 @@ struct ResOp {
   uint32_t out_slot;                 // store slot of a program output
 };
 
+#ifndef FHEGPU_RES_HINT
+#define FHEGPU_RES_HINT 0    // 1: program inputs and outputs move with an L2 evict_first policy
+#endif
+
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 // Slot order of a group (host side, fhegpu_prog_set_resident): the W * n_ops slots (gate o of
 // lane w) in the order the CTA runs them, one byte each: o | w << 3 | 32 (left operand reused) |
 // 64 (right operand reused).  Slot t runs in TMEM / B buffer t & 1, so a gate placed two slots
@@ -405,8 +418,12 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
         for (uint32_t w = 0; w < valid; ++w) {
           const uint32_t ln = ln0 + w;
           for (uint32_t i = 0; i < n_in; ++i)
-            bulk_g2s(in_ptr(set, w, i), store + ((uint64_t)in_slots[i] * lanes + ln) * R::CT_WORDS, R::CT_BYTES,
-                     &in_full[set]);
+            if (FHEGPU_RES_HINT)
+              bulk_g2s_hint(in_ptr(set, w, i), store + ((uint64_t)in_slots[i] * lanes + ln) * R::CT_WORDS,
+                            R::CT_BYTES, &in_full[set], policy_evict_first());
+            else
+              bulk_g2s(in_ptr(set, w, i), store + ((uint64_t)in_slots[i] * lanes + ln) * R::CT_WORDS, R::CT_BYTES,
+                       &in_full[set]);
         }
       }
     }
@@ -713,8 +730,11 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
         const uint32_t ob = t % R::N_OUT, ou = t / R::N_OUT;
         mbar_wait(&tail_ready[ob], ou & 1u);
         const uint32_t ln = lane_of_group(g, w);
-        if ((si.bits & 4u) && ln < lanes)                 // partial last group: no store
-          bulk_s2g(store + ((uint64_t)s_plan[o].out_slot * lanes + ln) * R::CT_WORDS, out_st, R::CT_BYTES);
+        if ((si.bits & 4u) && ln < lanes) {               // partial last group: no store
+          uint32_t *dst = store + ((uint64_t)s_plan[o].out_slot * lanes + ln) * R::CT_WORDS;
+          if (FHEGPU_RES_HINT) bulk_s2g_hint(dst, out_st, R::CT_BYTES, policy_evict_first());
+          else bulk_s2g(dst, out_st, R::CT_BYTES);
+        }
         if (next_hazard) {                         // the next gate rewrites this buffer
           bulk_wait_read_n<0>();
           mbar_arrive(&out_free[(t + 1) % R::N_OUT]);

@@ -288,25 +288,30 @@ def test_tiled_program_refuses_level_fallback():
 @pytest.mark.parametrize("lanes", [4096, 4097])
 def test_resident_schedule_equals_levels_bit_exact(lanes):
     """schedule='resident': XOR + AND per lane in one lane-resident launch (inputs loaded once,
-    intermediates in shared memory) -- every output ciphertext equals the level schedule's, also
-    with a lane count that leaves the last 3-lane group partial."""
+    intermediates in shared memory) -- every output ciphertext equals the level schedule's, with
+    and without operand reuse between a lane's consecutive gates, also with a lane count that
+    leaves the last 3-lane group partial."""
     scheme = GswScheme(DEFAULT_PARAMS)
     keys = scheme.keygen(1)
     bits = np.random.default_rng(9).integers(0, 2, (lanes, 2))
     outs = {}
-    for schedule in ("levels", "resident"):
+    for variant in ("levels", "resident", "resident-noreuse"):
+        schedule = variant.split("-")[0]
         eng = GpuEngine(scheme, keys=keys, rng=np.random.default_rng(1), batch_size=lanes,
                         device_encrypt=True, schedule=schedule)
+        eng.ctx.set_debug(1 << 20 if variant == "resident-noreuse" else 0)   # bit 20: no operand reuse
         a, b = eng.input_block(bits)
         x, y = xor_(a, b), and_(a, b)
         prog = eng.flush()
         if schedule == "resident":
             assert prog.launches == 1                      # partial last lane group included
-        outs[schedule] = eng.node_values([x, y])
+        outs[variant] = eng.node_values([x, y])
         assert (eng.read_back_bits([x, y]) == np.stack([bits[:, 0] ^ bits[:, 1], bits[:, 0] & bits[:, 1]])).all()
         prog.run(lanes)                                    # re-running rewrites identical values
-        assert np.array_equal(eng.node_values([x, y]), outs[schedule])
+        assert np.array_equal(eng.node_values([x, y]), outs[variant])
+        eng.ctx.set_debug(0)
     assert np.array_equal(outs["levels"], outs["resident"])
+    assert np.array_equal(outs["levels"], outs["resident-noreuse"])
 
 
 def test_resident_random_small_programs_equal_levels():
