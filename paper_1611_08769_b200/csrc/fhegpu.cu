@@ -55,6 +55,7 @@ struct fhegpu_ctx {
   int num_sms = 0;
   uint32_t *store = nullptr;
   uint64_t capacity = 0;  // ciphertexts
+  uint64_t store_gen = 0; // bumped whenever the store moves (captured graphs bake its address)
   // staging
   uint32_t *d_stage = nullptr;
   size_t stage_bytes = 0;
@@ -96,6 +97,7 @@ struct fhegpu_prog {
   tc::ResOp *d_rplan = nullptr;
   uint32_t *d_rin = nullptr;
   uint32_t r_ops = 0, r_in = 0, r_local = 0, r_out = 0;
+  uint64_t r_slots = 0;           // 1 + the largest store slot the plan reads or writes
   bool r_deps = true;             // the slot order has operands produced < 5 slots back
   // CUDA graph of one full run (all level launches), captured on first use per
   // (lanes, stream, kernel choice, debug bits); replayed with a single cudaGraphLaunch
@@ -104,6 +106,7 @@ struct fhegpu_prog {
   cudaStream_t graph_stream = nullptr;
   int graph_kernel = -1;
   uint32_t graph_dbg = 0;
+  uint64_t graph_store_gen = 0;
 };
 
 namespace {
@@ -338,9 +341,11 @@ int launch_resident(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
   DevParams p = c->p;
   const bool pm = pm_ok(c->p.q, c->p.ell) && !(c->p.dbg & 2u);
   // plans whose slot order has no operand produced < 5 slots back compile the RAW waits out
-  auto kern = pm ? (pr->r_deps ? tc::resident_tc_kernel<9, 29, true, FHEGPU_ENC_RESIDENT, true>
+  // dbg bit 21 forces the instantiation with every RAW wait compiled in (parity tests)
+  const bool deps = pr->r_deps || (c->p.dbg & (1u << 21));
+  auto kern = pm ? (deps ? tc::resident_tc_kernel<9, 29, true, FHEGPU_ENC_RESIDENT, true>
                                : tc::resident_tc_kernel<9, 29, true, FHEGPU_ENC_RESIDENT, false>)
-                 : (pr->r_deps ? tc::resident_tc_kernel<9, 29, false, FHEGPU_ENC_RESIDENT, true>
+                 : (deps ? tc::resident_tc_kernel<9, 29, false, FHEGPU_ENC_RESIDENT, true>
                                : tc::resident_tc_kernel<9, 29, false, FHEGPU_ENC_RESIDENT, false>);
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<grid, R::THREADS, smem, c->stream>>>(c->store, pr->d_rplan, pr->d_rin, pr->r_ops, pr->r_in, pr->r_local,
@@ -470,6 +475,7 @@ int fhegpu_store_reserve(fhegpu_ctx *c, uint64_t n_cts) {
   }
   c->store = nw;
   c->capacity = n_cts;
+  ++c->store_gen;
   return FHEGPU_OK;
 }
 
@@ -671,6 +677,11 @@ int fhegpu_prog_run_range(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes, uint32
   if (!c || !pr) return fail(FHEGPU_EINVAL, "null argument");
   const uint32_t n_levels = (uint32_t)pr->offsets.size() - 1;
   last = std::min(last, n_levels);
+  // every slot the program (or its resident plan) names, for every lane, must be in the store
+  const uint64_t slots = std::max(pr->n_slots, pr->use_resident ? pr->r_slots : 0);
+  if (lanes && slots && (slots > c->capacity / lanes || slots * lanes > c->capacity))
+    return fail(FHEGPU_EINVAL, "program needs " + std::to_string(slots) + " slots x " + std::to_string(lanes) +
+                                   " lanes; store holds " + std::to_string(c->capacity) + " ciphertexts");
   CUDA_TRY(cudaSetDevice(c->device));
   if (pr->use_resident && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
     const int rc = launch_resident(c, pr, lanes);
@@ -706,7 +717,7 @@ int fhegpu_prog_run(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
   CUDA_TRY(cudaSetDevice(c->device));
   const int kern = effective_kernel(c);
   if (!pr->graph || pr->graph_lanes != lanes || pr->graph_stream != c->stream ||
-      pr->graph_kernel != kern || pr->graph_dbg != c->p.dbg) {
+      pr->graph_kernel != kern || pr->graph_dbg != c->p.dbg || pr->graph_store_gen != c->store_gen) {
     if (pr->graph) {
       cudaGraphExecDestroy(pr->graph);
       pr->graph = nullptr;
@@ -729,6 +740,7 @@ int fhegpu_prog_run(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
     pr->graph_stream = c->stream;
     pr->graph_kernel = kern;
     pr->graph_dbg = c->p.dbg;
+    pr->graph_store_gen = c->store_gen;
     return FHEGPU_OK;                  // this call already ran the program once
   }
   CUDA_TRY(cudaGraphLaunch(pr->graph, c->stream));
@@ -954,6 +966,25 @@ int fhegpu_prog_set_resident(fhegpu_ctx *c, fhegpu_prog *pr, const fhegpu_res_op
       return fail(FHEGPU_EINVAL, "bad resident op " + std::to_string(i));
     n_out += o.is_out;
   }
+  // buffer rules the kernel's store-hazard and reuse logic rely on (fhegpu.h): a buffer holds
+  // outputs only or temporaries only, and no gate overwrites a buffer whose value still has a
+  // reader later in the plan
+  for (uint32_t i = 0; i < n_ops; ++i)
+    for (uint32_t j = i + 1; j < n_ops; ++j) {
+      if (plan[j].dest != plan[i].dest) continue;
+      if (plan[j].is_out != plan[i].is_out)
+        return fail(FHEGPU_EINVAL, "resident ops " + std::to_string(i) + " and " + std::to_string(j) +
+                                       " share a buffer between an output and a temporary");
+      for (uint32_t r = j + 1; r < n_ops; ++r)
+        if ((plan[r].lkind && plan[r].lprod == (int32_t)i) || (plan[r].rkind && plan[r].rprod == (int32_t)i))
+          return fail(FHEGPU_EINVAL, "resident op " + std::to_string(j) + " overwrites buffer " +
+                                         std::to_string(plan[i].dest) + " before op " + std::to_string(r) +
+                                         " reads op " + std::to_string(i) + "'s value");
+    }
+  uint64_t r_slots = 0;
+  for (uint32_t i = 0; i < n_in; ++i) r_slots = std::max<uint64_t>(r_slots, uint64_t(in_slots[i]) + 1);
+  for (uint32_t i = 0; i < n_ops; ++i)
+    if (plan[i].is_out) r_slots = std::max<uint64_t>(r_slots, uint64_t(plan[i].out_slot) + 1);
   CUDA_TRY(cudaSetDevice(c->device));
   cudaFree(pr->d_rplan);
   cudaFree(pr->d_rin);
@@ -974,6 +1005,7 @@ int fhegpu_prog_set_resident(fhegpu_ctx *c, fhegpu_prog *pr, const fhegpu_res_op
   pr->r_in = n_in;
   pr->r_local = n_local;
   pr->r_out = n_out;
+  pr->r_slots = r_slots;
   pr->use_resident = true;
   return FHEGPU_OK;
 }

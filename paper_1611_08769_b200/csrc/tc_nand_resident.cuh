@@ -391,8 +391,11 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
     // A producer >= 5 slots back needs no wait: the builder's a_free wait for slot t implies
     // main_done(t-2), hence the MMA of t-2 was issued after d_free(t-4), which every epilogue
     // warp arrives on only after finishing slot t-5 (outputs written, out_ready published).
-    si.dep_l = op.lkind && tid - slot_l < 5 ? (uint8_t)slot_l : (uint8_t)0xFF;
-    si.dep_r = op.rkind && tid - slot_r < 5 ? (uint8_t)slot_r : (uint8_t)0xFF;
+    // (dbg bit 21, with the DEPS instantiation: wait on every local producer -- parity tests of
+    // the rule above)
+    const uint32_t near = (p.dbg & (1u << 21)) ? S : 5u;
+    si.dep_l = op.lkind && tid - slot_l < near ? (uint8_t)slot_l : (uint8_t)0xFF;
+    si.dep_r = op.rkind && tid - slot_r < near ? (uint8_t)slot_r : (uint8_t)0xFF;
     s_slot[tid] = si;
   }
   for (uint32_t w = tid; w < 2 * R::B_BYTES / 4; w += R::THREADS) reinterpret_cast<uint32_t *>(s_b)[w] = 0u;

@@ -256,6 +256,10 @@ class GpuEngine(LevelledNetlist):
         self.schedule = schedule
         if lane_rngs is not None and len(lane_rngs) != batch_size:
             raise UsageError("need one rng per lane")
+        if not isinstance(scheme, GswScheme):
+            # the reference's own GswScheme (cli.cmd_fft builds one from the container's
+            # params, cli.py:74-75): evaluate on this package's scheme for the same params
+            scheme = GswScheme(scheme.params)
         self.scheme = scheme
         self.params = scheme.params
         self.public_key = keys.public_key if keys is not None else public_key
@@ -456,14 +460,35 @@ class GpuEngine(LevelledNetlist):
         return GpuBit(self, node, 0, False, None, wire)
 
     def import_ct(self, ct) -> GpuBit:
-        """Wire from a Ciphertext (batch 1) or a list of one Ciphertext per lane."""
+        """Wire from a Ciphertext (batch 1) or a list of one Ciphertext per lane.
+
+        Accepts this package's compact ``Ciphertext`` and any object with the reference's
+        fields ``matrix`` / ``level`` / ``noise_est`` (fhe.py:148-161) -- e.g. the
+        ``fhefft.fhe.Ciphertext(matrix=..., level=...)`` that the reference's
+        ``fileio.read_ciphertext_signal`` builds (fileio.py:186-191)."""
         cts = ct if isinstance(ct, (list, tuple)) else [ct]
         if len(cts) != self.batch_size:
             raise UsageError(f"import_ct needs {self.batch_size} ciphertexts (one per lane)")
-        vals = np.stack([np.asarray(c.v, dtype=np.uint32) for c in cts])
+        vals = np.stack([self._compact_of(c) for c in cts])
         node = self._new_node(max(c.level for c in cts), max(c.noise_est for c in cts))
         self._queue_upload(node, vals)
         return GpuBit(self, node, 0, False, None, -1)
+
+    def _compact_of(self, c) -> np.ndarray:
+        p = self.params
+        v = getattr(c, "v", None)
+        if v is None:
+            mat = getattr(c, "matrix", None)
+            if mat is None:
+                raise UsageError(f"cannot import {type(c).__name__}: no compact v or matrix")
+            mat = np.asarray(mat)
+            if mat.shape != (p.n_ct, p.n_ct):
+                raise UsageError(f"ciphertext matrix shape {mat.shape} does not match N={p.n_ct}")
+            return Ciphertext.from_matrix(mat, p).v
+        v = np.asarray(v, dtype=np.uint32)
+        if v.shape != (p.n_ct, p.k):
+            raise UsageError(f"compact ciphertext shape {v.shape} does not match {(p.n_ct, p.k)}")
+        return v
 
     def nand(self, a: GpuBit, b: GpuBit) -> GpuBit:
         if a.engine is not self or b.engine is not self:

@@ -80,6 +80,17 @@ class SchemeParams:
                     f"q={self.q} too small for noise_bound={self.noise_bound} at "
                     f"depth_budget={self.depth_budget}: need q > 8*nb*(N+1)^depth")
 
+    _FIELDS = ("n", "q", "m", "noise_bound", "depth_budget")
+
+    def __eq__(self, other):
+        """Equal to any parameter object with the same five fields -- in particular the
+        reference's own ``fhefft.fhe.SchemeParams``, which ``fileio.read_ciphertext_signal``
+        compares against ``engine.scheme.params`` (fileio.py:172-174)."""
+        try:
+            return all(getattr(self, f) == getattr(other, f) for f in self._FIELDS)
+        except AttributeError:
+            return NotImplemented
+
     def digest(self) -> str:
         """Same text and hash as fhe.py:97-100, so digests interoperate."""
         text = f"{self.n},{self.q},{self.m},{self.noise_bound},{self.depth_budget}"
@@ -121,19 +132,34 @@ class KeyPair:
     secret_key: np.ndarray
 
 
-@dataclass(eq=False)
+@dataclass(eq=False, init=False)
 class Ciphertext:
     """One bit (or Z_q value) in compact form: V (N x k, u32, values < q).
 
     ``level`` and ``noise_est`` carry the reference's bookkeeping
     (fhe.py:148-161).  ``matrix`` is the reference's flattened float64 N x N
-    0/1 matrix, rebuilt on demand.
+    0/1 matrix, rebuilt on demand.  Like the reference's constructor,
+    ``Ciphertext(matrix=..., level=...)`` builds one from a matrix (``params``
+    then required: the compact form needs q and ell).
     """
 
     v: np.ndarray
     level: int = 0
     noise_est: int = 0
     params: SchemeParams | None = field(default=None, repr=False)
+
+    def __init__(self, v=None, level: int = 0, noise_est: int = 0, params: SchemeParams | None = None,
+                 *, matrix=None):
+        if (v is None) == (matrix is None):
+            raise ValueError("Ciphertext needs exactly one of v (compact) or matrix")
+        if matrix is not None:
+            if params is None:
+                raise ValueError("Ciphertext(matrix=...) needs params to recompose the matrix")
+            v = _recompose(np.asarray(matrix), params)
+        self.v = v
+        self.level = level
+        self.noise_est = noise_est
+        self.params = params
 
     @property
     def matrix(self) -> np.ndarray:
@@ -168,10 +194,22 @@ def _recompose(mat: np.ndarray, params: SchemeParams) -> np.ndarray:
     return np.mod(vals, params.q).astype(np.uint32)
 
 
+def as_params(p) -> SchemeParams:
+    """This package's SchemeParams for any object with the five parameter fields (e.g. the
+    reference's ``fhefft.fhe.SchemeParams``, which ``cli.cmd_fft`` reads from a container)."""
+    if isinstance(p, SchemeParams):
+        return p
+    try:
+        return SchemeParams(**{f: int(getattr(p, f)) for f in SchemeParams._FIELDS})
+    except AttributeError as exc:
+        raise ParameterError(f"not a parameter set: {p!r}") from exc
+
+
 class GswScheme:
     """Scheme operations for one parameter set (fhe.py:164-379 surface)."""
 
     def __init__(self, params: SchemeParams = DEFAULT_PARAMS, device: int = 0):
+        params = as_params(params)
         self.params = params
         self.device = device
         self._g = _gadget(params)

@@ -134,3 +134,29 @@ def word_ints(engine, word, signed=True):
 def wrap(v, width):
     v %= 1 << width
     return v - (1 << width) if v >> (width - 1) else v
+
+
+REF_PATHS = (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src")
+
+
+def reference_root():
+    """Directory holding the reference package ``fhefft``: the driver's install at
+    baseline/_ref (it travels to the GPU box) or the read-only source tree in the build
+    container.  None when neither exists."""
+    for p in REF_PATHS:
+        if os.path.isfile(os.path.join(p, "fhefft", "__init__.py")):
+            return p
+    return None
+
+
+def reference_modules():
+    """(fhe, engine, fileio, fft, arith, gates) of the reference, or None."""
+    import importlib
+    import sys
+    root = reference_root()
+    if root is None:
+        return None
+    if root not in sys.path:
+        sys.path.append(root)
+    return tuple(importlib.import_module(f"fhefft.{m}")
+                 for m in ("fhe", "engine", "fileio", "fft", "arith", "gates"))

@@ -136,6 +136,35 @@ def test_cfg4_all_lanes_outputs():
     assert eng.launches == golden_json("trace_cfg4.json")["max_depth"]   # one launch per level
 
 
+@pytest.mark.parametrize("normalize", [False, True])
+def test_ifft_cfg4_geometry_all_lanes(normalize):
+    """ifft_1d on the GPU (cfg4 geometry: 1024 lanes of 16-point Q4.12 signals, DEFAULT0,
+    device encryption with per-lane generators): every lane's decrypted output equals the
+    integer model of swap(fft(swap(x))) (>> log2 M when normalising).  The reference has no
+    inverse, so the integer model (oracle/fixedfft.py) is the oracle."""
+    from oracle import fixedfft
+    from paper_1611_08769_b200.fft import ifft_1d
+    scheme = GswScheme(DEFAULT0_PARAMS)
+    keys = scheme.keygen(4)
+    lanes, M, F, f = 1024, 16, 16, 12
+    rngs, vals = [], []
+    for lane in range(lanes):
+        r, x = config_signal("cfg4", lane)
+        rngs.append(r)
+        vals.append(x)
+    vals = np.array(vals)
+    eng = GpuEngine(scheme, keys=keys, batch_size=lanes, lane_rngs=rngs, device_encrypt=True)
+    out = ifft_1d(input_signal(eng, vals, FixedFormat(F, f)), normalize=normalize)
+    got = read_signal_ints(eng, out)
+    re = fixedfft.encode_lanes(vals.real, F, f)
+    im = fixedfft.encode_lanes(vals.imag, F, f)
+    o_im, o_re = fixedfft.fft_1d(im, re, F, f)
+    if normalize:
+        o_re, o_im = o_re >> 4, o_im >> 4
+    assert np.array_equal(got, fixedfft.interleave(o_re, o_im))
+    assert eng.nand_count == golden_json("trace_cfg4.json")["nand_count"]
+
+
 def test_cfg4_lane0_gate_by_gate():
     eng, out, _ = run_fft_config("cfg4", device_encrypt=True)
     ref = golden_json("cts_cfg4.json")
@@ -266,6 +295,86 @@ def test_cfg1_full_size_every_lane_decrypts():
     assert (got[0] == (bits[:, 0] ^ bits[:, 1])).all()
     assert (got[1] == (bits[:, 0] & bits[:, 1])).all()
     assert eng.nand_count == 6 and eng.max_depth == 3
+
+
+def _store_view(ctx, first_ct, count):
+    """torch view (count, ct_words) u32 of a store range, on the device (no host copy)."""
+    import torch
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (count, ctx.ct_words), "typestr": "<u4", "version": 3,
+                                    "data": (ctx.store_ptr() + first_ct * ctx.ct_words * 4, False),
+                                    "strides": None}
+    return torch.as_tensor(_Arr(), device="cuda")
+
+
+def test_cfg1_full_range_sample_vs_oracle_and_rule_check():
+    """configs[1] at full size on the default lane-resident launch (148 CTAs, 3-lane groups,
+    partial last group), checked over the WHOLE lane range:
+    * a seeded random sample of 4,096 pairs spread over all 2^20 lanes (plus the first and last
+      lane of every CTA's first group, the CTA-stride boundary and the partial last group):
+      XOR and AND ciphertexts equal the oracle's compact NAND chain on host-encrypted inputs
+      (each pair's generator position reached by PCG64 jump-ahead: independent of device
+      encryption);
+    * every one of the 2^21 output ciphertexts is identical with the instantiation that waits
+      on every in-group producer (dbg bit 21) -- the check of the compiled-out RAW waits rule
+      (tc_nand_resident.cuh slot table);
+    * every output decrypts to the right bit."""
+    import torch
+    from oracle import gsw
+    lanes = 1 << 20
+    scheme = GswScheme(DEFAULT_PARAMS)
+    keys = scheme.keygen(1)
+    rng = np.random.default_rng(1)
+    bits = rng.integers(0, 2, (lanes, 2))
+    enc_state = rng.bit_generator.state                  # generator position of pair 0's a
+    eng = GpuEngine(scheme, keys=keys, rng=rng, batch_size=lanes, device_encrypt=True)
+    a, b = eng.input_block(bits)
+    x, y = xor_(a, b), and_(a, b)
+    prog = eng.flush()
+    assert eng.last_compile["schedule"] == "resident" and prog.launches == 1
+    got = eng.read_back_bits([x, y])
+    assert (got[0] == (bits[:, 0] ^ bits[:, 1])).all()
+    assert (got[1] == (bits[:, 0] & bits[:, 1])).all()
+    # sample: random lanes + structural boundaries of the resident launch
+    n_groups, grid = -(-lanes // 3), 148
+    special = [0, 1, 2, 3 * grid - 1, 3 * grid, 3 * grid + 1, lanes - 2, lanes - 1]
+    special += [3 * c for c in range(grid)] + [3 * c + 2 for c in range(grid)]
+    smp = np.unique(np.concatenate([np.random.default_rng(2024).choice(lanes, 4096, replace=False),
+                                    np.array(special)]))
+    vx, vy = (eng.read_nodes([h.node], [0], lanes=smp)[0] for h in (x, y))
+    p = gsw.DEFAULT
+    step = p.n_ct * p.m // 2                              # raw 64-bit draws per ciphertext
+    gen = np.random.Generator(np.random.PCG64())
+    bad = []
+    for i, lane in enumerate(smp.tolist()):
+        ins = []
+        for j in (0, 1):
+            gen.bit_generator.state = enc_state
+            gen.bit_generator.advance((2 * lane + j) * step)
+            ins.append(scheme.encrypt_many(keys.public_key, [int(bits[lane, j])], gen)[0].astype(np.int64))
+        va, vb = ins
+        n1 = gsw.hom_nand_compact(p, va, vb)
+        t1 = gsw.hom_nand_compact(p, n1, va)              # n1 is noisier: swapped left
+        t2 = gsw.hom_nand_compact(p, n1, vb)
+        want_x = gsw.hom_nand_compact(p, t1, t2)
+        want_y = gsw.hom_nand_compact(p, n1, n1)
+        if not (np.array_equal(vx[i], want_x) and np.array_equal(vy[i], want_y)):
+            bad.append(lane)
+    assert not bad, f"{len(bad)} sampled pairs differ from the oracle, first lanes {bad[:8]}"
+    # the compiled-out waits: same outputs with every in-group producer awaited
+    ctx = eng.ctx
+    sx, sy = (eng._slot[h.node] * lanes for h in (x, y))
+    ref = [_store_view(ctx, s0, lanes).clone() for s0 in (sx, sy)]
+    ctx.set_debug(1 << 21)
+    prog.run(lanes)
+    ctx.sync()
+    ctx.set_debug(0)
+    torch.cuda.synchronize()
+    for r, s0 in zip(ref, (sx, sy)):
+        assert torch.equal(r, _store_view(ctx, s0, lanes))
+    del ref
+    torch.cuda.empty_cache()
 
 
 def test_tiled_program_refuses_level_fallback():

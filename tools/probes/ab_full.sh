@@ -12,7 +12,7 @@ for lib in "$@"; do
     timeout -s KILL 600 python -m pytest tests/test_gpu_kernels.py -x -q -m gpu 2>&1 | tail -2
   fi
   for sch in auto levels; do
-    timeout -s KILL 120 python tools/power_probe.py $LANES $SECS 0 $sch 2>&1 | tail -1
+    timeout -s KILL 120 python tools/probes/power_probe.py $LANES $SECS 0 $sch 2>&1 | tail -1
   done
 done
 cp /tmp/libfhegpu_orig.so paper_1611_08769_b200/libfhegpu.so

@@ -4,6 +4,6 @@ LANES=${LANES:-131072}
 cp paper_1611_08769_b200/libfhegpu.so /tmp/libfhegpu_orig.so
 for lib in "$@"; do
   cp "$lib" paper_1611_08769_b200/libfhegpu.so
-  echo "== $lib"; timeout -s KILL 120 python tools/power_probe.py $LANES 4 2>&1 | tail -1
+  echo "== $lib"; timeout -s KILL 120 python tools/probes/power_probe.py $LANES 4 2>&1 | tail -1
 done
 cp /tmp/libfhegpu_orig.so paper_1611_08769_b200/libfhegpu.so

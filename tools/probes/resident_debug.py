@@ -5,7 +5,7 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
+sys.path.insert(0, "/root/repo")
 from paper_1611_08769_b200 import DEFAULT0_PARAMS, GswScheme  # noqa: E402
 from paper_1611_08769_b200 import _native as nat  # noqa: E402
 from paper_1611_08769_b200.engine import GpuEngine  # noqa: E402
