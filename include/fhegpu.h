@@ -118,6 +118,15 @@ int fhegpu_store_write_range(fhegpu_ctx *ctx, uint64_t first, uint64_t count,
 int fhegpu_store_read_range(fhegpu_ctx *ctx, uint64_t first, uint64_t count, uint32_t *host_v,
                             int async);
 
+/* Device-side copies of whole slots: for i < n, ciphertexts [src_slots[i] * lanes, +lanes)
+ * -> [dst_slots[i] * lanes, +lanes).  Destinations must be distinct and must not be a
+ * source of another pair.  Used to bind a cached program's private input slots to the
+ * wires a caller holds and to hand its outputs back (no counterpart in the reference:
+ * its Ciphertext values are immutable Python objects, fhe.py:148-161).  Asynchronous on the
+ * context stream. */
+int fhegpu_store_copy_slots(fhegpu_ctx *ctx, const uint32_t *src_slots, const uint32_t *dst_slots, uint32_t n,
+                            uint64_t lanes);
+
 /* Store range <-> the reference's serialised ciphertexts (FHEGPU_HOST_PACKED rows of
  * ceil(N*N/8) bytes: fileio.py:72-79, one ciphertext of an EFT1 payload).  Synchronous. */
 int fhegpu_store_write_packed(fhegpu_ctx *ctx, uint64_t first, uint64_t count, const uint8_t *host_bytes);

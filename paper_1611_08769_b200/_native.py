@@ -70,6 +70,7 @@ SIGNATURES = [
     ("fhegpu_res_slot_order", ctypes.c_int, [_P, ctypes.c_uint32, ctypes.c_uint32, _P]),
     ("fhegpu_store_write_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     ("fhegpu_store_read_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
+    ("fhegpu_store_copy_slots", ctypes.c_int, [_P, _U32P, _U32P, ctypes.c_uint32, ctypes.c_uint64]),
     ("fhegpu_prog_run_host", ctypes.c_int, [_P, _P, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int,
                                             ctypes.c_uint32, _P, _P, ctypes.c_uint32, _P, _P]),
     ("fhegpu_prog_destroy", None, [_P]),
@@ -322,6 +323,15 @@ class DeviceContext:
         """Store range -> serialised ciphertexts (ceil(N^2/8) bytes each)."""
         _check(_lib.fhegpu_store_read_packed(self.handle, first, count, ctypes.c_void_p(host_ptr)),
                "store_read_packed")
+
+    def copy_slots(self, src_slots, dst_slots, lanes: int):
+        """Whole-slot device copies: slot src[i] -> dst[i] over `lanes` ciphertexts each."""
+        src = np.ascontiguousarray(src_slots, dtype=np.uint32)
+        dst = np.ascontiguousarray(dst_slots, dtype=np.uint32)
+        if src.shape != dst.shape:
+            raise ValueError("copy_slots: source and destination counts differ")
+        _check(_lib.fhegpu_store_copy_slots(self.handle, _ptr(src, ctypes.c_uint32), _ptr(dst, ctypes.c_uint32),
+                                            len(src), int(lanes)), "store_copy_slots")
 
     def read(self, idx, complement=None) -> np.ndarray:
         idx = np.ascontiguousarray(idx, dtype=np.uint64)

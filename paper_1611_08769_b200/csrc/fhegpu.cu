@@ -63,6 +63,8 @@ struct fhegpu_ctx {
   size_t idx_cap = 0;
   uint8_t *d_comp = nullptr;
   size_t comp_cap = 0;
+  uint32_t *d_copy = nullptr;  // slot pairs of fhegpu_store_copy_slots (only written stream-ordered)
+  size_t copy_cap = 0;
   OpRec *d_tmp_ops = nullptr;
   size_t tmp_ops_cap = 0;
   JumpTable *d_jump = nullptr;  // PCG64 jump-ahead constants (lazily uploaded)
@@ -410,6 +412,7 @@ void fhegpu_ctx_destroy(fhegpu_ctx *c) {
   cudaFree(c->d_stage);
   cudaFree(c->d_idx);
   cudaFree(c->d_comp);
+  cudaFree(c->d_copy);
   cudaFree(c->d_tmp_ops);
   cudaFree(c->d_jump);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -550,6 +553,42 @@ int fhegpu_store_read(fhegpu_ctx *c, const uint64_t *idx, const uint8_t *comp, u
 int fhegpu_store_read_rows(fhegpu_ctx *c, const uint64_t *idx, const uint8_t *comp, uint64_t count,
                            uint32_t row, uint32_t *host_rows) {
   return read_impl(c, idx, comp, count, (int)row, host_rows);
+}
+
+int fhegpu_store_copy_slots(fhegpu_ctx *c, const uint32_t *src_slots, const uint32_t *dst_slots, uint32_t n,
+                            uint64_t lanes) {
+  if (!c || (n && (!src_slots || !dst_slots))) return fail(FHEGPU_EINVAL, "null argument");
+  if (n == 0 || lanes == 0) return FHEGPU_OK;
+  std::vector<uint32_t> both(2 * (size_t)n);
+  for (uint32_t i = 0; i < n; ++i) {
+    if (((uint64_t)src_slots[i] + 1) * lanes > c->capacity || ((uint64_t)dst_slots[i] + 1) * lanes > c->capacity)
+      return fail(FHEGPU_EINVAL, "slot " + std::to_string(std::max(src_slots[i], dst_slots[i])) + " x " +
+                                     std::to_string(lanes) + " lanes beyond store capacity " +
+                                     std::to_string(c->capacity));
+    both[i] = src_slots[i];
+    both[n + i] = dst_slots[i];
+  }
+  {  // no destination may be written twice or read by another pair
+    std::vector<uint32_t> dsts(both.begin() + n, both.end());
+    std::sort(dsts.begin(), dsts.end());
+    for (uint32_t i = 1; i < n; ++i)
+      if (dsts[i] == dsts[i - 1]) return fail(FHEGPU_EINVAL, "duplicate destination slot " + std::to_string(dsts[i]));
+    for (uint32_t i = 0; i < n; ++i)
+      if (both[i] != both[n + i] && std::binary_search(dsts.begin(), dsts.end(), both[i]))
+        return fail(FHEGPU_EINVAL, "source slot " + std::to_string(both[i]) + " is another pair's destination");
+  }
+  CUDA_TRY(cudaSetDevice(c->device));
+  // a dedicated buffer, written only by stream-ordered copies: the previous call's kernel has
+  // read it before this upload lands, so the call stays asynchronous
+  if (int rc = ensure((void **)&c->d_copy, &c->copy_cap, both.size() * 4)) return rc;
+  uint32_t *d = c->d_copy;
+  CUDA_TRY(cudaMemcpyAsync(d, both.data(), both.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  const uint64_t run_u4 = lanes * c->p.ct_words / 4;
+  dim3 grid((unsigned)std::max<uint64_t>(1, std::min<uint64_t>((run_u4 + 255) / 256, 1024)),
+            std::min<uint32_t>(n, 65535u));
+  copy_slots_kernel<<<grid, 256, 0, c->stream>>>(c->store, d, d + n, n, run_u4);
+  CUDA_TRY(cudaGetLastError());
+  return FHEGPU_OK;
 }
 
 int fhegpu_store_write_range(fhegpu_ctx *c, uint64_t first, uint64_t count, const uint32_t *host_v,

@@ -113,6 +113,21 @@ __global__ void scatter_kernel(uint32_t *__restrict__ store, const uint64_t *__r
   }
 }
 
+// Slot blocks -> slot blocks (fhegpu_store_copy_slots): slot s holds ciphertexts
+// [s * lanes, (s + 1) * lanes), one contiguous run of lanes * ct_words u32, copied as uint4
+// (ct_words is a multiple of 4).  blockIdx.y strides the pairs, blockIdx.x the run.
+__global__ void copy_slots_kernel(uint32_t *__restrict__ store, const uint32_t *__restrict__ src,
+                                  const uint32_t *__restrict__ dst, uint32_t n, uint64_t run_u4) {
+  uint4 *st = reinterpret_cast<uint4 *>(store);
+  for (uint32_t i = blockIdx.y; i < n; i += gridDim.y) {
+    const uint4 *from = st + (uint64_t)src[i] * run_u4;
+    uint4 *to = st + (uint64_t)dst[i] * run_u4;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < run_u4;
+         t += (uint64_t)gridDim.x * blockDim.x)
+      to[t] = from[t];
+  }
+}
+
 // Host-streaming repack (fhegpu_prog_run_host): rows of `words` u32 (dense, as the host
 // holds them) <-> store rows of ct_words (padding zeroed).  One row per block iteration.
 __global__ void dense_to_store_kernel(uint32_t *__restrict__ store, const uint32_t *__restrict__ dense,

@@ -75,6 +75,36 @@ class GpuBit:
         return None if self.const else self.engine.export_ct(self)
 
 
+class CircuitTemplate:
+    """A recorded circuit call (e.g. one ``fft_1d`` over one word format), replayable on any
+    inputs with the same structure without re-running the Python circuit code.
+
+    The netlist of the reference's circuits depends only on the call's static arguments and
+    on the input wires' structure (which bits alias which node, complement flags, constants)
+    and their level / noise estimates -- never on the encrypted data (fft.py:137-174 calls
+    engine.nand in a fixed order; the fold and swap rules of engine.py:168-187 / fhe.py:336
+    read only that bookkeeping).  Local node ids: 0..n_in-1 are the distinct input nodes,
+    n_in.. the nodes the call created.  ``outs`` rows: (kind, value, neg), kind 0 = public
+    constant `value`, 1 = local node `value`."""
+
+    _next_uid = 0
+
+    def __init__(self, n_in, in_levels, in_ests, ops, levels, ests, outs, nand_count, executed,
+                 max_level, wires):
+        CircuitTemplate._next_uid += 1
+        self.uid = CircuitTemplate._next_uid
+        self.n_in = n_in
+        self.in_levels, self.in_ests = in_levels, in_ests
+        self.ops = ops                      # (n_ops, 5) int64: left, lneg, right, rneg, out (local ids)
+        self.levels, self.ests = levels, ests
+        self.outs = outs
+        self.nand_count, self.executed = nand_count, executed
+        self.max_level, self.wires = max_level, wires
+        out_nodes = outs[outs[:, 0] == 1, 1]
+        self.out_internal = np.unique(out_nodes[out_nodes >= n_in])     # local ids, sorted
+        self.compiled: dict = {}            # (batch, schedule pref, kernel) -> region compile | None
+
+
 class LevelledNetlist:
     """Lazy netlist recorder shared by the GPU engines: node tables (level, noise estimate,
     slot, live-handle refcount), pending gates, and the level sort + liveness slot allocation
@@ -295,6 +325,11 @@ class GpuEngine(LevelledNetlist):
         self._enc_stream_id: dict = {}
         self._enc_rows: list[np.ndarray] = []     # per chunk: (stream_idx, u32_off, mu, target)
         self._draws_per_ct = self.params.n_ct * self.params.m
+        # circuit templates (`circuit`): a replayed call stays one lazy macro until flush
+        self._macros: list[tuple] = []      # (template, input nodes, real node per out_internal)
+        self._capturing = False
+        self._regions: dict = {}            # template uid -> (base slot, Program, compile)
+        self.template_hits = 0
 
     # -- protocol attributes -----------------------------------------------------------
 
@@ -493,6 +528,8 @@ class GpuEngine(LevelledNetlist):
     def nand(self, a: GpuBit, b: GpuBit) -> GpuBit:
         if a.engine is not self or b.engine is not self:
             raise UsageError("cannot mix handles from different engines")
+        if self._macros:
+            self._expand_macros()
         if a.const or b.const:
             return self._fold(a, b)
         la, lb = self._level[a.node], self._level[b.node]
@@ -619,12 +656,251 @@ class GpuEngine(LevelledNetlist):
         cts = [Ciphertext(vals[l], lvl, est, self.params) for l in range(self.batch_size)]
         return cts[0] if self.batch_size == 1 else cts
 
+    # -- circuit templates ------------------------------------------------------------------
+
+    _TEMPLATES: "dict" = {}            # shared by engines: (key, params, input pattern) -> template
+    TEMPLATE_CACHE = 16
+
+    def circuit(self, key, fn, in_bits, flatten, rebuild):
+        """Run ``fn()`` -- a circuit call over the wires ``in_bits`` whose netlist is a function
+        of ``key`` and the inputs' structure alone -- recording it once as a template and
+        replaying the template on later calls with the same key (no Python per gate).
+
+        ``flatten(result)`` lists the output wires of a call's return value and
+        ``rebuild(handles)`` turns such a list back into one.  Falls back to plain recording
+        when a trace or CSE is on."""
+        if self._capturing or self.trace is not None or self._cse_map is not None:
+            return fn()
+        pattern, in_nodes = self._input_pattern(in_bits)
+        if pattern is None:
+            return fn()
+        p = self.params
+        full = (key, (p.n, p.q, p.m, p.noise_bound, p.depth_budget), pattern)
+        tpl = self._TEMPLATES.get(full)
+        if tpl is not None:
+            self._TEMPLATES[full] = self._TEMPLATES.pop(full)          # LRU touch
+            self.template_hits += 1
+            return rebuild(self._apply_template(tpl, in_nodes))
+        if self._macros:
+            self._expand_macros()
+        n0, op0 = len(self._level), len(self._pending_ops)
+        nand0, exec0, wire0 = self.nand_count, self.executed_nands, self._wire
+        self._capturing = True
+        try:
+            result = fn()
+        finally:
+            self._capturing = False
+        tpl = self._capture(in_nodes, n0, op0, flatten(result), nand0, exec0, wire0)
+        if tpl is not None:
+            self._TEMPLATES[full] = tpl
+            while len(self._TEMPLATES) > self.TEMPLATE_CACHE:
+                self._TEMPLATES.pop(next(iter(self._TEMPLATES)))
+        return result
+
+    def _input_pattern(self, in_bits):
+        """Hashable structure of the input wires: per bit ('c', value) or (distinct-node index,
+        complement), plus each distinct node's (level, noise estimate)."""
+        index, nodes, pat = {}, [], []
+        for h in in_bits:
+            if getattr(h, "engine", None) is not self:
+                return None, None
+            if h.const:
+                pat.append((-1, int(h.plain)))
+                continue
+            i = index.get(h.node)
+            if i is None:
+                i = index[h.node] = len(nodes)
+                nodes.append(h.node)
+            pat.append((i, h.neg))
+        info = tuple((self._level[n], self._est[n]) for n in nodes)
+        return (tuple(pat), info), nodes
+
+    def _capture(self, in_nodes, n0, op0, out_handles, nand0, exec0, wire0):
+        """Template of the ops recorded since (n0, op0), or None if the call reached outside
+        its inputs (then it is simply not cached)."""
+        n_in = len(in_nodes)
+        ops = np.asarray(self._pending_ops[op0:], dtype=np.int64).reshape(-1, 5)
+        n1 = len(self._level)
+        local = {nd: i for i, nd in enumerate(in_nodes)}
+
+        def to_local(arr):
+            out = np.empty(arr.shape, dtype=np.int64)
+            new = arr >= n0
+            out[new] = arr[new] - n0 + n_in
+            for j in np.flatnonzero(~new):
+                li = local.get(int(arr[j]))
+                if li is None:
+                    return None
+                out[j] = li
+            return out
+
+        cols = [to_local(ops[:, c]) for c in (0, 2, 4)]
+        if any(c is None for c in cols):
+            return None
+        lops = np.stack([cols[0], ops[:, 1], cols[1], ops[:, 3], cols[2]], axis=1)
+        outs = np.empty((len(out_handles), 3), dtype=np.int64)
+        for j, h in enumerate(out_handles):
+            if h.const:
+                outs[j] = (0, int(h.plain), 0)
+                continue
+            if h.node >= n0:
+                outs[j] = (1, h.node - n0 + n_in, h.neg)
+            elif h.node in local:
+                outs[j] = (1, local[h.node], h.neg)
+            else:
+                return None
+        levels = np.asarray(self._level[n0:n1], dtype=np.int64)
+        ests = np.asarray(self._est[n0:n1], dtype=np.int64)
+        return CircuitTemplate(n_in, [self._level[n] for n in in_nodes], [self._est[n] for n in in_nodes],
+                               lops, levels, ests, outs, self.nand_count - nand0,
+                               self.executed_nands - exec0, int(levels.max()) if len(levels) else 0,
+                               self._wire - wire0)
+
+    def _apply_template(self, tpl, in_nodes):
+        """Replay: account the gates, create nodes only for the outputs; the call's gates stay
+        one pending macro (expanded into ops only if something else joins the program)."""
+        self.nand_count += tpl.nand_count
+        self.executed_nands += tpl.executed
+        if tpl.max_level > self.max_depth:
+            self.max_depth = tpl.max_level
+        self._wire += tpl.wires
+        real = {}
+        for li in tpl.out_internal.tolist():
+            k = li - tpl.n_in
+            real[li] = self._new_node(int(tpl.levels[k]), int(tpl.ests[k]))
+        for i, nd in enumerate(in_nodes):
+            real[i] = nd
+        self._macros.append((tpl, list(in_nodes), [real[li] for li in tpl.out_internal.tolist()]))
+        if len(self._macros) > 1 or self._pending_ops:
+            self._expand_macros()
+        out = []
+        for kind, val, neg in tpl.outs.tolist():
+            out.append(self.constant(val) if kind == 0 else GpuBit(self, real[val], neg, False, None, -1))
+        return out
+
+    def _expand_macros(self):
+        """Materialise pending template replays as ordinary nodes and ops."""
+        macros, self._macros = self._macros, []
+        for tpl, in_nodes, out_real in macros:
+            n_local = tpl.n_in + len(tpl.levels)
+            m = np.empty(n_local, dtype=np.int64)
+            m[:tpl.n_in] = in_nodes
+            have = np.zeros(n_local, dtype=bool)
+            have[:tpl.n_in] = True
+            m[tpl.out_internal] = out_real
+            have[tpl.out_internal] = True
+            fresh = np.flatnonzero(~have)
+            base = len(self._level)
+            m[fresh] = base + np.arange(len(fresh))
+            k = fresh - tpl.n_in
+            self._level.extend(tpl.levels[k].tolist())
+            self._est.extend(tpl.ests[k].tolist())
+            self._slot.extend([-1] * len(fresh))
+            self._refs.extend([0] * len(fresh))
+            ops = tpl.ops.copy()
+            for c in (0, 2, 4):
+                ops[:, c] = m[ops[:, c]]
+            self._pending_ops.extend(ops.ravel().tolist())
+
+    def _template_compile(self, tpl):
+        """The template compiled once as a self-contained program over private slots
+        0..S-1 (inputs at 0..n_in-1, every output kept), or None when the schedule it
+        would get here (tiled / resident: shallow programs) needs the engine's own layout."""
+        ck = (self.batch_size, self.schedule, None if self.dry_run else self.ctx.kernel)
+        if ck in tpl.compiled:
+            return tpl.compiled[ck]
+        saved = (self._level, self._est, self._slot, self._refs, self._free, self._n_slots,
+                 self._pending_ops, self.keep_all)
+        n_in = tpl.n_in
+        try:
+            self._level = list(tpl.in_levels) + tpl.levels.tolist()
+            self._est = list(tpl.in_ests) + tpl.ests.tolist()
+            n_local = len(self._level)
+            self._slot = list(range(n_in)) + [-1] * (n_local - n_in)
+            refs = np.zeros(n_local, dtype=np.int64)
+            refs[tpl.out_internal] = 1
+            refs[tpl.outs[(tpl.outs[:, 0] == 1) & (tpl.outs[:, 1] < n_in), 1]] = 1   # pass-through inputs
+            self._refs = refs.tolist()
+            self._free, self._n_slots, self.keep_all = [], n_in, False
+            self._pending_ops = tpl.ops.ravel().tolist()
+            sched = self._pick_schedule()
+            comp = None
+            if sched not in ("tiled", "resident"):
+                prog = self._compile(ssa=sched in ("dataflow", "queue"))
+                prog["schedule"] = sched
+                out_slots = np.asarray(self._slot, dtype=np.int64)[tpl.out_internal]
+                comp = {"prog": prog, "n_slots": self._n_slots, "out_slots": out_slots}
+        finally:
+            (self._level, self._est, self._slot, self._refs, self._free, self._n_slots,
+             self._pending_ops, self.keep_all) = saved
+        tpl.compiled[ck] = comp
+        return comp
+
+    def _run_macro(self, macro):
+        """Flush of exactly one template replay: bind the inputs into the template's private
+        slot region (device copies), run its cached program, copy the held outputs out.
+        None when the template has no region program here (then it is expanded)."""
+        tpl, in_nodes, out_real = macro
+        if self.dry_run or self.keep_all:
+            return None
+        comp = self._template_compile(tpl)
+        if comp is None:
+            return None
+        lanes = self.batch_size
+        reg = self._regions.get(tpl.uid)
+        if reg is None:
+            base = self._n_slots                       # a private block, never in the free list
+            self._n_slots += comp["n_slots"]
+            self._ensure_capacity()
+            prog = comp["prog"]
+            table = prog["ops"].copy()
+            for f in ("left", "right", "out"):
+                table[f] += np.uint32(base)
+            program = self.ctx.program(table, prog["offsets"])
+            if prog["schedule"] in ("dataflow", "queue"):
+                program.set_deps(prog["deps"])
+            if prog["schedule"] == "queue":
+                program.set_queue(True)
+            reg = self._regions[tpl.uid] = (base, program)
+        base, program = reg
+        self._ensure_capacity()
+        src = [self._slot[n] for n in in_nodes]
+        if min(src) < 0:
+            raise UsageError("template input has no live ciphertext")
+        self.ctx.copy_slots(src, [base + i for i in range(tpl.n_in)], lanes)
+        program.run(lanes)
+        held = [j for j, nd in enumerate(out_real) if self._refs[nd] > 0]
+        dst = []
+        for j in held:
+            slot = self._alloc_slot()
+            self._slot[out_real[j]] = slot
+            dst.append(slot)
+        self._ensure_capacity()
+        if held:
+            self.ctx.copy_slots([base + int(comp["out_slots"][j]) for j in held], dst, lanes)
+        for nd in in_nodes:                              # inputs nobody holds any more
+            if self._refs[nd] <= 0 and self._slot[nd] >= 0:
+                self._free.append(self._slot[nd])
+                self._slot[nd] = -1
+        self.last_program = program
+        self.last_compile = dict(comp["prog"], template=tpl.uid)
+        self.programs_run += 1
+        self.launches += program.launches
+        return program
+
     # -- compile + run ------------------------------------------------------------------------
 
     def flush(self):
         """Evaluate every pending gate: one kernel launch per level over all lanes."""
         if not self.dry_run:
             self._upload_inputs()
+        if self._macros:
+            if len(self._macros) == 1 and not self._pending_ops:
+                program = self._run_macro(self._macros[0])
+                if program is not None:
+                    self._macros = []
+                    return program
+            self._expand_macros()
         if not self._pending_ops:
             return None
         sched = self._pick_schedule()

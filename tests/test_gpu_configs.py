@@ -303,7 +303,7 @@ def _store_view(ctx, first_ct, count):
 
     class _Arr:
         __cuda_array_interface__ = {"shape": (count, ctx.ct_words), "typestr": "<u4", "version": 3,
-                                    "data": (ctx.store_ptr() + first_ct * ctx.ct_words * 4, False),
+                                    "data": (ctx.store_ptr + first_ct * ctx.ct_words * 4, False),
                                     "strides": None}
     return torch.as_tensor(_Arr(), device="cuda")
 
