@@ -110,6 +110,13 @@ int fhegpu_store_read(fhegpu_ctx *ctx, const uint64_t *idx, const uint8_t *compl
 int fhegpu_store_read_rows(fhegpu_ctx *ctx, const uint64_t *idx, const uint8_t *complement,
                            uint64_t count, uint32_t row, uint32_t *host_rows /* count x k */);
 
+/* Batched decryption phase (fhe.py:267-286, the sum before rounding): for each ciphertext,
+ * x = sum_{i<k, b<ell} bit_b(V[row][i]) * pw[i*ell + b] mod q, centred to (-q/2, q/2], where
+ * pw[i*ell + b] = (sk_i << b) mod q comes from the caller (the secret key never enters the
+ * library).  The caller rounds x to the bit and applies the reference's noise check. */
+int fhegpu_store_decrypt_rows(fhegpu_ctx *ctx, const uint64_t *idx, const uint8_t *complement,
+                              uint64_t count, uint32_t row, const uint32_t *pw, int32_t *host_x);
+
 /* Contiguous ciphertext ranges [first, first + count) <-> dense host rows (N*k u32 each),
  * one strided async copy (pinned host memory reaches full PCIe bandwidth).  async = 0
  * synchronises the context stream before returning. */

@@ -71,6 +71,9 @@ SIGNATURES = [
     ("fhegpu_store_write_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     ("fhegpu_store_read_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     ("fhegpu_store_copy_slots", ctypes.c_int, [_P, _U32P, _U32P, ctypes.c_uint32, ctypes.c_uint64]),
+    ("fhegpu_store_decrypt_rows", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint8),
+                                                 ctypes.c_uint64, ctypes.c_uint32, _U32P,
+                                                 ctypes.POINTER(ctypes.c_int32)]),
     ("fhegpu_prog_run_host", ctypes.c_int, [_P, _P, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int,
                                             ctypes.c_uint32, _P, _P, ctypes.c_uint32, _P, _P]),
     ("fhegpu_prog_destroy", None, [_P]),
@@ -351,6 +354,18 @@ class DeviceContext:
                                            len(idx), int(row), _ptr(out, ctypes.c_uint32)),
                "store_read_rows")
         return out
+
+    def decrypt_rows(self, idx, row: int, pw: np.ndarray, complement=None) -> np.ndarray:
+        """Centred decryption sums x (int64) of row `row` of each ciphertext (see the header)."""
+        idx = np.ascontiguousarray(idx, dtype=np.uint64)
+        pw = np.ascontiguousarray(pw, dtype=np.uint32)
+        out = np.empty(len(idx), dtype=np.int32)
+        comp = None if complement is None else np.ascontiguousarray(complement, dtype=np.uint8)
+        _check(_lib.fhegpu_store_decrypt_rows(self.handle, _ptr(idx, ctypes.c_uint64),
+                                              None if comp is None else _ptr(comp, ctypes.c_uint8),
+                                              len(idx), int(row), _ptr(pw, ctypes.c_uint32),
+                                              _ptr(out, ctypes.c_int32)), "store_decrypt_rows")
+        return out.astype(np.int64)
 
     # -- programs and scheme operators ------------------------------------------------
     def program(self, ops: np.ndarray, level_offsets) -> Program:

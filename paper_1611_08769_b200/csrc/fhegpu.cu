@@ -555,6 +555,38 @@ int fhegpu_store_read_rows(fhegpu_ctx *c, const uint64_t *idx, const uint8_t *co
   return read_impl(c, idx, comp, count, (int)row, host_rows);
 }
 
+int fhegpu_store_decrypt_rows(fhegpu_ctx *c, const uint64_t *idx, const uint8_t *comp, uint64_t count,
+                              uint32_t row, const uint32_t *pw, int32_t *host_x) {
+  if (!c || !pw || (count && (!idx || !host_x))) return fail(FHEGPU_EINVAL, "null argument");
+  if (row >= c->p.rows) return fail(FHEGPU_EINVAL, "row out of range");
+  if (c->p.k * c->p.ell > 16 * 32) return fail(FHEGPU_EUNSUP, "k * ell beyond 512");
+  if (int rc = check_idx(c, idx, count)) return rc;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t pw_bytes = (size_t)c->p.k * c->p.ell * 4;
+  const uint64_t chunk = std::max<uint64_t>(1, (kStagingCap - pw_bytes) / 4);
+  for (uint64_t s = 0; s < count; s += chunk) {
+    const uint64_t n = std::min(chunk, count - s);
+    if (int rc = ensure((void **)&c->d_stage, &c->stage_bytes, pw_bytes + n * 4)) return rc;
+    if (int rc = ensure((void **)&c->d_idx, &c->idx_cap, n * 8)) return rc;
+    uint32_t *d_pw = c->d_stage;
+    int32_t *d_x = reinterpret_cast<int32_t *>(c->d_stage + c->p.k * c->p.ell);
+    CUDA_TRY(cudaMemcpyAsync(d_pw, pw, pw_bytes, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->d_idx, idx + s, n * 8, cudaMemcpyHostToDevice, c->stream));
+    const uint8_t *dcomp = nullptr;
+    if (comp) {
+      if (int rc = ensure((void **)&c->d_comp, &c->comp_cap, n)) return rc;
+      CUDA_TRY(cudaMemcpyAsync(c->d_comp, comp + s, n, cudaMemcpyHostToDevice, c->stream));
+      dcomp = c->d_comp;
+    }
+    decrypt_rows_kernel<<<grid_for(n, c->num_sms), 256, 0, c->stream>>>(c->store, c->d_idx, dcomp, d_pw, d_x, n,
+                                                                        row, c->p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(host_x + s, d_x, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  return FHEGPU_OK;
+}
+
 int fhegpu_store_copy_slots(fhegpu_ctx *c, const uint32_t *src_slots, const uint32_t *dst_slots, uint32_t n,
                             uint64_t lanes) {
   if (!c || (n && (!src_slots || !dst_slots))) return fail(FHEGPU_EINVAL, "null argument");

@@ -214,6 +214,30 @@ __global__ void store_to_packed_kernel(uint8_t *__restrict__ packed, const uint3
 }
 
 // dense[c] <- store[idx[c]] (complemented when comp[c]); row >= 0 selects one row only.
+// Decryption phase of row `row` (fhe.py:267-286): x = sum_{i,b} bit_b(V[row][i]) * pw[i][b] mod q,
+// pw[i][b] = (sk_i << b) mod q, centred to (-q/2, q/2].  One thread per ciphertext; the host
+// turns x into the bit and checks the noise threshold.
+__global__ void decrypt_rows_kernel(const uint32_t *__restrict__ store, const uint64_t *__restrict__ idx,
+                                    const uint8_t *__restrict__ comp, const uint32_t *__restrict__ pw,
+                                    int32_t *__restrict__ out, uint64_t count, uint32_t row, DevParams p) {
+  __shared__ uint32_t s_pw[16 * 32];
+  for (uint32_t t = threadIdx.x; t < p.k * p.ell; t += blockDim.x) s_pw[t] = pw[t];
+  __syncthreads();
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < count;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t acc = 0;
+    const uint32_t *v_row = store + idx[c] * p.ct_words + (uint64_t)row * p.k;
+    for (uint32_t i = 0; i < p.k; ++i) {
+      uint32_t v = v_row[i];
+      if (comp != nullptr && comp[c]) v = sub_mod(gadget(p, row, i), v, p.q);
+      for (uint32_t b = 0; b < p.ell; ++b)
+        if ((v >> b) & 1u) acc += s_pw[i * p.ell + b];
+    }
+    const uint32_t x = (uint32_t)(acc % p.q);
+    out[c] = x > p.q / 2 ? (int32_t)((int64_t)x - p.q) : (int32_t)x;
+  }
+}
+
 __global__ void gather_kernel(const uint32_t *__restrict__ store, const uint64_t *__restrict__ idx,
                               const uint8_t *__restrict__ comp, uint32_t *__restrict__ dense,
                               uint64_t count, int row, DevParams p) {

@@ -622,8 +622,10 @@ class GpuEngine(LevelledNetlist):
         slots = np.array([self._slot[handles[i].node] for i in var], dtype=np.uint64)
         idx = (slots[:, None] * np.uint64(lanes) + np.arange(lanes, dtype=np.uint64)).ravel()
         comp = np.repeat(np.array([handles[i].neg for i in var], dtype=np.uint8), lanes)
-        rows = self.ctx.read_rows(idx, self._decrypt_row(), comp)
-        bits = self.scheme.decrypt_bits_from_rows(self.secret_key, rows).reshape(len(var), lanes)
+        # the decryption sums on the device (one int per ciphertext crosses PCIe), rounding and
+        # the noise check on the host
+        x = self.ctx.decrypt_rows(idx, self._decrypt_row(), self.scheme.decrypt_weights(self.secret_key), comp)
+        bits = self.scheme.decrypt_bits_from_sums(x).reshape(len(var), lanes)
         out[var] = bits
         return out
 

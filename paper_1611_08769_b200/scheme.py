@@ -308,14 +308,27 @@ class GswScheme:
 
         v_row: (count, k).  Raises NoiseOverflowError like the reference."""
         p = self.params
-        j = (p.q // 2).bit_length() - 1
-        pw = np.array([(int(secret_key[i]) << b) % p.q for i in range(p.k) for b in range(p.ell)],
-                      dtype=np.int64).reshape(p.k, p.ell)
+        pw = self.decrypt_weights(secret_key).astype(np.int64).reshape(p.k, p.ell)
         v = np.asarray(v_row, dtype=np.int64)
         bits = (v[:, :, None] >> np.arange(p.ell, dtype=np.int64)) & 1
         # sum of up to N terms each < q < 2^31 -> < 2^40: exact in int64
         x = np.mod((bits * pw[None]).sum(axis=(1, 2)), p.q)
         x = np.where(x > p.q // 2, x - p.q, x)
+        return self.decrypt_bits_from_sums(x)
+
+    def decrypt_weights(self, secret_key) -> np.ndarray:
+        """pw[i*ell + b] = (sk_i << b) mod q: the weights of row n*ell + j's bits in the
+        reference's <C[row], recompose-weighted sk> (fhe.py:267-286), u32."""
+        p = self.params
+        return np.array([(int(secret_key[i]) << b) % p.q for i in range(p.k) for b in range(p.ell)],
+                        dtype=np.uint32)
+
+    def decrypt_bits_from_sums(self, x: np.ndarray) -> np.ndarray:
+        """Bits from centred decryption sums x in (-q/2, q/2] (fhegpu_store_decrypt_rows), with the
+        reference's rounding and noise check (fhe.py:278-286)."""
+        p = self.params
+        x = np.asarray(x, dtype=np.int64)
+        j = (p.q // 2).bit_length() - 1
         scale = 1 << j
         mu = (2 * x + scale) // (2 * scale)
         noise = np.abs(x - mu * scale)
