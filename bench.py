@@ -5,20 +5,23 @@ Workload (BASELINE.json configs[1], the gate microbenchmark): 2^20 independent
 pairs of encrypted random bits (DEFAULT params, N = 261, keys seed 1, bits and
 encryptions from default_rng(1), pair-major), one XOR + one AND per pair =
 6 NANDs per pair as the reference counts them (gates.py:13-24).  A "step" is
-one evaluation of that whole netlist: 3 levels, one kernel launch each, every
-launch spanning every pair.  Secondary: configs[4], 1024 x 16-point Q4.12
-FFTs (DEFAULT dims, noise-free), reported as FFTs/s.
+one evaluation of that whole netlist: ONE lane-resident launch
+(resident_tc_kernel: each CTA runs the 6-gate per-pair program on 3 lanes at a
+time, intermediates in shared memory).  Secondary lines: configs[4] (1024 x
+16-point Q4.12 FFTs, level launches) and configs[0]/[2]/[3] (single-signal
+FFTs), each with first-call host costs (encrypt / record / compile) and an
+API-level e2e after the first call (circuit template replay).
 
   value      NAND/s, inputs resident in HBM, device time (CUDA events, max over ranks)
   e2e        same metric through the C-ABI with host buffers: pinned H2D of the
              step's input ciphertexts + evaluation + D2H of every output ciphertext
-  roofline   level_tc_ws_kernel: algorithmic bytes 3*ceil(N^2/8) per NAND / avg launch time
-             (cfg1 runs as ONE tiled dataflow launch per step: launch time = step time)
-  cpu_baseline  the reference algorithm (oracle/gsw.py restates fhe.py:325-341:
-             float64 N x N product + flatten) on this box's host cores, time-boxed sample
+  roofline   the resident kernel: algorithmic bytes 3*ceil(N^2/8) per NAND / launch time
+             (one launch per step: launch time = step time)
+  cpu_baseline  the unmodified reference (baseline/_ref: FheEngine + gates, fhe.py:325-341)
+             on this box's host cores, one process per core, time-boxed sample; the numpy
+             restatement oracle/gsw.py only when baseline/_ref is absent (kind "port")
 
-`--impl reference` times that CPU path alone (the reference's own implementation,
-restated; the Python reference cannot travel to the GPU box) on every host core.
+`--impl reference` times that same CPU path alone on every host core.
 """
 
 from __future__ import annotations
@@ -41,7 +44,18 @@ UNIT = "NAND/s"
 PAIRS_FULL = 1 << 20
 ALG_BYTES_PER_NAND_261 = 3 * math.ceil(261 * 261 / 8)   # 25,548 B
 MMA_MAC_SLOTS_PER_NAND = 2 * 9 * 128 * 48 * 32 + 9 * 64 * 48 * 32   # 4,423,680 (tc_nand_ws.cuh)
-I8_DENSE_TOPS = 4500.0                                   # B200 dense int8 spec
+I8_DENSE_TOPS = 4500.0                                   # B200 dense int8 spec (fallback)
+ALG_U8_MACS_PER_NAND = 261 * 261 * 9 * 4                 # N^2 k MACs x 4 byte digits
+
+
+def _i8_peak():
+    """Measured dense i8 tcgen05 peak (tools/micro/mma_bench.cu peak mode, profiles/i8_peak.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "i8_peak.json")) as fh:
+            d = json.load(fh)
+        return float(d["i8_dense_tops"]), "measured: " + d.get("shape", "") + " (profiles/i8_peak.json)"
+    except Exception:
+        return I8_DENSE_TOPS, "spec (B200 dense int8; profiles/i8_peak.json absent)"
 
 
 def _fft_roofline(nand_per_s: float, n_ct: int) -> dict:
@@ -65,10 +79,45 @@ def _peaks():
 # CPU reference leg (oracle port of the reference algorithm), process pool
 # ----------------------------------------------------------------------------------------
 
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")      # the driver's install of the reference
+
+
+def reference_available() -> bool:
+    return os.path.isfile(os.path.join(REF_PATH, "fhefft", "engine.py"))
+
+
 def _cpu_worker(args):
-    seconds, seed = args
+    """One host process: XOR + AND pairs (gates.py:13-24, 6 NANDs) for `seconds`.
+
+    kind "reference": the unmodified reference from baseline/_ref through its own public API
+    (fhefft.engine.FheEngine, threads=1 -> GswScheme.hom_nand, fhe.py:325-341);
+    kind "port": oracle/gsw.py's restatement of the same float64 algorithm (fallback)."""
+    seconds, seed, kind = args
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     import numpy as np
+    if kind == "reference":
+        sys.path.insert(0, REF_PATH)
+        from fhefft.engine import FheEngine
+        from fhefft.fhe import DEFAULT_PARAMS, GswScheme
+        from fhefft.gates import and_, xor_
+        scheme = GswScheme(DEFAULT_PARAMS)
+        keys = scheme.keygen(seed=1)
+        eng = FheEngine(scheme, keys, rng=np.random.default_rng(1000 + seed), threads=1)
+        plain = [int(b) for b in np.random.default_rng(2000 + seed).integers(0, 2, 8)]
+        ins = [eng.input_bit(b) for b in plain]
+        x, y = xor_(ins[0], ins[3]), and_(ins[0], ins[3])          # correctness, untimed
+        assert eng.read_back(x) == plain[0] ^ plain[3] and eng.read_back(y) == plain[0] & plain[3]
+        eng.nand_count = 0
+        t0 = time.perf_counter()
+        i = 0
+        while True:
+            a, b = ins[i % 8], ins[(i + 3) % 8]
+            xor_(a, b)
+            and_(a, b)
+            i += 1
+            el = time.perf_counter() - t0
+            if el >= seconds:
+                return eng.nand_count, el
     from oracle import gsw
     p = gsw.DEFAULT
     pk, _ = gsw.keygen(p, 1)
@@ -93,17 +142,28 @@ def _cpu_worker(args):
             return nands, el
 
 
-def cpu_reference(seconds: float, workers: int | None = None):
-    """Aggregate NAND/s of the reference algorithm on `workers` host processes."""
+def cpu_reference(seconds: float, workers: int | None = None, kind: str | None = None):
+    """Aggregate NAND/s of the reference on `workers` host processes (one per core, each
+    single-threaded, OPENBLAS_NUM_THREADS=1 set before numpy loads: SURVEY 8(d))."""
     import multiprocessing as mp
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    kind = kind or ("reference" if reference_available() else "port")
     workers = workers or os.cpu_count() or 1
     ctx = mp.get_context("spawn")
     with ctx.Pool(workers) as pool:
-        res = pool.map(_cpu_worker, [(seconds, i) for i in range(workers)])
+        res = pool.map(_cpu_worker, [(seconds, i, kind) for i in range(workers)])
     total = sum(n for n, _ in res)
     wall = max(t for _, t in res)
-    return total / wall, workers, total
+    return total / wall, workers, total, kind
+
+
+def _cpu_sample_text(kind, cores, seconds, total):
+    what = ("the unmodified reference (baseline/_ref: fhefft.engine.FheEngine threads=1 + gates.xor_/and_ "
+            "-> GswScheme.hom_nand, fhe.py:325-341)" if kind == "reference" else
+            "oracle/gsw.py hom_nand_matrix (the reference's float64 N x N product + flatten restated, "
+            "fhe.py:325-341; baseline/_ref absent)")
+    return (f"{cores} processes x {seconds:.0f} s time-boxed XOR+AND pairs ({total} NANDs) of {what}, "
+            f"DEFAULT params, OPENBLAS_NUM_THREADS=1")
 
 
 # ----------------------------------------------------------------------------------------
@@ -391,46 +451,151 @@ def e2e_gates(eng, scheme, prog, lanes, inputs, outputs, stream, args, world, bi
             }
 
 
+def _api_calls(eng, values, fmt, dims, n_calls, two_d=False):
+    """Wall time of whole API calls on `eng` (the circuit template is already recorded):
+    encrypt the host plaintext (device PCG64 encryption), fft_1d / fft_2d, flush (the
+    template's cached program), decrypt every output bit back to host words."""
+    import torch
+
+    from paper_1611_08769_b200 import fft_1d, fft_2d, input_signal
+    from paper_1611_08769_b200.fft import read_signal_ints
+    times = []
+    words = None
+    for _ in range(n_calls):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sig = input_signal(eng, values, fmt, dims=dims)
+        out = fft_2d(sig) if two_d else fft_1d(sig)
+        eng.flush()
+        words = read_signal_ints(eng, out)
+        times.append(time.perf_counter() - t0)
+        del sig, out
+    return statistics.median(times), words
+
+
 def bench_fft(args, world, rank, local):
     """configs[4]: 1024 independent 16-point Q4.12 FFTs as lanes of one netlist."""
     import numpy as np
     import torch
 
     from paper_1611_08769_b200 import DEFAULT0_PARAMS, FixedFormat, GpuEngine, GswScheme, fft_1d, input_signal
-    from paper_1611_08769_b200.fft import read_signal_ints
+    from paper_1611_08769_b200.fft import read_signal_ints, signal_words
     lanes = args.fft_lanes
     scheme = GswScheme(DEFAULT0_PARAMS, device=local)
     keys = scheme.keygen(4)
-    rngs, vals = [], []
-    for lane in range(lanes):
-        r = np.random.default_rng(4 + lane + rank * lanes)
-        re = r.uniform(-1, 1, 16)
-        im = r.uniform(-1, 1, 16)
-        rngs.append(r)
-        vals.append(re + 1j * im)
-    t0 = time.perf_counter()
-    eng = GpuEngine(scheme, keys=keys, batch_size=lanes, lane_rngs=rngs, device_encrypt=True)
+    fmt = FixedFormat(16, 12)
+
+    def lane_inputs():
+        rngs, vals = [], []
+        for lane in range(lanes):
+            r = np.random.default_rng(4 + lane + rank * lanes)
+            re = r.uniform(-1, 1, 16)
+            im = r.uniform(-1, 1, 16)
+            rngs.append(r)
+            vals.append(re + 1j * im)
+        return rngs, np.array(vals)
+    rngs, vals = lane_inputs()
     stream = torch.cuda.Stream(device=local)
     torch.cuda.set_stream(stream)
     scheme.ctx.use_torch_stream(stream)
-    out = fft_1d(input_signal(eng, np.array(vals), FixedFormat(16, 12)))
-    build_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    eng = GpuEngine(scheme, keys=keys, batch_size=lanes, lane_rngs=rngs, device_encrypt=True)
+    sig = input_signal(eng, vals, fmt)
+    t1 = time.perf_counter()
+    out = fft_1d(sig)
+    t2 = time.perf_counter()
     prog = eng.flush()
-    torch.cuda.synchronize()
+    t3 = time.perf_counter()
     got = read_signal_ints(eng, out)
+    t4 = time.perf_counter()
+    first = {"encrypt_s": t1 - t0, "record_s": t2 - t1, "compile_s": t3 - t2, "run_read_s": t4 - t3,
+             "total_s": t4 - t0}
     ok = None
+    want = None
     if rank == 0:
         try:
             from tests.helpers import golden_npz
-            ok = bool(np.array_equal(got, golden_npz("clear_cfg4.npz")["words"][:lanes]))
+            want = golden_npz("clear_cfg4.npz")["words"][:lanes]
+            ok = bool(np.array_equal(got, want))
         except Exception:
             ok = None
     ms = time_program(prog, lanes, stream, max(2, args.steps // 2), min(args.warmup, 3), world)
-    return {"ms": ms, "ffts_per_s": lanes * world / (ms / 1e3),
-            "nand_per_s": eng.nand_count * lanes * world / (ms / 1e3),
-            "nand_per_fft": eng.nand_count, "levels": prog.n_levels, "lanes": lanes,
-            "build_s": build_s, "ok": ok,
-            "roofline": _fft_roofline(eng.nand_count * lanes * world / (ms / 1e3), scheme.params.n_ct)}
+    res = {"ms": ms, "ffts_per_s": lanes * world / (ms / 1e3),
+           "nand_per_s": eng.nand_count * lanes * world / (ms / 1e3),
+           "nand_per_fft": eng.nand_count, "levels": prog.n_levels, "lanes": lanes,
+           "launches": prog.launches, "first_call": first, "ok": ok,
+           "schedule": eng.last_compile.get("schedule", "levels"),
+           "roofline": _fft_roofline(eng.nand_count * lanes * world / (ms / 1e3), scheme.params.n_ct)}
+    if args.e2e:
+        res["e2e_ct"] = e2e_fft_ciphertexts(eng, prog, sig, out, lanes, stream, world, args)
+    # whole API calls after the first (circuit template replayed, no per-gate Python)
+    del sig, out
+    rngs, vals = lane_inputs()
+    eng.lane_rngs = rngs
+    api_s, words = _api_calls(eng, vals, fmt, None, 3)
+    res["api"] = {"s_per_call": api_s, "ffts_per_s": lanes * world / api_s,
+                  "ok": None if want is None else bool(np.array_equal(words, want)),
+                  "template_hits": eng.template_hits,
+                  "h2d_bytes": int(lanes * 16 * 2 * 16 * 32), "d2h_bytes": int(lanes * 16 * 2 * 16 * 4)}
+    return res
+
+
+def e2e_fft_ciphertexts(eng, prog, sig, out, lanes, stream, world, args):
+    """configs[4] with the ciphertexts in HOST memory, as a server receives them: every step
+    copies the 512 input ciphertexts of every signal (the reference's serialised bytes, an EFT1
+    payload row each) host -> device, runs the level program, and copies the 512 output
+    ciphertexts back (fhegpu_prog_run_host: lane chunks, copy-in / kernels / copy-out overlapped)."""
+    import numpy as np
+    import torch
+
+    from paper_1611_08769_b200.fft import signal_words
+    p = eng.params
+    ins = [h for w in signal_words(sig) for h in w.bits]
+    outs = [h for w in signal_words(out) for h in w.bits]
+    if any(h.neg or h.const for h in ins + outs):
+        return {"skipped": "complemented or constant wires"}
+    bytes_ct = (p.n_ct * p.n_ct + 7) // 8
+    t0 = time.perf_counter()
+    host_in = [torch.empty((lanes, bytes_ct), dtype=torch.uint8, pin_memory=True) for _ in ins]
+    host_out = [torch.empty((lanes, bytes_ct), dtype=torch.uint8, pin_memory=True) for _ in outs]
+    for h, buf in zip(ins, host_in):
+        eng.ctx.read_packed(eng._slot[h.node] * lanes, lanes, buf.data_ptr())
+    ref_words = None
+    pin_s = time.perf_counter() - t0
+    chunk = args.fft_e2e_chunk
+
+    def step():
+        eng.run_host(prog, list(zip(ins, host_in)), outs, chunk_lanes=chunk, out=host_out, sync=False,
+                     packed=True)
+    step()
+    torch.cuda.synchronize()
+    steps = 2
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    _barrier(world)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    # decrypt lane 0's outputs from the host bytes: the reference's words for signal 0
+    from paper_1611_08769_b200 import Ciphertext
+    from paper_1611_08769_b200.fileio import unpack_compact
+    bits = [eng.scheme.decrypt_bit(eng.secret_key, Ciphertext(unpack_compact(b.numpy()[:1], p)[0], 0, 0, p))
+            for b in host_out]
+    w = []
+    for i in range(0, len(bits), 16):
+        u = sum(b << k for k, b in enumerate(bits[i:i + 16]))
+        w.append(u - (1 << 16) if u >> 15 else u)
+    try:
+        from tests.helpers import golden_npz
+        ref_words = golden_npz("clear_cfg4.npz")["words"][0].tolist()
+    except Exception:
+        pass
+    return {"ms": ms, "ffts_per_s": lanes * world / (ms / 1e3), "steps": steps,
+            "h2d_bytes_per_step": len(ins) * lanes * bytes_ct, "d2h_bytes_per_step": len(outs) * lanes * bytes_ct,
+            "chunk_lanes": chunk, "pin_s": pin_s, "bytes_per_ciphertext": bytes_ct,
+            "decrypt_check_lane0": None if ref_words is None else w == ref_words}
 
 
 def bench_fft_single(args, world, rank, local, cfg):
@@ -447,40 +612,58 @@ def bench_fft_single(args, world, rank, local, cfg):
     seed = {"cfg0": 0, "cfg2": 2, "cfg3": 3}[cfg]
     scheme = GswScheme(EXACT_PARAMS if cfg == "cfg0" else DEFAULT0_PARAMS, device=local)
     keys = scheme.keygen(seed)
-    rng = np.random.default_rng(seed)
-    if cfg == "cfg0":
-        vals = rng.uniform(-1, 1, 8).astype(complex)
-        fmt, dims = FixedFormat(16, 12), None
-    elif cfg == "cfg2":
-        vals = rng.uniform(-1, 1, 32) + 1j * rng.uniform(-1, 1, 32)
-        fmt, dims = FixedFormat(32, 24), None
-    else:
-        vals = (rng.integers(0, 256, (8, 8)) / 255.0).ravel().astype(complex)
-        fmt, dims = FixedFormat(16, 7), (8, 8)
-    eng = GpuEngine(scheme, keys=keys, rng=rng, device_encrypt=True)
+
+    def signal():
+        rng = np.random.default_rng(seed)
+        if cfg == "cfg0":
+            return rng, rng.uniform(-1, 1, 8).astype(complex), FixedFormat(16, 12), None
+        if cfg == "cfg2":
+            return rng, rng.uniform(-1, 1, 32) + 1j * rng.uniform(-1, 1, 32), FixedFormat(32, 24), None
+        return rng, (rng.integers(0, 256, (8, 8)) / 255.0).ravel().astype(complex), FixedFormat(16, 7), (8, 8)
+    rng, vals, fmt, dims = signal()
     stream = torch.cuda.Stream(device=local)
     torch.cuda.set_stream(stream)
     scheme.ctx.use_torch_stream(stream)
+    t0 = time.perf_counter()
+    eng = GpuEngine(scheme, keys=keys, rng=rng, device_encrypt=True)
     sig = input_signal(eng, vals, fmt, dims=dims)
+    t1 = time.perf_counter()
     out = fft_2d(sig) if dims else fft_1d(sig)
+    t2 = time.perf_counter()
     prog = eng.flush()
-    torch.cuda.synchronize()
+    t3 = time.perf_counter()
     got = read_signal_ints(eng, out)[0]
+    t4 = time.perf_counter()
     ok = None
     try:
         want = np.load(os.path.join(ROOT, "tests", "golden", f"clear_{cfg}.npz"))["words"][0]
         ok = bool(np.array_equal(got, want))
     except OSError:
-        pass
+        want = None
     ms = time_program(prog, 1, stream, max(3, args.steps // 2), min(args.warmup, 3), world)
+    sched = eng.last_compile.get("schedule", "levels")
+    launches = prog.launches
+    nand = eng.nand_count                      # one transform (the API calls below add theirs)
+    del sig, out
+    rng, vals, fmt, dims = signal()
+    eng.rng = rng
+    api_s, words = _api_calls(eng, vals, fmt, dims, 5, two_d=dims is not None)
     name = {"cfg0": "8-pt Q4.12 (EXACT params)", "cfg2": "32-pt Q8.24", "cfg3": "8x8 Q9.7 2-D"}[cfg]
+    n_bits = len(vals) * 2 * fmt.total_bits
     return {"metric": f"{name} FHE FFTs/s (configs[{cfg[-1]}], one signal)",
             "value": world / (ms / 1e3), "unit": "FFT/s", "ms_per_fft": ms,
-            "nand_per_s": eng.nand_count * world / (ms / 1e3), "nand_per_fft": eng.nand_count,
-            "levels": prog.n_levels, "launches_per_fft": prog.launches,
-            "schedule": eng.last_compile.get("schedule", "levels"),
-            "roofline": _fft_roofline(eng.nand_count * world / (ms / 1e3), scheme.params.n_ct),
-            "decrypt_check_vs_reference": ok}
+            "nand_per_s": nand * world / (ms / 1e3), "nand_per_fft": nand,
+            "levels": prog.n_levels, "launches_per_fft": launches, "schedule": sched,
+            "roofline": _fft_roofline(nand * world / (ms / 1e3), scheme.params.n_ct),
+            "decrypt_check_vs_reference": ok,
+            "first_call": {"encrypt_s": t1 - t0, "record_s": t2 - t1, "compile_s": t3 - t2,
+                           "run_read_s": t4 - t3, "total_s": t4 - t0},
+            "e2e": {"value": world / api_s, "unit": "FFT/s", "ms_per_call": api_s * 1e3,
+                    "h2d_bytes_per_step": n_bits * 32, "d2h_bytes_per_step": n_bits * 4,
+                    "decrypt_check_vs_reference": None if want is None else bool(np.array_equal(words[0], want)),
+                    "path": "API call after the first: input_signal (device encryption from host plaintext) -> "
+                            "fft (circuit template replay) -> flush (cached program) -> read_signal_ints "
+                            "(device decryption sums -> host words)"}}
 
 
 def run_ours(args):
@@ -499,16 +682,15 @@ def run_ours(args):
             single[cfg] = bench_fft_single(args, world, rank, local, cfg)
     cpu = None
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
-        v, cores, total = cpu_reference(args.cpu_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{cores} processes x {args.cpu_seconds:.0f} s time-boxed XOR+AND pairs "
-                         f"({total} NANDs) of oracle/gsw.py hom_nand_matrix (the reference's float64 "
-                         f"N x N product + flatten, fhe.py:325-341), OPENBLAS_NUM_THREADS=1"}
+        v, cores, total, kind = cpu_reference(args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": _cpu_sample_text(kind, cores, args.cpu_seconds, total)}
     if rank != 0:
         _barrier(world)
         return
     ms = res["ms"]
     value = res["nand_per_step"] * world / (ms / 1e3)
+    i8_peak, i8_src = _i8_peak()
     sched = res["schedule"].split()[0]
     kernel = {"resident": "fhegpu::tc::resident_tc_kernel<9,29,true,2,false>",
               "tiled": "fhegpu::tc::level_tc_ws_kernel<9,29,true,1>"}.get(
@@ -542,10 +724,12 @@ def run_ours(args):
         "roofline_compute": {
             "bound": "tensor", "unit": "TOPS",
             "achieved": 2 * MMA_MAC_SLOTS_PER_NAND * value / world / 1e12,
-            "peak": I8_DENSE_TOPS, "frac": 2 * MMA_MAC_SLOTS_PER_NAND * value / world / 1e12 / I8_DENSE_TOPS,
-            "peak_source": "spec (B200 dense int8, not measured here)",
-            "note": "per NAND 4,423,680 executed MAC slots (N padded 36 -> 48, tail M = 64 for 5 rows); "
-                    "a kind::i8 MMA with N <= 64 issues no faster than every ~46 cycles (DESIGN.md 4.1)"},
+            "peak": i8_peak, "frac": 2 * MMA_MAC_SLOTS_PER_NAND * value / world / 1e12 / i8_peak,
+            "algorithmic_frac": 2 * ALG_U8_MACS_PER_NAND * value / world / 1e12 / i8_peak,
+            "peak_source": i8_src,
+            "note": "achieved/frac: 4,423,680 executed MAC slots per NAND (N padded 36 -> 48, tail M = 64 for "
+                    "5 rows); algorithmic_frac: 2,452,356 u8 MACs per NAND (N^2 k x 4 digits); a kind::i8 MMA "
+                    "with N <= 64 issues no faster than every ~46 cycles (DESIGN.md 4.1)"},
         "gpu_launches": res["launches_per_step"] * args.steps,
         "clocks": res["clocks"],
     }
@@ -562,8 +746,20 @@ def run_ours(args):
         line["fft"] = {"metric": "16-pt Q4.12 FHE FFTs/s (configs[4])", "value": fft["ffts_per_s"],
                        "unit": "FFT/s", "nand_per_s": fft["nand_per_s"], "ms_per_step": fft["ms"],
                        "lanes": fft["lanes"], "nand_per_fft": fft["nand_per_fft"],
-                       "levels": fft["levels"], "roofline": fft["roofline"],
-                       "decrypt_check_vs_reference": fft["ok"]}
+                       "levels": fft["levels"], "launches_per_step": fft["launches"],
+                       "schedule": fft["schedule"], "roofline": fft["roofline"],
+                       "decrypt_check_vs_reference": fft["ok"], "first_call": fft["first_call"]}
+        api = fft["api"]
+        line["fft"]["e2e"] = {
+            "value": api["ffts_per_s"], "unit": "FFT/s", "s_per_call": api["s_per_call"],
+            "h2d_bytes_per_step": api["h2d_bytes"], "d2h_bytes_per_step": api["d2h_bytes"],
+            "decrypt_check_vs_reference": api["ok"],
+            "path": "API call after the first: input_signal of 1024 host signals (device encryption) -> fft_1d "
+                    "(template replay) -> flush -> read_signal_ints (device decryption sums)"}
+        if "e2e_ct" in fft:
+            line["fft"]["e2e_ciphertexts"] = dict(fft["e2e_ct"], path=(
+                "fhegpu_prog_run_host: 512 input ciphertexts per signal in the reference's serialised bytes "
+                "(pinned host) -> chunked H2D | unpack + level kernels + pack | D2H of all 512 outputs"))
     if single:
         line["fft_single"] = single
     if cpu is not None:
@@ -583,7 +779,7 @@ def run_reference(args):
     vals, totals = [], 0
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        v, cores, total = cpu_reference(seconds)
+        v, cores, total, kind = cpu_reference(seconds)
         vals.append(v)
         totals += total
     wall = time.perf_counter() - t0
@@ -595,9 +791,8 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64 (exact integers)", "data": "synthetic",
         "config": {"workload": "configs[1] gate microbenchmark: XOR + AND pairs, DEFAULT params "
                                "(N=261); each step a time-boxed sample on every host core"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"per step {cores} processes x {seconds:.0f} s of XOR+AND pairs "
-                                   f"({totals} NANDs total) with oracle/gsw.py hom_nand_matrix"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": "per step: " + _cpu_sample_text(kind, cores, seconds, totals)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -619,6 +814,7 @@ def main():
     ap.add_argument("--no-fft-single", dest="fft_single", action="store_false",
                     help="skip configs[0]/[2]/[3] single-signal FFT latency")
     ap.add_argument("--fft-lanes", type=int, default=1024)
+    ap.add_argument("--fft-e2e-chunk", type=int, default=128, help="lanes per streamed chunk (cfg4 ciphertext e2e)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--ref-step-seconds", type=float, default=4.0)
     args = ap.parse_args()

@@ -60,7 +60,32 @@ void run(const char *name, int sms) {
   cudaFree(d);
 }
 
-int main() {
+// Dense i8 tensor peak as a rate: every SM issues back-to-back M128 N256 K32 MMAs (A and B in
+// shared memory, the shape that reaches the full datapath), timed with CUDA events.
+void peak(int sms) {
+  uint64_t *d; cudaMalloc(&d, sms * 8);
+  auto k = bench<256, false, false, 1, 128>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 50 * 1024);
+  const int iters = 200000;
+  k<<<sms, 128, 50 * 1024>>>(d, 1000);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  k<<<sms, 128, 50 * 1024>>>(d, iters);
+  cudaEventRecord(e1);
+  cudaError_t e = cudaDeviceSynchronize();
+  float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
+  uint64_t h[148]; cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
+  double avg = 0; for (int i = 0; i < sms; ++i) avg += h[i]; avg /= sms;
+  const double macs = (double)sms * iters * 128.0 * 256 * 32;
+  printf("{\"i8_dense_tops\": %.1f, \"mac_per_clk_per_sm\": %.0f, \"ms\": %.3f, \"sms\": %d, "
+         "\"shape\": \"M128 N256 K32 kind::i8, A and B smem\", \"err\": \"%s\"}\n",
+         2.0 * macs / (ms * 1e-3) / 1e12, 128.0 * 256 * 32 / (avg / iters), ms, sms,
+         e == cudaSuccess ? "" : cudaGetErrorString(e));
+  cudaFree(d);
+}
+
+int main(int argc, char **argv) {
+  if (argc > 1 && argv[1][0] == 'p') { peak(148); return 0; }
   for (int sms : {148}) {
     run<48, false, true, 1, 64>("M64 N48 smemA", sms);
     run<48, true, true, 1, 64>("M64 N48 tmemA", sms);
