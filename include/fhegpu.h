@@ -93,6 +93,7 @@ int fhegpu_ctx_set_stream(fhegpu_ctx *ctx, void *cuda_stream); /* NULL = legacy 
 void *fhegpu_ctx_own_stream(const fhegpu_ctx *ctx);           /* the stream a new context starts on */
 int fhegpu_ctx_set_kernel(fhegpu_ctx *ctx, int kernel);        /* FHEGPU_KERNEL_* */
 int fhegpu_ctx_kernel(const fhegpu_ctx *ctx);                  /* kernel a level launch will use */
+int fhegpu_ctx_num_sms(const fhegpu_ctx *ctx);                 /* SMs = the widest launch's CTAs */
 int fhegpu_ctx_set_debug(fhegpu_ctx *ctx, uint32_t dbg);       /* test knobs; 0 in production */
 int fhegpu_ctx_set_graphs(fhegpu_ctx *ctx, int enable);        /* replay programs as CUDA graphs (default on) */
 uint32_t fhegpu_ct_words(const fhegpu_ctx *ctx);
@@ -224,6 +225,54 @@ int fhegpu_prog_set_resident(fhegpu_ctx *ctx, fhegpu_prog *prog, const fhegpu_re
  * tests and tools.  lanes <= 4, lanes * n_ops <= 32. */
 int fhegpu_res_slot_order(const fhegpu_res_op *plan, uint32_t n_ops, uint32_t lanes, uint8_t *order);
 uint32_t fhegpu_prog_launches(const fhegpu_prog *prog);       /* launches one run issues */
+/* Register-file launches (tc_nand_regfile.cuh): one lane at a time per CTA runs a whole
+ * per-lane netlist with a pool of shared-memory ciphertext buffers as registers -- operands
+ * come from buffers, outputs go to buffers; values that do not fit are spilled (stored at
+ * their producer) and filled back; program inputs are fills from their store slots; program
+ * outputs (held wires) are stored to theirs.  Replaces the level launches of deep programs
+ * over many lanes (configs[4]: every butterfly of 1024 signals, fft.py:137-174) and moves
+ * ~0.4 instead of 3 ciphertexts per gate through L2/HBM.
+ *
+ * fhegpu_rf_plan schedules and allocates (host only; see rf_plan.h):
+ *   gates     n_gates gates in a topological order; operand ids: input i -> i, the output of
+ *             gate j -> n_in + j; flags bit 0 / 1: complement left / right (fused hom_not);
+ *             held: the output is a program output, stored to out_slot
+ *   in_slots  store slot of each program input
+ *   n_buf     shared-memory buffers (<= 20 fit next to the pipeline's operand buffers)
+ *   min_dist  preferred slot distance between a gate and its producers (pipeline depth: 5)
+ *   lookahead fills are issued this many slots before their first reader
+ * outputs: order[slot] = gate, slots[slot], fills[0 .. *n_fills) (fill_cap >= 2 * n_gates),
+ * *n_spill = spill slots per CTA. */
+typedef struct fhegpu_rf_gate {
+  uint32_t left, right;
+  uint8_t flags, held;
+  uint16_t pad;
+  uint32_t out_slot;
+} fhegpu_rf_gate;
+typedef struct fhegpu_rf_slot {
+  uint8_t lbuf, rbuf, dbuf, bits; /* bits: 1/2 complement l/r, 4 store, 8 dest held a stored
+                                     value, 16 ... stored by the previous slot, 32 first write
+                                     of dest in the lane */
+  uint32_t lwait, rwait;          /* 0xFFFFFFFF none; bit 31: fill id, else producer slot */
+  uint32_t store;                 /* bit 31: spill index, else store slot (with bits & 4) */
+} fhegpu_rf_slot;
+typedef struct fhegpu_rf_fill {
+  uint32_t buf, src;              /* src bit 31: spill index, else store slot */
+  uint32_t consumer;              /* first reading slot */
+  uint32_t w_built, w_epi, w_st;  /* wait until the kernel's counters reach these slots */
+  uint32_t flags, pad;            /* flags bit 0: first use of the buffer in the lane */
+} fhegpu_rf_fill;
+int fhegpu_rf_plan(const fhegpu_rf_gate *gates, uint32_t n_gates, const uint32_t *in_slots, uint32_t n_in,
+                   uint32_t n_buf, uint32_t min_dist, uint32_t lookahead, uint32_t *order,
+                   fhegpu_rf_slot *slots, fhegpu_rf_fill *fills, uint32_t fill_cap, uint32_t *n_fills,
+                   uint32_t *n_spill, uint32_t *stats /* [3]: stalls, stores, fills; may be NULL */);
+/* Attach a plan to a program: fhegpu_prog_run then runs it as ONE register-file launch
+ * (tcgen05, k = 9, ell = 29), else level by level.  Spills of CTA c use ciphertexts
+ * [spill_base + c * n_spill, + n_spill) of the store.  n_slots = 0 detaches. */
+int fhegpu_prog_set_regfile(fhegpu_ctx *ctx, fhegpu_prog *prog, const fhegpu_rf_slot *slots, uint32_t n_slots,
+                            const fhegpu_rf_fill *fills, uint32_t n_fills, uint32_t n_buf, uint32_t n_spill,
+                            uint64_t spill_base);
+
 void fhegpu_prog_destroy(fhegpu_prog *prog);
 
 /* Scheme operators on host buffers (count independent gates, one launch).

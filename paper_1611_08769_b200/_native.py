@@ -21,6 +21,12 @@ HOST_COMPACT, HOST_PACKED = 0, 1      # fhegpu_prog_run_host host formats
 KERNEL_NAMES = {KERNEL_AUTO: "auto", KERNEL_SIMT: "simt", KERNEL_TCGEN05: "tcgen05"}
 
 OP_DTYPE = np.dtype([("left", "<u4"), ("right", "<u4"), ("out", "<u4"), ("flags", "<u4")])
+RF_GATE_DTYPE = np.dtype([("left", "<u4"), ("right", "<u4"), ("flags", "u1"), ("held", "u1"), ("pad", "<u2"),
+                          ("out_slot", "<u4")])                                          # fhegpu_rf_gate
+RF_SLOT_DTYPE = np.dtype([("lbuf", "u1"), ("rbuf", "u1"), ("dbuf", "u1"), ("bits", "u1"), ("lwait", "<u4"),
+                          ("rwait", "<u4"), ("store", "<u4")])                             # fhegpu_rf_slot
+RF_FILL_DTYPE = np.dtype([("buf", "<u4"), ("src", "<u4"), ("consumer", "<u4"), ("w_built", "<u4"),
+                          ("w_epi", "<u4"), ("w_st", "<u4"), ("flags", "<u4"), ("pad", "<u4")])   # fhegpu_rf_fill
 RES_OP_DTYPE = np.dtype([("lkind", "u1"), ("lidx", "u1"), ("rkind", "u1"), ("ridx", "u1"),
                          ("dest", "u1"), ("is_out", "u1"), ("flags", "u1"), ("pad", "u1"),
                          ("lprod", "<i2"), ("rprod", "<i2"), ("out_slot", "<u4")])   # fhegpu_res_op
@@ -68,6 +74,11 @@ SIGNATURES = [
     ("fhegpu_prog_set_resident", ctypes.c_int, [_P, _P, _P, ctypes.c_uint32, _P, ctypes.c_uint32,
                                                 ctypes.c_uint32]),
     ("fhegpu_res_slot_order", ctypes.c_int, [_P, ctypes.c_uint32, ctypes.c_uint32, _P]),
+    ("fhegpu_ctx_num_sms", ctypes.c_int, [_P]),
+    ("fhegpu_rf_plan", ctypes.c_int, [_P, ctypes.c_uint32, _P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                      ctypes.c_uint32, _P, _P, _P, ctypes.c_uint32, _U32P, _U32P, _U32P]),
+    ("fhegpu_prog_set_regfile", ctypes.c_int, [_P, _P, _P, ctypes.c_uint32, _P, ctypes.c_uint32, ctypes.c_uint32,
+                                               ctypes.c_uint32, ctypes.c_uint64]),
     ("fhegpu_store_write_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     ("fhegpu_store_read_packed", ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     ("fhegpu_store_copy_slots", ctypes.c_int, [_P, _U32P, _U32P, ctypes.c_uint32, ctypes.c_uint64]),
@@ -147,6 +158,28 @@ def res_slot_order(plan: np.ndarray, lanes: int = 3) -> np.ndarray:
     return order
 
 
+def rf_plan(gates: np.ndarray, in_slots, n_buf: int = 20, min_dist: int = 5, lookahead: int = 4):
+    """Register-file plan of a per-lane netlist (fhegpu_rf_plan; host only): returns
+    (order, slots, fills, n_spill, stats) -- see include/fhegpu.h."""
+    if _lib is None:
+        load_library()
+    gates = np.ascontiguousarray(gates, dtype=RF_GATE_DTYPE)
+    ins = np.ascontiguousarray(np.asarray(in_slots, dtype=np.uint32).reshape(-1))
+    n = len(gates)
+    order = np.zeros(n, dtype=np.uint32)
+    slots = np.zeros(n, dtype=RF_SLOT_DTYPE)
+    fills = np.zeros(2 * n + 16, dtype=RF_FILL_DTYPE)
+    n_fills, n_spill = ctypes.c_uint32(), ctypes.c_uint32()
+    stats = np.zeros(3, dtype=np.uint32)
+    _check(_lib.fhegpu_rf_plan(gates.ctypes.data_as(ctypes.c_void_p), n, ins.ctypes.data_as(ctypes.c_void_p),
+                               len(ins), int(n_buf), int(min_dist), int(lookahead),
+                               order.ctypes.data_as(ctypes.c_void_p), slots.ctypes.data_as(ctypes.c_void_p),
+                               fills.ctypes.data_as(ctypes.c_void_p), len(fills), ctypes.byref(n_fills),
+                               ctypes.byref(n_spill), _ptr(stats, ctypes.c_uint32)), "rf_plan")
+    return order, slots, fills[:n_fills.value].copy(), int(n_spill.value), \
+        {"stalls": int(stats[0]), "stores": int(stats[1]), "fills": int(stats[2])}
+
+
 def _ptr(arr, ctype):
     return arr.ctypes.data_as(ctypes.POINTER(ctype))
 
@@ -216,6 +249,16 @@ class Program:
                                              int(n_local)), "prog_set_resident")
         self.launches = int(_lib.fhegpu_prog_launches(self.handle))
 
+    def set_regfile(self, slots: np.ndarray, fills: np.ndarray, n_buf: int, n_spill: int, spill_base: int):
+        """Register-file mode (fhegpu_prog_set_regfile): a plan from rf_plan; spills of CTA c at
+        store ciphertexts spill_base + c * n_spill.  Empty slots disable."""
+        slots = np.ascontiguousarray(slots, dtype=RF_SLOT_DTYPE)
+        fills = np.ascontiguousarray(fills, dtype=RF_FILL_DTYPE)
+        _check(_lib.fhegpu_prog_set_regfile(self.ctx.handle, self.handle, slots.ctypes.data_as(ctypes.c_void_p),
+                                            len(slots), fills.ctypes.data_as(ctypes.c_void_p), len(fills),
+                                            int(n_buf), int(n_spill), int(spill_base)), "prog_set_regfile")
+        self.launches = int(_lib.fhegpu_prog_launches(self.handle))
+
     def run_host(self, lanes: int, chunk_lanes: int, in_slots, in_ptrs, out_slots, out_ptrs,
                  host_format: int = 0):
         """fhegpu_prog_run_host: stream `lanes` host-resident lanes through the device in
@@ -276,6 +319,9 @@ class DeviceContext:
 
     def set_kernel(self, kernel: int):
         _check(_lib.fhegpu_ctx_set_kernel(self.handle, int(kernel)), "set_kernel")
+
+    def num_sms(self) -> int:
+        return int(_lib.fhegpu_ctx_num_sms(self.handle))
 
     @property
     def kernel(self) -> str:

@@ -18,6 +18,7 @@
 #include "tc_nand.cuh"
 #include "tc_nand_ws.cuh"
 #include "tc_nand_resident.cuh"
+#include "tc_nand_regfile.cuh"
 #include "encrypt.cuh"
 #include "bits.cuh"
 
@@ -101,6 +102,13 @@ struct fhegpu_prog {
   uint32_t r_ops = 0, r_in = 0, r_local = 0, r_out = 0;
   uint64_t r_slots = 0;           // 1 + the largest store slot the plan reads or writes
   bool r_deps = true;             // the slot order has operands produced < 5 slots back
+  // register-file launches (fhegpu_prog_set_regfile): per-lane slot table + fill list
+  bool use_regfile = false;
+  fhegpu_rf_slot *d_rfslots = nullptr;
+  fhegpu_rf_fill *d_rffills = nullptr;
+  uint32_t rf_ops = 0, rf_fills = 0, rf_buf = 0, rf_spill = 0;
+  uint64_t rf_spill_base = 0;
+  uint64_t rf_slots = 0;          // 1 + the largest store slot the plan reads or writes
   // CUDA graph of one full run (all level launches), captured on first use per
   // (lanes, stream, kernel choice, debug bits); replayed with a single cudaGraphLaunch
   cudaGraphExec_t graph = nullptr;
@@ -356,6 +364,28 @@ int launch_resident(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
   return FHEGPU_OK;
 }
 
+// A whole deep per-lane program in one register-file launch (tc_nand_regfile.cuh).
+int launch_regfile(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
+  if (lanes == 0 || pr->rf_ops == 0) return FHEGPU_OK;
+  if (effective_kernel(c) != FHEGPU_KERNEL_TCGEN05 || (c->p.dbg & 4u)) return FHEGPU_EUNSUP;
+  if (!(c->p.k == 9 && c->p.ell == 29)) return FHEGPU_EUNSUP;
+  using F = tc::GeoRF<9, 29>;
+  const uint32_t smem = F::smem_bytes(pr->rf_buf);
+  if (smem > 227u * 1024u) return FHEGPU_EUNSUP;
+  const unsigned grid = (unsigned)std::min<uint64_t>(lanes, (uint64_t)c->num_sms);
+  if (pr->rf_spill_base + (uint64_t)grid * pr->rf_spill > c->capacity)
+    return fail(FHEGPU_EINVAL, "register-file spill region beyond store capacity");
+  DevParams p = c->p;
+  const bool pm = pm_ok(c->p.q, c->p.ell) && !(c->p.dbg & 2u);
+  auto kern = pm ? tc::regfile_tc_kernel<9, 29, true, FHEGPU_ENC_RESIDENT>
+                 : tc::regfile_tc_kernel<9, 29, false, FHEGPU_ENC_RESIDENT>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, F::THREADS, smem, c->stream>>>(c->store, pr->d_rfslots, pr->d_rffills, pr->rf_ops, pr->rf_fills,
+                                               pr->rf_buf, lanes, pr->rf_spill_base, pr->rf_spill, p);
+  CUDA_TRY(cudaGetLastError());
+  return FHEGPU_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -446,6 +476,8 @@ int fhegpu_ctx_set_kernel(fhegpu_ctx *c, int kernel) {
 }
 
 int fhegpu_ctx_kernel(const fhegpu_ctx *c) { return c ? effective_kernel(c) : -1; }
+
+int fhegpu_ctx_num_sms(const fhegpu_ctx *c) { return c ? c->num_sms : 0; }
 
 int fhegpu_ctx_set_debug(fhegpu_ctx *c, uint32_t dbg) {
   if (!c) return fail(FHEGPU_EINVAL, "null ctx");
@@ -749,12 +781,17 @@ int fhegpu_prog_run_range(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes, uint32
   const uint32_t n_levels = (uint32_t)pr->offsets.size() - 1;
   last = std::min(last, n_levels);
   // every slot the program (or its resident plan) names, for every lane, must be in the store
-  const uint64_t slots = std::max(pr->n_slots, pr->use_resident ? pr->r_slots : 0);
+  const uint64_t slots = std::max({pr->n_slots, pr->use_resident ? pr->r_slots : 0,
+                                    pr->use_regfile ? pr->rf_slots : 0});
   if (lanes && slots && (slots > c->capacity / lanes || slots * lanes > c->capacity))
     return fail(FHEGPU_EINVAL, "program needs " + std::to_string(slots) + " slots x " + std::to_string(lanes) +
                                    " lanes; store holds " + std::to_string(c->capacity) + " ciphertexts");
   CUDA_TRY(cudaSetDevice(c->device));
-  if (pr->use_resident && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
+  if (pr->use_regfile && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
+    const int rc = launch_regfile(c, pr, lanes);
+    if (rc != FHEGPU_EUNSUP) return rc;
+    // else: level by level (register-file programs keep their level structure)
+  } else if (pr->use_resident && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
     const int rc = launch_resident(c, pr, lanes);
     if (rc != FHEGPU_EUNSUP) return rc;
     // else: level by level (resident programs keep their level structure)
@@ -1081,6 +1118,82 @@ int fhegpu_prog_set_resident(fhegpu_ctx *c, fhegpu_prog *pr, const fhegpu_res_op
   return FHEGPU_OK;
 }
 
+int fhegpu_rf_plan(const fhegpu_rf_gate *gates, uint32_t n_gates, const uint32_t *in_slots, uint32_t n_in,
+                   uint32_t n_buf, uint32_t min_dist, uint32_t lookahead, uint32_t *order, fhegpu_rf_slot *slots,
+                   fhegpu_rf_fill *fills, uint32_t fill_cap, uint32_t *n_fills, uint32_t *n_spill, uint32_t *stats) {
+  if (!gates || (n_in && !in_slots) || !order || !slots || !fills || !n_fills || !n_spill)
+    return fail(FHEGPU_EINVAL, "null argument");
+  rf::Planner pl;
+  pl.gates = gates, pl.n = n_gates, pl.n_in = n_in, pl.in_slots = in_slots;
+  pl.n_buf = n_buf, pl.dist = std::max(1u, min_dist), pl.look = lookahead;
+  if (!pl.run()) return fail(FHEGPU_EINVAL, pl.err);
+  if (pl.fills.size() > fill_cap)
+    return fail(FHEGPU_EINVAL, "fill_cap " + std::to_string(fill_cap) + " < " + std::to_string(pl.fills.size()));
+  std::memcpy(order, pl.order.data(), n_gates * sizeof(uint32_t));
+  std::memcpy(slots, pl.slots.data(), n_gates * sizeof(fhegpu_rf_slot));
+  if (!pl.fills.empty()) std::memcpy(fills, pl.fills.data(), pl.fills.size() * sizeof(fhegpu_rf_fill));
+  *n_fills = (uint32_t)pl.fills.size();
+  *n_spill = pl.n_spill;
+  if (stats) stats[0] = pl.stalls, stats[1] = pl.n_stores, stats[2] = (uint32_t)pl.fills.size();
+  return FHEGPU_OK;
+}
+
+int fhegpu_prog_set_regfile(fhegpu_ctx *c, fhegpu_prog *pr, const fhegpu_rf_slot *slots, uint32_t n_slots,
+                            const fhegpu_rf_fill *fills, uint32_t n_fills, uint32_t n_buf, uint32_t n_spill,
+                            uint64_t spill_base) {
+  if (!c || !pr) return fail(FHEGPU_EINVAL, "null argument");
+  if (pr->graph) {
+    cudaGraphExecDestroy(pr->graph);
+    pr->graph = nullptr;
+  }
+  if (n_slots == 0) {
+    pr->use_regfile = false;
+    return FHEGPU_OK;
+  }
+  if (!slots || (n_fills && !fills)) return fail(FHEGPU_EINVAL, "null argument");
+  if (n_buf < 4 || tc::GeoRF<9, 29>::smem_bytes(n_buf) > 227u * 1024u)
+    return fail(FHEGPU_EINVAL, "register file of " + std::to_string(n_buf) + " buffers does not fit shared memory");
+  static_assert(sizeof(fhegpu_rf_slot) == 16 && sizeof(fhegpu_rf_fill) == 32, "plan record layout");
+  uint64_t rf_slots = 0;
+  auto loc = [&](uint32_t x) {
+    if (x & rf::STORE_SPILL) return (x & ~rf::STORE_SPILL) < n_spill;
+    rf_slots = std::max<uint64_t>(rf_slots, uint64_t(x) + 1);
+    return true;
+  };
+  for (uint32_t t = 0; t < n_slots; ++t) {
+    const fhegpu_rf_slot &s = slots[t];
+    bool ok = s.lbuf < n_buf && s.rbuf < n_buf && s.dbuf < n_buf;
+    for (uint32_t w : {s.lwait, s.rwait})
+      if (w != rf::NONE) ok = ok && ((w & rf::WAIT_FILL) ? (w & ~rf::WAIT_FILL) < n_fills : w < t);
+    if (s.bits & rf::SB_STORE) ok = ok && loc(s.store);
+    if (!ok) return fail(FHEGPU_EINVAL, "bad register-file slot " + std::to_string(t));
+  }
+  for (uint32_t f = 0; f < n_fills; ++f) {
+    const fhegpu_rf_fill &x = fills[f];
+    // a fill's conditions look back only (else the producer would wait on its own consumers)
+    if (x.buf >= n_buf || !loc(x.src) || x.consumer >= n_slots || x.w_built > x.consumer ||
+        x.w_epi > x.consumer || x.w_st > x.consumer || (f && x.consumer < fills[f - 1].consumer))
+      return fail(FHEGPU_EINVAL, "bad register-file fill " + std::to_string(f));
+  }
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaFree(pr->d_rfslots);
+  cudaFree(pr->d_rffills);
+  pr->d_rfslots = nullptr;
+  pr->d_rffills = nullptr;
+  CUDA_TRY(cudaMalloc(&pr->d_rfslots, (size_t)n_slots * sizeof(fhegpu_rf_slot)));
+  CUDA_TRY(cudaMalloc(&pr->d_rffills, std::max<size_t>(1, n_fills) * sizeof(fhegpu_rf_fill)));
+  CUDA_TRY(cudaMemcpy(pr->d_rfslots, slots, (size_t)n_slots * sizeof(fhegpu_rf_slot), cudaMemcpyHostToDevice));
+  if (n_fills) CUDA_TRY(cudaMemcpy(pr->d_rffills, fills, (size_t)n_fills * sizeof(fhegpu_rf_fill), cudaMemcpyHostToDevice));
+  pr->rf_ops = n_slots;
+  pr->rf_fills = n_fills;
+  pr->rf_buf = n_buf;
+  pr->rf_spill = n_spill;
+  pr->rf_spill_base = spill_base;
+  pr->rf_slots = rf_slots;
+  pr->use_regfile = true;
+  return FHEGPU_OK;
+}
+
 int fhegpu_res_slot_order(const fhegpu_res_op *plan, uint32_t n_ops, uint32_t lanes, uint8_t *order) {
   if (!plan || !order) return fail(FHEGPU_EINVAL, "null argument");
   if (lanes < 1 || lanes > 4 || n_ops > (uint32_t)tc::RES_MAX_OPS || lanes * n_ops > 32)
@@ -1103,7 +1216,7 @@ int fhegpu_ctx_set_graphs(fhegpu_ctx *c, int enable) {
 
 uint32_t fhegpu_prog_launches(const fhegpu_prog *pr) {
   if (!pr) return 0;
-  if (pr->use_resident) return 1;               // lane-resident: one launch
+  if (pr->use_regfile || pr->use_resident) return 1;   // register-file / lane-resident: one launch
   if (pr->use_queue) return 2;                  // ready queue: state reset + one launch
   if (pr->d_deps) return 1;                     // dataflow: one launch (tcgen05 parameter sets)
   uint32_t n = 0;
@@ -1120,6 +1233,8 @@ void fhegpu_prog_destroy(fhegpu_prog *pr) {
   cudaFree(pr->d_qrun);
   cudaFree(pr->d_rplan);
   cudaFree(pr->d_rin);
+  cudaFree(pr->d_rfslots);
+  cudaFree(pr->d_rffills);
   cudaFree(pr->d_ops);
   delete pr;
 }

@@ -280,9 +280,9 @@ class GpuEngine(LevelledNetlist):
             raise UsageError("threads must be >= 1")
         if batch_size < 1:
             raise UsageError("batch_size must be >= 1")
-        if schedule not in ("auto", "levels", "dataflow", "queue", "tiled", "resident"):
-            raise UsageError(f"schedule must be 'auto', 'levels', 'dataflow', 'queue', 'tiled' or "
-                             f"'resident', got {schedule!r}")
+        if schedule not in ("auto", "levels", "dataflow", "queue", "tiled", "resident", "regfile"):
+            raise UsageError(f"schedule must be 'auto', 'levels', 'dataflow', 'queue', 'tiled', "
+                             f"'resident' or 'regfile', got {schedule!r}")
         self.schedule = schedule
         if lane_rngs is not None and len(lane_rngs) != batch_size:
             raise UsageError("need one rng per lane")
@@ -330,6 +330,7 @@ class GpuEngine(LevelledNetlist):
         self._capturing = False
         self._regions: dict = {}            # template uid -> (base slot, Program, compile)
         self.template_hits = 0
+        self._spill_block = (0, 0)          # (first slot, slots): register-file spill space
 
     # -- protocol attributes -----------------------------------------------------------
 
@@ -828,10 +829,12 @@ class GpuEngine(LevelledNetlist):
             sched = self._pick_schedule()
             comp = None
             if sched not in ("tiled", "resident"):
-                prog = self._compile(ssa=sched in ("dataflow", "queue"))
+                prog = self._compile(ssa=sched in ("dataflow", "queue", "regfile"))
                 prog["schedule"] = sched
                 out_slots = np.asarray(self._slot, dtype=np.int64)[tpl.out_internal]
                 comp = {"prog": prog, "n_slots": self._n_slots, "out_slots": out_slots}
+                if sched == "regfile":
+                    comp["regfile"] = self._regfile_plan(prog)
         finally:
             (self._level, self._est, self._slot, self._refs, self._free, self._n_slots,
              self._pending_ops, self.keep_all) = saved
@@ -863,6 +866,8 @@ class GpuEngine(LevelledNetlist):
                 program.set_deps(prog["deps"])
             if prog["schedule"] == "queue":
                 program.set_queue(True)
+            if prog["schedule"] == "regfile":
+                self._attach_regfile(program, comp["regfile"], base)
             reg = self._regions[tpl.uid] = (base, program)
         base, program = reg
         self._ensure_capacity()
@@ -908,7 +913,9 @@ class GpuEngine(LevelledNetlist):
         sched = self._pick_schedule()
         dataflow = sched in ("dataflow", "queue", "tiled")
         ring = self.TILE_RING if sched == "tiled" and self._ring_ok() else 0
-        prog = self._compile(ssa=dataflow, ring_temps=ring > 0)
+        # register-file programs read inputs and write outputs in their own order: no slot is
+        # reused inside the program (single assignment)
+        prog = self._compile(ssa=dataflow or sched == "regfile", ring_temps=ring > 0)
         prog["schedule"] = sched
         self._pending_ops = []
         if self._cse_map is not None:
@@ -948,12 +955,84 @@ class GpuEngine(LevelledNetlist):
                 plan = self._resident_plan(prog)
                 if plan is not None:                 # else: the level launches of `program`
                     program.set_resident(*plan)
+            if sched == "regfile":
+                self._attach_regfile(program, self._regfile_plan(prog), 0)
         program.run(lanes)
         self.last_program = program
         self.last_compile = prog
         self.programs_run += 1
         self.launches += program.launches
         return program
+
+    # register-file launches (csrc/tc_nand_regfile.cuh): shared-memory buffers per CTA, the
+    # planner's dependency distance and fill lookahead (csrc/rf_plan.h)
+    RF_BUFFERS = int(os.environ.get("FHEGPU_RF_BUFFERS", "20"))
+    RF_DIST, RF_LOOK = 5, 4
+    REGFILE_MIN_LANES = 296        # 'auto': deep programs over >= 2 lanes per SM
+    REGFILE_MIN_LEVELS = 16
+    REGFILE_AUTO = os.environ.get("FHEGPU_REGFILE", "1") != "0"
+
+    @staticmethod
+    def _regfile_gates(prog):
+        """fhegpu_rf_gate records of a compiled per-lane program (gates in level order) and the
+        store slots of its inputs: operand ids are input i -> i (first-use order), the output of
+        gate j -> n_in + j."""
+        from ._native import RF_GATE_DTYPE
+        table, nodes, held = prog["ops"], prog["nodes"], prog["held"]
+        n = len(table)
+        maxn = int(nodes.max()) + 1 if n else 1
+        producer = np.full(maxn, -1, dtype=np.int64)
+        producer[nodes[:, 2]] = np.arange(n)
+        flat = nodes[:, :2].ravel()
+        pflat = producer[flat]
+        is_in = pflat < 0
+        in_nodes = flat[is_in]
+        uniq, first = np.unique(in_nodes, return_index=True)
+        by_use = np.argsort(first, kind="stable")
+        uniq, first = uniq[by_use], first[by_use]
+        in_id = np.full(maxn, -1, dtype=np.int64)
+        in_id[uniq] = np.arange(len(uniq))
+        slot_flat = np.stack([table["left"], table["right"]], axis=1).ravel()
+        in_slots = slot_flat[is_in][first].astype(np.uint32)
+        ids = np.where(is_in, in_id[flat], len(uniq) + pflat).reshape(n, 2)
+        gates = np.zeros(n, dtype=RF_GATE_DTYPE)
+        gates["left"], gates["right"] = ids[:, 0], ids[:, 1]
+        gates["flags"] = table["flags"] & 3
+        gates["held"] = held.astype(np.uint8)
+        gates["out_slot"] = np.where(held, table["out"], 0)
+        return gates, in_slots
+
+    def _regfile_plan(self, prog):
+        """Schedule + buffer plan of a compiled program (fhegpu_rf_plan), store slots as compiled."""
+        from ._native import rf_plan
+        gates, in_slots = self._regfile_gates(prog)
+        order, slots, fills, n_spill, stats = rf_plan(gates, in_slots, self.RF_BUFFERS, self.RF_DIST, self.RF_LOOK)
+        prog["regfile"] = dict(stats, n_spill=n_spill, buffers=self.RF_BUFFERS,
+                               ct_per_gate=(stats["fills"] + stats["stores"]) / max(1, len(gates)))
+        return slots, fills, n_spill
+
+    def _attach_regfile(self, program, plan, slot_offset: int):
+        """Attach a register-file plan to `program`, store slots shifted by `slot_offset` (a
+        template's private region); spills go to this engine's spill block."""
+        from ._csrc_consts import RF
+        slots, fills, n_spill = plan
+        if slot_offset:
+            slots, fills = slots.copy(), fills.copy()
+            st = (slots["bits"] & RF.SB_STORE) != 0
+            st &= (slots["store"] & RF.STORE_SPILL) == 0
+            slots["store"][st] += np.uint32(slot_offset)
+            fs = (fills["src"] & RF.STORE_SPILL) == 0
+            fills["src"][fs] += np.uint32(slot_offset)
+        lanes = self.batch_size
+        grid = min(self.ctx.num_sms(), lanes)
+        need = -(-(grid * n_spill) // lanes)          # slots of spill space
+        base, have = self._spill_block
+        if have < need:
+            base, have = self._n_slots, need
+            self._n_slots += need
+            self._spill_block = (base, have)
+            self._ensure_capacity()
+        program.set_regfile(slots, fills, self.RF_BUFFERS, n_spill, base * lanes)
 
     # tiled dataflow: lanes per chunk, and the single-assignment store budget it may use
     TILE_LANES = int(os.environ.get("FHEGPU_TILE_LANES", "128"))
@@ -996,6 +1075,10 @@ class GpuEngine(LevelledNetlist):
             return "levels"
         if self.batch_size >= self.RESIDENT_MIN_LANES and self.ctx.kernel == "tcgen05" and self._resident_ok():
             return "resident"
+        if self.REGFILE_AUTO and self.batch_size >= self.REGFILE_MIN_LANES and self.ctx.kernel == "tcgen05":
+            outs = np.asarray(self._pending_ops[4::5], dtype=np.int64)
+            if len(np.unique(np.asarray(self._level, dtype=np.int64)[outs])) >= self.REGFILE_MIN_LEVELS:
+                return "regfile"           # deep programs over many lanes: one register-file launch
         C = self.TILE_LANES
         if self.batch_size % C or self.batch_size < 8 * C:
             return "queue" if self._pick_queue() else "levels"

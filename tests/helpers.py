@@ -160,3 +160,107 @@ def reference_modules():
         sys.path.append(root)
     return tuple(importlib.import_module(f"fhefft.{m}")
                  for m in ("fhe", "engine", "fileio", "fft", "arith", "gates"))
+
+
+def regfile_gates(prog):
+    """fhegpu_rf_gate records + input slots of a compiled program (GpuEngine._regfile_gates)."""
+    from paper_1611_08769_b200.engine import GpuEngine
+    return GpuEngine._regfile_gates(prog)
+
+
+def replay_regfile(gates, in_slots, order, slots, fills, n_buf, store, mask, E=4, R=1, W=3, fill_lat=2):
+    """Timed model of a register-file launch (one lane per CTA) over lane-packed bits.
+
+    Clock steps: fills are issued in order as soon as the counters allow (landing fill_lat
+    steps later), slot b is built when its waits hold (fills landed; near producers' outputs
+    in their buffers), its epilogue writes the buffer E steps after the build, a store takes
+    its snapshot of the buffer R steps after the epilogue and reaches the store W steps after
+    that.  Hazards the plan leaves uncovered therefore read stale or clobbered data.  Returns
+    the store dict (slot -> bits; spills under ('s', k))."""
+    from paper_1611_08769_b200._csrc_consts import RF
+    n = len(order)
+    bufs = [None] * n_buf
+    g_store = dict(store)
+    built = epi = st = 0
+    fill_at = {}                      # fill id -> step its data lands
+    fptr = 0
+    b_time = {}
+    pend_epi = []                     # (time, slot)
+    pend_snap = []                    # (time, slot, dest buf)
+    pend_write = []                   # (time, slot, key, value)
+    vals = {}                         # slot -> (a, b) values read at build
+    done_store = set()
+    stores_issued = []
+    tau = 0
+    landed = []                       # (time, fill id)
+
+    def key_of(x):
+        return ("s", x & ~RF.STORE_SPILL) if x & RF.STORE_SPILL else int(x)
+
+    while epi < n or pend_write or pend_snap:
+        # fills land
+        for tm, f in list(landed):
+            if tm <= tau:
+                landed.remove((tm, f))
+                fr = fills[f]
+                bufs[int(fr["buf"])] = g_store[key_of(int(fr["src"]))]
+                fill_at[f] = tm
+        # issue fills whose conditions hold
+        while fptr < len(fills):
+            fr = fills[fptr]
+            if built >= fr["w_built"] and epi >= fr["w_epi"] and st >= fr["w_st"] and \
+                    (fptr < RF.RING or built > fills[fptr - RF.RING]["consumer"]):
+                landed.append((tau + fill_lat, fptr))
+                fptr += 1
+            else:
+                break
+        # epilogue writes
+        for tm, s in sorted(pend_epi):
+            if tm > tau or s != epi:
+                break
+            pend_epi.remove((tm, s))
+            sl = slots[s]
+            if sl["bits"] & (RF.SB_DEST_STORED | RF.SB_HAZARD):       # stores have read their buffers
+                for (_, s2, db) in sorted(pend_snap):
+                    pend_write.append((tau + W, s2, key_of(int(slots[s2]["store"])), bufs[db]))
+                pend_snap.clear()
+            a, b = vals.pop(s)
+            g = gates[order[s]]
+            a ^= mask if g["flags"] & 1 else 0
+            b ^= mask if g["flags"] & 2 else 0
+            bufs[int(sl["dbuf"])] = ~(a & b) & mask
+            if sl["bits"] & RF.SB_STORE:
+                pend_snap.append((tau + R, s, int(sl["dbuf"])))
+            epi += 1
+        for item in sorted(pend_snap):
+            if item[0] <= tau:
+                pend_snap.remove(item)
+                _, s2, db = item
+                pend_write.append((tau + W, s2, key_of(int(slots[s2]["store"])), bufs[db]))
+        for item in sorted(pend_write, key=lambda x: x[0]):
+            if item[0] <= tau:
+                pend_write.remove(item)
+                g_store[item[2]] = item[3]
+                done_store.add(item[1])
+        # st: every store of slots < st complete
+        while st < epi and (not (slots[st]["bits"] & RF.SB_STORE) or st in done_store):
+            st += 1
+        # build the next slot when its operands are ready
+        if built < n and built <= epi + 2:
+            sl = slots[built]
+            ok = True
+            for w in (int(sl["lwait"]), int(sl["rwait"])):
+                if w == RF.NONE:
+                    continue
+                if w & RF.WAIT_FILL:
+                    ok &= (w & ~RF.WAIT_FILL) in fill_at
+                else:
+                    ok &= epi > w
+            if ok:
+                vals[built] = (bufs[int(sl["lbuf"])], bufs[int(sl["rbuf"])])
+                pend_epi.append((tau + E, built))
+                built += 1
+        tau += 1
+        if tau > 50 * n + 1000:
+            raise AssertionError(f"model deadlock: built {built} epi {epi} st {st} fill {fptr}")
+    return g_store

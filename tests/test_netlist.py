@@ -246,8 +246,9 @@ def test_tiled_ring_temporaries_replay_and_war_order():
 
 def test_auto_schedule_policy():
     """'auto' on the tcgen05 geometry: resident for small per-lane programs (<= 8 gates) over
-    >= 1024 lanes; tiled for wide (batch % 128 == 0, >= 1024 lanes), shallow (<= 32 levels)
-    programs whose store fits; levels otherwise."""
+    >= 1024 lanes; regfile for deep (>= 16 levels) programs over >= 296 lanes; tiled for wide
+    (batch % 128 == 0, >= 1024 lanes), shallow (<= 32 levels) programs whose store fits;
+    levels otherwise."""
     from paper_1611_08769_b200 import and_, xor_
 
     def pick(lanes, params=DEFAULT_PARAMS, depth=1, kernel="tcgen05"):
@@ -267,7 +268,9 @@ def test_auto_schedule_policy():
     assert pick(512) == "levels"                  # too narrow to fill the SMs
     assert pick(4000, DEFAULT0_PARAMS, depth=2) == "levels"  # not a multiple of the tiled chunk
     assert pick(4096, EXACT_PARAMS) == "levels"   # no warp-specialised kernel for N = 51
-    assert pick(4096, DEFAULT0_PARAMS, depth=12) == "levels"   # 36 levels: hop bound
+    assert pick(4096, DEFAULT0_PARAMS, depth=12) == "regfile"  # 36 levels: one register-file launch
+    assert pick(296, DEFAULT0_PARAMS, depth=12) == "regfile"
+    assert pick(200, DEFAULT0_PARAMS, depth=12) == "levels"    # < 2 lanes per SM
     assert pick(4096, kernel="simt") == "levels"  # dataflow launches need the tcgen05 kernel
 
 
