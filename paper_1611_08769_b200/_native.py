@@ -14,7 +14,7 @@ import numpy as np
 from .errors import DeviceError, ParameterError, UsageError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfhegpu.so")
+LIB_PATH = os.environ.get("FHEGPU_LIB") or os.path.join(_HERE, "libfhegpu.so")   # FHEGPU_LIB: debug builds
 
 KERNEL_AUTO, KERNEL_SIMT, KERNEL_TCGEN05 = 0, 1, 2
 HOST_COMPACT, HOST_PACKED = 0, 1      # fhegpu_prog_run_host host formats

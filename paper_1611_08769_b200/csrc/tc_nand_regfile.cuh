@@ -14,7 +14,7 @@
 //  * the producer warp issues the plan's fills (bulk copies into buffers) as soon as their
 //    conditions hold, on a ring of RF_FILL_RING completion barriers;
 //  * progress is published as three shared-memory counters (slots, per CTA, across lanes):
-//      built  operands of slots < built have been read      (MMA warp, after op_full)
+//      built  operands of slots < built have been read      (tail warp, after main_done)
 //      epi    outputs of slots < epi are in their buffers    (epilogue, after the tail rows)
 //      st     stores of slots < st have completed            (epilogue store thread, on request)
 //    and every hazard the planner found is a wait on one of them;
@@ -32,10 +32,11 @@ struct GeoRF {
   using R = GeoRes<K, ELL>;
   static constexpr int CT_BYTES = R::CT_BYTES, CT_WORDS = R::CT_WORDS, B_BYTES = R::B_BYTES,
                        TA_BYTES = R::TA_BYTES;
-  static constexpr int THREADS = R::THREADS;
+  static constexpr int WARP_ST = R::THREADS / 32;   // + the store warp
+  static constexpr int THREADS = R::THREADS + 32;
   static constexpr int N_OUT = 3;
   static constexpr int RING = (int)rf::RF_FILL_RING;
-  static constexpr int N_BARS = 8 + 2 * N_OUT + RING;
+  static constexpr int N_BARS = 8 + 3 * N_OUT + RING + 4;
   __host__ __device__ static uint32_t off_b(uint32_t n_buf) { return ((n_buf * CT_BYTES + 127u) / 128u) * 128u; }
   __host__ __device__ static uint32_t off_ta(uint32_t n_buf) { return off_b(n_buf) + 2u * B_BYTES; }
   __host__ __device__ static uint32_t off_bar(uint32_t n_buf) {
@@ -95,8 +96,10 @@ struct RFPos {
   }
 };
 
-// Operand wait of a builder / B copier for one side: a fill's completion barrier, or a near
-// producer's epilogue (epi counter).
+// Operand waits of a builder (own = left) or B copier (own = right): its own operand's fill
+// barrier or near producer's epilogue (epi counter), and ALSO the other operand's fill -- a
+// fill is waited on only by its first reading slot, so both roles must wait there: a later
+// reader in the other role is ordered after this slot by that role's own program order only.
 __device__ __forceinline__ void rf_operand_wait(uint32_t w, uint32_t it, uint32_t base, uint32_t n_fills,
                                                 uint64_t *fill_full, const uint32_t *ctr_epi) {
   if (w == rf::NONE) return;
@@ -106,6 +109,12 @@ __device__ __forceinline__ void rf_operand_wait(uint32_t w, uint32_t it, uint32_
   } else {
     rf_wait_ge(ctr_epi, base + w + 1);
   }
+}
+
+// A slot whose output buffer last held a stored value (or, in a later lane, may have): its
+// epilogue and tail rows wait for the store warp to see those stores read (dest_ok).
+__device__ __forceinline__ bool rf_dest_guarded(const fhegpu_rf_slot &si, uint32_t it) {
+  return (si.bits & (rf::SB_DEST_STORED | rf::SB_HAZARD)) || ((si.bits & rf::SB_DEST_FIRST) && it > 0);
 }
 
 template <int K, int ELL, bool PM, int ENC>
@@ -125,8 +134,10 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
   uint64_t *main_done = bar + 2;            // [2]
   uint64_t *a_free = bar + 4;               // [2]
   uint64_t *d_free = bar + 6;               // [2]
-  uint64_t *out_free = bar + 8;             // [N_OUT] tail rows of slot t may be written
-  uint64_t *tail_ready = bar + 8 + F::N_OUT;
+  uint64_t *rows_ready = bar + 8;           // [N_OUT] epilogue rows of slot t written (every epilogue warp)
+  uint64_t *tail_ready = bar + 8 + F::N_OUT;  // [N_OUT] tail rows of slot t written
+  uint64_t *slot_free = bar + 8 + 2 * F::N_OUT + F::RING;   // [N_OUT] the store warp is done with slot t
+  uint64_t *dest_ok = slot_free + F::N_OUT;   // [4] slot t's buffer may be written (store warp)
   uint64_t *fill_full = bar + 8 + 2 * F::N_OUT;   // [RING]
   uint32_t *ctr = reinterpret_cast<uint32_t *>(bar + F::N_BARS);
   uint32_t *ctr_built = ctr, *ctr_epi = ctr + 1, *ctr_st = ctr + 2, *ctr_streq = ctr + 3;
@@ -148,9 +159,11 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
       mbar_init(&d_free[i], R::NE_WARPS);
     }
     for (int i = 0; i < F::N_OUT; ++i) {
-      mbar_init(&out_free[i], 1);
+      mbar_init(&rows_ready[i], R::NE_WARPS);
       mbar_init(&tail_ready[i], 1);
     }
+    for (int i = 0; i < F::N_OUT; ++i) mbar_init(&slot_free[i], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&dest_ok[i], 1);
     for (int i = 0; i < F::RING; ++i) mbar_init(&fill_full[i], 1);
     for (int i = 0; i < 8; ++i) ctr[i] = 0;
     fence_mbar_init();
@@ -167,7 +180,73 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
   const uint32_t tmem_base = *tmem_slot;
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  if (warp == G::WARP_PROD) {
+  if (warp == F::WARP_ST) {
+    // ------------------------------ store warp: outputs, spills, progress ------------------------------
+    // Per slot, once the epilogue rows and the tail rows are in the buffer: publish epi, store a
+    // program output / spill, and allow the next slot's writes (dest_ok) once every store has
+    // read its buffer when that slot's buffer held a stored value.  st (store completion) is
+    // published as stores drain and on the producer's request (a fill of a recent spill).
+    if (lane == 0) {
+      uint32_t st_done = 0;
+#ifndef FHEGPU_RF_ST_LAG
+#define FHEGPU_RF_ST_LAG 1
+#endif
+      constexpr uint32_t LAG = FHEGPU_RF_ST_LAG;  // stores kept in flight before st advances
+      uint32_t st_ring[LAG];
+      uint32_t n_st = 0;
+#pragma unroll
+      for (uint32_t i = 0; i < LAG; ++i) st_ring[i] = 0;
+      auto serve = [&](uint32_t upto) {
+        if (ld_volatile_smem(ctr_streq) > st_done) {
+          bulk_wait_n<0>();
+          st_done = upto;
+          st_release_cta_smem(ctr_st, upto);
+        }
+      };
+      mbar_arrive(&dest_ok[0]);                     // slot 0
+      RFPos pos;
+      fhegpu_rf_slot nxt = rf_load_slot(slots, 0);
+      for (uint32_t t = 0; t < n_slots; ++t, pos.next(n_ops)) {
+        const fhegpu_rf_slot si = nxt;
+        nxt = rf_load_slot(slots, pos.r + 1 == n_ops ? 0u : pos.r + 1);
+        const uint32_t ob = t % F::N_OUT, ou = t / F::N_OUT;
+        uint32_t spins = 0;
+        while (!mbar_try(&rows_ready[ob], ou & 1u)) {   // serve requests while waiting
+          serve(t);
+          if (++spins > (1u << 22)) __trap();
+        }
+        rf_mbar_wait(&tail_ready[ob], ou & 1u);
+        st_release_cta_smem(ctr_epi, t + 1);          // slot t's output is readable in its buffer
+        if (si.bits & rf::SB_STORE) {
+          const uint32_t ln = lane_of(pos.it);
+          uint32_t *dst = (si.store & rf::STORE_SPILL)
+                              ? store + (spill_base + (uint64_t)blockIdx.x * n_spill + (si.store & ~rf::STORE_SPILL)) *
+                                            R::CT_WORDS
+                              : store + ((uint64_t)si.store * lanes + ln) * R::CT_WORDS;
+          bulk_s2g(dst, buf(si.dbuf), R::CT_BYTES);
+#pragma unroll
+          for (uint32_t i = LAG - 1; i > 0; --i) st_ring[i] = st_ring[i - 1];
+          st_ring[0] = t;
+          if (++n_st > LAG) {
+            bulk_wait_n<LAG>();                       // stores older than the last LAG are done
+            if (st_ring[LAG - 1] > st_done) {
+              st_done = st_ring[LAG - 1];
+              st_release_cta_smem(ctr_st, st_done);
+            }
+          }
+        }
+        mbar_arrive(&slot_free[ob]);
+        if (t + 1 < n_slots) {
+          const uint32_t it1 = pos.r + 1 == n_ops ? pos.it + 1 : pos.it;
+          if (rf_dest_guarded(nxt, it1)) bulk_wait_read_n<0>();   // its buffer's stores have read it
+          mbar_arrive(&dest_ok[(t + 1) & 3u]);
+        }
+        serve(t + 1);
+        trace_ev(p, t, 11);
+      }
+      bulk_wait_all();
+    }
+  } else if (warp == G::WARP_PROD) {
     // ------------------------------ producer: the plan's fills, in order ------------------------------
     if (lane == 0) {
       for (uint32_t it = 0; it < my_lanes; ++it) {
@@ -208,8 +287,9 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
     for (uint32_t t = 0; t < n_slots; ++t) {
       const uint32_t b = t & 1u, u = t >> 1;
       rf_mbar_wait(&op_full[b], u & 1u);
-      if (lane == 0) st_release_cta_smem(ctr_built, t + 1);   // slot t's operand buffers are read
+      if (lane == 0) trace_ev(p, t, 2);
       rf_mbar_wait(&d_free[b], (u & 1u) ^ 1u);
+      if (lane == 0) trace_ev(p, t, 3);
       tc_fence_after();
       const uint32_t tb = tmem_base + b * G::BUF_COLS;
       const uint64_t bd_b = bdesc0 + ((b * R::B_BYTES) >> 4);
@@ -232,24 +312,34 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
       __syncwarp();
       if (elect_one()) mma_commit(&main_done[b]);
       __syncwarp();
+      if (lane == 0) trace_ev(p, t, 4);
     }
   } else if (warp == G::WARP_TAIL) {
     // ------------------------------ tail rows, into the gate's buffer ------------------------------
     if constexpr (G::TAIL > 0) {
       RFPos pos;
+      fhegpu_rf_slot nxt = rf_load_slot(slots, 0);
       for (uint32_t t = 0; t < n_slots; ++t, pos.next(n_ops)) {
         const uint32_t b = t & 1u, u = t >> 1;
-        const fhegpu_rf_slot si = rf_load_slot(slots, pos.r);
+        const fhegpu_rf_slot si = nxt;
+        nxt = rf_load_slot(slots, pos.r + 1 == n_ops ? 0u : pos.r + 1);
         rf_mbar_wait(&main_done[b], u & 1u);
+        if (lane == 0) trace_ev(p, t, 12);
         tc_fence_after();
         uint32_t d[36];
         load_acc36(tmem_base + b * G::BUF_COLS + G::D_COLS, d, false);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&a_free[b]);
-        const uint32_t ob = t % F::N_OUT, ou = t / F::N_OUT;
-        rf_mbar_wait(&out_free[ob], ou & 1u);
+        if (lane == 0) {
+          mbar_arrive(&a_free[b]);
+          // slot t's MMAs are done, so its operand buffers were read long before (op_full):
+          // publish from here -- a release on the MMA warp would sit on its issue path
+          st_release_cta_smem(ctr_built, t + 1);
+        }
+        const uint32_t ob = t % F::N_OUT;
+        if (rf_dest_guarded(si, pos.it)) rf_mbar_wait(&dest_ok[t & 3u], (t >> 2) & 1u);
+        if (lane == 0) trace_ev(p, t, 13);
         uint32_t *out_st = buf(si.dbuf);
         if (lane < G::TAIL) {
           const int row = G::MMA_ROWS + lane;
@@ -259,7 +349,12 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tail_ready[ob]);
+        // tail_ready(t) reuses the entry of slot t - 3: the store warp must be done with it
+        if (lane == 0) {
+          rf_mbar_wait(&slot_free[ob], ((t / F::N_OUT) & 1u) ^ 1u);
+          mbar_arrive(&tail_ready[ob]);
+        }
+        if (lane == 0) trace_ev(p, t, 14);
       }
     }
   } else if (warp >= R::WARP_BC0 && warp < R::WARP_EPI0) {
@@ -284,8 +379,11 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
       const uint32_t b = t & 1u, u = t >> 1;
       const fhegpu_rf_slot si = nxt;
       nxt = rf_load_slot(slots, pos.r + 1 == n_ops ? 0u : pos.r + 1);
+      if (bc == 0) trace_ev(p, t, 0);
       rf_mbar_wait(&a_free[b], (u & 1u) ^ 1u);        // B(b) was last read by the MMAs of slot t - 2
       rf_operand_wait(si.rwait, pos.it, pos.base, n_fills, fill_full, ctr_epi);
+      if (si.lwait != rf::NONE && (si.lwait & rf::WAIT_FILL))
+        rf_operand_wait(si.lwait, pos.it, pos.base, n_fills, fill_full, ctr_epi);
       const uint32_t *v2 = buf(si.rbuf);
       const bool comp2 = si.bits & rf::SB_RNEG;
       uint8_t *bb = s_b + b * R::B_BYTES;
@@ -313,6 +411,7 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&op_full[b]);
+      if (bc == 0) trace_ev(p, t, 1);
     }
   } else if (warp < R::WARP_EPI0) {
     // ------------------------------ A operand builders ------------------------------
@@ -329,8 +428,13 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
       const uint32_t b = t & 1u, u = t >> 1;
       const fhegpu_rf_slot si = nxt;
       nxt = rf_load_slot(slots, pos.r + 1 == n_ops ? 0u : pos.r + 1);
+      if (bt == 0) trace_ev(p, t, 5);
       rf_mbar_wait(&a_free[b], (u & 1u) ^ 1u);
+      if (bt == 0) trace_ev(p, t, 7);
       rf_operand_wait(si.lwait, pos.it, pos.base, n_fills, fill_full, ctr_epi);
+      if (si.rwait != rf::NONE && (si.rwait & rf::WAIT_FILL))
+        rf_operand_wait(si.rwait, pos.it, pos.base, n_fills, fill_full, ctr_epi);
+      if (bt == 0) trace_ev(p, t, 6);
       tc_fence_after();
       const uint32_t *v1 = buf(si.lbuf);
       const bool comp1 = si.bits & rf::SB_LNEG;
@@ -356,9 +460,12 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&op_full[b]);
+      if (bt == 0) trace_ev(p, t, 8);
     }
   } else {
     // ------------------------------ epilogue, into the gate's buffer ------------------------------
+    // Each warp on its own (no CTA barrier per slot): TMEM -> fold -> rows of the gate's
+    // buffer -> rows_ready.  Stores and progress counters belong to the store warp.
     const int et = tid - 32 * R::WARP_EPI0;
     const int ew = et >> 5;
     const int quad = warp & 3;
@@ -366,17 +473,6 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
     const int row = 128 * tile + 32 * quad + lane;
     const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
     const int row_blk = row / ELL, row_bit = row - row_blk * ELL;
-    constexpr uint32_t NE_THREADS = 32 * R::NE_WARPS;
-    if (et == 0) mbar_arrive(&out_free[0]);
-    uint32_t st_done = 0;                           // (store thread) slots whose stores are known complete
-    // the store thread drains its bulk stores when the producer asks (a fill waits on a spill)
-    auto serve = [&](uint32_t upto) {
-      if (ld_volatile_smem(ctr_streq) > st_done) {
-        bulk_wait_n<0>();
-        st_done = upto;
-        st_release_cta_smem(ctr_st, upto);
-      }
-    };
     RFPos pos;
     fhegpu_rf_slot nxt = rf_load_slot(slots, 0);
     for (uint32_t t = 0; t < n_slots; ++t, pos.next(n_ops)) {
@@ -384,64 +480,28 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
       const fhegpu_rf_slot si = nxt;
       nxt = rf_load_slot(slots, pos.r + 1 == n_ops ? 0u : pos.r + 1);
       uint32_t *out_st = buf(si.dbuf);
-      if (et == 0) {
-        uint32_t spins = 0;
-        while (!mbar_test(&main_done[b], u & 1u)) {
-          serve(t);                                  // stores of slots < t were all issued
-          if (++spins > FHEGPU_SPIN_LIMIT) __trap();
-        }
-      } else {
-        rf_mbar_wait(&main_done[b], u & 1u);
-      }
-      if (si.bits & rf::SB_HAZARD) named_bar(2, NE_THREADS);   // slot t-1's store has read the buffer
+      rf_mbar_wait(&main_done[b], u & 1u);
+      if (et == 0) trace_ev(p, t, 9);
       tc_fence_after();
       const uint32_t dcol = tmem_base + b * G::BUF_COLS + lane_off + tile * G::NPAD;
-      {
-        uint32_t d[36];
-        load_acc36(dcol, d, false);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&d_free[b]);
+      uint32_t d[36];
+      load_acc36(dcol, d, false);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&d_free[b]);
+      if (rf_dest_guarded(si, pos.it)) rf_mbar_wait(&dest_ok[t & 3u], (t >> 2) & 1u);
 #pragma unroll
-        for (int i = 0; i < K; ++i)
-          out_st[row * K + i] = finish_neg<ELL, PM, ENC>(&d[i * 4], i == row_blk ? (1u << row_bit) : 0u, p);
-      }
+      for (int i = 0; i < K; ++i)
+        out_st[row * K + i] = finish_neg<ELL, PM, ENC>(&d[i * 4], i == row_blk ? (1u << row_bit) : 0u, p);
       fence_proxy_async_smem();
-      const bool last = t + 1 == n_slots;
-      const bool next_first = pos.r + 1 == n_ops;   // the next slot starts a new lane
-      const bool next_hazard = !last && (nxt.bits & rf::SB_HAZARD);
-      if (et == 0 && !last) {
-        // the next gate overwrites a buffer whose value was stored (this lane, or the previous
-        // one): every store must have read its source before the epilogue writes it
-        if ((nxt.bits & rf::SB_DEST_STORED) || (next_first && (nxt.bits & rf::SB_DEST_FIRST))) bulk_wait_read_n<0>();
-        if (!next_hazard) mbar_arrive(&out_free[(t + 1) % F::N_OUT]);
+      __syncwarp();
+      if (lane == 0) {                             // (entry reuse: as tail_ready)
+        rf_mbar_wait(&slot_free[t % F::N_OUT], ((t / F::N_OUT) & 1u) ^ 1u);
+        mbar_arrive(&rows_ready[t % F::N_OUT]);
       }
-      named_bar(1, NE_THREADS);
-      if (et == 0) {
-        const uint32_t ob = t % F::N_OUT, ou = t / F::N_OUT;
-        rf_mbar_wait(&tail_ready[ob], ou & 1u);
-        if (si.bits & rf::SB_STORE) {
-          const uint32_t ln = lane_of(pos.it);
-          uint32_t *dst = (si.store & rf::STORE_SPILL)
-                              ? store + (spill_base + (uint64_t)blockIdx.x * n_spill + (si.store & ~rf::STORE_SPILL)) *
-                                            R::CT_WORDS
-                              : store + ((uint64_t)si.store * lanes + ln) * R::CT_WORDS;
-          bulk_s2g(dst, out_st, R::CT_BYTES);
-        }
-        if (next_hazard) {                         // the next gate rewrites this buffer
-          bulk_wait_read_n<0>();
-          mbar_arrive(&out_free[(t + 1) % F::N_OUT]);
-        }
-        serve(t + 1);
-      } else if (et == 32) {
-        // the gate's output is readable in its buffer (tail rows included)
-        const uint32_t ob = t % F::N_OUT, ou = t / F::N_OUT;
-        rf_mbar_wait(&tail_ready[ob], ou & 1u);
-        st_release_cta_smem(ctr_epi, t + 1);
-      }
+      if (et == 0) trace_ev(p, t, 10);
     }
-    if (et == 0) bulk_wait_all();
   }
 
   tc_fence_before();

@@ -161,7 +161,7 @@ class LevelledNetlist:
             out[s:e] = seg
         return out
 
-    def _compile(self, ssa: bool = False, ring_temps: bool = False):
+    def _compile(self, ssa: bool = False, ring_temps: bool = False, pin_old: bool = False):
         """Level-sort the pending gates and assign ciphertext slots by liveness.
 
         A slot read at level L is released before the launch of level L + 1 at
@@ -171,6 +171,10 @@ class LevelledNetlist:
         ssa=True (dataflow programs, one launch without level boundaries): no slot is
         reused within the program -- slots released by it return to the pool only after
         it -- and ``deps`` gives, per op, the op indices that produced its operands.
+
+        pin_old=True (register-file programs, which read inputs and write outputs in their own
+        order): slots of nodes that existed before the program are not reused inside it, the
+        program's own temporaries reuse slots as in level launches.
 
         ring_temps=True (tiled programs): outputs nobody holds after the program
         ("temporaries") get no batch-wide slot; ``temp`` (per op: left, right, out) carries
@@ -216,12 +220,15 @@ class LevelledNetlist:
         free = self._free
         deferred = []
         first_lv = int(lv_vals[0]) if len(lv_vals) else 0
+        was_slotted = slot >= 0                    # nodes from before this program
         for lv, s, e in zip(lv_vals.tolist(), lv_start.tolist(), lv_end.tolist()):
             hi = int(np.searchsorted(cand_at, lv, side="right"))
             if hi > ptr:
                 rel = slot[cand[ptr:hi]]
-                if ssa:                            # only slots this program never reads
+                if ssa or pin_old:                 # only slots this program never reads
                     untouched = free_at[cand[ptr:hi]] <= first_lv
+                    if pin_old and not ssa:
+                        untouched |= ~was_slotted[cand[ptr:hi]]
                     free.extend(rel[(rel >= 0) & untouched].tolist())
                     deferred.extend(rel[(rel >= 0) & ~untouched].tolist())
                 else:
@@ -829,7 +836,7 @@ class GpuEngine(LevelledNetlist):
             sched = self._pick_schedule()
             comp = None
             if sched not in ("tiled", "resident"):
-                prog = self._compile(ssa=sched in ("dataflow", "queue", "regfile"))
+                prog = self._compile(ssa=sched in ("dataflow", "queue"), pin_old=sched == "regfile")
                 prog["schedule"] = sched
                 out_slots = np.asarray(self._slot, dtype=np.int64)[tpl.out_internal]
                 comp = {"prog": prog, "n_slots": self._n_slots, "out_slots": out_slots}
@@ -913,9 +920,9 @@ class GpuEngine(LevelledNetlist):
         sched = self._pick_schedule()
         dataflow = sched in ("dataflow", "queue", "tiled")
         ring = self.TILE_RING if sched == "tiled" and self._ring_ok() else 0
-        # register-file programs read inputs and write outputs in their own order: no slot is
-        # reused inside the program (single assignment)
-        prog = self._compile(ssa=dataflow or sched == "regfile", ring_temps=ring > 0)
+        # register-file programs read inputs and write outputs in their own order: input slots
+        # are not reused inside the program
+        prog = self._compile(ssa=dataflow, ring_temps=ring > 0, pin_old=sched == "regfile")
         prog["schedule"] = sched
         self._pending_ops = []
         if self._cse_map is not None:
@@ -967,7 +974,8 @@ class GpuEngine(LevelledNetlist):
     # register-file launches (csrc/tc_nand_regfile.cuh): shared-memory buffers per CTA, the
     # planner's dependency distance and fill lookahead (csrc/rf_plan.h)
     RF_BUFFERS = int(os.environ.get("FHEGPU_RF_BUFFERS", "20"))
-    RF_DIST, RF_LOOK = 5, 4
+    RF_DIST = int(os.environ.get("FHEGPU_RF_DIST", "5"))
+    RF_LOOK = int(os.environ.get("FHEGPU_RF_LOOK", "10"))    # fills >= 8 slots ahead of their readers
     REGFILE_MIN_LANES = 296        # 'auto': deep programs over >= 2 lanes per SM
     REGFILE_MIN_LEVELS = 16
     REGFILE_AUTO = os.environ.get("FHEGPU_REGFILE", "1") != "0"

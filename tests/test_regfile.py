@@ -106,3 +106,15 @@ def test_plan_records_are_consistent():
                 assert t - 5 < w < t                                          # only near producers wait
     with pytest.raises(Exception, match="n_buf"):
         rf_plan(gates, np.arange(8, dtype=np.uint32), 2, 5, 3)
+
+
+def test_regfile_compile_keeps_input_slots_and_outputs_apart():
+    """The register-file kernel fills inputs and stores outputs in its own order: the compile
+    (pin_old) never hands an input's slot to an output, outputs get distinct slots, and the
+    program's temporaries still reuse slots (the store stays level-launch sized)."""
+    eng, prog = _program("cfg4", 4)
+    gates, ins = regfile_gates(prog)
+    outs = gates["out_slot"][gates["held"] == 1]
+    assert len(set(outs.tolist())) == len(outs)
+    assert not set(outs.tolist()) & set(ins.tolist())
+    assert eng._n_slots < 6000                     # ~3.6k live values per signal, not 108k

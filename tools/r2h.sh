@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 300 python tools/probes/regfile_timing.py > gpurun_out/rf_timing.txt 2>&1
+RF_LANES=148 RF_REPS=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:regfile_tc --launch-skip 1 --launch-count 1 -o gpurun_out/rf_full python tools/probes/regfile_timing.py regfile > gpurun_out/rf_ncu.log 2>&1
+echo ncu rc=$?

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 600 python tools/probes/regfile_synth.py > gpurun_out/rf_synth.txt 2>&1
+timeout 300 python tools/probes/regfile_timing.py regfile >> gpurun_out/rf_synth.txt 2>&1
