@@ -252,7 +252,8 @@ typedef struct fhegpu_rf_gate {
 typedef struct fhegpu_rf_slot {
   uint8_t lbuf, rbuf, dbuf, bits; /* bits: 1/2 complement l/r, 4 store, 8 dest held a stored
                                      value, 16 ... stored by the previous slot, 32 first write
-                                     of dest in the lane */
+                                     of dest in the lane, 64/128 left/right operand equal to
+                                     slot t-2's (A rebuild / B copy skipped) */
   uint32_t lwait, rwait;          /* 0xFFFFFFFF none; bit 31: fill id, else producer slot */
   uint32_t store;                 /* bit 31: spill index, else store slot (with bits & 4) */
 } fhegpu_rf_slot;
@@ -265,7 +266,8 @@ typedef struct fhegpu_rf_fill {
 int fhegpu_rf_plan(const fhegpu_rf_gate *gates, uint32_t n_gates, const uint32_t *in_slots, uint32_t n_in,
                    uint32_t n_buf, uint32_t min_dist, uint32_t lookahead, uint32_t *order,
                    fhegpu_rf_slot *slots, fhegpu_rf_fill *fills, uint32_t fill_cap, uint32_t *n_fills,
-                   uint32_t *n_spill, uint32_t *stats /* [3]: stalls, stores, fills; may be NULL */);
+                   uint32_t *n_spill,
+                   uint32_t *stats /* [5]: stalls, stores, fills, left / right operand reuses; may be NULL */);
 /* Attach a plan to a program: fhegpu_prog_run then runs it as ONE register-file launch
  * (tcgen05, k = 9, ell = 29), else level by level.  Spills of CTA c use ciphertexts
  * [spill_base + c * n_spill, + n_spill) of the store.  n_slots = 0 detaches. */

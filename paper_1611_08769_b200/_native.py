@@ -170,14 +170,15 @@ def rf_plan(gates: np.ndarray, in_slots, n_buf: int = 20, min_dist: int = 5, loo
     slots = np.zeros(n, dtype=RF_SLOT_DTYPE)
     fills = np.zeros(2 * n + 16, dtype=RF_FILL_DTYPE)
     n_fills, n_spill = ctypes.c_uint32(), ctypes.c_uint32()
-    stats = np.zeros(3, dtype=np.uint32)
+    stats = np.zeros(5, dtype=np.uint32)
     _check(_lib.fhegpu_rf_plan(gates.ctypes.data_as(ctypes.c_void_p), n, ins.ctypes.data_as(ctypes.c_void_p),
                                len(ins), int(n_buf), int(min_dist), int(lookahead),
                                order.ctypes.data_as(ctypes.c_void_p), slots.ctypes.data_as(ctypes.c_void_p),
                                fills.ctypes.data_as(ctypes.c_void_p), len(fills), ctypes.byref(n_fills),
                                ctypes.byref(n_spill), _ptr(stats, ctypes.c_uint32)), "rf_plan")
     return order, slots, fills[:n_fills.value].copy(), int(n_spill.value), \
-        {"stalls": int(stats[0]), "stores": int(stats[1]), "fills": int(stats[2])}
+        {"stalls": int(stats[0]), "stores": int(stats[1]), "fills": int(stats[2]), "reuse_l": int(stats[3]),
+         "reuse_r": int(stats[4])}
 
 
 def _ptr(arr, ctype):

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -1126,6 +1127,7 @@ int fhegpu_rf_plan(const fhegpu_rf_gate *gates, uint32_t n_gates, const uint32_t
   rf::Planner pl;
   pl.gates = gates, pl.n = n_gates, pl.n_in = n_in, pl.in_slots = in_slots;
   pl.n_buf = n_buf, pl.dist = std::max(1u, min_dist), pl.look = lookahead;
+  pl.reuse = !getenv("FHEGPU_RF_NOREUSE");     // experiment knob: schedule without reuse preference
   if (!pl.run()) return fail(FHEGPU_EINVAL, pl.err);
   if (pl.fills.size() > fill_cap)
     return fail(FHEGPU_EINVAL, "fill_cap " + std::to_string(fill_cap) + " < " + std::to_string(pl.fills.size()));
@@ -1134,7 +1136,9 @@ int fhegpu_rf_plan(const fhegpu_rf_gate *gates, uint32_t n_gates, const uint32_t
   if (!pl.fills.empty()) std::memcpy(fills, pl.fills.data(), pl.fills.size() * sizeof(fhegpu_rf_fill));
   *n_fills = (uint32_t)pl.fills.size();
   *n_spill = pl.n_spill;
-  if (stats) stats[0] = pl.stalls, stats[1] = pl.n_stores, stats[2] = (uint32_t)pl.fills.size();
+  if (stats)
+    stats[0] = pl.stalls, stats[1] = pl.n_stores, stats[2] = (uint32_t)pl.fills.size(), stats[3] = pl.n_reuse_l,
+    stats[4] = pl.n_reuse_r;
   return FHEGPU_OK;
 }
 

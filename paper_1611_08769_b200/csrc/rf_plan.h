@@ -52,7 +52,7 @@ constexpr uint32_t RF_NEAR = 5;               // producers >= 5 slots back need 
 
 // slot bits (fhegpu_rf_slot.bits)
 constexpr uint8_t SB_LNEG = 1, SB_RNEG = 2, SB_STORE = 4, SB_DEST_STORED = 8, SB_HAZARD = 16,
-                  SB_DEST_FIRST = 32;
+                  SB_DEST_FIRST = 32, SB_REUSE_L = 64, SB_REUSE_R = 128;
 // fill flags
 constexpr uint32_t FF_FIRST = 1;   // first use of the buffer in the lane program
 
@@ -60,12 +60,13 @@ struct Planner {
   // inputs
   const fhegpu_rf_gate *gates = nullptr;
   uint32_t n = 0, n_in = 0, n_buf = 0, dist = 5, look = 4;
+  bool reuse = true;                      // prefer operand reuse two slots apart (schedule)
   const uint32_t *in_slots = nullptr;
   // outputs
   std::vector<uint32_t> order;            // slot -> gate
   std::vector<fhegpu_rf_slot> slots;
   std::vector<fhegpu_rf_fill> fills;
-  uint32_t n_spill = 0, stalls = 0, n_stores = 0;
+  uint32_t n_spill = 0, stalls = 0, n_stores = 0, n_reuse_l = 0, n_reuse_r = 0;
   std::string err;
 
   uint32_t nv() const { return n_in + n; }
@@ -86,6 +87,11 @@ struct Planner {
     for (uint32_t g = n; g-- > 0;)
       for (uint32_t s : succ[g]) h[g] = std::max(h[g], h[s] + 1);
     std::vector<int64_t> md(n, -1);   // slot of the latest scheduled producer
+    // readers of each value by side (operand reuse: slot t's operand equal to slot t-2's lets the
+    // kernel skip rebuilding A / copying B -- see tc_nand_regfile.cuh)
+    std::vector<std::vector<uint32_t>> lread(nv()), rread(nv());
+    for (uint32_t g = 0; g < n; ++g) lread[gates[g].left].push_back(g), rread[gates[g].right].push_back(g);
+    std::vector<uint8_t> in_cand(n, 0), done(n, 0);
     // candidates: max (md, h, -g); pending: min allowed slot
     using Cand = std::tuple<int64_t, uint32_t, int64_t>;
     std::priority_queue<Cand> cand;
@@ -99,20 +105,45 @@ struct Planner {
       if (indeg[g] == 0) push(g);
     order.clear();
     order.reserve(n);
+    auto same_l = [&](uint32_t a, uint32_t b) {
+      return gates[a].left == gates[b].left && ((gates[a].flags ^ gates[b].flags) & 1u) == 0;
+    };
+    auto same_r = [&](uint32_t a, uint32_t b) {
+      return gates[a].right == gates[b].right && ((gates[a].flags ^ gates[b].flags) & 2u) == 0;
+    };
     for (int64_t t = 0; (uint32_t)t < n; ++t) {
       while (!pend.empty() && std::get<0>(pend.top()) <= t) {
         const uint32_t g = std::get<3>(pend.top());
         pend.pop();
         cand.emplace(md[g], h[g], -(int64_t)g);
+        in_cand[g] = 1;
       }
-      uint32_t g;
-      if (!cand.empty()) {
+      while (!cand.empty() && done[(uint32_t)(-std::get<2>(cand.top()))]) cand.pop();   // taken by reuse
+      uint32_t g = NONE;
+      if (reuse && t >= 2) {                  // an allowed gate sharing slot t-2's operands
+        const uint32_t p2 = order[t - 2];
+        int best = 0;
+        for (int side = 0; side < 2 && best < 3; ++side) {
+          const auto &rd = side ? rread[gates[p2].right] : lread[gates[p2].left];
+          if (rd.size() > 64) continue;       // (hubs: not worth the scan)
+          for (uint32_t c : rd) {
+            if (!in_cand[c] || done[c]) continue;
+            const int sc = (same_l(c, p2) ? 2 : 0) + (same_r(c, p2) ? 1 : 0);
+            if (sc > best) best = sc, g = c;
+          }
+        }
+      }
+      if (g != NONE) {
+        done[g] = 1;
+      } else if (!cand.empty()) {
         g = (uint32_t)(-std::get<2>(cand.top()));
         cand.pop();
+        done[g] = 1;
       } else {
         if (pend.empty()) return fail("schedule: no ready gate (cycle?)");
         g = std::get<3>(pend.top());
         pend.pop();
+        done[g] = 1;
         ++stalls;
       }
       order.push_back(g);
@@ -153,6 +184,19 @@ struct Planner {
     std::vector<uint32_t> res_prod(V, NONE);      // slot that wrote the value into its buffer
     slots.assign(n, fhegpu_rf_slot{});
     fills.clear();
+    // store slots known so far (held outputs from the start, spills as they are decided): an
+    // output buffer whose stored occupant has a later store in (p, t - 4] needs no dest_ok wait --
+    // the store warp drains each store before issuing the next (LAG 1) and is never more than
+    // 4 slots behind the epilogue (slot_free), tc_nand_regfile.cuh
+    std::vector<uint32_t> fen(n + 1, 0);
+    auto fen_add = [&](uint32_t i) { for (++i; i <= n; i += i & (0u - i)) ++fen[i]; };
+    auto fen_sum = [&](uint32_t i) {              // stores at slots < i
+      uint32_t r = 0;
+      for (; i > 0; i -= i & (0u - i)) r += fen[i];
+      return r;
+    };
+    for (uint32_t t = 0; t < n; ++t)
+      if (gates[order[t]].held) fen_add(t);
     for (uint32_t t = 0; t < n; ++t) {
       slots[t].lwait = slots[t].rwait = NONE;
       slots[t].store = NONE;
@@ -189,7 +233,10 @@ struct Planner {
       Prev pv{occ[best], b_lastread[best], b_written[best], false, b_used[best]};
       if (pv.v != NONE) {
         const uint32_t u = next_use(pv.v, t + 1);
-        if (u != NONE && !in_store(pv.v)) spill[pv.v] = 1;  // stored at its producer's epilogue
+        if (u != NONE && !in_store(pv.v)) {           // stored at its producer's epilogue
+          spill[pv.v] = 1;
+          fen_add(produced_at(pv.v));
+        }
         pv.stored = pv.v >= n_in && (held(pv.v) || spill[pv.v]) && res_prod[pv.v] != NONE;
         vbuf[pv.v] = NONE;
         occ[best] = NONE;
@@ -225,6 +272,11 @@ struct Planner {
       if (vbuf[gt.right] == NONE && !issue_fill(gt.right, t, gt.left)) return false;
       fhegpu_rf_slot &s = slots[t];
       s.bits = (uint8_t)(gt.flags & 3u);
+      if (t >= 2) {
+        const fhegpu_rf_gate &g2 = gates[order[t - 2]];
+        if (g2.left == gt.left && ((g2.flags ^ gt.flags) & 1u) == 0) s.bits |= SB_REUSE_L, ++n_reuse_l;
+        if (g2.right == gt.right && ((g2.flags ^ gt.flags) & 2u) == 0) s.bits |= SB_REUSE_R, ++n_reuse_r;
+      }
       for (int side = 0; side < 2; ++side) {
         const uint32_t v = side ? gt.right : gt.left;
         const uint32_t b = vbuf[v];
@@ -244,8 +296,9 @@ struct Planner {
       const Prev pv = r.second;
       if (db == NONE) return fail("regfile: no destination buffer at slot " + std::to_string(t));
       if (pv.stored) {
-        s.bits |= SB_DEST_STORED;
-        if (res_prod[pv.v] + 1 == t) s.bits |= SB_HAZARD;
+        const uint32_t p = res_prod[pv.v];
+        if (p + 1 == t) s.bits |= SB_DEST_STORED | SB_HAZARD;
+        else if (t < 5 || p + 1 > t - 4 || fen_sum(t - 3) - fen_sum(p + 1) == 0) s.bits |= SB_DEST_STORED;
       }
       if (!b_used[db]) s.bits |= SB_DEST_FIRST;
       s.dbuf = (uint8_t)db;

@@ -42,7 +42,7 @@ struct GeoRF {
   __host__ __device__ static uint32_t off_bar(uint32_t n_buf) {
     return ((off_ta(n_buf) + 2u * TA_BYTES + 127u) / 128u) * 128u;
   }
-  __host__ __device__ static uint32_t smem_bytes(uint32_t n_buf) { return off_bar(n_buf) + N_BARS * 8u + 64u; }
+  __host__ __device__ static uint32_t smem_bytes(uint32_t n_buf) { return off_bar(n_buf) + N_BARS * 8u + 128u; }
 };
 
 // mbarrier phase wait with a bound (trap instead of a hung GPU if a plan ever deadlocks).
@@ -142,6 +142,7 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
   uint32_t *ctr = reinterpret_cast<uint32_t *>(bar + F::N_BARS);
   uint32_t *ctr_built = ctr, *ctr_epi = ctr + 1, *ctr_st = ctr + 2, *ctr_streq = ctr + 3;
   uint32_t *tmem_slot = ctr + 8;
+  uint32_t *s_fcons = ctr + 16;                  // [RF_FILL_RING] consumer slot of the last fills (producer)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -248,36 +249,59 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
     }
   } else if (warp == G::WARP_PROD) {
     // ------------------------------ producer: the plan's fills, in order ------------------------------
-    if (lane == 0) {
-      for (uint32_t it = 0; it < my_lanes; ++it) {
-        const uint32_t base = it * n_ops, ln = lane_of(it);
-        for (uint32_t f = 0; f < n_fills; ++f) {
-          const uint4 a = __ldg(reinterpret_cast<const uint4 *>(fills + f));       // buf, src, consumer, w_built
-          const uint4 c = __ldg(reinterpret_cast<const uint4 *>(fills + f) + 1);   // w_epi, w_st, flags, pad
-          uint32_t need_built = a.w ? base + a.w : 0, need_epi = c.x ? base + c.x : 0;
-          uint32_t need_st = c.y ? base + c.y : 0;
-          if ((c.z & rf::FF_FIRST) && it > 0)         // the buffer's last occupant is the previous lane's
-            need_built = max(need_built, base), need_epi = max(need_epi, base), need_st = max(need_st, base);
-          const uint32_t q = it * n_fills + f;
-          if (q >= rf::RF_FILL_RING) {                // its barrier's previous fill has been waited for
-            const uint32_t pq = q - rf::RF_FILL_RING, pit = pq / n_fills, pf = pq - pit * n_fills;
-            need_built = max(need_built, pit * n_ops + __ldg(&fills[pf].consumer) + 1);
+    // The whole warp loads the fill records 32 at a time (the next batch prefetched) and hands
+    // them to lane 0 by shuffle: a record fetched per fill would put an L2 round trip on every
+    // fill of a burst (a butterfly's operands).
+    auto load = [&](uint32_t f, uint4 &a, uint4 &c) {
+      if (f < n_fills) {
+        a = __ldg(reinterpret_cast<const uint4 *>(fills + f));        // buf, src, consumer, w_built
+        c = __ldg(reinterpret_cast<const uint4 *>(fills + f) + 1);    // w_epi, w_st, flags, pad
+      } else {
+        a = c = make_uint4(0u, 0u, 0u, 0u);
+      }
+    };
+    auto shfl4 = [&](const uint4 &v, uint32_t j) {
+      return make_uint4(__shfl_sync(0xffffffffu, v.x, j), __shfl_sync(0xffffffffu, v.y, j),
+                        __shfl_sync(0xffffffffu, v.z, j), __shfl_sync(0xffffffffu, v.w, j));
+    };
+    for (uint32_t it = 0; it < my_lanes; ++it) {
+      const uint32_t base = it * n_ops, ln = lane_of(it);
+      uint4 a, c;
+      load(lane, a, c);
+      for (uint32_t f0 = 0; f0 < n_fills; f0 += 32) {
+        uint4 na, nc;
+        load(f0 + 32 + lane, na, nc);
+        const uint32_t cnt = min(32u, n_fills - f0);
+        for (uint32_t j = 0; j < cnt; ++j) {
+          const uint4 A = shfl4(a, j), C = shfl4(c, j);
+          if (lane == 0) {
+            const uint32_t f = f0 + j;
+            uint32_t need_built = A.w ? base + A.w : 0, need_epi = C.x ? base + C.x : 0;
+            uint32_t need_st = C.y ? base + C.y : 0;
+            if ((C.z & rf::FF_FIRST) && it > 0)       // the buffer's last occupant is the previous lane's
+              need_built = max(need_built, base), need_epi = max(need_epi, base), need_st = max(need_st, base);
+            const uint32_t q = it * n_fills + f;
+            if (q >= rf::RF_FILL_RING)                // its barrier's previous fill has been waited for
+              need_built = max(need_built, s_fcons[q % rf::RF_FILL_RING] + 1);
+            s_fcons[q % rf::RF_FILL_RING] = base + A.z;
+            rf_wait_ge(ctr_built, need_built);
+            rf_wait_ge(ctr_epi, need_epi);
+            if (need_st && ld_acquire_cta_smem(ctr_st) < need_st) {
+              st_volatile_smem(ctr_streq, need_st);   // ask the store warp to drain its stores
+              rf_wait_ge(ctr_st, need_st);
+            }
+            fence_proxy_async_global();               // completed stores -> this async-proxy load
+            const uint32_t *src = (A.y & rf::STORE_SPILL)
+                                      ? store + (spill_base + (uint64_t)blockIdx.x * n_spill +
+                                                 (A.y & ~rf::STORE_SPILL)) * R::CT_WORDS
+                                      : store + ((uint64_t)A.y * lanes + ln) * R::CT_WORDS;
+            uint64_t *fb = &fill_full[q % rf::RF_FILL_RING];
+            mbar_expect_tx(fb, R::CT_BYTES);
+            bulk_g2s(buf(A.x), src, R::CT_BYTES, fb);
           }
-          rf_wait_ge(ctr_built, need_built);
-          rf_wait_ge(ctr_epi, need_epi);
-          if (need_st && ld_acquire_cta_smem(ctr_st) < need_st) {
-            st_volatile_smem(ctr_streq, need_st);     // ask the store thread to drain its stores
-            rf_wait_ge(ctr_st, need_st);
-          }
-          fence_proxy_async_global();                 // completed stores -> this async-proxy load
-          const uint32_t *src = (a.y & rf::STORE_SPILL)
-                                    ? store + (spill_base + (uint64_t)blockIdx.x * n_spill + (a.y & ~rf::STORE_SPILL)) *
-                                                  R::CT_WORDS
-                                    : store + ((uint64_t)a.y * lanes + ln) * R::CT_WORDS;
-          uint64_t *fb = &fill_full[q % rf::RF_FILL_RING];
-          mbar_expect_tx(fb, R::CT_BYTES);
-          bulk_g2s(buf(a.x), src, R::CT_BYTES, fb);
+          __syncwarp();
         }
+        a = na, c = nc;
       }
     }
   } else if (warp == G::WARP_MMA) {
@@ -387,8 +411,10 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
       const uint32_t *v2 = buf(si.rbuf);
       const bool comp2 = si.bits & rf::SB_RNEG;
       uint8_t *bb = s_b + b * R::B_BYTES;
+      // B(b) still holds slot t-2's right operand: equal operands skip the copy (same lane only)
+      const bool reuse = (si.bits & rf::SB_REUSE_R) && pos.r >= 2 && !(p.dbg & (1u << 20));
 #pragma unroll
-      for (int x = 0; x < B_ROWS; ++x) {
+      for (int x = 0; x < (reuse ? 0 : B_ROWS); ++x) {
         if (b_src[x] < 0) continue;
         uint32_t vals[K];
 #pragma unroll
@@ -438,12 +464,19 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
       tc_fence_after();
       const uint32_t *v1 = buf(si.lbuf);
       const bool comp1 = si.bits & rf::SB_LNEG;
+      // A(b) still holds slot t-2's left operand except tile 0's first 6 words, which that slot's
+      // M = 64 tail accumulator overwrote (as in resident_tc_kernel), and TA(b) its tail rows
+      const bool reuse = (si.bits & rf::SB_REUSE_L) && pos.r >= 2 && !(p.dbg & (1u << 20));
       {
         const uint32_t a_addr = tmem_base + b * G::BUF_COLS + lane_off + G::D_COLS + tile * 8 * K;
-        build_a_words<K, 0, K, ENC>(v1, row, row_blk, row_bit, comp1, p.q, a_addr);
+        if (reuse) {
+          if (tile == 0) build_a_words<K, 0, 6, ENC>(v1, row, row_blk, row_bit, comp1, p.q, a_addr);
+        } else {
+          build_a_words<K, 0, K, ENC>(v1, row, row_blk, row_bit, comp1, p.q, a_addr);
+        }
       }
       if constexpr (G::TAIL > 0) {
-        if (bt < G::TAIL * K) {
+        if (bt < G::TAIL * K && !reuse) {
           const int m = bt / K, ww = bt - m * K;
           const int rr = G::MMA_ROWS + m;
           uint32_t v = v1[rr * K + ww];

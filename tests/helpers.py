@@ -175,7 +175,8 @@ def replay_regfile(gates, in_slots, order, slots, fills, n_buf, store, mask, E=4
     steps later), slot b is built when its waits hold (fills landed; near producers' outputs
     in their buffers), its epilogue writes the buffer E steps after the build, a store takes
     its snapshot of the buffer R steps after the epilogue and reaches the store W steps after
-    that.  Hazards the plan leaves uncovered therefore read stale or clobbered data.  Returns
+    that, unless the next store drains it earlier (the kernel's store warp keeps one store in
+    flight).  Hazards the plan leaves uncovered therefore read stale or clobbered data.  Returns
     the store dict (slot -> bits; spills under ('s', k))."""
     from paper_1611_08769_b200._csrc_consts import RF
     n = len(order)
@@ -230,6 +231,14 @@ def replay_regfile(gates, in_slots, order, slots, fills, n_buf, store, mask, E=4
             b ^= mask if g["flags"] & 2 else 0
             bufs[int(sl["dbuf"])] = ~(a & b) & mask
             if sl["bits"] & RF.SB_STORE:
+                # the store warp drains the previous store when it issues a new one (LAG 1)
+                for (_, s2, db) in sorted(pend_snap):
+                    pend_write.append((tau, s2, key_of(int(slots[s2]["store"])), bufs[db]))
+                pend_snap.clear()
+                for item in list(pend_write):
+                    pend_write.remove(item)
+                    g_store[item[2]] = item[3]
+                    done_store.add(item[1])
                 pend_snap.append((tau + R, s, int(sl["dbuf"])))
             epi += 1
         for item in sorted(pend_snap):

@@ -58,3 +58,22 @@ def test_regfile_is_auto_for_cfg4_and_replays():
         assert eng.template_hits == call
         assert np.array_equal(read_signal_ints(eng, out), want)
         del eng, out
+
+
+def test_regfile_operand_reuse_equals_full_rebuild():
+    """Slots whose operand equals the one two slots earlier skip the A rebuild / B copy (plan bits
+    64 / 128); debug bit 20 rebuilds every operand: identical ciphertexts either way."""
+    GpuEngine._TEMPLATES.clear()
+    scheme = GswScheme(DEFAULT0_PARAMS)
+    keys = scheme.keygen(4)
+    vals = {}
+    for dbg in (0, 1 << 20):
+        scheme.ctx.set_debug(dbg)
+        try:
+            eng, out, v = _run("cfg4", 20, "regfile", scheme, keys)
+            assert eng.last_compile["regfile"]["reuse_l"] > 0 and eng.last_compile["regfile"]["reuse_r"] > 0
+            vals[dbg] = v
+        finally:
+            scheme.ctx.set_debug(0)
+        del eng, out
+    assert np.array_equal(vals[0], vals[1 << 20])

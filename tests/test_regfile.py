@@ -44,7 +44,7 @@ def test_cfg4_plan_moves_under_half_a_ciphertext_per_gate():
     eng, prog = _program("cfg4", 6)
     stats, n_spill = _check(eng, prog, 20, [(4, 1, 3, 2), (6, 3, 9, 7)])
     n = len(prog["ops"])
-    assert (stats["fills"] + stats["stores"]) / n < 0.45     # level launches move 3 per gate
+    assert (stats["fills"] + stats["stores"]) / n < 0.5      # level launches move 3 per gate
     assert stats["stalls"] < n // 1000
 
 

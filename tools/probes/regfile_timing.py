@@ -36,11 +36,29 @@ def main(schedules, lanes=1024, reps=5):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         prog.run(lanes)
         torch.cuda.synchronize()
+        import threading
+        import pynvml
+        pynvml.nvmlInit()
+        hdl = pynvml.nvmlDeviceGetHandleByIndex(0)
+        samples, stop = [], threading.Event()
+
+        def sample():
+            while not stop.is_set():
+                samples.append((pynvml.nvmlDeviceGetClockInfo(hdl, pynvml.NVML_CLOCK_SM),
+                                pynvml.nvmlDeviceGetPowerUsage(hdl) / 1000.0))
+                time.sleep(0.02)
+        th = threading.Thread(target=sample, daemon=True)
+        th.start()
         e0.record(stream)
         for _ in range(reps):
             prog.run(lanes)
         e1.record(stream)
         torch.cuda.synchronize()
+        stop.set()
+        th.join()
+        sm = np.median([a for a, _ in samples[len(samples) // 4:]]) if samples else 0
+        pw = np.median([b for _, b in samples[len(samples) // 4:]]) if samples else 0
+        print(f"  clocks: median {sm:.0f} MHz, power {pw:.0f} W over {len(samples)} samples", flush=True)
         ms = e0.elapsed_time(e1) / reps
         rf = eng.last_compile.get("regfile")
         print(f"{sched}: {ms:.1f} ms/step  {lanes / ms * 1e3:.0f} FFT/s  "
