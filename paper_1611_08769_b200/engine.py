@@ -332,12 +332,15 @@ class GpuEngine(LevelledNetlist):
         self._enc_stream_id: dict = {}
         self._enc_rows: list[np.ndarray] = []     # per chunk: (stream_idx, u32_off, mu, target)
         self._draws_per_ct = self.params.n_ct * self.params.m
+        # per-gate bookkeeping reads these (SchemeParams derives them on every access)
+        self._n_ct, self._q, self._budget = self.params.n_ct, self.params.q, self.params.depth_budget
         # circuit templates (`circuit`): a replayed call stays one lazy macro until flush
         self._macros: list[tuple] = []      # (template, input nodes, real node per out_internal)
-        self._capturing = False
+        self._capturing = 0                 # nesting depth of circuit() recordings
         self._regions: dict = {}            # template uid -> (base slot, Program, compile)
         self.template_hits = 0
         self._spill_block = (0, 0)          # (first slot, slots): register-file spill space
+        self._loose: list[int] = []         # nodes given a slot outside _compile (inputs, replay outputs)
 
     # -- protocol attributes -----------------------------------------------------------
 
@@ -363,6 +366,7 @@ class GpuEngine(LevelledNetlist):
         """values: (lanes, N, k) compact ciphertexts of one node."""
         slot = self._alloc_slot()
         self._slot[node] = slot
+        self._loose.append(node)
         self._pending_in_idx.append(self._lane_idx(slot))
         self._pending_in_val.append(np.ascontiguousarray(values, dtype=np.uint32))
         self._pending_in_bytes += values.nbytes
@@ -452,6 +456,7 @@ class GpuEngine(LevelledNetlist):
         slots = np.array([self._alloc_slot() for _ in range(n)], dtype=np.uint64)
         for node, slot in zip(nodes, slots.tolist()):
             self._slot[node] = slot
+        self._loose.extend(nodes)
         lane_ix = np.arange(lanes, dtype=np.uint64)
         target = (slots[None, :] * np.uint64(lanes) + lane_ix[:, None])        # (lanes, n)
         if self.lane_rngs is None:
@@ -542,15 +547,15 @@ class GpuEngine(LevelledNetlist):
             return self._fold(a, b)
         la, lb = self._level[a.node], self._level[b.node]
         level = (la if la >= lb else lb) + 1
-        if level > self.params.depth_budget:
+        if level > self._budget:
             raise NoiseOverflowError(
                 f"NAND at level {level} would exceed depth budget {self.params.depth_budget}")
         ea, eb = self._est[a.node], self._est[b.node]
         if eb > ea:                                   # fhe.py:336-337: noisier operand left
             a, b, ea, eb = b, a, eb, ea
-        est = ea + self.params.n_ct * eb
-        if est > self.params.q:
-            est = self.params.q
+        est = ea + self._n_ct * eb
+        if est > self._q:
+            est = self._q
         self.nand_count += 1
         if level > self.max_depth:
             self.max_depth = level
@@ -669,7 +674,7 @@ class GpuEngine(LevelledNetlist):
     # -- circuit templates ------------------------------------------------------------------
 
     _TEMPLATES: "dict" = {}            # shared by engines: (key, params, input pattern) -> template
-    TEMPLATE_CACHE = 16
+    TEMPLATE_CACHE = 512
 
     def circuit(self, key, fn, in_bits, flatten, rebuild):
         """Run ``fn()`` -- a circuit call over the wires ``in_bits`` whose netlist is a function
@@ -679,7 +684,7 @@ class GpuEngine(LevelledNetlist):
         ``flatten(result)`` lists the output wires of a call's return value and
         ``rebuild(handles)`` turns such a list back into one.  Falls back to plain recording
         when a trace or CSE is on."""
-        if self._capturing or self.trace is not None or self._cse_map is not None:
+        if self.trace is not None or self._cse_map is not None:
             return fn()
         pattern, in_nodes = self._input_pattern(in_bits)
         if pattern is None:
@@ -695,11 +700,13 @@ class GpuEngine(LevelledNetlist):
             self._expand_macros()
         n0, op0 = len(self._level), len(self._pending_ops)
         nand0, exec0, wire0 = self.nand_count, self.executed_nands, self._wire
-        self._capturing = True
+        self._capturing += 1
         try:
             result = fn()
+            if self._macros:                 # replays of nested calls become ordinary ops
+                self._expand_macros()
         finally:
-            self._capturing = False
+            self._capturing -= 1
         tpl = self._capture(in_nodes, n0, op0, flatten(result), nand0, exec0, wire0)
         if tpl is not None:
             self._TEMPLATES[full] = tpl
@@ -781,7 +788,7 @@ class GpuEngine(LevelledNetlist):
         for i, nd in enumerate(in_nodes):
             real[i] = nd
         self._macros.append((tpl, list(in_nodes), [real[li] for li in tpl.out_internal.tolist()]))
-        if len(self._macros) > 1 or self._pending_ops:
+        if len(self._macros) > 1 or self._pending_ops or self._capturing:
             self._expand_macros()
         out = []
         for kind, val, neg in tpl.outs.tolist():
@@ -811,6 +818,20 @@ class GpuEngine(LevelledNetlist):
             for c in (0, 2, 4):
                 ops[:, c] = m[ops[:, c]]
             self._pending_ops.extend(ops.ravel().tolist())
+
+    def _reclaim(self):
+        """Free the slots of inputs / replay outputs nobody holds any more (an ordinary compile
+        releases dead nodes itself; replays only run cached programs, so they sweep here)."""
+        keep = []
+        for nd in self._loose:
+            if self._slot[nd] < 0:
+                continue
+            if self._refs[nd] <= 0 and not self.keep_all:
+                self._free.append(self._slot[nd])
+                self._slot[nd] = -1
+            else:
+                keep.append(nd)
+        self._loose = keep
 
     def _template_compile(self, tpl):
         """The template compiled once as a self-contained program over private slots
@@ -859,6 +880,7 @@ class GpuEngine(LevelledNetlist):
         if comp is None:
             return None
         lanes = self.batch_size
+        self._reclaim()
         reg = self._regions.get(tpl.uid)
         if reg is None:
             base = self._n_slots                       # a private block, never in the free list
@@ -889,6 +911,7 @@ class GpuEngine(LevelledNetlist):
             slot = self._alloc_slot()
             self._slot[out_real[j]] = slot
             dst.append(slot)
+        self._loose.extend(out_real[j] for j in held)
         self._ensure_capacity()
         if held:
             self.ctx.copy_slots([base + int(comp["out_slots"][j]) for j in held], dst, lanes)

@@ -11,10 +11,11 @@ items = int(sys.argv[1])
 label = sys.argv[2] if len(sys.argv) > 2 else "resident"
 KERNEL = {"resident": "resident_tc_kernel<9,29,true,2,false>", "tiled": "level_tc_ws_kernel<9,29,true,1>"}.get(
     label, "level_tc_ws_kernel<9,29,true,2>")
-FNAME = "r1_ncu_full_resident" if label == "resident" else f"r1_ncu_full_level_tc_ws_{label}"
-shutil.copy(os.path.join(G, "bench_default.json"), os.path.join(P, "r1_bench_default_final.json"))
-shutil.copy(os.path.join(G, "launches.csv"), os.path.join(P, "r1_launches_bench_default.csv"))
-rows = list(csv.reader(open(os.path.join(P, "r1_launches_bench_default.csv"))))
+RND = os.environ.get("ROUND", "r2")
+FNAME = f"{RND}_ncu_full_resident" if label == "resident" else f"{RND}_ncu_full_level_tc_ws_{label}"
+shutil.copy(os.path.join(G, "bench_default.json"), os.path.join(P, f"{RND}_bench_default_final.json"))
+shutil.copy(os.path.join(G, "launches.csv"), os.path.join(P, f"{RND}_launches_bench_default.csv"))
+rows = list(csv.reader(open(os.path.join(P, f"{RND}_launches_bench_default.csv"))))
 i = [j for j, r in enumerate(rows) if r and r[0] == "ID"][0]
 h, data = rows[i], rows[i + 1:]
 ki, vi = h.index("Kernel Name"), h.index("Metric Value")
@@ -26,11 +27,11 @@ for r in data:
 tot = sum(t.values())
 lines = ["# ncu --metrics gpu__time_duration.sum --clock-control none -c 600 python bench.py (default args)",
          "# per-kernel totals over the first 600 launches (cold-cache, serialised: shares, not absolutes)",
-         "# cfg1 runs as ONE lane-resident launch per step (resident_tc_kernel); cfg4 and cfg0 as level launches"
+         "# cfg1 runs as ONE lane-resident launch per step (resident_tc_kernel); cfg4 as ONE register-file launch (regfile_tc_kernel), cfg0 as level launches"
          " (level_tc_ws_kernel / level_tc_kernel), cfg2/cfg3 as ready-queue launches",
          f"# total {tot / 1e6:.2f} ms over {len(data)} launches"]
 lines += [f"{v / 1e6:10.3f} ms  {100 * v / tot:5.1f}%  n={c[k]:4d}  {k}" for k, v in sorted(t.items(), key=lambda x: -x[1])]
-open(os.path.join(P, "r1_launches_summary.txt"), "w").write("\n".join(lines) + "\n")
+open(os.path.join(P, f"{RND}_launches_summary.txt"), "w").write("\n".join(lines) + "\n")
 rep = os.path.join(G, "ws_full.ncu-rep")
 summ = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep], capture_output=True, text=True).stdout
 open(os.path.join(P, f"{FNAME}.txt"), "w").write(summ)
