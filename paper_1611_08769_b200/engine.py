@@ -450,6 +450,8 @@ class GpuEngine(LevelledNetlist):
         if self._draws_per_ct % 2:
             raise UsageError("device encryption needs N*m even")
         from ._native import pcg64_stream
+        if not self._macros and not self._pending_ops:
+            self._reclaim()                    # nothing pending can still read a dead wire
         n = bits.shape[1]
         step = self._draws_per_ct
         nodes = [self._new_node(0, self._fresh_noise) for _ in range(n)]
@@ -880,7 +882,6 @@ class GpuEngine(LevelledNetlist):
         if comp is None:
             return None
         lanes = self.batch_size
-        self._reclaim()
         reg = self._regions.get(tpl.uid)
         if reg is None:
             base = self._n_slots                       # a private block, never in the free list
@@ -904,6 +905,7 @@ class GpuEngine(LevelledNetlist):
         if min(src) < 0:
             raise UsageError("template input has no live ciphertext")
         self.ctx.copy_slots(src, [base + i for i in range(tpl.n_in)], lanes)
+        self._reclaim()                                  # (after the copy: the inputs may be dead)
         program.run(lanes)
         held = [j for j, nd in enumerate(out_real) if self._refs[nd] > 0]
         dst = []

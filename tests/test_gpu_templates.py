@@ -56,3 +56,22 @@ def test_replay_equals_recording(cfg, lanes):
         _, o3 = _call(scheme, keys, cfg, lanes, eng=e2)
         assert np.array_equal(read_signal_ints(e2, o3), want)
     assert e2.template_hits == 3 and len(e2._regions) == 1
+
+
+def test_replay_with_unheld_inputs_and_a_new_context():
+    """A replay whose input wires nobody holds any more (fft_1d(input_signal(...)) in one
+    expression) on a fresh scheme / device context, repeated: inputs are bound before their
+    slots are reclaimed, and the store does not grow from call to call."""
+    GpuEngine._TEMPLATES.clear()
+    want = golden_npz("clear_cfg0.npz")["words"][0].tolist()
+    caps = []
+    for i in range(5):
+        scheme = GswScheme(EXACT_PARAMS) if i < 2 else scheme
+        rng, vals = config_signal("cfg0")
+        eng = GpuEngine(scheme, keys=scheme.keygen(0), rng=rng, device_encrypt=True) if i < 3 else eng
+        eng.rng = rng
+        out = fft_1d(input_signal(eng, vals, FixedFormat(16, 12)))
+        assert read_signal_ints(eng, out)[0].tolist() == want
+        caps.append(eng._n_slots)
+        del out
+    assert caps[4] == caps[3] == caps[2]
