@@ -562,7 +562,9 @@ def e2e_fft_ciphertexts(eng, prog, sig, out, lanes, stream, world, args):
         eng.ctx.read_packed(eng._slot[h.node] * lanes, lanes, buf.data_ptr())
     ref_words = None
     pin_s = time.perf_counter() - t0
-    chunk = args.fft_e2e_chunk
+    # register-file programs run each chunk as one launch: two lanes per SM per chunk (fewer,
+    # wider chunks keep every SM busy); level programs stream 128-lane chunks
+    chunk = args.fft_e2e_chunk or (2 * 148 if eng.last_compile.get("schedule") == "regfile" else 128)
 
     def step():
         eng.run_host(prog, list(zip(ins, host_in)), outs, chunk_lanes=chunk, out=host_out, sync=False,
@@ -759,7 +761,8 @@ def run_ours(args):
         if "e2e_ct" in fft:
             line["fft"]["e2e_ciphertexts"] = dict(fft["e2e_ct"], path=(
                 "fhegpu_prog_run_host: 512 input ciphertexts per signal in the reference's serialised bytes "
-                "(pinned host) -> chunked H2D | unpack + level kernels + pack | D2H of all 512 outputs"))
+                "(pinned host) -> chunked H2D | unpack + the program (one register-file launch per chunk, else level "
+                "kernels) + pack | D2H of all 512 outputs"))
     if single:
         line["fft_single"] = single
     if cpu is not None:
@@ -814,7 +817,8 @@ def main():
     ap.add_argument("--no-fft-single", dest="fft_single", action="store_false",
                     help="skip configs[0]/[2]/[3] single-signal FFT latency")
     ap.add_argument("--fft-lanes", type=int, default=1024)
-    ap.add_argument("--fft-e2e-chunk", type=int, default=128, help="lanes per streamed chunk (cfg4 ciphertext e2e)")
+    ap.add_argument("--fft-e2e-chunk", type=int, default=0,
+                    help="lanes per streamed chunk (cfg4 ciphertext e2e; 0: 296 for register-file programs, else 128)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--ref-step-seconds", type=float, default=4.0)
     args = ap.parse_args()

@@ -270,7 +270,8 @@ int fhegpu_rf_plan(const fhegpu_rf_gate *gates, uint32_t n_gates, const uint32_t
                    uint32_t *stats /* [5]: stalls, stores, fills, left / right operand reuses; may be NULL */);
 /* Attach a plan to a program: fhegpu_prog_run then runs it as ONE register-file launch
  * (tcgen05, k = 9, ell = 29), else level by level.  Spills of CTA c use ciphertexts
- * [spill_base + c * n_spill, + n_spill) of the store.  n_slots = 0 detaches. */
+ * [spill_base + c * n_spill, + n_spill) of the store (fhegpu_prog_run_host: right after its
+ * streaming regions when the store holds them, one launch per chunk).  n_slots = 0 detaches. */
 int fhegpu_prog_set_regfile(fhegpu_ctx *ctx, fhegpu_prog *prog, const fhegpu_rf_slot *slots, uint32_t n_slots,
                             const fhegpu_rf_fill *fills, uint32_t n_fills, uint32_t n_buf, uint32_t n_spill,
                             uint64_t spill_base);

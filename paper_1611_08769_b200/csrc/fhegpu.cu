@@ -366,7 +366,7 @@ int launch_resident(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
 }
 
 // A whole deep per-lane program in one register-file launch (tc_nand_regfile.cuh).
-int launch_regfile(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
+int launch_regfile(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes, uint32_t *store, uint32_t *spill = nullptr) {
   if (lanes == 0 || pr->rf_ops == 0) return FHEGPU_OK;
   if (effective_kernel(c) != FHEGPU_KERNEL_TCGEN05 || (c->p.dbg & 4u)) return FHEGPU_EUNSUP;
   if (!(c->p.k == 9 && c->p.ell == 29)) return FHEGPU_EUNSUP;
@@ -374,15 +374,18 @@ int launch_regfile(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
   const uint32_t smem = F::smem_bytes(pr->rf_buf);
   if (smem > 227u * 1024u) return FHEGPU_EUNSUP;
   const unsigned grid = (unsigned)std::min<uint64_t>(lanes, (uint64_t)c->num_sms);
-  if (pr->rf_spill_base + (uint64_t)grid * pr->rf_spill > c->capacity)
-    return fail(FHEGPU_EINVAL, "register-file spill region beyond store capacity");
+  if (spill == nullptr) {
+    if (pr->rf_spill_base + (uint64_t)grid * pr->rf_spill > c->capacity)
+      return fail(FHEGPU_EINVAL, "register-file spill region beyond store capacity");
+    spill = c->store + pr->rf_spill_base * c->p.ct_words;
+  }
   DevParams p = c->p;
   const bool pm = pm_ok(c->p.q, c->p.ell) && !(c->p.dbg & 2u);
   auto kern = pm ? tc::regfile_tc_kernel<9, 29, true, FHEGPU_ENC_RESIDENT>
                  : tc::regfile_tc_kernel<9, 29, false, FHEGPU_ENC_RESIDENT>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<grid, F::THREADS, smem, c->stream>>>(c->store, pr->d_rfslots, pr->d_rffills, pr->rf_ops, pr->rf_fills,
-                                               pr->rf_buf, lanes, pr->rf_spill_base, pr->rf_spill, p);
+  kern<<<grid, F::THREADS, smem, c->stream>>>(store, pr->d_rfslots, pr->d_rffills, pr->rf_ops, pr->rf_fills,
+                                               pr->rf_buf, lanes, spill, pr->rf_spill, p);
   CUDA_TRY(cudaGetLastError());
   return FHEGPU_OK;
 }
@@ -789,7 +792,7 @@ int fhegpu_prog_run_range(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes, uint32
                                    " lanes; store holds " + std::to_string(c->capacity) + " ciphertexts");
   CUDA_TRY(cudaSetDevice(c->device));
   if (pr->use_regfile && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
-    const int rc = launch_regfile(c, pr, lanes);
+    const int rc = launch_regfile(c, pr, lanes, c->store);
     if (rc != FHEGPU_EUNSUP) return rc;
     // else: level by level (register-file programs keep their level structure)
   } else if (pr->use_resident && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
@@ -821,7 +824,10 @@ int fhegpu_prog_run_range(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes, uint32
 int fhegpu_prog_run(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
   if (!pr) return fail(FHEGPU_EINVAL, "null prog");
   const uint32_t n_levels = (uint32_t)pr->offsets.size() - 1;
-  if (!c || !c->use_graphs || n_levels < 4 || c->stream == nullptr)
+  // graphs pay off for chains of level launches; whole-program launches (register-file,
+  // lane-resident, ready-queue, dataflow) run directly
+  if (!c || !c->use_graphs || n_levels < 4 || c->stream == nullptr || pr->use_regfile || pr->use_resident ||
+      pr->use_queue || pr->d_deps)
     return fhegpu_prog_run_range(c, pr, lanes, 0, n_levels);
   CUDA_TRY(cudaSetDevice(c->device));
   const int kern = effective_kernel(c);
@@ -910,6 +916,11 @@ int fhegpu_prog_run_host(fhegpu_ctx *c, fhegpu_prog *pr, uint64_t lanes, uint32_
   if (int rc = ensure((void **)&c->d_hstage, &c->hstage_bytes, regions * stage_rows * row_bytes)) return rc;
   const uint32_t n_levels = (uint32_t)pr->offsets.size() - 1;
   const unsigned repack_grid = (unsigned)std::max(1, c->num_sms * 8);
+  // register-file programs run each chunk as one launch, spilling right after the streaming
+  // regions when the store has room for it (else level launches)
+  const uint64_t rf_spill_cts = (uint64_t)c->num_sms * pr->rf_spill;
+  const bool use_rf = pr->use_regfile && !(c->p.dbg & 32768u) && region_cts * regions + rf_spill_cts <= c->capacity;
+  uint32_t *rf_spill_ptr = c->store + region_cts * regions * c->p.ct_words;
   if (packed)
     if (int rc = set_pack_smem(c)) return rc;
   // everything queued on the context stream so far happens before the first copy
@@ -942,9 +953,15 @@ int fhegpu_prog_run_host(fhegpu_ctx *c, fhegpu_prog *pr, uint64_t lanes, uint32_
         dense_to_store_kernel<<<g, 256, 0, c->stream>>>(dst, (const uint32_t *)src, cl, c->p);
     }
     CUDA_TRY(cudaGetLastError());
-    for (uint32_t l = 0; l < n_levels; ++l) {
-      const uint64_t a = pr->offsets[l], b = pr->offsets[l + 1];
-      if (int rc = launch_level(c, base, pr->d_ops + a, (uint32_t)(b - a), (uint32_t)cl)) return rc;
+    int rc = FHEGPU_EUNSUP;
+    if (use_rf) rc = launch_regfile(c, pr, (uint32_t)cl, base, rf_spill_ptr);   // the whole chunk in one launch
+    if (rc == FHEGPU_EUNSUP) {
+      for (uint32_t l = 0; l < n_levels; ++l) {
+        const uint64_t a = pr->offsets[l], b = pr->offsets[l + 1];
+        if (int rc2 = launch_level(c, base, pr->d_ops + a, (uint32_t)(b - a), (uint32_t)cl)) return rc2;
+      }
+    } else if (rc) {
+      return rc;
     }
     for (uint32_t i = 0; i < n_out; ++i) {
       uint8_t *dst = stage_out + (uint64_t)i * chunk * row_bytes;

@@ -121,7 +121,7 @@ template <int K, int ELL, bool PM, int ENC>
 __global__ void __launch_bounds__(GeoRF<K, ELL>::THREADS, 1)
 regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict__ slots,
                   const fhegpu_rf_fill *__restrict__ fills, uint32_t n_ops, uint32_t n_fills, uint32_t n_buf,
-                  uint32_t lanes, uint64_t spill_base, uint32_t n_spill, DevParams p) {
+                  uint32_t lanes, uint32_t *__restrict__ spill, uint32_t n_spill, DevParams p) {
   using R = GeoRes<K, ELL>;
   using F = GeoRF<K, ELL>;
   using G = GeoWS<K, ELL, PM, ENC, false>;       // roles, TMEM columns, MMA descriptors
@@ -221,7 +221,7 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
         if (si.bits & rf::SB_STORE) {
           const uint32_t ln = lane_of(pos.it);
           uint32_t *dst = (si.store & rf::STORE_SPILL)
-                              ? store + (spill_base + (uint64_t)blockIdx.x * n_spill + (si.store & ~rf::STORE_SPILL)) *
+                              ? spill + ((uint64_t)blockIdx.x * n_spill + (si.store & ~rf::STORE_SPILL)) *
                                             R::CT_WORDS
                               : store + ((uint64_t)si.store * lanes + ln) * R::CT_WORDS;
           bulk_s2g(dst, buf(si.dbuf), R::CT_BYTES);
@@ -292,7 +292,7 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
             }
             fence_proxy_async_global();               // completed stores -> this async-proxy load
             const uint32_t *src = (A.y & rf::STORE_SPILL)
-                                      ? store + (spill_base + (uint64_t)blockIdx.x * n_spill +
+                                      ? spill + ((uint64_t)blockIdx.x * n_spill +
                                                  (A.y & ~rf::STORE_SPILL)) * R::CT_WORDS
                                       : store + ((uint64_t)A.y * lanes + ln) * R::CT_WORDS;
             uint64_t *fb = &fill_full[q % rf::RF_FILL_RING];

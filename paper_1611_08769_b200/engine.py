@@ -1337,6 +1337,9 @@ class GpuEngine(LevelledNetlist):
         chunk = max(1, min(int(chunk_lanes), lanes))
         regions = min(3, -(-lanes // chunk))
         need = regions * n_slots * chunk
+        rf = self.last_compile.get("regfile") if self.last_program is program else None
+        if rf:                                        # register-file chunks spill after the regions
+            need += self.ctx.num_sms() * rf["n_spill"]
         if self.ctx.capacity < need:
             self.ctx.reserve(need)
         program.level_program().run_host(lanes, chunk, in_slots, in_ptrs, out_slots, out_ptrs,

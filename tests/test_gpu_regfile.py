@@ -77,3 +77,33 @@ def test_regfile_operand_reuse_equals_full_rebuild():
             scheme.ctx.set_debug(0)
         del eng, out
     assert np.array_equal(vals[0], vals[1 << 20])
+
+
+def test_regfile_host_streaming_equals_device_run():
+    """fhegpu_prog_run_host on a register-file program (one launch per streamed chunk, spill
+    space outside the streaming regions): the output ciphertexts equal the device run's."""
+    GpuEngine._TEMPLATES.clear()
+    scheme = GswScheme(DEFAULT0_PARAMS)
+    keys = scheme.keygen(4)
+    lanes = 300
+    rngs, vals = zip(*[config_signal("cfg4", l) for l in range(lanes)])
+    eng = GpuEngine(scheme, keys=keys, batch_size=lanes, lane_rngs=list(rngs), device_encrypt=True,
+                    schedule="regfile")
+    sig = input_signal(eng, np.array(vals), FixedFormat(16, 12))
+    out = fft_1d(sig)
+    prog = eng.flush()
+    assert eng.last_compile["schedule"] == "regfile"
+    ins = [h for w in signal_words(sig) for h in w.bits]
+    outs = [h for w in signal_words(out) for h in w.bits]
+    want = eng.node_values(outs)
+    host_in = [eng.node_values([h])[0] for h in ins]
+    got = eng.run_host(prog, list(zip(ins, host_in)), outs, chunk_lanes=148)
+    assert np.array_equal(np.stack(got), want)
+    # the streamed run took the register-file path: one launch per chunk, not 218 level launches
+    # (debug bit 15 forces level launches; both must agree)
+    scheme.ctx.set_debug(1 << 15)
+    try:
+        got_lv = eng.run_host(prog, list(zip(ins, host_in)), outs, chunk_lanes=148)
+    finally:
+        scheme.ctx.set_debug(0)
+    assert np.array_equal(np.stack(got_lv), want)
