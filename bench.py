@@ -173,7 +173,7 @@ def _cpu_sample_text(kind, cores, seconds, total):
 class ClockSampler:
     def __init__(self, device: int, period: float = 0.02):
         self.device, self.period = device, period
-        self.samples, self.reasons = [], set()
+        self.samples, self.reasons, self.power = [], set(), []
         self._stop = threading.Event()
         self.max_mhz = None
         self.ok = True
@@ -194,6 +194,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.power.append(nv.nvmlDeviceGetPowerUsage(self._h) / 1000.0)
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
                 for bit, name in self._BITS.items():
                     if r & bit:
@@ -217,7 +218,8 @@ class ClockSampler:
         if not self.ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "power_w_median": statistics.median(self.power) if self.power else None}
 
 
 # ----------------------------------------------------------------------------------------
@@ -349,6 +351,15 @@ def bench_gates(args, world, rank, local):
     comp = eng.last_compile
     widths_items = [int(w) * lanes for w in comp["widths"]]
     lv_ms = level_launch_times(prog, lanes, stream)
+    sustained = None
+    if args.sustain_s > 0:
+        # the same step back to back for ~sustain_s seconds: the board settles at its power limit
+        # (the 20-step timed region above is ~0.6 s, shorter than the power controller's window)
+        n_sus = max(1, int(args.sustain_s * 1e3 / ms))
+        sampler2 = ClockSampler(local, period=0.05)
+        ms_sus = time_program(prog, lanes, stream, n_sus, 0, world, sampler2)
+        sustained = {"value": nand_per_step * world / (ms_sus / 1e3), "unit": UNIT, "steps": n_sus,
+                     "seconds": n_sus * ms_sus / 1e3, "ms_per_step": ms_sus, "clocks": sampler2.summary()}
     peak, peak_kind = _peaks()
     bytes_per_launch = [w * ALG_BYTES_PER_NAND_261 for w in widths_items]
     achieved = sum(bytes_per_launch) / (sum(lv_ms) / 1e3) / 1e9        # GB/s
@@ -358,7 +369,7 @@ def bench_gates(args, world, rank, local):
         "launches_per_step": prog.launches, "widths": [int(w) for w in comp["widths"]],
         "level_ms": lv_ms, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
         "traffic": traffic, "traffic_info": tinfo, "ok": ok, "setup_s": setup_s,
-        "clocks": sampler.summary(), "kernel": scheme.ctx.kernel,
+        "clocks": sampler.summary(), "kernel": scheme.ctx.kernel, "sustained": sustained,
         "slots": eng._n_slots, "store_gb": eng._n_slots * lanes * scheme.ctx.ct_words * 4 / 1e9,
         "schedule": comp.get("schedule", "levels") + (
             f" ({prog.tile_lanes}-lane chunks, one wavefront dataflow launch per step)" if prog.tile_lanes
@@ -734,6 +745,7 @@ def run_ours(args):
                     "with N <= 64 issues no faster than every ~46 cycles (DESIGN.md 4.1)"},
         "gpu_launches": res["launches_per_step"] * args.steps,
         "clocks": res["clocks"],
+        "sustained": res["sustained"],
     }
     if "e2e" in res:
         e = res["e2e"]
@@ -820,6 +832,8 @@ def main():
     ap.add_argument("--fft-e2e-chunk", type=int, default=0,
                     help="lanes per streamed chunk (cfg4 ciphertext e2e; 0: 296 for register-file programs, else 128)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--sustain-s", type=float, default=5.0,
+                    help="also run the gate benchmark back to back for this long (power-limited rate)")
     ap.add_argument("--ref-step-seconds", type=float, default=4.0)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
