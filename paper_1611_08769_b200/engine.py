@@ -133,6 +133,26 @@ class LevelledNetlist:
         self._refs.append(0)
         return len(self._level) - 1
 
+    def _new_nodes(self, levels, ests, slots=None) -> range:
+        """Bulk _new_node: len(levels) nodes (ids returned as a range)."""
+        n0, n = len(self._level), len(levels)
+        self._level.extend(levels)
+        self._est.extend(ests)
+        self._slot.extend([-1] * n if slots is None else slots)
+        self._refs.extend([0] * n)
+        return range(n0, n0 + n)
+
+    def _alloc_slots(self, n: int) -> list:
+        """n slots: the most recently freed first (as _alloc_slot), then fresh ones."""
+        take = min(n, len(self._free))
+        out = self._free[len(self._free) - take:][::-1] if take else []
+        if take:
+            del self._free[len(self._free) - take:]
+        if n > take:
+            out.extend(range(self._n_slots, self._n_slots + n - take))
+            self._n_slots += n - take
+        return out
+
     def _alloc_slot(self) -> int:
         if self._free:
             return self._free.pop()
@@ -454,10 +474,9 @@ class GpuEngine(LevelledNetlist):
             self._reclaim()                    # nothing pending can still read a dead wire
         n = bits.shape[1]
         step = self._draws_per_ct
-        nodes = [self._new_node(0, self._fresh_noise) for _ in range(n)]
-        slots = np.array([self._alloc_slot() for _ in range(n)], dtype=np.uint64)
-        for node, slot in zip(nodes, slots.tolist()):
-            self._slot[node] = slot
+        slot_list = self._alloc_slots(n)
+        nodes = self._new_nodes([0] * n, [self._fresh_noise] * n, slot_list)
+        slots = np.asarray(slot_list, dtype=np.uint64)
         self._loose.extend(nodes)
         lane_ix = np.arange(lanes, dtype=np.uint64)
         target = (slots[None, :] * np.uint64(lanes) + lane_ix[:, None])        # (lanes, n)
@@ -783,17 +802,21 @@ class GpuEngine(LevelledNetlist):
         if tpl.max_level > self.max_depth:
             self.max_depth = tpl.max_level
         self._wire += tpl.wires
-        real = {}
-        for li in tpl.out_internal.tolist():
-            k = li - tpl.n_in
-            real[li] = self._new_node(int(tpl.levels[k]), int(tpl.ests[k]))
+        oi = tpl.out_internal
+        if not hasattr(tpl, "out_levels"):            # per template, once
+            tpl.out_levels = tpl.levels[oi - tpl.n_in].tolist()
+            tpl.out_ests = tpl.ests[oi - tpl.n_in].tolist()
+            tpl.out_list = oi.tolist()
+            tpl.outs_list = tpl.outs.tolist()
+        new = self._new_nodes(tpl.out_levels, tpl.out_ests)
+        real = dict(zip(tpl.out_list, new))
         for i, nd in enumerate(in_nodes):
             real[i] = nd
-        self._macros.append((tpl, list(in_nodes), [real[li] for li in tpl.out_internal.tolist()]))
+        self._macros.append((tpl, list(in_nodes), list(new)))
         if len(self._macros) > 1 or self._pending_ops or self._capturing:
             self._expand_macros()
         out = []
-        for kind, val, neg in tpl.outs.tolist():
+        for kind, val, neg in tpl.outs_list:
             out.append(self.constant(val) if kind == 0 else GpuBit(self, real[val], neg, False, None, -1))
         return out
 
