@@ -57,6 +57,10 @@ typedef struct {
  * Flags bit 3 (FHEGPU_OP_STREAM_OUT, a hint): nothing later in the same program reads `out`;
  * its store is marked L2 evict-first so it does not displace the program's temporaries. */
 #define FHEGPU_OP_STREAM_OUT 8u
+/* Flags bit 4 (FHEGPU_OP_TEMP, a hint): nothing outside the program reads `out` (no read-back,
+ * no later program).  Launches that pass operands on chip (warp-dataflow) skip its store;
+ * level launches ignore it. */
+#define FHEGPU_OP_TEMP 16u
 typedef struct {
   uint32_t left;
   uint32_t right;
@@ -194,6 +198,33 @@ int fhegpu_prog_set_deps(fhegpu_ctx *ctx, fhegpu_prog *prog, const int32_t *deps
  * (engine.py:168-178 driving fhe.py:325-341) like fhegpu_prog_run. */
 int fhegpu_prog_set_queue(fhegpu_ctx *ctx, fhegpu_prog *prog, int enable);
 
+/* Opt-in warp-dataflow execution of a single-lane program at a small geometry (k = 3, ell =
+ * 17, q <= 2^17: the reference's EXACT preset, fhe.py:110) whose dependencies are set
+ * (fhegpu_prog_set_deps): one launch in which every warp runs a host-scheduled list of gates
+ * on the CUDA cores and operands pass through shared-memory rings and a tagged scratch array
+ * (csrc/flow_nand.cuh).  A single-signal FFT there is bound by its dependency chain (148 levels
+ * of <= 360 gates), which level launches pay at ~2.5 us per level.  model_cycles (optional)
+ * receives the schedule's modelled makespan, stats (optional, 4 values) the ring / scratch /
+ * store operand counts and the longest worker list.  Runs over other lane counts fall back to
+ * level launches.  Same results as level launches (SSA slots required, as for dataflow).
+ * Replaces the reference's sequential gate loop (engine.py:168-178 driving fhe.py:325-341)
+ * like fhegpu_prog_run. */
+int fhegpu_prog_set_flow(fhegpu_ctx *ctx, fhegpu_prog *prog, int enable, double *model_cycles,
+                         uint32_t *stats);
+
+/* The warp-dataflow schedule on its own (host only, no device): ops in level order, deps as for
+ * fhegpu_prog_set_deps, n_cta CTAs of FHEGPU_FLOW_WARPS workers.  entries receives n_ops
+ * records of 8 u32 grouped by worker in execution order -- {left index, right index, out slot,
+ * gate index, left meta, right meta, position + 1, 0}; an index is a store slot (meta kind 0)
+ * or the producing gate's index (kind 1: scratch, kind 2: ring first); meta = kind | complement
+ * << 2 | producer's warp << 4 | (producer's position + 1) << 8 -- and worker_off the n_cta *
+ * FHEGPU_FLOW_WARPS + 1 list boundaries. */
+#define FHEGPU_FLOW_WARPS 4
+#define FHEGPU_FLOW_RING 4
+int fhegpu_flow_plan(const fhegpu_op *ops, const int32_t *deps, uint64_t n_ops, const uint64_t *level_offsets,
+                     uint32_t n_levels, uint32_t n_cta, uint32_t *entries, uint32_t *worker_off,
+                     double *model_cycles);
+
 /* One gate of a lane-resident program (fhegpu_prog_set_resident), 16 bytes. */
 typedef struct {
   uint8_t lkind, lidx;   /* left operand: kind 0 = program input lidx, 1 = local buffer lidx */
@@ -312,6 +343,7 @@ int fhegpu_encrypt(fhegpu_ctx *ctx, const uint32_t *pk, const fhegpu_pcg64 *stre
 
 /* Debug only: timeline probe of the pipelined kernel (64 gates x 16 events, clock64). */
 int fhegpu_debug_ws_trace(uint64_t *host_out);
+int fhegpu_debug_flow_trace(uint32_t *host_out, uint32_t n_gates);
 
 /* -- Bitsliced cleartext engine (replaces CleartextEngine's evaluation, engine.py:69-121) --
  * A wire is `lanes` plaintext bits packed 32 per u32 word (bit l of word w = lane 32w + l);

@@ -71,6 +71,9 @@ SIGNATURES = [
     ("fhegpu_prog_launches", ctypes.c_uint32, [_P]),
     ("fhegpu_prog_set_deps", ctypes.c_int, [_P, _P, _P]),
     ("fhegpu_prog_set_queue", ctypes.c_int, [_P, _P, ctypes.c_int]),
+    ("fhegpu_prog_set_flow", ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.POINTER(ctypes.c_double), _U32P]),
+    ("fhegpu_flow_plan", ctypes.c_int, [_P, _P, ctypes.c_uint64, _P, ctypes.c_uint32, ctypes.c_uint32, _P, _P,
+                                        ctypes.POINTER(ctypes.c_double)]),
     ("fhegpu_prog_set_resident", ctypes.c_int, [_P, _P, _P, ctypes.c_uint32, _P, ctypes.c_uint32,
                                                 ctypes.c_uint32]),
     ("fhegpu_res_slot_order", ctypes.c_int, [_P, ctypes.c_uint32, ctypes.c_uint32, _P]),
@@ -101,6 +104,7 @@ SIGNATURES = [
     ("fhegpu_mult_batch", ctypes.c_int, [_P, _U32P, _U32P, _U32P, ctypes.c_uint64]),
     ("fhegpu_const_mult_batch", ctypes.c_int, [_P, ctypes.c_uint32, _U32P, _U32P, ctypes.c_uint64]),
     ("fhegpu_debug_ws_trace", ctypes.c_int, [_U64P]),
+    ("fhegpu_debug_flow_trace", ctypes.c_int, [_U32P, ctypes.c_uint32]),
     ("fhegpu_encrypt", ctypes.c_int, [_P, _U32P, _P, ctypes.c_uint32, _U32P, _U64P, _U32P, _U64P,
                                       ctypes.c_uint64]),
 ]
@@ -181,6 +185,28 @@ def rf_plan(gates: np.ndarray, in_slots, n_buf: int = 20, min_dist: int = 5, loo
          "reuse_r": int(stats[4])}
 
 
+FLOW_WARPS, FLOW_RING = 4, 4      # FHEGPU_FLOW_WARPS / FHEGPU_FLOW_RING (include/fhegpu.h)
+
+
+def flow_plan(ops: np.ndarray, deps: np.ndarray, level_offsets, n_cta: int):
+    """Warp-dataflow schedule of a levelised program (fhegpu_flow_plan; host only): returns
+    (entries (n, 8) u32 grouped by worker, worker_off (n_cta * FLOW_WARPS + 1), model cycles)."""
+    if _lib is None:
+        load_library()
+    ops = np.ascontiguousarray(ops, dtype=OP_DTYPE)
+    deps = np.ascontiguousarray(deps, dtype=np.int32).reshape(-1)
+    offs = np.ascontiguousarray(level_offsets, dtype=np.uint64)
+    n = len(ops)
+    ents = np.zeros((n, 8), dtype=np.uint32)
+    woff = np.zeros(n_cta * FLOW_WARPS + 1, dtype=np.uint32)
+    cyc = ctypes.c_double(0.0)
+    _check(_lib.fhegpu_flow_plan(ops.ctypes.data_as(ctypes.c_void_p), deps.ctypes.data_as(ctypes.c_void_p), n,
+                                 offs.ctypes.data_as(ctypes.c_void_p), len(offs) - 1, int(n_cta),
+                                 ents.ctypes.data_as(ctypes.c_void_p), woff.ctypes.data_as(ctypes.c_void_p),
+                                 ctypes.byref(cyc)), "flow_plan")
+    return ents, woff, cyc.value
+
+
 def _ptr(arr, ctype):
     return arr.ctypes.data_as(ctypes.POINTER(ctype))
 
@@ -239,6 +265,18 @@ class Program:
         whose producers have completed (needs set_deps first)."""
         _check(_lib.fhegpu_prog_set_queue(self.ctx.handle, self.handle, int(bool(enable))), "prog_set_queue")
         self.launches = int(_lib.fhegpu_prog_launches(self.handle))
+
+    def set_flow(self, enable: bool = True) -> dict:
+        """Warp-dataflow mode (fhegpu_prog_set_flow; EXACT geometry, single lane): one launch,
+        every warp a worker with a host-scheduled gate list (needs set_deps first).  Returns
+        the schedule's model makespan and operand statistics."""
+        cyc = ctypes.c_double(0.0)
+        stats = (ctypes.c_uint32 * 4)()
+        _check(_lib.fhegpu_prog_set_flow(self.ctx.handle, self.handle, int(bool(enable)), ctypes.byref(cyc), stats),
+               "prog_set_flow")
+        self.launches = int(_lib.fhegpu_prog_launches(self.handle))
+        return {"model_cycles": cyc.value, "ring_operands": stats[0], "scratch_operands": stats[1],
+                "store_operands": stats[2], "max_gates_per_worker": stats[3]}
 
     def set_resident(self, plan: np.ndarray, in_slots, n_local: int):
         """Lane-resident mode (fhegpu_prog_set_resident): plan = RES_OP_DTYPE records of the

@@ -20,6 +20,7 @@
 #include "tc_nand_ws.cuh"
 #include "tc_nand_resident.cuh"
 #include "tc_nand_regfile.cuh"
+#include "flow_nand.cuh"
 #include "encrypt.cuh"
 #include "bits.cuh"
 
@@ -110,6 +111,14 @@ struct fhegpu_prog {
   uint32_t rf_ops = 0, rf_fills = 0, rf_buf = 0, rf_spill = 0;
   uint64_t rf_spill_base = 0;
   uint64_t rf_slots = 0;          // 1 + the largest store slot the plan reads or writes
+  // warp-dataflow launches (fhegpu_prog_set_flow): per-worker gate lists + tagged scratch
+  bool use_flow = false;
+  uint4 *d_flow_ents = nullptr;
+  uint32_t *d_flow_off = nullptr;
+  uint4 *d_flow_scratch = nullptr;
+  uint32_t flow_ctas = 0, flow_epoch = 0;
+  double flow_makespan = 0;
+  uint32_t flow_stats[4] = {0, 0, 0, 0};   // ring / scratch / store operands, max gates per worker
   // CUDA graph of one full run (all level launches), captured on first use per
   // (lanes, stream, kernel choice, debug bits); replayed with a single cudaGraphLaunch
   cudaGraphExec_t graph = nullptr;
@@ -334,6 +343,19 @@ int launch_queue(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
                                                                 lanes, nullptr, nullptr, qa);
 }
 
+
+// A whole single-lane program in one warp-dataflow launch (flow_nand.cuh).
+int launch_flow(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
+  if (pr->n_ops == 0 || lanes == 0) return FHEGPU_OK;
+  if (lanes != 1 || !(c->p.k == 3 && c->p.ell == 17) || (c->p.dbg & 4u)) return FHEGPU_EUNSUP;
+  if (effective_kernel(c) != FHEGPU_KERNEL_TCGEN05) return FHEGPU_EUNSUP;   // 'simt': the cross-check kernel
+  pr->flow_epoch = pr->flow_epoch % flow::TAG_MAX + 1u;
+  const uint32_t q_magic = (uint32_t)((1ull << 32) / c->p.q);
+  flow::flow_kernel<3, 17><<<pr->flow_ctas, 32 * flow::WARPS, 0, c->stream>>>(
+      c->store, pr->d_flow_scratch, pr->d_flow_ents, pr->d_flow_off, pr->flow_epoch, q_magic, c->p);
+  CUDA_TRY(cudaGetLastError());
+  return FHEGPU_OK;
+}
 
 #ifndef FHEGPU_ENC_RESIDENT
 #define FHEGPU_ENC_RESIDENT 2     // {0,128} A operand: builders pace this pipeline (+4.5%, measured)
@@ -752,7 +774,7 @@ int fhegpu_prog_create(fhegpu_ctx *c, const fhegpu_op *ops, uint64_t n_ops,
   uint64_t n_slots = 0;
   for (uint64_t i = 0; i < n_ops; ++i) {
     const uint32_t mx = std::max(ops[i].left, std::max(ops[i].right, ops[i].out));
-    if (mx >= (1u << 31) || (ops[i].flags & ~(3u | FHEGPU_OP_STREAM_OUT)))
+    if (mx >= (1u << 31) || (ops[i].flags & ~(3u | FHEGPU_OP_STREAM_OUT | FHEGPU_OP_TEMP)))
       return fail(FHEGPU_EINVAL, "bad op record " + std::to_string(i));
     n_slots = std::max<uint64_t>(n_slots, uint64_t(mx) + 1);
   }
@@ -799,6 +821,10 @@ int fhegpu_prog_run_range(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes, uint32
     const int rc = launch_resident(c, pr, lanes);
     if (rc != FHEGPU_EUNSUP) return rc;
     // else: level by level (resident programs keep their level structure)
+  } else if (pr->use_flow && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
+    const int rc = launch_flow(c, pr, lanes);
+    if (rc != FHEGPU_EUNSUP) return rc;
+    // else: level by level (flow programs keep their level structure)
   } else if (pr->use_queue && first == 0 && last == n_levels && !(c->p.dbg & 32768u)) {
     const int rc = launch_queue(c, pr, lanes);
     if (rc != FHEGPU_EUNSUP) return rc;
@@ -1065,6 +1091,70 @@ int fhegpu_prog_set_queue(fhegpu_ctx *c, fhegpu_prog *pr, int enable) {
   return FHEGPU_OK;
 }
 
+int fhegpu_flow_plan(const fhegpu_op *ops, const int32_t *deps, uint64_t n_ops, const uint64_t *level_offsets,
+                     uint32_t n_levels, uint32_t n_cta, uint32_t *entries, uint32_t *worker_off,
+                     double *model_cycles) {
+  if (!ops || !deps || !level_offsets || !entries || !worker_off || n_cta == 0)
+    return fail(FHEGPU_EINVAL, "null argument");
+  if (n_ops == 0 || n_ops >= flow::MAX_GATES || level_offsets[0] != 0 || level_offsets[n_levels] != n_ops)
+    return fail(FHEGPU_EINVAL, "bad program");
+  for (uint64_t i = 0; i < 2 * n_ops; ++i)
+    if (deps[i] < -1 || (int64_t)deps[i] >= (int64_t)(i / 2))
+      return fail(FHEGPU_EINVAL, "dependency " + std::to_string(i) + " is not an earlier op");
+  static_assert(sizeof(fhegpu_op) == sizeof(OpRec), "op record layout");
+  const flow::FlowPlan pl = flow::flow_plan(reinterpret_cast<const OpRec *>(ops), deps, n_ops, level_offsets,
+                                            n_levels, n_cta);
+  std::memcpy(entries, pl.ents.data(), n_ops * sizeof(flow::Entry));
+  std::memcpy(worker_off, pl.worker_off.data(), pl.worker_off.size() * sizeof(uint32_t));
+  if (model_cycles) *model_cycles = pl.makespan;
+  return FHEGPU_OK;
+}
+
+int fhegpu_prog_set_flow(fhegpu_ctx *c, fhegpu_prog *pr, int enable, double *model_cycles, uint32_t *stats) {
+  if (!c || !pr) return fail(FHEGPU_EINVAL, "null argument");
+  pr->use_flow = false;
+  if (!enable) return FHEGPU_OK;
+  const uint64_t n = pr->n_ops;
+  if (pr->deps_host.size() != 2 * n) return fail(FHEGPU_EINVAL, "set the program's dependencies first");
+  if (!pr->levels_valid) return fail(FHEGPU_EINVAL, "warp-dataflow programs need a level structure");
+  if (!(c->p.k == 3 && c->p.ell == 17) || c->p.q > (1u << flow::VBITS))
+    return fail(FHEGPU_EUNSUP, "warp-dataflow launches serve k = 3, ell = 17, q <= 2^17");
+  if (n == 0 || n >= flow::MAX_GATES) return fail(FHEGPU_EUNSUP, "program size outside the warp-dataflow range");
+  CUDA_TRY(cudaSetDevice(c->device));
+  std::vector<OpRec> ops(n);
+  CUDA_TRY(cudaMemcpy(ops.data(), pr->d_ops, n * sizeof(OpRec), cudaMemcpyDeviceToHost));
+  const uint32_t n_cta = (uint32_t)std::max(c->num_sms, 1);
+  const flow::FlowPlan pl = flow::flow_plan(ops.data(), pr->deps_host.data(), n, pr->offsets.data(),
+                                            (uint32_t)pr->offsets.size() - 1, n_cta);
+  if (pl.max_gates_per_worker > flow::TAG_MAX)
+    return fail(FHEGPU_EUNSUP, "too many gates per worker for the ring tags");
+  cudaFree(pr->d_flow_ents);
+  cudaFree(pr->d_flow_off);
+  cudaFree(pr->d_flow_scratch);
+  pr->d_flow_ents = nullptr, pr->d_flow_off = nullptr, pr->d_flow_scratch = nullptr;
+  const size_t scratch_bytes = n * (size_t)(c->p.rows) * sizeof(uint4);
+  CUDA_TRY(cudaMalloc(&pr->d_flow_ents, n * sizeof(flow::Entry)));
+  CUDA_TRY(cudaMalloc(&pr->d_flow_off, pl.worker_off.size() * sizeof(uint32_t)));
+  CUDA_TRY(cudaMalloc(&pr->d_flow_scratch, scratch_bytes));
+  CUDA_TRY(cudaMemcpy(pr->d_flow_ents, pl.ents.data(), n * sizeof(flow::Entry), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(pr->d_flow_off, pl.worker_off.data(), pl.worker_off.size() * sizeof(uint32_t),
+                      cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemset(pr->d_flow_scratch, 0, scratch_bytes));      // tag 0: never written
+  pr->flow_ctas = n_cta;
+  pr->flow_epoch = 0;
+  pr->flow_makespan = pl.makespan;
+  pr->flow_stats[0] = pl.ring_operands, pr->flow_stats[1] = pl.scratch_operands;
+  pr->flow_stats[2] = pl.store_operands, pr->flow_stats[3] = pl.max_gates_per_worker;
+  if (model_cycles) *model_cycles = pl.makespan;
+  if (stats) std::copy(pr->flow_stats, pr->flow_stats + 4, stats);
+  if (pr->graph) {                      // launch structure changes
+    cudaGraphExecDestroy(pr->graph);
+    pr->graph = nullptr;
+  }
+  pr->use_flow = true;
+  return FHEGPU_OK;
+}
+
 int fhegpu_prog_set_resident(fhegpu_ctx *c, fhegpu_prog *pr, const fhegpu_res_op *plan, uint32_t n_ops,
                              const uint32_t *in_slots, uint32_t n_in, uint32_t n_local) {
   if (!c || !pr) return fail(FHEGPU_EINVAL, "null argument");
@@ -1237,7 +1327,8 @@ int fhegpu_ctx_set_graphs(fhegpu_ctx *c, int enable) {
 
 uint32_t fhegpu_prog_launches(const fhegpu_prog *pr) {
   if (!pr) return 0;
-  if (pr->use_regfile || pr->use_resident) return 1;   // register-file / lane-resident: one launch
+  if (pr->use_regfile || pr->use_resident || pr->use_flow) return 1;   // register-file / lane-resident /
+                                                                       // warp-dataflow: one launch
   if (pr->use_queue) return 2;                  // ready queue: state reset + one launch
   if (pr->d_deps) return 1;                     // dataflow: one launch (tcgen05 parameter sets)
   uint32_t n = 0;
@@ -1256,6 +1347,9 @@ void fhegpu_prog_destroy(fhegpu_prog *pr) {
   cudaFree(pr->d_rin);
   cudaFree(pr->d_rfslots);
   cudaFree(pr->d_rffills);
+  cudaFree(pr->d_flow_ents);
+  cudaFree(pr->d_flow_off);
+  cudaFree(pr->d_flow_scratch);
   cudaFree(pr->d_ops);
   delete pr;
 }
@@ -1442,6 +1536,14 @@ int fhegpu_encrypt(fhegpu_ctx *c, const uint32_t *pk, const fhegpu_pcg64 *stream
 int fhegpu_debug_ws_trace(uint64_t *host) {
   if (!host) return fail(FHEGPU_EINVAL, "null argument");
   CUDA_TRY(cudaMemcpyFromSymbol(host, tc::g_ws_trace, sizeof(uint64_t) * 64 * 16));
+  return FHEGPU_OK;
+}
+
+// Debug: copy the warp-dataflow kernel's per-gate probe (8 u32 per gate; -DFHEGPU_TRACE=1 builds).
+int fhegpu_debug_flow_trace(uint32_t *host, uint32_t n_gates) {
+  if (!host) return fail(FHEGPU_EINVAL, "null argument");
+  if (n_gates > flow::FLOW_TRACE_GATES) return fail(FHEGPU_EUNSUP, "not a trace build");
+  CUDA_TRY(cudaMemcpyFromSymbol(host, flow::g_flow_trace, sizeof(uint32_t) * 8 * n_gates));
   return FHEGPU_OK;
 }
 

@@ -1,0 +1,457 @@
+// flow_nand.cuh -- warp-dataflow launches for small geometries (EXACT: k = 3, ell = 17, N = 51).
+//
+// A single-signal FFT at the toy parameter set (configs[0]: 28,401 gates, 148 levels of <= 360
+// gates, a 612-byte ciphertext) is bound by the latency of its dependency chain, not by
+// bandwidth or arithmetic: level launches cost ~2.45 us per level whatever the kernel does
+// inside.  Here the whole program is ONE launch in which every warp is a worker that runs a
+// host-scheduled list of gates, each gate start to finish on the CUDA cores (7,803 conditional
+// adds: one lane per output row, the right operand broadcast from shared memory), and operands
+// travel by the shortest path that exists:
+//   * ring     each warp keeps its last RING outputs in shared memory; gates scheduled on the
+//              same CTA read them there (~100 cycles after the producer's last store);
+//   * scratch  every output is also written to a single-assignment scratch array in global
+//              memory (L2), which any SM can read (~1,300 cycles producer to consumer);
+//   * store    program inputs are read from the ciphertext store; every output is written
+//              there too in the store's plain layout (read-back, later programs).
+// There are no flags, fences or counters: every 32-bit word of a ring or scratch row carries a
+// tag next to its 17-bit value -- the run's epoch (scratch) or the producer's position in its
+// worker's list (ring) -- and a consumer polls the rows it needs until every word carries the
+// tag it expects.  A word is written by one store instruction, so a row is valid exactly when
+// all its tags match, however the stores of different words are ordered or torn; a ring entry
+// overwritten before (or while) a late consumer reads it fails the tag check and the consumer
+// falls back to the scratch copy, which is never overwritten within a run.
+//
+// The schedule (FlowPlanner, host side) is a list schedule over a latency model: gates in level
+// order, each appended to the worker that can start it earliest among the least loaded warp of
+// the CTAs that produced its operands and the globally earliest-free worker.  Appending in a
+// topological order makes every worker's list deadlock-free as long as all workers are
+// resident (one CTA per SM, grid <= SM count).
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <queue>
+#include <vector>
+
+#include "../../include/fhegpu.h"
+#include "common.cuh"
+
+namespace fhegpu {
+namespace flow {
+
+#ifndef FHEGPU_FLOW_RING_BUILD
+#define FHEGPU_FLOW_RING_BUILD FHEGPU_FLOW_RING
+#endif
+constexpr int RING = FHEGPU_FLOW_RING_BUILD;    // outputs each warp keeps in shared memory
+#ifndef FHEGPU_FLOW_WARPS_BUILD
+#define FHEGPU_FLOW_WARPS_BUILD FHEGPU_FLOW_WARPS
+#endif
+constexpr int WARPS = FHEGPU_FLOW_WARPS_BUILD;  // workers per CTA
+constexpr uint32_t VBITS = 17;          // value bits of a tagged word (q <= 2^17)
+constexpr uint32_t VMASK = (1u << VBITS) - 1u;
+constexpr uint32_t TAG_MAX = 32767u;    // tags 1..32767 (15 bits; 0 = never written): the run's
+                                        // epoch, or a gate's position + 1 in its worker's list
+constexpr uint32_t MAX_GATES = 1u << 24;
+constexpr uint32_t NO_STORE = 0xFFFFFFFFu;   // out slot of a temporary (FHEGPU_OP_TEMP): no plain copy
+
+// Operand meta word: bits 0-1 kind, bit 2 complement, bits 4-7 producer's warp in the CTA,
+// bits 8-22 producer's position + 1 in its worker's list (ring operands; <= TAG_MAX).
+enum : uint32_t { K_STORE = 0, K_SCRATCH = 1, K_RING = 2 };
+
+// One scheduled gate (32 bytes): a = {left index, right index, out store slot, own scratch
+// index}, b = {left meta, right meta, own position + 1, 0}; out slot NO_STORE: a temporary.  An index is a store slot (kind
+// store) or the producing gate's scratch index.
+struct Entry {
+  uint4 a, b;
+};
+
+#ifdef __CUDACC__
+
+#ifndef FHEGPU_FLOW_RELAXED
+#define FHEGPU_FLOW_RELAXED 0
+#endif
+#if FHEGPU_FLOW_RELAXED
+#define FLOW_LD_G "ld.relaxed.gpu.global.v4.u32"
+#define FLOW_ST_G "st.relaxed.gpu.global.v4.u32"
+#else
+#define FLOW_LD_G "ld.volatile.global.v4.u32"
+#define FLOW_ST_G "st.volatile.global.v4.u32"
+#endif
+__device__ __forceinline__ uint4 ld_volatile_global_v4(const uint4 *p) {
+  uint4 v;
+  asm volatile(FLOW_LD_G " {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_volatile_global_v4(uint4 *p, const uint4 &v) {
+  asm volatile(FLOW_ST_G " [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ uint4 ld_volatile_shared_v4(const uint4 *p) {
+  uint4 v;
+  asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"((uint32_t)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_volatile_shared_v4(uint4 *p, const uint4 &v) {
+  asm volatile("st.volatile.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"((uint32_t)__cvta_generic_to_shared(p)),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ bool tags_ok(const uint4 &v, uint32_t tag) {
+  return ((v.x >> VBITS) == tag) & ((v.y >> VBITS) == tag) & ((v.z >> VBITS) == tag) & ((v.w >> VBITS) == tag);
+}
+
+// acc += row where word has the mask bit set: one predicate + three predicated adds (left to
+// itself the compiler builds an all-ones mask and ANDs every term: 6.5 instead of 4
+// instructions per (row, bit)).
+__device__ __forceinline__ void cond_add3(uint32_t word, uint32_t mask, const uint4 &row, uint32_t (&acc)[3]) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+      "and.b32 t, %3, %4;\n\t"
+      "setp.ne.u32 p, t, 0;\n\t"
+      "@p add.u32 %0, %0, %5;\n\t"
+      "@p add.u32 %1, %1, %6;\n\t"
+      "@p add.u32 %2, %2, %7;\n\t}"
+      : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2])
+      : "r"(word), "r"(mask), "r"(row.x), "r"(row.y), "r"(row.z));
+}
+
+// Timeline probe (-DFHEGPU_TRACE=1 builds only, tools/probes/flow_trace.py): per gate (index <
+// FLOW_TRACE_GATES) {right wait, left wait, compute, total} in SM clocks, {operand paths taken |
+// worker << 16, globaltimer (ns, low word) after the right operand, after the left, at the end}.
+#ifndef FHEGPU_TRACE
+#define FHEGPU_TRACE 0
+#endif
+constexpr uint32_t FLOW_TRACE_GATES = FHEGPU_TRACE ? 32768u : 1u;
+__device__ uint32_t g_flow_trace[8 * FLOW_TRACE_GATES];
+
+__device__ __forceinline__ bool tags_newer(const uint4 &v, uint32_t tag) {
+  return ((v.x >> VBITS) > tag) | ((v.y >> VBITS) > tag) | ((v.z >> VBITS) > tag) | ((v.w >> VBITS) > tag);
+}
+
+#ifndef FHEGPU_FLOW_SPIN_LIMIT
+#define FHEGPU_FLOW_SPIN_LIMIT (1u << 24)   // polls before a worker gives up (trap, not a hung GPU)
+#endif
+
+// The two rows (lane, lane + 32) of one operand into v[2][K], complement applied.  Returns
+// when every lane of the warp holds valid rows.
+template <int K, int ELL>
+__device__ __forceinline__ uint32_t acquire_rows(uint32_t idx, uint32_t meta, const uint32_t *store,
+                                             const uint4 *scratch, const uint4 *ring_base, uint32_t epoch,
+                                             uint32_t ct_words, uint32_t q, int lane, uint32_t (&v)[2][K]) {
+  constexpr int ROWS = K * ELL;
+  const uint32_t kind = meta & 3u;
+  const bool has1 = lane + 32 < ROWS;
+  uint32_t path = kind == K_STORE ? K_STORE : K_SCRATCH;
+  if (kind == K_STORE) {
+    const uint32_t *src = store + (uint64_t)idx * ct_words;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      v[0][c] = lane < ROWS ? __ldcg(src + lane * K + c) : 0u;
+      v[1][c] = has1 ? __ldcg(src + (lane + 32) * K + c) : 0u;
+    }
+  } else {
+    const uint4 *g = scratch + (uint64_t)idx * ROWS;
+    const uint32_t pos1 = meta >> 8;
+    const uint4 *r = ring_base + ((meta >> 4) & 15u) * (RING * ROWS) + ((pos1 - 1u) % RING) * ROWS;
+    uint4 x0 = make_uint4(0u, 0u, 0u, 0u), x1 = x0;
+    uint32_t spins = 0;
+    bool hit = false;
+    if (kind == K_RING) {
+      // Tags of one ring entry only grow (positions of the producing worker, same residue mod
+      // RING): all equal to the expected one = the rows are there; any larger = overwritten,
+      // take the scratch copy; otherwise the producer has not finished -- keep polling shared
+      // memory only (a scratch poll in flight would cost its L2 round trip even on a hit).
+      // poll ONE word (the last row's tag word, written by the producer's last ring store),
+      // all lanes the same address: seven warps polling whole entries would take half the
+      // shared-memory pipe from the warp that computes
+      const uint32_t *flag = reinterpret_cast<const uint32_t *>(r + (ROWS - 1)) + 3;
+      for (;;) {
+        uint32_t f;
+        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(f) : "r"((uint32_t)__cvta_generic_to_shared(flag)) : "memory");
+        if ((f >> VBITS) < pos1) {
+          if (++spins > FHEGPU_FLOW_SPIN_LIMIT) __trap();
+          continue;
+        }
+        x0 = ld_volatile_shared_v4(r + lane);
+        if (has1) x1 = ld_volatile_shared_v4(r + lane + 32);
+        const bool ok = tags_ok(x0, pos1) && (!has1 || tags_ok(x1, pos1));
+        const bool gone = tags_newer(x0, pos1) || (has1 && tags_newer(x1, pos1));
+        if (__all_sync(0xffffffffu, ok)) {
+          hit = true;
+          break;
+        }
+        if (__any_sync(0xffffffffu, gone)) break;
+        if (++spins > FHEGPU_FLOW_SPIN_LIMIT) __trap();
+      }
+    }
+    if (hit) {
+      path = K_RING;
+    } else {
+      for (;;) {
+        x0 = ld_volatile_global_v4(g + lane);
+        if (has1) x1 = ld_volatile_global_v4(g + lane + 32);
+        if (__all_sync(0xffffffffu, tags_ok(x0, epoch) && (!has1 || tags_ok(x1, epoch)))) break;
+        if (++spins > FHEGPU_FLOW_SPIN_LIMIT) __trap();
+      }
+    }
+    v[0][0] = x0.x & VMASK;
+    v[1][0] = x1.x & VMASK;
+    if (K > 1) v[0][1] = x0.y & VMASK, v[1][1] = x1.y & VMASK;
+    if (K > 2) v[0][2] = x0.z & VMASK, v[1][2] = x1.z & VMASK;
+  }
+  if (meta & 4u) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = lane + 32 * h;
+#pragma unroll
+      for (int c = 0; c < K; ++c)
+        v[h][c] = row < ROWS ? sub_mod(gadget_ct<ELL>(row, c), v[h][c], q) : 0u;
+    }
+  }
+  return path;
+}
+
+// One CTA = WARPS workers.  ents: every worker's gates in its order; worker_off[w] .. [w+1].
+template <int K, int ELL>
+__global__ void __launch_bounds__(32 * WARPS, 1)
+flow_kernel(uint32_t *__restrict__ store, uint4 *__restrict__ scratch, const uint4 *__restrict__ ents,
+            const uint32_t *__restrict__ worker_off, uint32_t epoch, uint32_t q_magic, DevParams p) {
+  static_assert(K <= 3 && K * ELL <= 64 && ELL <= (int)VBITS, "flow kernel geometry");
+  constexpr int ROWS = K * ELL;
+  __shared__ uint4 s_ring[WARPS * RING * ROWS];
+  __shared__ uint4 s_stage[WARPS * ROWS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < WARPS * RING * ROWS; i += 32 * WARPS) s_ring[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+  const uint32_t worker = blockIdx.x * WARPS + warp;
+  const uint32_t e0 = worker_off[worker], e1 = worker_off[worker + 1];
+  uint4 *stage = s_stage + warp * ROWS;
+  uint4 *my_ring = s_ring + warp * (RING * ROWS);
+  const bool has1 = lane + 32 < ROWS;
+  uint4 na, nb;
+  if (e0 < e1) na = __ldg(ents + 2 * e0), nb = __ldg(ents + 2 * e0 + 1);
+  for (uint32_t e = e0; e < e1; ++e) {
+    const uint4 A = na, B = nb;
+    if (e + 1 < e1) na = __ldg(ents + 2 * (e + 1)), nb = __ldg(ents + 2 * (e + 1) + 1);
+    uint32_t a[2][K], b[2][K];
+#if FHEGPU_TRACE
+    uint32_t gt0;
+    asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(gt0));
+    const long long t0 = clock64();
+#endif
+    const uint32_t path_r = acquire_rows<K, ELL>(A.y, B.y, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, b);
+#if FHEGPU_TRACE
+    const long long t1 = clock64();
+    uint32_t gt1;
+    asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(gt1));
+#endif
+    __syncwarp();                                   // the previous gate's readers are done with stage
+    stage[lane] = make_uint4(b[0][0], K > 1 ? b[0][1] : 0u, K > 2 ? b[0][2] : 0u, 0u);
+    if (has1) stage[lane + 32] = make_uint4(b[1][0], K > 1 ? b[1][1] : 0u, K > 2 ? b[1][2] : 0u, 0u);
+    const uint32_t path_l = acquire_rows<K, ELL>(A.x, B.x, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, a);
+    __syncwarp();
+#if FHEGPU_TRACE
+    const long long t2 = clock64();
+    uint32_t gt2;
+    asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(gt2));
+#else
+    (void)path_r, (void)path_l;
+#endif
+    uint32_t acc[2][3] = {{0u, 0u, 0u}, {0u, 0u, 0u}};
+#pragma unroll
+    for (int w = 0; w < K; ++w) {
+#pragma unroll
+      for (int bit = 0; bit < ELL; ++bit) {
+        const uint4 row = stage[w * ELL + bit];     // broadcast
+        cond_add3(a[0][w], 1u << bit, row, acc[0]);
+        cond_add3(a[1][w], 1u << bit, row, acc[1]);
+      }
+    }
+#if FHEGPU_TRACE
+    const long long t3 = clock64();
+#endif
+    // out = (G - S mod q) mod q;  S < N * q < 2^32: one-correction Barrett with floor(2^32 / q)
+    const uint32_t pos1 = B.z;
+    const uint32_t rt = pos1 << VBITS, et = epoch << VBITS;
+    uint4 *rdst = my_ring + ((pos1 - 1u) % RING) * ROWS;
+    uint4 *gdst = scratch + (uint64_t)A.w * ROWS;
+    uint32_t *sdst = store + (uint64_t)A.z * p.ct_words;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = lane + 32 * h;
+      if (row < ROWS) {
+        uint32_t o[3] = {0u, 0u, 0u};
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          uint32_t s = acc[h][c];
+          s -= __umulhi(s, q_magic) * p.q;
+          if (s >= p.q) s -= p.q;
+          o[c] = sub_mod(gadget_ct<ELL>(row, c), s, p.q);
+        }
+        st_volatile_shared_v4(rdst + row, make_uint4(o[0] | rt, o[1] | rt, o[2] | rt, rt));
+        st_volatile_global_v4(gdst + row, make_uint4(o[0] | et, o[1] | et, o[2] | et, et));
+        if (A.z != NO_STORE) {
+#pragma unroll
+          for (int c = 0; c < K; ++c) sdst[row * K + c] = o[c];
+        }
+      }
+    }
+#if FHEGPU_TRACE
+    if (lane == 0 && A.w < FLOW_TRACE_GATES) {
+      uint32_t gt3;
+      asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(gt3));
+      uint32_t *tr = g_flow_trace + 8 * A.w;
+      tr[0] = (uint32_t)(t1 - t0), tr[1] = (uint32_t)(t2 - t1), tr[2] = (uint32_t)(t3 - t2);
+      tr[3] = (uint32_t)(clock64() - t0);
+      tr[4] = path_r | path_l << 4 | (B.y & 3u) << 8 | (B.x & 3u) << 12 | worker << 16;
+      tr[5] = gt1, tr[6] = gt2, tr[7] = gt3;
+      (void)gt0;
+    }
+#endif
+  }
+}
+
+#endif  // __CUDACC__
+
+// ------------------------------------------------------------------------------------------
+// Host: list schedule of a levelised program onto n_cta * WARPS workers.
+struct FlowPlan {
+  std::vector<Entry> ents;            // grouped by worker, in execution order
+  std::vector<uint32_t> worker_off;   // n_workers + 1
+  double makespan = 0;                // model cycles
+  uint32_t ring_operands = 0, scratch_operands = 0, store_operands = 0;
+  uint32_t max_gates_per_worker = 0;
+};
+
+// Latency model (cycles at ~1.9 GHz; measured orders of magnitude)
+// Swept on configs[0] (tools/probes/flow_timing.py): measured values are ~1,000 / ~3,000 / ~700
+// cycles (tools/probes/flow_trace.py); the greedy does best planning a little optimistically,
+// and much worse counting on more than the last 2 ring entries (it then piles gates onto the
+// producers' CTAs: 212 -> 350-440 us even with an 8-entry ring).
+struct FlowModel {
+  double comp = 800;      // a gate on one warp, operands at hand, to its ring store
+  double remote = 2500;   // producer's scratch store -> consumer's poll sees it (through L2)
+  double local = 300;     // the same through the CTA's shared-memory ring
+  uint32_t ring_eff = 2;  // ring entries a consumer can count on (of RING)
+  FlowModel() {
+    if (const char *e = std::getenv("FHEGPU_FLOW_MODEL")) {   // experiments: "comp,remote,local,ring"
+      double c, r, l;
+      unsigned k;
+      if (std::sscanf(e, "%lf,%lf,%lf,%u", &c, &r, &l, &k) == 4) comp = c, remote = r, local = l, ring_eff = k;
+    }
+  }
+};
+
+// ops: n records {left, right, out, flags} in level order; deps: 2 per op (producing op or -1);
+// level_off: n_levels + 1.
+inline FlowPlan flow_plan(const OpRec *ops, const int32_t *deps, uint64_t n, const uint64_t *level_off,
+                          uint32_t n_levels, uint32_t n_cta, const FlowModel &m = FlowModel()) {
+  const uint32_t W = n_cta * WARPS;
+  FlowPlan pl;
+  // bottom level of every gate (longest chain of consumers below it): the priority in a level
+  std::vector<uint32_t> bl(n, 1);
+  for (uint64_t i = n; i-- > 0;) {
+    for (int s = 0; s < 2; ++s) {
+      const int32_t d = deps[2 * i + s];
+      if (d >= 0) bl[d] = std::max(bl[d], bl[i] + 1);
+    }
+  }
+  std::vector<uint32_t> order(n);
+  for (uint64_t i = 0; i < n; ++i) order[i] = (uint32_t)i;
+  for (uint32_t l = 0; l < n_levels; ++l)
+    std::stable_sort(order.begin() + level_off[l], order.begin() + level_off[l + 1],
+                     [&](uint32_t x, uint32_t y) { return bl[x] > bl[y]; });
+  std::vector<double> fin(n, 0.0), free_at(W, 0.0);
+  std::vector<uint32_t> wk(n, 0), pos(n, 0), cnt(W, 0);
+  using QE = std::pair<double, uint32_t>;
+  std::priority_queue<QE, std::vector<QE>, std::greater<QE>> heap;    // (free time, worker), lazy
+  for (uint32_t w = 0; w < W; ++w) heap.push({0.0, w});
+  std::vector<std::vector<uint32_t>> lists(W);
+  auto start_on = [&](uint32_t g, uint32_t w) {
+    double r = 0;
+    for (int s = 0; s < 2; ++s) {
+      const int32_t d = deps[2 * g + s];
+      if (d < 0) continue;
+      const bool near = wk[d] / WARPS == w / WARPS && cnt[wk[d]] - pos[d] <= m.ring_eff;
+      r = std::max(r, fin[d] + (near ? m.local : m.remote));
+    }
+    return std::max(r, free_at[w]);
+  };
+  for (uint64_t oi = 0; oi < n; ++oi) {
+    const uint32_t g = order[oi];
+    while (heap.top().first != free_at[heap.top().second]) {
+      const uint32_t w = heap.top().second;
+      heap.pop();
+      heap.push({free_at[w], w});
+    }
+    uint32_t best_w = heap.top().second;
+    double best = start_on(g, best_w);
+    for (int s = 0; s < 2; ++s) {
+      const int32_t d = deps[2 * g + s];
+      if (d < 0) continue;
+      const uint32_t c0 = wk[d] / WARPS * WARPS;
+      uint32_t lw = c0;
+      for (uint32_t w = c0; w < c0 + WARPS; ++w)
+        if (free_at[w] < free_at[lw]) lw = w;
+      for (uint32_t w : {lw, wk[d]}) {
+        const double st = start_on(g, w);
+        if (st < best) best = st, best_w = w;
+      }
+    }
+    fin[g] = best + m.comp;
+    wk[g] = best_w;
+    pos[g] = cnt[best_w]++;
+    free_at[best_w] = fin[g];
+    heap.push({fin[g], best_w});
+    lists[best_w].push_back(g);
+    pl.makespan = std::max(pl.makespan, fin[g]);
+  }
+  pl.worker_off.assign(W + 1, 0);
+  for (uint32_t w = 0; w < W; ++w) {
+    pl.worker_off[w + 1] = pl.worker_off[w] + (uint32_t)lists[w].size();
+    pl.max_gates_per_worker = std::max<uint32_t>(pl.max_gates_per_worker, (uint32_t)lists[w].size());
+  }
+  pl.ents.resize(n);
+  for (uint32_t w = 0; w < W; ++w) {
+    for (uint32_t i = 0; i < lists[w].size(); ++i) {
+      const uint32_t g = lists[w][i];
+      Entry &e = pl.ents[pl.worker_off[w] + i];
+      uint32_t idx[2], meta[2];
+      for (int s = 0; s < 2; ++s) {
+        const int32_t d = deps[2 * g + s];
+        const uint32_t comp = (ops[g].flags >> s) & 1u;
+        if (d < 0) {
+          idx[s] = s ? ops[g].right : ops[g].left;
+          meta[s] = K_STORE | comp << 2;
+          ++pl.store_operands;
+        } else {
+          idx[s] = (uint32_t)d;
+          // ring operands: same CTA and not yet overwritten when this gate is reached IF the
+          // workers ran in lockstep with the model; the tag check decides at run time
+          const bool same_cta = wk[d] / WARPS == w / WARPS;
+          const bool ring = same_cta && (wk[d] != w || i - pos[d] <= (uint32_t)RING);
+          meta[s] = (ring ? K_RING : K_SCRATCH) | comp << 2 | (wk[d] % WARPS) << 4 | (pos[d] + 1u) << 8;
+          ++(ring ? pl.ring_operands : pl.scratch_operands);
+        }
+      }
+      e.a = make_uint4(idx[0], idx[1], (ops[g].flags & FHEGPU_OP_TEMP) ? NO_STORE : ops[g].out, g);
+      e.b = make_uint4(meta[0], meta[1], i + 1u, 0u);
+    }
+  }
+  return pl;
+}
+
+}  // namespace flow
+}  // namespace fhegpu

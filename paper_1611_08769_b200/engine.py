@@ -37,6 +37,7 @@ from .scheme import Ciphertext, GswScheme, KeyPair
 
 _UPLOAD_BATCH_BYTES = 256 << 20
 STREAM_OUT = 8          # fhegpu_op flag (include/fhegpu.h): output not read later in the program
+OP_TEMP = 16            # fhegpu_op flag: output read by nothing outside the program
 
 
 @dataclass(frozen=True)
@@ -307,9 +308,9 @@ class GpuEngine(LevelledNetlist):
             raise UsageError("threads must be >= 1")
         if batch_size < 1:
             raise UsageError("batch_size must be >= 1")
-        if schedule not in ("auto", "levels", "dataflow", "queue", "tiled", "resident", "regfile"):
+        if schedule not in ("auto", "levels", "dataflow", "queue", "tiled", "resident", "regfile", "flow"):
             raise UsageError(f"schedule must be 'auto', 'levels', 'dataflow', 'queue', 'tiled', "
-                             f"'resident' or 'regfile', got {schedule!r}")
+                             f"'resident', 'regfile' or 'flow', got {schedule!r}")
         self.schedule = schedule
         if lane_rngs is not None and len(lane_rngs) != batch_size:
             raise UsageError("need one rng per lane")
@@ -882,8 +883,10 @@ class GpuEngine(LevelledNetlist):
             sched = self._pick_schedule()
             comp = None
             if sched not in ("tiled", "resident"):
-                prog = self._compile(ssa=sched in ("dataflow", "queue"), pin_old=sched == "regfile")
+                prog = self._compile(ssa=sched in ("dataflow", "queue", "flow"), pin_old=sched == "regfile")
                 prog["schedule"] = sched
+                if sched == "flow":
+                    prog["ops"]["flags"] |= np.where(prog["held"], 0, OP_TEMP).astype(np.uint32)
                 out_slots = np.asarray(self._slot, dtype=np.int64)[tpl.out_internal]
                 comp = {"prog": prog, "n_slots": self._n_slots, "out_slots": out_slots}
                 if sched == "regfile":
@@ -915,10 +918,12 @@ class GpuEngine(LevelledNetlist):
             for f in ("left", "right", "out"):
                 table[f] += np.uint32(base)
             program = self.ctx.program(table, prog["offsets"])
-            if prog["schedule"] in ("dataflow", "queue"):
+            if prog["schedule"] in ("dataflow", "queue", "flow"):
                 program.set_deps(prog["deps"])
             if prog["schedule"] == "queue":
                 program.set_queue(True)
+            if prog["schedule"] == "flow":
+                prog["flow"] = program.set_flow(True)
             if prog["schedule"] == "regfile":
                 self._attach_regfile(program, comp["regfile"], base)
             reg = self._regions[tpl.uid] = (base, program)
@@ -966,12 +971,14 @@ class GpuEngine(LevelledNetlist):
         if not self._pending_ops:
             return None
         sched = self._pick_schedule()
-        dataflow = sched in ("dataflow", "queue", "tiled")
+        dataflow = sched in ("dataflow", "queue", "tiled", "flow")
         ring = self.TILE_RING if sched == "tiled" and self._ring_ok() else 0
         # register-file programs read inputs and write outputs in their own order: input slots
         # are not reused inside the program
         prog = self._compile(ssa=dataflow, ring_temps=ring > 0, pin_old=sched == "regfile")
         prog["schedule"] = sched
+        if sched == "flow":              # temporaries stay on chip (their store slot is never read)
+            prog["ops"]["flags"] |= np.where(prog["held"], 0, OP_TEMP).astype(np.uint32)
         self._pending_ops = []
         if self._cse_map is not None:
             self._cse_map = {}
@@ -1006,6 +1013,8 @@ class GpuEngine(LevelledNetlist):
                 program.set_deps(prog["deps"])
             if sched == "queue":
                 program.set_queue(True)
+            if sched == "flow":
+                prog["flow"] = program.set_flow(True)
             if sched == "resident":
                 plan = self._resident_plan(prog)
                 if plan is not None:                 # else: the level launches of `program`
@@ -1127,6 +1136,8 @@ class GpuEngine(LevelledNetlist):
                   whose single-assignment store fits TILED_MAX_BYTES."""
         if self.schedule != "auto":
             return self.schedule
+        if self._pick_flow():
+            return "flow"
         if self.dry_run or (self.params.k, self.params.ell) != (9, 29):
             return "levels"
         if self.batch_size >= self.RESIDENT_MIN_LANES and self.ctx.kernel == "tcgen05" and self._resident_ok():
@@ -1150,6 +1161,22 @@ class GpuEngine(LevelledNetlist):
         if len(np.unique(np.asarray(self._level, dtype=np.int64)[outs])) > self.TILED_MAX_LEVELS:
             return "levels"                    # deep programs are dependency-hop bound (4.8)
         return "tiled"
+
+    FLOW_MIN_LEVELS = 16           # 'auto' runs deeper single-lane EXACT programs as one warp-dataflow launch
+    FLOW_MAX_OPS = 1 << 22
+
+    def _pick_flow(self) -> bool:
+        """Deep single-lane programs at the EXACT geometry (configs[0]): one warp-dataflow launch
+        (csrc/flow_nand.cuh) instead of a ~2.5 us launch per level."""
+        if self.dry_run or self.batch_size != 1 or (self.params.k, self.params.ell) != (3, 17):
+            return False
+        if self.params.q > 1 << 17 or self.ctx.kernel == "simt":
+            return False
+        n_ops = len(self._pending_ops) // 5
+        if not 0 < n_ops <= self.FLOW_MAX_OPS:
+            return False
+        outs = np.asarray(self._pending_ops[4::5], dtype=np.int64)
+        return len(np.unique(np.asarray(self._level, dtype=np.int64)[outs])) >= self.FLOW_MIN_LEVELS
 
     QUEUE_MIN_LEVELS = 64          # 'auto' runs deeper single-signal programs over the ready queue
     QUEUE_MAX_BYTES = 40 << 30     # ... when their single-assignment store fits this

@@ -77,6 +77,41 @@ def test_cfg0_gate_by_gate(device_encrypt):
     assert (eng.nand_count, eng.max_depth) == (ref["nand_count"], ref["max_depth"])
 
 
+@pytest.mark.parametrize("schedule", ["flow", "auto"])
+def test_cfg0_flow_gate_by_gate(schedule):
+    """configs[0] as ONE warp-dataflow launch (csrc/flow_nand.cuh; 'auto' picks it for deep
+    single-lane EXACT programs): every gate's ciphertext equals the reference's, and stays so
+    over repeated runs of the same program (the scratch tags advance with every run)."""
+    eng, out, x = run_fft_config("cfg0", True, schedule=schedule)
+    assert eng.last_compile["schedule"] == "flow" and eng.last_program.launches == 1
+    assert eng.last_compile["flow"]["ring_operands"] > eng.last_compile["flow"]["scratch_operands"]
+    ref = golden_json("cts_cfg0.json")
+    gd = golden_npz("cts_cfg0.npz")["gate_digests"].view(np.uint8).reshape(-1, 8)
+    want = [bytes(r).hex() for r in gd]
+    for runs in (0, 3):
+        for _ in range(runs):
+            eng.last_program.run(1)
+        ins, gates = gate_digests(eng)
+        assert digest.chain_digest(ins) == ref["inputs_chain"]
+        first_bad = next((i for i, (a, b) in enumerate(zip(gates, want)) if a != b), None)
+        assert first_bad is None, f"first differing gate {first_bad} after {runs} reruns"
+    assert read_signal_ints(eng, out)[0].tolist() == ref["output_words"]
+    assert (eng.nand_count, eng.max_depth) == (ref["nand_count"], ref["max_depth"])
+
+
+def test_cfg0_flow_epoch_wraps():
+    """More runs of one warp-dataflow program than there are scratch tags (32,767): a stale
+    row of an earlier run is never taken for the current one."""
+    eng, out, x = run_fft_config("cfg0", True, keep_all=False, schedule="flow")
+    ref = golden_json("cts_cfg0.json")
+    handles = [h for w in signal_words(out) for h in w.bits]
+    v0 = eng.node_values(handles)
+    for _ in range(32767 + 5):
+        eng.last_program.run(1)
+    assert np.array_equal(eng.node_values(handles), v0)
+    assert read_signal_ints(eng, out)[0].tolist() == ref["output_words"]
+
+
 def test_cfg1_sample_pairs_bit_exact():
     """First 4096 pairs of the 2^20-pair gate benchmark: every XOR/AND ciphertext."""
     ref = golden_json("cts_cfg1.json")
