@@ -592,7 +592,7 @@ resident_tc_kernel(uint32_t *__restrict__ store, const ResOp *__restrict__ plan,
       mbar_wait(&a_free[b], (u & 1u) ^ 1u);
       // operands produced in this group: wait until the epilogue has put them in their buffers
       // (one mbarrier phase per lane group; the producer's next group runs after this slot)
-      if (DEPS && !(p.dbg & (1u << 19))) {         // dbg bit 19: no waits (timing only)
+      if (DEPS && !FHEGPU_ABL(p, 1u << 19)) {         // dbg bit 19: no waits (timing only)
         if (si.dep_l != 0xFF) mbar_wait(&out_ready[si.dep_l], g & 1u);
         if (si.dep_r != 0xFF) mbar_wait(&out_ready[si.dep_r], g & 1u);
       }

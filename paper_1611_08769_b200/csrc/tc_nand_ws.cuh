@@ -40,6 +40,13 @@ namespace tc {
 #ifndef FHEGPU_TRACE
 #define FHEGPU_TRACE 0
 #endif
+// Stage-ablation knobs (debug bits that skip loads, operand builds, MMAs, epilogue math or
+// stores; results invalid -- tools/probes/ablate.py): compiled in only with -DFHEGPU_ABLATE=1,
+// so release kernels carry none of their branches.
+#ifndef FHEGPU_ABLATE
+#define FHEGPU_ABLATE 0
+#endif
+#define FHEGPU_ABL(p, mask) (FHEGPU_ABLATE && ((p).dbg & (mask)))
 __device__ uint64_t g_ws_trace[64 * 16];
 __device__ __forceinline__ void trace_ev(const DevParams &p, uint32_t t, int ev) {
 #if FHEGPU_TRACE
@@ -568,7 +575,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
         // builders read the second operand from the first buffer (flag bit 2)
         const bool same = op.left == op.right;
         s_flags[s] = op.flags | (same ? 4u : 0u); // published to the builders by in_full's arrive
-        if (p.dbg & 256u) {                       // timing experiment: no operand loads
+        if (FHEGPU_ABL(p, 256u)) {                       // timing experiment: no operand loads
           mbar_arrive(&in_full[s]);
           continue;
         }
@@ -603,17 +610,17 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
       // descriptor address field is (addr >> 4): advance by adding byte offsets >> 4
       const uint64_t bd_b = bdesc0 + ((b * G::B_BYTES) >> 4);
       const uint64_t td_b = tdesc0 + ((b * G::TA_BYTES) >> 4);
-      if (!(p.dbg & 128u)) {
+      if (!FHEGPU_ABL(p, 128u)) {
         if (elect_one()) {
 #pragma unroll
           for (int mt = 0; mt < G::MT; ++mt) {
-            if (p.dbg & (1u << 18)) break;             // ablation: no tile MMAs (results invalid)
+            if (FHEGPU_ABL(p, 1u << 18)) break;             // ablation: no tile MMAs (results invalid)
 #pragma unroll
             for (int s = 0; s < K; ++s)
               mma_i8_ts(tb + mt * G::NPAD, tb + G::D_COLS + mt * 8 * K + 8 * s,
                         bd_b + ((s * 4 * G::LBO) >> 4), idesc, s > 0 ? 1u : 0u);
           }
-          if (G::TAIL > 0 && !(p.dbg & (1u << 17))) {  // ablation bit 17: no tail MMAs
+          if (G::TAIL > 0 && !FHEGPU_ABL(p, 1u << 17)) {  // ablation bit 17: no tail MMAs
 #pragma unroll
             for (int s = 0; s < K; ++s)
               mma_i8_ss(tb + G::D_COLS, td_b + ((s * 2 * G::TA_LBO) >> 4),
@@ -665,7 +672,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
         mbar_wait(&out_free[o], ou & 1u);            // gate t-N_OUT's store has read staging o
         if (lane == 0) trace_ev(p, t, 14);
         uint32_t *out_st = s_out + o * G::CT_WORDS;
-        if (lane < G::TAIL && !(p.dbg & 1024u)) {
+        if (lane < G::TAIL && !FHEGPU_ABL(p, 1024u)) {
           const int r = G::MMA_ROWS + lane;
           const int rb = r / ELL, rbit = r - rb * ELL;
 #pragma unroll
@@ -863,7 +870,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
       const int kr = bt + x * 128 * G::MT;
       const int w = kr >> 5, kk = kr & 31;
       const int j = 8 * (kk & 3) + (kk >> 2);
-      const bool ok = kr < G::KB && j < ELL && !(p.dbg & 32u);   // padding rows stay zero
+      const bool ok = kr < G::KB && j < ELL && !FHEGPU_ABL(p, 32u);   // padding rows stay zero
       b_src[x] = ok ? (w * ELL + j) * K : -1;
       b_dst[x] = (kr >> 3) * G::LBO + (kr & 7) * 16;
       b_w[x] = w;
@@ -888,7 +895,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
       const uint32_t *v2 = (flags & 4u) ? v1 : v1 + G::CT_WORDS;   // NAND(x, x): one buffer
       uint8_t *bb = s_b + b * G::B_BYTES;
       // A (TMEM tiles): this thread's row
-      if (!(p.dbg & 16u)) {
+      if (!FHEGPU_ABL(p, 16u)) {
         uint32_t words[K];
 #pragma unroll
         for (int i = 0; i < K; ++i) words[i] = v1[row * K + i];
@@ -921,7 +928,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
       }
       // A of the smem tail tile (TA[b] was last read by the MMAs of gate t-2: a_free above)
       if constexpr (G::TAIL > 0) {
-        if (bt < G::TAIL * K && !(p.dbg & 16u)) {
+        if (bt < G::TAIL * K && !FHEGPU_ABL(p, 16u)) {
           const int m = bt / K, w = bt - m * K;
           const int r = G::MMA_ROWS + m;
           uint32_t v = v1[r * K + w];
@@ -1006,7 +1013,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
         if (!mbar_test(&main_done[b], u & 1u)) {
           bulk_wait_n<0>();
           publish(progress, t);
-        } else if (t >= FHEGPU_PUBLISH_LAG && !(p.dbg & 65536u)) {
+        } else if (t >= FHEGPU_PUBLISH_LAG && !FHEGPU_ABL(p, 65536u)) {
           bulk_wait_n<FHEGPU_PUBLISH_LAG>();        // stores older than LAG gates are complete
           post_local(s_pub, t - FHEGPU_PUBLISH_LAG);  // the tail warp relays it
         }
@@ -1016,12 +1023,12 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
       if (et == 0) trace_ev(p, t, 9);
       tc_fence_after();
       uint32_t d[36];
-      load_acc36(tmem_base + b * G::BUF_COLS + lane_off + tile * G::NPAD, d, (p.dbg & 4096u) != 0);
+      load_acc36(tmem_base + b * G::BUF_COLS + lane_off + tile * G::NPAD, d, FHEGPU_ABL(p, 4096u));
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&d_free[b]);
-      if (!(p.dbg & 64u)) {
+      if (!FHEGPU_ABL(p, 64u)) {
 #pragma unroll
         for (int i = 0; i < K; ++i) {
           const uint32_t g = (i == row_blk) ? (1u << row_bit) : 0u;
@@ -1043,7 +1050,7 @@ level_tc_ws_kernel(uint32_t *__restrict__ store, const OpRec *__restrict__ ops, 
       }
       if (Q && et == 0) {
         bulk_s2g(store + (uint64_t)s_qout[t % G::QR] * G::CT_WORDS, out_st, G::CT_BYTES);
-      } else if (et == 0 && !(p.dbg & 512u)) {
+      } else if (et == 0 && !FHEGPU_ABL(p, 512u)) {
         const uint32_t ln = lane_of(item, lanes, p.lanes_magic);
         uint32_t *dst = store + ((uint64_t)op_cur.out * lanes + ln) * G::CT_WORDS;
         if (op_cur.flags & 8u) bulk_s2g_hint(dst, out_st, G::CT_BYTES, pol_stream);

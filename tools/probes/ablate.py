@@ -1,4 +1,5 @@
-"""Timing ablation of the level kernel: skip stages via debug bits (results invalid)."""
+"""(Needs a -DFHEGPU_ABLATE=1 build of libfhegpu.so, FHEGPU_LIB=...: release kernels compile the ablation bits out.)
+Timing ablation of the level kernel: skip stages via debug bits (results invalid)."""
 import sys
 import numpy as np, torch
 sys.path.insert(0, '/root/repo')
