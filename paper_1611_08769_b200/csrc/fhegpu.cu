@@ -351,7 +351,7 @@ int launch_flow(fhegpu_ctx *c, fhegpu_prog *pr, uint32_t lanes) {
   if (effective_kernel(c) != FHEGPU_KERNEL_TCGEN05) return FHEGPU_EUNSUP;   // 'simt': the cross-check kernel
   pr->flow_epoch = pr->flow_epoch % flow::TAG_MAX + 1u;
   const uint32_t q_magic = (uint32_t)((1ull << 32) / c->p.q);
-  flow::flow_kernel<3, 17><<<pr->flow_ctas, 32 * flow::WARPS, 0, c->stream>>>(
+  flow::flow_kernel<3, 17><<<pr->flow_ctas, 32 * flow::WARPS * flow::SPLIT, 0, c->stream>>>(
       c->store, pr->d_flow_scratch, pr->d_flow_ents, pr->d_flow_off, pr->flow_epoch, q_magic, c->p);
   CUDA_TRY(cudaGetLastError());
   return FHEGPU_OK;
@@ -1539,11 +1539,11 @@ int fhegpu_debug_ws_trace(uint64_t *host) {
   return FHEGPU_OK;
 }
 
-// Debug: copy the warp-dataflow kernel's per-gate probe (8 u32 per gate; -DFHEGPU_TRACE=1 builds).
+// Debug: copy the warp-dataflow kernel's per-gate probe (12 u32 per gate; -DFHEGPU_TRACE=1 builds).
 int fhegpu_debug_flow_trace(uint32_t *host, uint32_t n_gates) {
   if (!host) return fail(FHEGPU_EINVAL, "null argument");
   if (n_gates > flow::FLOW_TRACE_GATES) return fail(FHEGPU_EUNSUP, "not a trace build");
-  CUDA_TRY(cudaMemcpyFromSymbol(host, flow::g_flow_trace, sizeof(uint32_t) * 8 * n_gates));
+  CUDA_TRY(cudaMemcpyFromSymbol(host, flow::g_flow_trace, sizeof(uint32_t) * flow::FLOW_TRACE_WORDS * n_gates));
   return FHEGPU_OK;
 }
 

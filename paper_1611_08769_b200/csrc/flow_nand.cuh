@@ -49,6 +49,12 @@ constexpr int RING = FHEGPU_FLOW_RING_BUILD;    // outputs each warp keeps in sh
 #define FHEGPU_FLOW_WARPS_BUILD FHEGPU_FLOW_WARPS
 #endif
 constexpr int WARPS = FHEGPU_FLOW_WARPS_BUILD;  // workers per CTA
+#ifndef FHEGPU_FLOW_SPLIT
+#define FHEGPU_FLOW_SPLIT 1
+#endif
+constexpr int SPLIT = FHEGPU_FLOW_SPLIT;        // warps per worker (2: output rows split between two warps --
+                                                // measured slower, 232 vs 213 us: a gate's arithmetic is
+                                                // not what its dependency chain waits for)
 constexpr uint32_t VBITS = 17;          // value bits of a tagged word (q <= 2^17)
 constexpr uint32_t VMASK = (1u << VBITS) - 1u;
 constexpr uint32_t TAG_MAX = 32767u;    // tags 1..32767 (15 bits; 0 = never written): the run's
@@ -69,16 +75,9 @@ struct Entry {
 
 #ifdef __CUDACC__
 
-#ifndef FHEGPU_FLOW_RELAXED
-#define FHEGPU_FLOW_RELAXED 0
-#endif
-#if FHEGPU_FLOW_RELAXED
-#define FLOW_LD_G "ld.relaxed.gpu.global.v4.u32"
-#define FLOW_ST_G "st.relaxed.gpu.global.v4.u32"
-#else
+// (ld/st.relaxed.gpu and weak stores measured the same as volatile accesses: configs[0] 213-215 us)
 #define FLOW_LD_G "ld.volatile.global.v4.u32"
 #define FLOW_ST_G "st.volatile.global.v4.u32"
-#endif
 __device__ __forceinline__ uint4 ld_volatile_global_v4(const uint4 *p) {
   uint4 v;
   asm volatile(FLOW_LD_G " {%0, %1, %2, %3}, [%4];"
@@ -129,12 +128,14 @@ __device__ __forceinline__ void cond_add3(uint32_t word, uint32_t mask, const ui
 
 // Timeline probe (-DFHEGPU_TRACE=1 builds only, tools/probes/flow_trace.py): per gate (index <
 // FLOW_TRACE_GATES) {right wait, left wait, compute, total} in SM clocks, {operand paths taken |
-// worker << 16, globaltimer (ns, low word) after the right operand, after the left, at the end}.
+// worker << 16, globaltimer (ns, low word) after the right operand, after the left, at the end},
+// {clock64 (low word) at the ring store, after the right operand, after the left; SM id}.
 #ifndef FHEGPU_TRACE
 #define FHEGPU_TRACE 0
 #endif
 constexpr uint32_t FLOW_TRACE_GATES = FHEGPU_TRACE ? 32768u : 1u;
-__device__ uint32_t g_flow_trace[8 * FLOW_TRACE_GATES];
+constexpr int FLOW_TRACE_WORDS = 12;
+__device__ uint32_t g_flow_trace[FLOW_TRACE_WORDS * FLOW_TRACE_GATES];
 
 __device__ __forceinline__ bool tags_newer(const uint4 &v, uint32_t tag) {
   return ((v.x >> VBITS) > tag) | ((v.y >> VBITS) > tag) | ((v.z >> VBITS) > tag) | ((v.w >> VBITS) > tag);
@@ -144,28 +145,31 @@ __device__ __forceinline__ bool tags_newer(const uint4 &v, uint32_t tag) {
 #define FHEGPU_FLOW_SPIN_LIMIT (1u << 24)   // polls before a worker gives up (trap, not a hung GPU)
 #endif
 
-// The two rows (lane, lane + 32) of one operand into v[2][K], complement applied.  Returns
-// when every lane of the warp holds valid rows.
-template <int K, int ELL>
+// Rows first + 32 h (h < NR) of one operand into v[NR][K], complement applied.  Returns (the
+// path taken) when every lane of the warp holds valid rows.
+template <int K, int ELL, int NR>
 __device__ __forceinline__ uint32_t acquire_rows(uint32_t idx, uint32_t meta, const uint32_t *store,
-                                             const uint4 *scratch, const uint4 *ring_base, uint32_t epoch,
-                                             uint32_t ct_words, uint32_t q, int lane, uint32_t (&v)[2][K]) {
+                                                 const uint4 *scratch, const uint4 *ring_base, uint32_t epoch,
+                                                 uint32_t ct_words, uint32_t q, int first, uint32_t (&v)[NR][K]) {
   constexpr int ROWS = K * ELL;
   const uint32_t kind = meta & 3u;
-  const bool has1 = lane + 32 < ROWS;
+  bool has[NR];
+#pragma unroll
+  for (int h = 0; h < NR; ++h) has[h] = first + 32 * h < ROWS;
   uint32_t path = kind == K_STORE ? K_STORE : K_SCRATCH;
   if (kind == K_STORE) {
     const uint32_t *src = store + (uint64_t)idx * ct_words;
 #pragma unroll
-    for (int c = 0; c < K; ++c) {
-      v[0][c] = lane < ROWS ? __ldcg(src + lane * K + c) : 0u;
-      v[1][c] = has1 ? __ldcg(src + (lane + 32) * K + c) : 0u;
-    }
+    for (int h = 0; h < NR; ++h)
+#pragma unroll
+      for (int c = 0; c < K; ++c) v[h][c] = has[h] ? __ldcg(src + (first + 32 * h) * K + c) : 0u;
   } else {
     const uint4 *g = scratch + (uint64_t)idx * ROWS;
     const uint32_t pos1 = meta >> 8;
     const uint4 *r = ring_base + ((meta >> 4) & 15u) * (RING * ROWS) + ((pos1 - 1u) % RING) * ROWS;
-    uint4 x0 = make_uint4(0u, 0u, 0u, 0u), x1 = x0;
+    uint4 x[NR];
+#pragma unroll
+    for (int h = 0; h < NR; ++h) x[h] = make_uint4(0u, 0u, 0u, 0u);
     uint32_t spins = 0;
     bool hit = false;
     if (kind == K_RING) {
@@ -173,21 +177,28 @@ __device__ __forceinline__ uint32_t acquire_rows(uint32_t idx, uint32_t meta, co
       // RING): all equal to the expected one = the rows are there; any larger = overwritten,
       // take the scratch copy; otherwise the producer has not finished -- keep polling shared
       // memory only (a scratch poll in flight would cost its L2 round trip even on a hit).
-      // poll ONE word (the last row's tag word, written by the producer's last ring store),
-      // all lanes the same address: seven warps polling whole entries would take half the
-      // shared-memory pipe from the warp that computes
+      // The poll reads ONE word (the last row's tag word, every lane the same address): warps
+      // polling whole entries would take half the shared-memory pipe from those that compute.
       const uint32_t *flag = reinterpret_cast<const uint32_t *>(r + (ROWS - 1)) + 3;
       for (;;) {
         uint32_t f;
-        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(f) : "r"((uint32_t)__cvta_generic_to_shared(flag)) : "memory");
+        asm volatile("ld.volatile.shared.u32 %0, [%1];"
+                     : "=r"(f)
+                     : "r"((uint32_t)__cvta_generic_to_shared(flag))
+                     : "memory");
         if ((f >> VBITS) < pos1) {
           if (++spins > FHEGPU_FLOW_SPIN_LIMIT) __trap();
           continue;
         }
-        x0 = ld_volatile_shared_v4(r + lane);
-        if (has1) x1 = ld_volatile_shared_v4(r + lane + 32);
-        const bool ok = tags_ok(x0, pos1) && (!has1 || tags_ok(x1, pos1));
-        const bool gone = tags_newer(x0, pos1) || (has1 && tags_newer(x1, pos1));
+        bool ok = true, gone = false;
+#pragma unroll
+        for (int h = 0; h < NR; ++h)                // (every load issued before the first check)
+          if (has[h]) x[h] = ld_volatile_shared_v4(r + first + 32 * h);
+#pragma unroll
+        for (int h = 0; h < NR; ++h) {
+          ok = ok & (!has[h] | tags_ok(x[h], pos1));
+          gone = gone | (has[h] & tags_newer(x[h], pos1));
+        }
         if (__all_sync(0xffffffffu, ok)) {
           hit = true;
           break;
@@ -200,58 +211,66 @@ __device__ __forceinline__ uint32_t acquire_rows(uint32_t idx, uint32_t meta, co
       path = K_RING;
     } else {
       for (;;) {
-        x0 = ld_volatile_global_v4(g + lane);
-        if (has1) x1 = ld_volatile_global_v4(g + lane + 32);
-        if (__all_sync(0xffffffffu, tags_ok(x0, epoch) && (!has1 || tags_ok(x1, epoch)))) break;
+        bool ok = true;
+#pragma unroll
+        for (int h = 0; h < NR; ++h)                // (both L2 round trips in flight together)
+          if (has[h]) x[h] = ld_volatile_global_v4(g + first + 32 * h);
+#pragma unroll
+        for (int h = 0; h < NR; ++h) ok = ok & (!has[h] | tags_ok(x[h], epoch));
+        if (__all_sync(0xffffffffu, ok)) break;
         if (++spins > FHEGPU_FLOW_SPIN_LIMIT) __trap();
       }
     }
-    v[0][0] = x0.x & VMASK;
-    v[1][0] = x1.x & VMASK;
-    if (K > 1) v[0][1] = x0.y & VMASK, v[1][1] = x1.y & VMASK;
-    if (K > 2) v[0][2] = x0.z & VMASK, v[1][2] = x1.z & VMASK;
+#pragma unroll
+    for (int h = 0; h < NR; ++h) {
+      v[h][0] = x[h].x & VMASK;
+      if (K > 1) v[h][1] = x[h].y & VMASK;
+      if (K > 2) v[h][2] = x[h].z & VMASK;
+    }
   }
   if (meta & 4u) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int row = lane + 32 * h;
+    for (int h = 0; h < NR; ++h) {
+      const int row = first + 32 * h;
 #pragma unroll
-      for (int c = 0; c < K; ++c)
-        v[h][c] = row < ROWS ? sub_mod(gadget_ct<ELL>(row, c), v[h][c], q) : 0u;
+      for (int c = 0; c < K; ++c) v[h][c] = has[h] ? sub_mod(gadget_ct<ELL>(row, c), v[h][c], q) : 0u;
     }
   }
   return path;
 }
 
-// One CTA = WARPS workers.  ents: every worker's gates in its order; worker_off[w] .. [w+1].
+// One CTA = WARPS workers of SPLIT warps.  The warps of a worker run the same gate list
+// independently: each computes the output rows lane + 32 * (part + SPLIT * h) from its own copy of
+// the right operand, so they never synchronise (a consumer's tag check covers all parts).
+// ents: every worker's gates in its order; worker_off[w] .. [w+1].
 template <int K, int ELL>
-__global__ void __launch_bounds__(32 * WARPS, 1)
+__global__ void __launch_bounds__(32 * WARPS * SPLIT, 1)
 flow_kernel(uint32_t *__restrict__ store, uint4 *__restrict__ scratch, const uint4 *__restrict__ ents,
             const uint32_t *__restrict__ worker_off, uint32_t epoch, uint32_t q_magic, DevParams p) {
   static_assert(K <= 3 && K * ELL <= 64 && ELL <= (int)VBITS, "flow kernel geometry");
   constexpr int ROWS = K * ELL;
+  constexpr int NL = 2 / SPLIT;                     // output (and left operand) rows per lane
   __shared__ uint4 s_ring[WARPS * RING * ROWS];
-  __shared__ uint4 s_stage[WARPS * ROWS];
+  __shared__ uint4 s_stage[WARPS * SPLIT * ROWS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < WARPS * RING * ROWS; i += 32 * WARPS) s_ring[i] = make_uint4(0u, 0u, 0u, 0u);
+  const int part = warp % SPLIT, wk = warp / SPLIT;
+  for (int i = threadIdx.x; i < WARPS * RING * ROWS; i += 32 * WARPS * SPLIT) s_ring[i] = make_uint4(0u, 0u, 0u, 0u);
   __syncthreads();
-  const uint32_t worker = blockIdx.x * WARPS + warp;
+  const uint32_t worker = blockIdx.x * WARPS + wk;
   const uint32_t e0 = worker_off[worker], e1 = worker_off[worker + 1];
   uint4 *stage = s_stage + warp * ROWS;
-  uint4 *my_ring = s_ring + warp * (RING * ROWS);
-  const bool has1 = lane + 32 < ROWS;
+  uint4 *my_ring = s_ring + wk * (RING * ROWS);
+  const int first = lane + 32 * part;               // my first output row
   uint4 na, nb;
   if (e0 < e1) na = __ldg(ents + 2 * e0), nb = __ldg(ents + 2 * e0 + 1);
   for (uint32_t e = e0; e < e1; ++e) {
     const uint4 A = na, B = nb;
     if (e + 1 < e1) na = __ldg(ents + 2 * (e + 1)), nb = __ldg(ents + 2 * (e + 1) + 1);
-    uint32_t a[2][K], b[2][K];
+    uint32_t a[NL][K], b[2][K];
 #if FHEGPU_TRACE
-    uint32_t gt0;
-    asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(gt0));
     const long long t0 = clock64();
 #endif
-    const uint32_t path_r = acquire_rows<K, ELL>(A.y, B.y, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, b);
+    const uint32_t path_r = acquire_rows<K, ELL, 2>(A.y, B.y, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, b);
 #if FHEGPU_TRACE
     const long long t1 = clock64();
     uint32_t gt1;
@@ -259,8 +278,9 @@ flow_kernel(uint32_t *__restrict__ store, uint4 *__restrict__ scratch, const uin
 #endif
     __syncwarp();                                   // the previous gate's readers are done with stage
     stage[lane] = make_uint4(b[0][0], K > 1 ? b[0][1] : 0u, K > 2 ? b[0][2] : 0u, 0u);
-    if (has1) stage[lane + 32] = make_uint4(b[1][0], K > 1 ? b[1][1] : 0u, K > 2 ? b[1][2] : 0u, 0u);
-    const uint32_t path_l = acquire_rows<K, ELL>(A.x, B.x, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, a);
+    if (lane + 32 < ROWS) stage[lane + 32] = make_uint4(b[1][0], K > 1 ? b[1][1] : 0u, K > 2 ? b[1][2] : 0u, 0u);
+    const uint32_t path_l =
+        acquire_rows<K, ELL, NL>(A.x, B.x, store, scratch, s_ring, epoch, p.ct_words, p.q, first, a);
     __syncwarp();
 #if FHEGPU_TRACE
     const long long t2 = clock64();
@@ -269,18 +289,23 @@ flow_kernel(uint32_t *__restrict__ store, uint4 *__restrict__ scratch, const uin
 #else
     (void)path_r, (void)path_l;
 #endif
-    uint32_t acc[2][3] = {{0u, 0u, 0u}, {0u, 0u, 0u}};
+    uint32_t acc[NL][3];
+#pragma unroll
+    for (int h = 0; h < NL; ++h) acc[h][0] = acc[h][1] = acc[h][2] = 0u;
 #pragma unroll
     for (int w = 0; w < K; ++w) {
 #pragma unroll
       for (int bit = 0; bit < ELL; ++bit) {
         const uint4 row = stage[w * ELL + bit];     // broadcast
-        cond_add3(a[0][w], 1u << bit, row, acc[0]);
-        cond_add3(a[1][w], 1u << bit, row, acc[1]);
+#pragma unroll
+        for (int h = 0; h < NL; ++h) cond_add3(a[h][w], 1u << bit, row, acc[h]);
       }
     }
 #if FHEGPU_TRACE
     const long long t3 = clock64();
+#endif
+#if FHEGPU_TRACE
+    long long t_ring = 0;
 #endif
     // out = (G - S mod q) mod q;  S < N * q < 2^32: one-correction Barrett with floor(2^32 / q)
     const uint32_t pos1 = B.z;
@@ -288,36 +313,55 @@ flow_kernel(uint32_t *__restrict__ store, uint4 *__restrict__ scratch, const uin
     uint4 *rdst = my_ring + ((pos1 - 1u) % RING) * ROWS;
     uint4 *gdst = scratch + (uint64_t)A.w * ROWS;
     uint32_t *sdst = store + (uint64_t)A.z * p.ct_words;
+    uint32_t o[NL][3];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int row = lane + 32 * h;
-      if (row < ROWS) {
-        uint32_t o[3] = {0u, 0u, 0u};
+    for (int h = 0; h < NL; ++h) {
+      const int row = first + 32 * SPLIT * h;
 #pragma unroll
-        for (int c = 0; c < K; ++c) {
-          uint32_t s = acc[h][c];
-          s -= __umulhi(s, q_magic) * p.q;
-          if (s >= p.q) s -= p.q;
-          o[c] = sub_mod(gadget_ct<ELL>(row, c), s, p.q);
-        }
-        st_volatile_shared_v4(rdst + row, make_uint4(o[0] | rt, o[1] | rt, o[2] | rt, rt));
-        st_volatile_global_v4(gdst + row, make_uint4(o[0] | et, o[1] | et, o[2] | et, et));
-        if (A.z != NO_STORE) {
+      for (int c = 0; c < 3; ++c) {
+        uint32_t s = c < K ? acc[h][c] : 0u;
+        s -= __umulhi(s, q_magic) * p.q;
+        if (s >= p.q) s -= p.q;
+        o[h][c] = c < K && row < ROWS ? sub_mod(gadget_ct<ELL>(row, c), s, p.q) : 0u;
+      }
+    }
+    // every ring store before the first global store: a consumer on this SM polls the last
+    // row's tag, and stores leave the warp in program order
 #pragma unroll
-          for (int c = 0; c < K; ++c) sdst[row * K + c] = o[c];
+    for (int h = 0; h < NL; ++h) {
+      const int row = first + 32 * SPLIT * h;
+      if (row < ROWS) st_volatile_shared_v4(rdst + row, make_uint4(o[h][0] | rt, o[h][1] | rt, o[h][2] | rt, rt));
+    }
+#if FHEGPU_TRACE
+    t_ring = clock64();
+#endif
+#pragma unroll
+    for (int h = 0; h < NL; ++h) {
+      const int row = first + 32 * SPLIT * h;
+      if (row < ROWS) st_volatile_global_v4(gdst + row, make_uint4(o[h][0] | et, o[h][1] | et, o[h][2] | et, et));
+    }
+    if (A.z != NO_STORE) {
+#pragma unroll
+      for (int h = 0; h < NL; ++h) {
+        const int row = first + 32 * SPLIT * h;
+        if (row < ROWS) {
+#pragma unroll
+          for (int c = 0; c < K; ++c) sdst[row * K + c] = o[h][c];
         }
       }
     }
 #if FHEGPU_TRACE
-    if (lane == 0 && A.w < FLOW_TRACE_GATES) {
+    if (lane == 0 && part == SPLIT - 1 && A.w < FLOW_TRACE_GATES) {
       uint32_t gt3;
       asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(gt3));
-      uint32_t *tr = g_flow_trace + 8 * A.w;
+      uint32_t *tr = g_flow_trace + FLOW_TRACE_WORDS * A.w;
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      tr[8] = (uint32_t)t_ring, tr[9] = (uint32_t)t1, tr[10] = (uint32_t)t2, tr[11] = smid;
       tr[0] = (uint32_t)(t1 - t0), tr[1] = (uint32_t)(t2 - t1), tr[2] = (uint32_t)(t3 - t2);
       tr[3] = (uint32_t)(clock64() - t0);
       tr[4] = path_r | path_l << 4 | (B.y & 3u) << 8 | (B.x & 3u) << 12 | worker << 16;
       tr[5] = gt1, tr[6] = gt2, tr[7] = gt3;
-      (void)gt0;
     }
 #endif
   }

@@ -26,9 +26,9 @@ while time.perf_counter() < t_end:                  # sustained load first: cloc
         prog.run(1)
     torch.cuda.synchronize()
 n = len(eng.last_compile["ops"])
-buf = np.zeros((n, 8), dtype=np.uint32)
+buf = np.zeros((n, 12), dtype=np.uint32)
 _native._lib.fhegpu_debug_flow_trace(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), n)
-wr, wl, comp, tot, paths, gt1, gt2, gt3 = buf.T.astype(np.int64)
+wr, wl, comp, tot, paths, gt1, gt2, gt3, c_ring, c_r, c_l, smid = buf.T.astype(np.int64)
 worker = paths >> 16
 pr, pl = paths & 15, (paths >> 4) & 15
 kr, kl = (paths >> 8) & 3, (paths >> 12) & 3
@@ -56,6 +56,18 @@ for side, w, path, got, col in (("right", wr, pr, gt1, 0), ("left", wl, pl, gt2,
             if m.any():
                 print(f"  {side}: planned {names[k]:8s} took {names[pth]:8s}: {m.sum():6d} operands, wait median "
                       f"{np.median(w[m]):.0f} cyc")
+# same-SM hops in SM clocks (clock64 is per SM): producer's ring store -> consumer holds the operand
+for side, w, path, cgot, col in (("right", wr, pr, c_r, 0), ("left", wl, pl, c_l, 1)):
+    d = deps[:, col]
+    m = (d >= 0) & (path == 2)
+    dd = np.maximum(d, 0)
+    m &= smid == smid[dd]
+    hopc = (cgot - c_ring[dd]) & 0xFFFFFFFF
+    hopc = np.where(hopc > 1 << 31, hopc - (1 << 32), hopc)
+    waited = m & (w > hopc) & (hopc > 0)
+    if waited.any():
+        print(f"  {side} ring hop in SM clocks (consumer already waiting): n {waited.sum()} median {np.median(hopc[waited]):.0f} "
+              f"p10 {np.percentile(hopc[waited], 10):.0f} p90 {np.percentile(hopc[waited], 90):.0f}")
 print(f"span: {(gt3.max() - gt1.min()) / 1e3:.1f} us; workers used {len(np.unique(worker))}")
 # real critical path: walk back from the last gate through the operand that arrived last
 g = int(np.argmax(gt3))
