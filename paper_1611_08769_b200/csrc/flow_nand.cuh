@@ -380,20 +380,31 @@ struct FlowPlan {
 };
 
 // Latency model (cycles at ~1.9 GHz; measured orders of magnitude)
-// Swept on configs[0] (tools/probes/flow_timing.py): measured values are ~1,000 / ~3,000 / ~700
-// cycles (tools/probes/flow_trace.py); the greedy does best planning a little optimistically,
-// and much worse counting on more than the last 2 ring entries (it then piles gates onto the
-// producers' CTAs: 212 -> 350-440 us even with an 8-entry ring).
+// Swept on configs[0] (tools/probes/flow_timing.py, FHEGPU_FLOW_MODEL).  What the trace measures
+// (tools/probes/flow_trace.py): ~970 cycles of service per gate, ~580 for a waited-for ring hop,
+// ~2,900 through L2.  What matters far more than the constants is how much locality the greedy
+// is allowed to chase: workers run their lists in order, so a gate queued behind one whose
+// operand is late waits with it, and every gate steered to a producer's CTA lengthens those
+// queues.  Counting on the producer's last output only (ring_eff 1; the kernel still takes any
+// ring entry that is there) gives 158-165 us for every choice of the other constants, the last
+// two outputs 213-235 us, more 350-500 us, no locality at all 188 us; planned idle time after
+// each gate (pad) is worth another 4%.
 struct FlowModel {
   double comp = 800;      // a gate on one warp, operands at hand, to its ring store
   double remote = 2500;   // producer's scratch store -> consumer's poll sees it (through L2)
-  double local = 300;     // the same through the CTA's shared-memory ring
-  uint32_t ring_eff = 2;  // ring entries a consumer can count on (of RING)
+  double local = 1000;    // the same through the CTA's shared-memory ring
+  uint32_t ring_eff = 1;  // ring entries a consumer can count on (of RING)
+  double own = 1000;      // an operand from the worker's own ring
+  double pad = 1600;      // idle time planned after every gate (slack against late operands)
   FlowModel() {
-    if (const char *e = std::getenv("FHEGPU_FLOW_MODEL")) {   // experiments: "comp,remote,local,ring"
-      double c, r, l;
+    if (const char *e = std::getenv("FHEGPU_FLOW_MODEL")) {   // experiments: "comp,remote,local,ring[,own]"
+      double c, r, l, o = -1, p = 0;
       unsigned k;
-      if (std::sscanf(e, "%lf,%lf,%lf,%u", &c, &r, &l, &k) == 4) comp = c, remote = r, local = l, ring_eff = k;
+      if (std::sscanf(e, "%lf,%lf,%lf,%u,%lf,%lf", &c, &r, &l, &k, &o, &p) >= 4) {
+        comp = c, remote = r, local = l, ring_eff = k;
+        own = o >= 0 ? o : l;
+        pad = p;
+      }
     }
   }
 };
@@ -429,7 +440,8 @@ inline FlowPlan flow_plan(const OpRec *ops, const int32_t *deps, uint64_t n, con
       const int32_t d = deps[2 * g + s];
       if (d < 0) continue;
       const bool near = wk[d] / WARPS == w / WARPS && cnt[wk[d]] - pos[d] <= m.ring_eff;
-      r = std::max(r, fin[d] + (near ? m.local : m.remote));
+      const bool mine = wk[d] == w && near;
+      r = std::max(r, fin[d] + (mine ? m.own : near ? m.local : m.remote));
     }
     return std::max(r, free_at[w]);
   };
@@ -457,8 +469,8 @@ inline FlowPlan flow_plan(const OpRec *ops, const int32_t *deps, uint64_t n, con
     fin[g] = best + m.comp;
     wk[g] = best_w;
     pos[g] = cnt[best_w]++;
-    free_at[best_w] = fin[g];
-    heap.push({fin[g], best_w});
+    free_at[best_w] = fin[g] + m.pad;
+    heap.push({free_at[best_w], best_w});
     lists[best_w].push_back(g);
     pl.makespan = std::max(pl.makespan, fin[g]);
   }
