@@ -8,9 +8,11 @@ encryptions from default_rng(1), pair-major), one XOR + one AND per pair =
 one evaluation of that whole netlist: ONE lane-resident launch
 (resident_tc_kernel: each CTA runs the 6-gate per-pair program on 3 lanes at a
 time, intermediates in shared memory).  Secondary lines: configs[4] (1024 x
-16-point Q4.12 FFTs, level launches) and configs[0]/[2]/[3] (single-signal
-FFTs), each with first-call host costs (encrypt / record / compile) and an
-API-level e2e after the first call (circuit template replay).
+16-point Q4.12 FFTs, one register-file launch) and configs[0]/[2]/[3]
+(single-signal FFTs: one warp-dataflow launch at the EXACT geometry, ready-queue
+launches at the default one), each with first-call host costs (encrypt /
+record / compile) and an API-level e2e after the first call (circuit template
+replay).
 
   value      NAND/s, inputs resident in HBM, device time (CUDA events, max over ranks)
   e2e        same metric through the C-ABI with host buffers: pinned H2D of the

@@ -27,8 +27,8 @@ for r in data:
 tot = sum(t.values())
 lines = ["# ncu --metrics gpu__time_duration.sum --clock-control none -c 600 python bench.py (default args)",
          "# per-kernel totals over the first 600 launches (cold-cache, serialised: shares, not absolutes)",
-         "# cfg1 runs as ONE lane-resident launch per step (resident_tc_kernel); cfg4 as ONE register-file launch (regfile_tc_kernel), cfg0 as level launches"
-         " (level_tc_ws_kernel / level_tc_kernel), cfg2/cfg3 as ready-queue launches",
+         "# cfg1 runs as ONE lane-resident launch per step (resident_tc_kernel); cfg4 as ONE register-file launch (regfile_tc_kernel), cfg0 as ONE warp-dataflow launch"
+         " (flow_kernel), cfg2/cfg3 as ready-queue launches (level_tc_ws_kernel with the queue)",
          f"# total {tot / 1e6:.2f} ms over {len(data)} launches"]
 lines += [f"{v / 1e6:10.3f} ms  {100 * v / tot:5.1f}%  n={c[k]:4d}  {k}" for k, v in sorted(t.items(), key=lambda x: -x[1])]
 open(os.path.join(P, f"{RND}_launches_summary.txt"), "w").write("\n".join(lines) + "\n")
