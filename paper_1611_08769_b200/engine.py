@@ -495,12 +495,16 @@ class GpuEngine(LevelledNetlist):
         self._enc_rows.append(np.stack([stream_idx.ravel().astype(np.uint64), off.ravel(),
                                         bits.ravel().astype(np.uint64), target.ravel()]))
         self._pending_in_bytes += lanes * n * 32
-        out = []
-        for node in nodes:
-            wire = self._new_wire()
-            if self.trace is not None:
+        if self.trace is None:
+            w0 = self._wire
+            self._wire += n
+            out = [GpuBit(self, node, 0, False, None, w0 + i) for i, node in enumerate(nodes)]
+        else:
+            out = []
+            for node in nodes:
+                wire = self._new_wire()
                 self.trace.append((2, -1, -1, wire, node, 0))
-            out.append(GpuBit(self, node, 0, False, None, wire))
+                out.append(GpuBit(self, node, 0, False, None, wire))
         if self._pending_in_bytes >= _UPLOAD_BATCH_BYTES:
             self._upload_inputs()
         return out
@@ -737,22 +741,43 @@ class GpuEngine(LevelledNetlist):
         return result
 
     def _input_pattern(self, in_bits):
-        """Hashable structure of the input wires: per bit ('c', value) or (distinct-node index,
-        complement), plus each distinct node's (level, noise estimate)."""
-        index, nodes, pat = {}, [], []
-        for h in in_bits:
-            if getattr(h, "engine", None) is not self:
+        """Hashable structure of the input wires -- per bit a public constant's value or
+        (distinct-node index in first-use order, complement), plus each distinct node's (level,
+        noise estimate) -- and the distinct nodes.  None if a wire is not this engine's."""
+        try:
+            if any(h.engine is not self for h in in_bits):
                 return None, None
-            if h.const:
-                pat.append((-1, int(h.plain)))
-                continue
-            i = index.get(h.node)
-            if i is None:
-                i = index[h.node] = len(nodes)
-                nodes.append(h.node)
-            pat.append((i, h.neg))
-        info = tuple((self._level[n], self._est[n]) for n in nodes)
-        return (tuple(pat), info), nodes
+        except AttributeError:
+            return None, None
+        all_nodes = [h.node for h in in_bits]
+        if all_nodes and min(all_nodes) < 0:              # public constants among the inputs
+            index, nodes, pat = {}, [], []
+            for h in in_bits:
+                if h.const:
+                    pat.append((-1, int(h.plain)))
+                    continue
+                i = index.get(h.node)
+                if i is None:
+                    i = index[h.node] = len(nodes)
+                    nodes.append(h.node)
+                pat.append((i, h.neg))
+            info = tuple((self._level[n], self._est[n]) for n in nodes)
+            return (tuple(pat), info), nodes
+        # the common case (a transform's input words), without a Python tuple per wire
+        arr = np.asarray(all_nodes, dtype=np.int64)
+        negs = bytes([h.neg for h in in_bits])
+        n = len(arr)
+        if n > 1 and (np.diff(arr) > 0).all():            # distinct nodes in creation order
+            nodes, idx = all_nodes, b""
+        else:
+            _, first, inv = np.unique(arr, return_index=True, return_inverse=True)
+            order = np.argsort(first, kind="stable")
+            rank = np.empty(len(order), dtype=np.int64)
+            rank[order] = np.arange(len(order))
+            idx = rank[inv].astype(np.int32).tobytes()
+            nodes = arr[first[order]].tolist()
+        info = (tuple(map(self._level.__getitem__, nodes)), tuple(map(self._est.__getitem__, nodes)))
+        return (n, idx, negs, info), nodes
 
     def _capture(self, in_nodes, n0, op0, out_handles, nand0, exec0, wire0):
         """Template of the ops recorded since (n0, op0), or None if the call reached outside
@@ -936,11 +961,9 @@ class GpuEngine(LevelledNetlist):
         self._reclaim()                                  # (after the copy: the inputs may be dead)
         program.run(lanes)
         held = [j for j, nd in enumerate(out_real) if self._refs[nd] > 0]
-        dst = []
-        for j in held:
-            slot = self._alloc_slot()
+        dst = self._alloc_slots(len(held))
+        for j, slot in zip(held, dst):
             self._slot[out_real[j]] = slot
-            dst.append(slot)
         self._loose.extend(out_real[j] for j in held)
         self._ensure_capacity()
         if held:
