@@ -126,6 +126,10 @@ __device__ __forceinline__ void cond_add3(uint32_t word, uint32_t mask, const ui
       : "r"(word), "r"(mask), "r"(row.x), "r"(row.y), "r"(row.z));
 }
 
+// (Packing a row's three 17-bit values into 21-bit fields of one 64-bit word would make it one
+// predicate + one add with carry, but ptxas does not predicate a carry chain or a wide
+// multiply-add: it selects the operands instead, 5 instructions per (row, bit).  Not kept.)
+
 // Timeline probe (-DFHEGPU_TRACE=1 builds only, tools/probes/flow_trace.py): per gate (index <
 // FLOW_TRACE_GATES) {right wait, left wait, compute, total} in SM clocks, {operand paths taken |
 // worker << 16, globaltimer (ns, low word) after the right operand, after the left, at the end},

@@ -489,3 +489,27 @@ def test_resident_random_small_programs_equal_levels():
             assert np.array_equal(res["levels"][0], res["resident"][0])
             checked += res["resident"][1] == 1
     assert checked >= 4
+
+
+def test_flow_schedule_falls_back_outside_its_range():
+    """schedule='flow' over 2 lanes keeps the program's level launches (the warp-dataflow launch
+    serves one lane); at the default geometry the C ABI refuses the mode and says why."""
+    from paper_1611_08769_b200.errors import DeviceError
+    pname, seed, (F, f), dims, _ = FFT_CONFIGS["cfg0"]
+    scheme = GswScheme(EXACT_PARAMS)
+    keys = scheme.keygen(seed)
+    rng, vals = config_signal("cfg0")
+    eng = GpuEngine(scheme, keys=keys, batch_size=2, lane_rngs=[np.random.default_rng(7), np.random.default_rng(8)],
+                    device_encrypt=True, schedule="flow")
+    out = fft_1d(input_signal(eng, np.stack([vals, vals[::-1]]), FixedFormat(F, f)))
+    got = read_signal_ints(eng, out)
+    assert eng.last_compile["schedule"] == "flow"
+    want = model_outputs("cfg0", np.stack([vals, vals[::-1]]))
+    assert np.array_equal(got, want)
+    # default geometry: fhegpu_prog_set_flow is unsupported, loudly
+    s2 = GswScheme(DEFAULT0_PARAMS)
+    k2 = s2.keygen(1)
+    e2 = GpuEngine(s2, keys=k2, rng=np.random.default_rng(1), schedule="flow")
+    a, b = e2.input_bit(1), e2.input_bit(0)
+    with pytest.raises(DeviceError, match="k = 3, ell = 17"):
+        e2.read_back(xor_(a, b))
