@@ -133,7 +133,8 @@ __device__ __forceinline__ void cond_add3(uint32_t word, uint32_t mask, const ui
 // Timeline probe (-DFHEGPU_TRACE=1 builds only, tools/probes/flow_trace.py): per gate (index <
 // FLOW_TRACE_GATES) {right wait, left wait, compute, total} in SM clocks, {operand paths taken |
 // worker << 16, globaltimer (ns, low word) after the right operand, after the left, at the end},
-// {clock64 (low word) at the ring store, after the right operand, after the left; SM id}.
+// {clock64 (low word) at the ring store, after the right operand, at the right operand's ring
+// flag; SM id}.
 #ifndef FHEGPU_TRACE
 #define FHEGPU_TRACE 0
 #endif
@@ -154,7 +155,8 @@ __device__ __forceinline__ bool tags_newer(const uint4 &v, uint32_t tag) {
 template <int K, int ELL, int NR>
 __device__ __forceinline__ uint32_t acquire_rows(uint32_t idx, uint32_t meta, const uint32_t *store,
                                                  const uint4 *scratch, const uint4 *ring_base, uint32_t epoch,
-                                                 uint32_t ct_words, uint32_t q, int first, uint32_t (&v)[NR][K]) {
+                                                 uint32_t ct_words, uint32_t q, int first, uint32_t (&v)[NR][K],
+                                                 long long *t_flag = nullptr) {
   constexpr int ROWS = K * ELL;
   const uint32_t kind = meta & 3u;
   bool has[NR];
@@ -194,6 +196,9 @@ __device__ __forceinline__ uint32_t acquire_rows(uint32_t idx, uint32_t meta, co
           if (++spins > FHEGPU_FLOW_SPIN_LIMIT) __trap();
           continue;
         }
+#if FHEGPU_TRACE
+        if (t_flag) *t_flag = clock64();
+#endif
         bool ok = true, gone = false;
 #pragma unroll
         for (int h = 0; h < NR; ++h)                // (every load issued before the first check)
@@ -274,7 +279,13 @@ flow_kernel(uint32_t *__restrict__ store, uint4 *__restrict__ scratch, const uin
 #if FHEGPU_TRACE
     const long long t0 = clock64();
 #endif
+#if FHEGPU_TRACE
+    long long t_flag = 0;
+    const uint32_t path_r =
+        acquire_rows<K, ELL, 2>(A.y, B.y, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, b, &t_flag);
+#else
     const uint32_t path_r = acquire_rows<K, ELL, 2>(A.y, B.y, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, b);
+#endif
 #if FHEGPU_TRACE
     const long long t1 = clock64();
     uint32_t gt1;
@@ -361,7 +372,7 @@ flow_kernel(uint32_t *__restrict__ store, uint4 *__restrict__ scratch, const uin
       uint32_t *tr = g_flow_trace + FLOW_TRACE_WORDS * A.w;
       uint32_t smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      tr[8] = (uint32_t)t_ring, tr[9] = (uint32_t)t1, tr[10] = (uint32_t)t2, tr[11] = smid;
+      tr[8] = (uint32_t)t_ring, tr[9] = (uint32_t)t1, tr[10] = (uint32_t)t_flag, tr[11] = smid;
       tr[0] = (uint32_t)(t1 - t0), tr[1] = (uint32_t)(t2 - t1), tr[2] = (uint32_t)(t3 - t2);
       tr[3] = (uint32_t)(clock64() - t0);
       tr[4] = path_r | path_l << 4 | (B.y & 3u) << 8 | (B.x & 3u) << 12 | worker << 16;
@@ -384,22 +395,21 @@ struct FlowPlan {
 };
 
 // Latency model (cycles at ~1.9 GHz; measured orders of magnitude)
-// Swept on configs[0] (tools/probes/flow_timing.py, FHEGPU_FLOW_MODEL).  What the trace measures
-// (tools/probes/flow_trace.py): ~970 cycles of service per gate, ~580 for a waited-for ring hop,
-// ~2,900 through L2.  What matters far more than the constants is how much locality the greedy
-// is allowed to chase: workers run their lists in order, so a gate queued behind one whose
-// operand is late waits with it, and every gate steered to a producer's CTA lengthens those
-// queues.  Counting on the producer's last output only (ring_eff 1; the kernel still takes any
-// ring entry that is there) gives 158-165 us for every choice of the other constants, the last
-// two outputs 213-235 us, more 350-500 us, no locality at all 188 us; planned idle time after
-// each gate (pad) is worth another 4%.
+// The constants are the trace's medians (tools/probes/flow_trace.py): ~970 cycles of service per
+// gate, ~385 from a producer's ring store to a waiting consumer on the same SM holding the
+// operand, ~1,060 through L2.  The planner's structure matters more than its constants
+// (tools/probes/flow_timing.py with FHEGPU_FLOW_MODEL): workers run their lists in order, so a
+// gate queued behind one whose operand is late waits with it.  With these constants configs[0]
+// takes 151 us; with a remote hop over-estimated at 2,500 the greedy chases locality, and counting
+// on more than the producer's last ring entry then costs 213-500 us (no locality preference at
+// all: 188 us); planned idle time after each gate (pad) is worth ~3%.
 struct FlowModel {
-  double comp = 800;      // a gate on one warp, operands at hand, to its ring store
-  double remote = 2500;   // producer's scratch store -> consumer's poll sees it (through L2)
-  double local = 1000;    // the same through the CTA's shared-memory ring
+  double comp = 970;      // a gate on one warp, operands at hand, to its ring store
+  double remote = 1060;   // producer's scratch store -> consumer's poll sees it (through L2)
+  double local = 385;     // the same through the CTA's shared-memory ring
   uint32_t ring_eff = 1;  // ring entries a consumer can count on (of RING)
-  double own = 1000;      // an operand from the worker's own ring
-  double pad = 1600;      // idle time planned after every gate (slack against late operands)
+  double own = 385;       // an operand from the worker's own ring
+  double pad = 800;       // idle time planned after every gate (slack against late operands)
   FlowModel() {
     if (const char *e = std::getenv("FHEGPU_FLOW_MODEL")) {   // experiments: "comp,remote,local,ring[,own]"
       double c, r, l, o = -1, p = 0;

@@ -28,7 +28,9 @@ while time.perf_counter() < t_end:                  # sustained load first: cloc
 n = len(eng.last_compile["ops"])
 buf = np.zeros((n, 12), dtype=np.uint32)
 _native._lib.fhegpu_debug_flow_trace(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), n)
-wr, wl, comp, tot, paths, gt1, gt2, gt3, c_ring, c_r, c_l, smid = buf.T.astype(np.int64)
+if os.environ.get("FLOW_TRACE_OUT"):                # raw records for offline analysis
+    np.savez_compressed(os.environ["FLOW_TRACE_OUT"], trace=buf, deps=eng.last_compile["deps"])
+wr, wl, comp, tot, paths, gt1, gt2, gt3, c_ring, c_r, c_flag, smid = buf.T.astype(np.int64)
 worker = paths >> 16
 pr, pl = paths & 15, (paths >> 4) & 15
 kr, kl = (paths >> 8) & 3, (paths >> 12) & 3
@@ -40,7 +42,7 @@ deps = eng.last_compile["deps"]
 WPC = int(os.environ.get("FLOW_WPC", "4"))
 ghz = float(np.median((tot - wr)[gt3 > gt1] / (gt3 - gt1)[gt3 > gt1]))
 print(f"SM clock from clock64 / globaltimer: {ghz:.3f} GHz")
-for side, w, path, got, col in (("right", wr, pr, gt1, 0), ("left", wl, pl, gt2, 1)):
+for side, w, path, got, col in (("right", wr, pr, gt1, 1), ("left", wl, pl, gt2, 0)):      # deps: (left, right)
     d = deps[:, col]
     has = d >= 0
     hop = np.where(has, got - gt3[np.maximum(d, 0)], 0)            # ns, producer's end -> consumer has it
@@ -57,7 +59,7 @@ for side, w, path, got, col in (("right", wr, pr, gt1, 0), ("left", wl, pl, gt2,
                 print(f"  {side}: planned {names[k]:8s} took {names[pth]:8s}: {m.sum():6d} operands, wait median "
                       f"{np.median(w[m]):.0f} cyc")
 # same-SM hops in SM clocks (clock64 is per SM): producer's ring store -> consumer holds the operand
-for side, w, path, cgot, col in (("right", wr, pr, c_r, 0), ("left", wl, pl, c_l, 1)):
+for side, w, path, cgot, col in (("right", wr, pr, c_r, 1),):
     d = deps[:, col]
     m = (d >= 0) & (path == 2)
     dd = np.maximum(d, 0)
@@ -66,6 +68,14 @@ for side, w, path, cgot, col in (("right", wr, pr, c_r, 0), ("left", wl, pl, c_l
     hopc = np.where(hopc > 1 << 31, hopc - (1 << 32), hopc)
     waited = m & (w > hopc) & (hopc > 0)
     if waited.any():
+        det = (c_flag - c_ring[dd]) & 0xFFFFFFFF
+        det = np.where(det > 1 << 31, det - (1 << 32), det)
+        post = (cgot - c_flag) & 0xFFFFFFFF
+        print(f"  {side} ring hop split: store -> flag seen median {np.median(det[waited]):.0f} p10 {np.percentile(det[waited], 10):.0f} "
+              f"p90 {np.percentile(det[waited], 90):.0f}; flag seen -> operand held median {np.median(post[waited]):.0f} "
+              f"p90 {np.percentile(post[waited], 90):.0f}")
+        same_w = waited & (worker == worker[dd])
+        print(f"  (of these, producer on the same worker: {same_w.sum()})")
         print(f"  {side} ring hop in SM clocks (consumer already waiting): n {waited.sum()} median {np.median(hopc[waited]):.0f} "
               f"p10 {np.percentile(hopc[waited], 10):.0f} p90 {np.percentile(hopc[waited], 90):.0f}")
 print(f"span: {(gt3.max() - gt1.min()) / 1e3:.1f} us; workers used {len(np.unique(worker))}")
