@@ -156,7 +156,7 @@ template <int K, int ELL, int NR>
 __device__ __forceinline__ uint32_t acquire_rows(uint32_t idx, uint32_t meta, const uint32_t *store,
                                                  const uint4 *scratch, const uint4 *ring_base, uint32_t epoch,
                                                  uint32_t ct_words, uint32_t q, int first, uint32_t (&v)[NR][K],
-                                                 long long *t_flag = nullptr) {
+                                                 const uint4 (&pre)[NR], bool use_pre, long long *t_flag = nullptr) {
   constexpr int ROWS = K * ELL;
   const uint32_t kind = meta & 3u;
   bool has[NR];
@@ -221,9 +221,15 @@ __device__ __forceinline__ uint32_t acquire_rows(uint32_t idx, uint32_t meta, co
     } else {
       for (;;) {
         bool ok = true;
+        if (use_pre) {                              // the first poll was issued by the caller
 #pragma unroll
-        for (int h = 0; h < NR; ++h)                // (both L2 round trips in flight together)
-          if (has[h]) x[h] = ld_volatile_global_v4(g + first + 32 * h);
+          for (int h = 0; h < NR; ++h) x[h] = pre[h];
+          use_pre = false;
+        } else {
+#pragma unroll
+          for (int h = 0; h < NR; ++h)              // (both L2 round trips in flight together)
+            if (has[h]) x[h] = ld_volatile_global_v4(g + first + 32 * h);
+        }
 #pragma unroll
         for (int h = 0; h < NR; ++h) ok = ok & (!has[h] | tags_ok(x[h], epoch));
         if (__all_sync(0xffffffffu, ok)) break;
@@ -279,12 +285,38 @@ flow_kernel(uint32_t *__restrict__ store, uint4 *__restrict__ scratch, const uin
 #if FHEGPU_TRACE
     const long long t0 = clock64();
 #endif
+    // The left operand's first scratch poll (or its store rows) is requested before the right
+    // operand is waited for: when the left one arrived long ago its L2 round trip overlaps the wait
+    // instead of following it (151.1 -> 149.8 us).  Taking a left operand that is already in its
+    // ring entry before the wait as well measured slower (155.5 us).
+    const uint32_t lkind = B.x & 3u;
+    uint4 lpre[NL], nopre[2];
+    uint32_t path_l = lkind;
+    bool left_done = false;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) nopre[h] = make_uint4(0u, 0u, 0u, 0u);
+    if (lkind == K_SCRATCH) {
+#pragma unroll
+      for (int h = 0; h < NL; ++h) {
+        lpre[h] = make_uint4(0u, 0u, 0u, 0u);
+        if (first + 32 * h < ROWS) lpre[h] = ld_volatile_global_v4(scratch + (uint64_t)A.x * ROWS + first + 32 * h);
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < NL; ++h) lpre[h] = make_uint4(0u, 0u, 0u, 0u);
+      if (lkind == K_STORE || left_done) {
+        path_l = acquire_rows<K, ELL, NL>(A.x, B.x, store, scratch, s_ring, epoch, p.ct_words, p.q, first, a, lpre,
+                                          false);
+        left_done = true;
+      }
+    }
 #if FHEGPU_TRACE
     long long t_flag = 0;
     const uint32_t path_r =
-        acquire_rows<K, ELL, 2>(A.y, B.y, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, b, &t_flag);
+        acquire_rows<K, ELL, 2>(A.y, B.y, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, b, nopre, false, &t_flag);
 #else
-    const uint32_t path_r = acquire_rows<K, ELL, 2>(A.y, B.y, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, b);
+    const uint32_t path_r =
+        acquire_rows<K, ELL, 2>(A.y, B.y, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, b, nopre, false);
 #endif
 #if FHEGPU_TRACE
     const long long t1 = clock64();
@@ -294,8 +326,9 @@ flow_kernel(uint32_t *__restrict__ store, uint4 *__restrict__ scratch, const uin
     __syncwarp();                                   // the previous gate's readers are done with stage
     stage[lane] = make_uint4(b[0][0], K > 1 ? b[0][1] : 0u, K > 2 ? b[0][2] : 0u, 0u);
     if (lane + 32 < ROWS) stage[lane + 32] = make_uint4(b[1][0], K > 1 ? b[1][1] : 0u, K > 2 ? b[1][2] : 0u, 0u);
-    const uint32_t path_l =
-        acquire_rows<K, ELL, NL>(A.x, B.x, store, scratch, s_ring, epoch, p.ct_words, p.q, first, a);
+    if (!left_done)
+      path_l = acquire_rows<K, ELL, NL>(A.x, B.x, store, scratch, s_ring, epoch, p.ct_words, p.q, first, a, lpre,
+                                        lkind == K_SCRATCH);
     __syncwarp();
 #if FHEGPU_TRACE
     const long long t2 = clock64();
