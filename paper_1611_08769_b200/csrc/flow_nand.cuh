@@ -108,8 +108,11 @@ __device__ __forceinline__ void st_volatile_shared_v4(uint4 *p, const uint4 &v) 
                : "memory");
 }
 
+// Every word of a row carries `tag` above its value bits: XOR with the tag in place, OR the
+// four words, and nothing may remain above the value bits (5 instructions per row).
 __device__ __forceinline__ bool tags_ok(const uint4 &v, uint32_t tag) {
-  return ((v.x >> VBITS) == tag) & ((v.y >> VBITS) == tag) & ((v.z >> VBITS) == tag) & ((v.w >> VBITS) == tag);
+  const uint32_t e = tag << VBITS;
+  return (((v.x ^ e) | (v.y ^ e) | (v.z ^ e) | (v.w ^ e)) >> VBITS) == 0u;
 }
 
 // acc += row where word has the mask bit set: one predicate + three predicated adds (left to
@@ -199,19 +202,19 @@ __device__ __forceinline__ uint32_t acquire_rows(uint32_t idx, uint32_t meta, co
 #if FHEGPU_TRACE
         if (t_flag) *t_flag = clock64();
 #endif
-        bool ok = true, gone = false;
+        bool ok = true;
 #pragma unroll
         for (int h = 0; h < NR; ++h)                // (every load issued before the first check)
           if (has[h]) x[h] = ld_volatile_shared_v4(r + first + 32 * h);
 #pragma unroll
-        for (int h = 0; h < NR; ++h) {
-          ok = ok & (!has[h] | tags_ok(x[h], pos1));
-          gone = gone | (has[h] & tags_newer(x[h], pos1));
-        }
+        for (int h = 0; h < NR; ++h) ok = ok & (!has[h] | tags_ok(x[h], pos1));
         if (__all_sync(0xffffffffu, ok)) {
           hit = true;
           break;
         }
+        bool gone = false;                          // (off the hit path)
+#pragma unroll
+        for (int h = 0; h < NR; ++h) gone = gone | (has[h] & tags_newer(x[h], pos1));
         if (__any_sync(0xffffffffu, gone)) break;
         if (++spins > FHEGPU_FLOW_SPIN_LIMIT) __trap();
       }

@@ -54,7 +54,7 @@ for side, w, path, got, col in (("right", wr, pr, gt1, 1), ("left", wl, pl, gt2,
                   f"({np.median(hop[m]) * ghz:.0f} cyc) p10 {np.percentile(hop[m], 10):.0f} p90 {np.percentile(hop[m], 90):.0f}")
     for k in (0, 1, 2):
         for pth in (0, 1, 2):
-            m = ((kr if col == 0 else kl) == k) & (path == pth)
+            m = ((kr if side == "right" else kl) == k) & (path == pth)
             if m.any():
                 print(f"  {side}: planned {names[k]:8s} took {names[pth]:8s}: {m.sum():6d} operands, wait median "
                       f"{np.median(w[m]):.0f} cyc")
