@@ -32,11 +32,15 @@ struct GeoRF {
   using R = GeoRes<K, ELL>;
   static constexpr int CT_BYTES = R::CT_BYTES, CT_WORDS = R::CT_WORDS, B_BYTES = R::B_BYTES,
                        TA_BYTES = R::TA_BYTES;
+#ifndef FHEGPU_RF_GATE
+#define FHEGPU_RF_GATE 1     // a gate warp waits for every slot's conditions on behalf of the builders
+#endif
   static constexpr int WARP_ST = R::THREADS / 32;   // + the store warp
-  static constexpr int THREADS = R::THREADS + 32;
+  static constexpr int WARP_GATE = WARP_ST + 1;     // + the gate warp (FHEGPU_RF_GATE)
+  static constexpr int THREADS = R::THREADS + 32 + (FHEGPU_RF_GATE ? 32 : 0);
   static constexpr int N_OUT = 3;
   static constexpr int RING = (int)rf::RF_FILL_RING;
-  static constexpr int N_BARS = 8 + 3 * N_OUT + RING + 4;
+  static constexpr int N_BARS = 8 + 3 * N_OUT + RING + 4 + 2;
   __host__ __device__ static uint32_t off_b(uint32_t n_buf) { return ((n_buf * CT_BYTES + 127u) / 128u) * 128u; }
   __host__ __device__ static uint32_t off_ta(uint32_t n_buf) { return off_b(n_buf) + 2u * B_BYTES; }
   __host__ __device__ static uint32_t off_bar(uint32_t n_buf) {
@@ -150,6 +154,7 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
   uint64_t *tail_ready = bar + 8 + F::N_OUT;  // [N_OUT] tail rows of slot t written
   uint64_t *slot_free = bar + 8 + 2 * F::N_OUT + F::RING;   // [N_OUT] the store warp is done with slot t
   uint64_t *dest_ok = slot_free + F::N_OUT;   // [4] slot t's buffer may be written (store warp)
+  uint64_t *go = dest_ok + 4;                 // [2] slot t's A/B buffers are free and its operands present (gate warp)
   uint64_t *fill_full = bar + 8 + 2 * F::N_OUT;   // [RING]
   uint32_t *ctr = reinterpret_cast<uint32_t *>(bar + F::N_BARS);
   uint32_t *ctr_built = ctr, *ctr_epi = ctr + 1, *ctr_st = ctr + 2, *ctr_streq = ctr + 3;
@@ -177,6 +182,7 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
     }
     for (int i = 0; i < F::N_OUT; ++i) mbar_init(&slot_free[i], 1);
     for (int i = 0; i < 4; ++i) mbar_init(&dest_ok[i], 1);
+    for (int i = 0; i < 2; ++i) mbar_init(&go[i], FHEGPU_RF_GATE ? 2 : 1);
     for (int i = 0; i < F::RING; ++i) mbar_init(&fill_full[i], 1);
     for (int i = 0; i < 8; ++i) ctr[i] = 0;
     fence_mbar_init();
@@ -259,6 +265,33 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
       }
       bulk_wait_all();
     }
+#if FHEGPU_RF_GATE
+  } else if (warp == F::WARP_GATE) {
+    // ------------------------------ gate: every slot's start conditions, once ------------------------------
+    // The A builders pace this pipeline, and each of their waits costs ~100-250 cycles of
+    // mbarrier / counter latency even when its condition has long held (timeline: 270 + 180
+    // cycles per slot).  This warp performs the operand waits (fill barriers, epi counter) ahead
+    // of time and arrives on go[t & 1]; the builders and B copiers wait on that one barrier.  (Release/acquire chains are cumulative:
+    // what the gate observed is visible to those who observe its arrival.)
+    if (lane == 0) {
+      RFPos pos;
+      fhegpu_rf_slot nxt = rf_load_slot(slots, 0);
+      for (uint32_t t = 0; t < n_slots; ++t, pos.next(n_ops)) {
+        const uint32_t b = t & 1u, u = t >> 1;
+        const fhegpu_rf_slot si = nxt;
+        nxt = rf_load_slot(slots, pos.r + 1 == n_ops ? 0u : pos.r + 1);
+        // go[b] takes two arrivals per slot: this one (operands present) and the tail warp's
+        // after it has read the accumulator of slot t - 2 (buffers free) -- the builders wake on
+        // the tail warp's arrival itself.  Slot t - 2's phase must have completed before slot
+        // t's first arrival; slots 0 and 1 have no earlier slot: the gate arrives for it.
+        if (t >= 2) rf_mbar_wait(&go[b], (u & 1u) ^ 1u);
+        rf_operand_wait(si.lwait, pos.it, pos.base, n_fills, fill_full, ctr_epi);
+        rf_operand_wait(si.rwait, pos.it, pos.base, n_fills, fill_full, ctr_epi);
+        mbar_arrive(&go[b]);
+        if (t < 2) mbar_arrive(&go[b]);
+      }
+    }
+#endif
   } else if (warp == G::WARP_PROD) {
     // ------------------------------ producer: the plan's fills, in order ------------------------------
     // The whole warp loads the fill records 32 at a time (the next batch prefetched) and hands
@@ -368,7 +401,11 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
+#if FHEGPU_RF_GATE
+          mbar_arrive(&go[b]);                        // A(b) / B(b) free for slot t + 2
+#else
           mbar_arrive(&a_free[b]);
+#endif
           // slot t's MMAs are done, so its operand buffers were read long before (op_full):
           // publish from here -- a release on the MMA warp would sit on its issue path
           st_release_cta_smem(ctr_built, t + 1);
@@ -416,10 +453,14 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
       const fhegpu_rf_slot si = nxt;
       nxt = rf_load_slot(slots, pos.r + 1 == n_ops ? 0u : pos.r + 1);
       if (bc == 0) trace_ev(p, t, 0);
+#if FHEGPU_RF_GATE
+      rf_mbar_wait(&go[b], u & 1u);                   // B(b) free (MMAs of slot t - 2 done), operands present
+#else
       rf_mbar_wait(&a_free[b], (u & 1u) ^ 1u);        // B(b) was last read by the MMAs of slot t - 2
       rf_operand_wait(si.rwait, pos.it, pos.base, n_fills, fill_full, ctr_epi);
       if (si.lwait != rf::NONE && (si.lwait & rf::WAIT_FILL))
         rf_operand_wait(si.lwait, pos.it, pos.base, n_fills, fill_full, ctr_epi);
+#endif
       const uint32_t *v2 = buf(si.rbuf);
       const bool comp2 = si.bits & rf::SB_RNEG;
       uint8_t *bb = s_b + b * R::B_BYTES;
@@ -462,17 +503,24 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
     const int row_blk = row / ELL, row_bit = row - row_blk * ELL;
     RFPos pos;
     fhegpu_rf_slot nxt = rf_load_slot(slots, 0);
+    // (trace builds: dbg bits 8-10 pick the builder warp whose events are recorded)
+    const bool tr0 = FHEGPU_TRACE ? bt == 32 * (int)((p.dbg >> 8) & 7u) : bt == 0;
     for (uint32_t t = 0; t < n_slots; ++t, pos.next(n_ops)) {
       const uint32_t b = t & 1u, u = t >> 1;
       const fhegpu_rf_slot si = nxt;
       nxt = rf_load_slot(slots, pos.r + 1 == n_ops ? 0u : pos.r + 1);
-      if (bt == 0) trace_ev(p, t, 5);
+      if (tr0) trace_ev(p, t, 5);
+#if FHEGPU_RF_GATE
+      rf_mbar_wait(&go[b], u & 1u);
+      if (tr0) trace_ev(p, t, 7);
+#else
       rf_mbar_wait(&a_free[b], (u & 1u) ^ 1u);
-      if (bt == 0) trace_ev(p, t, 7);
+      if (tr0) trace_ev(p, t, 7);
       rf_operand_wait(si.lwait, pos.it, pos.base, n_fills, fill_full, ctr_epi);
       if (si.rwait != rf::NONE && (si.rwait & rf::WAIT_FILL))
         rf_operand_wait(si.rwait, pos.it, pos.base, n_fills, fill_full, ctr_epi);
-      if (bt == 0) trace_ev(p, t, 6);
+#endif
+      if (tr0) trace_ev(p, t, 6);
       tc_fence_after();
       const uint32_t *v1 = buf(si.lbuf);
       const bool comp1 = si.bits & rf::SB_LNEG;
@@ -505,7 +553,7 @@ regfile_tc_kernel(uint32_t *__restrict__ store, const fhegpu_rf_slot *__restrict
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&op_full[b]);
-      if (bt == 0) trace_ev(p, t, 8);
+      if (tr0) trace_ev(p, t, 8);
     }
   } else {
     // ------------------------------ epilogue, into the gate's buffer ------------------------------

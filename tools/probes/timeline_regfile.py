@@ -20,7 +20,7 @@ eng = GpuEngine(s, keys=keys, batch_size=lanes, lane_rngs=list(rngs), device_enc
 out = fft_1d(input_signal(eng, np.array(vals), FixedFormat(16, 12)))
 prog = eng.flush()
 s.ctx.sync()
-s.ctx.set_debug(16384 | (window << 20))
+s.ctx.set_debug(16384 | (window << 20) | (int(os.environ.get("RF_TRACE_BUILDER", "0")) & 7) << 8)
 prog.run(lanes)
 s.ctx.sync()
 buf = np.zeros(64 * 16, dtype=np.uint64)
