@@ -66,6 +66,8 @@ def test_reference_server_step_on_gpu_is_byte_identical(tmp_path):
     assert out.read_bytes() == open(OUT_EFT, "rb").read()
     assert eng.nand_count == golden_json("eft1_exact.json")["nand_count"]
     assert eng.launches > 0
+    # the reference's own fft_1d netlist (EXACT geometry, one signal) ran as one warp-dataflow launch
+    assert eng.last_compile["schedule"] == "flow" and eng.last_program.launches == 1
 
 
 def _stub():
