@@ -21,11 +21,11 @@
 // overwritten before (or while) a late consumer reads it fails the tag check and the consumer
 // falls back to the scratch copy, which is never overwritten within a run.
 //
-// The schedule (FlowPlanner, host side) is a list schedule over a latency model: gates in level
-// order, each appended to the worker that can start it earliest among the least loaded warp of
-// the CTAs that produced its operands and the globally earliest-free worker.  Appending in a
-// topological order makes every worker's list deadlock-free as long as all workers are
-// resident (one CTA per SM, grid <= SM count).
+// The schedule (flow_plan, host side) is a list schedule over a latency model: gates by
+// decreasing length of the chain of consumers below them, each appended to the worker that can
+// start it earliest among the least loaded warp of the CTAs that produced its operands and the
+// globally earliest-free worker.  Appending in a topological order makes every worker's list
+// deadlock-free as long as all workers are resident (one CTA per SM, grid <= SM count).
 #pragma once
 
 #include <algorithm>
@@ -475,9 +475,17 @@ inline FlowPlan flow_plan(const OpRec *ops, const int32_t *deps, uint64_t n, con
   }
   std::vector<uint32_t> order(n);
   for (uint64_t i = 0; i < n; ++i) order[i] = (uint32_t)i;
-  for (uint32_t l = 0; l < n_levels; ++l)
-    std::stable_sort(order.begin() + level_off[l], order.begin() + level_off[l + 1],
-                     [&](uint32_t x, uint32_t y) { return bl[x] > bl[y]; });
+  // Gates by decreasing length of the longest chain of consumers below them (a topological
+  // order: a producer's chain is longer than its consumers'): 145 us on configs[0] against 149 in
+  // level order with the same priority inside a level (FHEGPU_FLOW_ORDER=0).
+  const char *oe = std::getenv("FHEGPU_FLOW_ORDER");
+  if (oe && std::atoi(oe) == 0) {
+    for (uint32_t l = 0; l < n_levels; ++l)
+      std::stable_sort(order.begin() + level_off[l], order.begin() + level_off[l + 1],
+                       [&](uint32_t x, uint32_t y) { return bl[x] > bl[y]; });
+  } else {
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return bl[x] > bl[y]; });
+  }
   std::vector<double> fin(n, 0.0), free_at(W, 0.0);
   std::vector<uint32_t> wk(n, 0), pos(n, 0), cnt(W, 0);
   using QE = std::pair<double, uint32_t>;
