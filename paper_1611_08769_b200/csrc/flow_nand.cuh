@@ -62,7 +62,8 @@ constexpr uint32_t TAG_MAX = 32767u;    // tags 1..32767 (15 bits; 0 = never wri
 constexpr uint32_t MAX_GATES = 1u << 24;
 constexpr uint32_t NO_STORE = 0xFFFFFFFFu;   // out slot of a temporary (FHEGPU_OP_TEMP): no plain copy
 
-// Operand meta word: bits 0-1 kind, bit 2 complement, bits 4-7 producer's warp in the CTA,
+// Operand meta word: bits 0-1 kind, bit 2 complement, bit 3 (left operand only) acquire before the
+// right operand, bits 4-7 producer's warp in the CTA,
 // bits 8-22 producer's position + 1 in its worker's list (ring operands; <= TAG_MAX).
 enum : uint32_t { K_STORE = 0, K_SCRATCH = 1, K_RING = 2 };
 
@@ -307,11 +308,13 @@ flow_kernel(uint32_t *__restrict__ store, uint4 *__restrict__ scratch, const uin
     } else {
 #pragma unroll
       for (int h = 0; h < NL; ++h) lpre[h] = make_uint4(0u, 0u, 0u, 0u);
-      if (lkind == K_STORE || left_done) {
-        path_l = acquire_rows<K, ELL, NL>(A.x, B.x, store, scratch, s_ring, epoch, p.ct_words, p.q, first, a, lpre,
-                                          false);
-        left_done = true;
-      }
+    }
+    // meta bit 3 (planner): the left operand is expected first -- take it before waiting for the
+    // right one, so that only the later operand's own read follows its arrival
+    if (lkind == K_STORE || (B.x & 8u)) {
+      path_l = acquire_rows<K, ELL, NL>(A.x, B.x, store, scratch, s_ring, epoch, p.ct_words, p.q, first, a, lpre,
+                                        lkind == K_SCRATCH);
+      left_done = true;
     }
 #if FHEGPU_TRACE
     long long t_flag = 0;
@@ -436,16 +439,18 @@ struct FlowPlan {
 // operand, ~1,060 through L2.  The planner's structure matters more than its constants
 // (tools/probes/flow_timing.py with FHEGPU_FLOW_MODEL): workers run their lists in order, so a
 // gate queued behind one whose operand is late waits with it.  With these constants configs[0]
-// takes 151 us; with a remote hop over-estimated at 2,500 the greedy chases locality, and counting
+// took 151 us; with a remote hop over-estimated at 2,500 the greedy chases locality, and counting
 // on more than the producer's last ring entry then costs 213-500 us (no locality preference at
-// all: 188 us); planned idle time after each gate (pad) is worth ~3%.
+// all: 188 us).  Planning the gates by chain length overall (not level by level): 145 us; telling
+// the kernel which operand to take first (meta bit 3): 137 us; planned idle time after each gate
+// (pad 1,200-1,600): 132 us.
 struct FlowModel {
   double comp = 970;      // a gate on one warp, operands at hand, to its ring store
   double remote = 1060;   // producer's scratch store -> consumer's poll sees it (through L2)
   double local = 385;     // the same through the CTA's shared-memory ring
   uint32_t ring_eff = 1;  // ring entries a consumer can count on (of RING)
   double own = 385;       // an operand from the worker's own ring
-  double pad = 800;       // idle time planned after every gate (slack against late operands)
+  double pad = 1300;      // idle time planned after every gate (slack against late operands; 1,200-1,600: flat)
   FlowModel() {
     if (const char *e = std::getenv("FHEGPU_FLOW_MODEL")) {   // experiments: "comp,remote,local,ring[,own]"
       double c, r, l, o = -1, p = 0;
@@ -537,6 +542,8 @@ inline FlowPlan flow_plan(const OpRec *ops, const int32_t *deps, uint64_t n, con
     pl.worker_off[w + 1] = pl.worker_off[w] + (uint32_t)lists[w].size();
     pl.max_gates_per_worker = std::max<uint32_t>(pl.max_gates_per_worker, (uint32_t)lists[w].size());
   }
+  const char *lf = std::getenv("FHEGPU_FLOW_LEFT_FIRST");
+  const bool left_first_on = !lf || std::atoi(lf) != 0;
   pl.ents.resize(n);
   for (uint32_t w = 0; w < W; ++w) {
     for (uint32_t i = 0; i < lists[w].size(); ++i) {
@@ -560,6 +567,13 @@ inline FlowPlan flow_plan(const OpRec *ops, const int32_t *deps, uint64_t n, con
           ++(ring ? pl.ring_operands : pl.scratch_operands);
         }
       }
+      // which operand the model expects first (with the final placement)
+      double arrive[2] = {0.0, 0.0};
+      for (int s = 0; s < 2; ++s) {
+        const int32_t d = deps[2 * g + s];
+        if (d >= 0) arrive[s] = fin[d] + (wk[d] == w ? m.own : wk[d] / WARPS == w / WARPS ? m.local : m.remote);
+      }
+      if (left_first_on && arrive[0] < arrive[1]) meta[0] |= 8u;
       e.a = make_uint4(idx[0], idx[1], (ops[g].flags & FHEGPU_OP_TEMP) ? NO_STORE : ops[g].out, g);
       e.b = make_uint4(meta[0], meta[1], i + 1u, 0u);
     }
