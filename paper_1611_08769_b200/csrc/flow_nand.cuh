@@ -309,6 +309,13 @@ flow_kernel(uint32_t *__restrict__ store, uint4 *__restrict__ scratch, const uin
 #pragma unroll
       for (int h = 0; h < NL; ++h) lpre[h] = make_uint4(0u, 0u, 0u, 0u);
     }
+    // (symmetrically: the right operand's first scratch poll goes out before a left operand that
+    // is waited for first)
+    const bool rpre_on = (B.x & 8u) && (B.y & 3u) == K_SCRATCH;
+    if (rpre_on) {
+      nopre[0] = ld_volatile_global_v4(scratch + (uint64_t)A.y * ROWS + lane);
+      if (lane + 32 < ROWS) nopre[1] = ld_volatile_global_v4(scratch + (uint64_t)A.y * ROWS + lane + 32);
+    }
     // meta bit 3 (planner): the left operand is expected first -- take it before waiting for the
     // right one, so that only the later operand's own read follows its arrival
     if (lkind == K_STORE || (B.x & 8u)) {
@@ -319,10 +326,10 @@ flow_kernel(uint32_t *__restrict__ store, uint4 *__restrict__ scratch, const uin
 #if FHEGPU_TRACE
     long long t_flag = 0;
     const uint32_t path_r =
-        acquire_rows<K, ELL, 2>(A.y, B.y, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, b, nopre, false, &t_flag);
+        acquire_rows<K, ELL, 2>(A.y, B.y, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, b, nopre, rpre_on, &t_flag);
 #else
     const uint32_t path_r =
-        acquire_rows<K, ELL, 2>(A.y, B.y, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, b, nopre, false);
+        acquire_rows<K, ELL, 2>(A.y, B.y, store, scratch, s_ring, epoch, p.ct_words, p.q, lane, b, nopre, rpre_on);
 #endif
 #if FHEGPU_TRACE
     const long long t1 = clock64();
