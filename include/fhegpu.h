@@ -219,7 +219,7 @@ int fhegpu_prog_set_flow(fhegpu_ctx *ctx, fhegpu_prog *prog, int enable, double 
  * or the producing gate's index (kind 1: scratch, kind 2: ring first); meta = kind | complement
  * << 2 | producer's warp << 4 | (producer's position + 1) << 8 -- and worker_off the n_cta *
  * FHEGPU_FLOW_WARPS + 1 list boundaries. */
-#define FHEGPU_FLOW_WARPS 4
+#define FHEGPU_FLOW_WARPS 8
 #define FHEGPU_FLOW_RING 4
 int fhegpu_flow_plan(const fhegpu_op *ops, const int32_t *deps, uint64_t n_ops, const uint64_t *level_offsets,
                      uint32_t n_levels, uint32_t n_cta, uint32_t *entries, uint32_t *worker_off,

@@ -185,7 +185,7 @@ def rf_plan(gates: np.ndarray, in_slots, n_buf: int = 20, min_dist: int = 5, loo
          "reuse_r": int(stats[4])}
 
 
-FLOW_WARPS, FLOW_RING = 4, 4      # FHEGPU_FLOW_WARPS / FHEGPU_FLOW_RING (include/fhegpu.h)
+FLOW_WARPS, FLOW_RING = 8, 4      # FHEGPU_FLOW_WARPS / FHEGPU_FLOW_RING (include/fhegpu.h)
 
 
 def flow_plan(ops: np.ndarray, deps: np.ndarray, level_offsets, n_cta: int):

@@ -450,14 +450,15 @@ struct FlowPlan {
 // on more than the producer's last ring entry then costs 213-500 us (no locality preference at
 // all: 188 us).  Planning the gates by chain length overall (not level by level): 145 us; telling
 // the kernel which operand to take first (meta bit 3): 137 us; planned idle time after each gate
-// (pad 1,200-1,600): 132 us.
+// (pad 1,200-1,600): 132 us; and with that planner 8 workers per CTA instead of 4 (pad 1,600-2,000):
+// 125 us (under the locality-chasing plans 8 had been slower than 4).
 struct FlowModel {
   double comp = 970;      // a gate on one warp, operands at hand, to its ring store
   double remote = 1060;   // producer's scratch store -> consumer's poll sees it (through L2)
   double local = 385;     // the same through the CTA's shared-memory ring
   uint32_t ring_eff = 1;  // ring entries a consumer can count on (of RING)
   double own = 385;       // an operand from the worker's own ring
-  double pad = 1300;      // idle time planned after every gate (slack against late operands; 1,200-1,600: flat)
+  double pad = 1800;      // idle time planned after every gate (slack against late operands; 1,600-2,000: flat)
   FlowModel() {
     if (const char *e = std::getenv("FHEGPU_FLOW_MODEL")) {   // experiments: "comp,remote,local,ring[,own]"
       double c, r, l, o = -1, p = 0;

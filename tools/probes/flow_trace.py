@@ -39,7 +39,7 @@ print(f"gates {n}; mean per gate: wait_r {wr.mean():.0f} wait_l {wl.mean():.0f} 
 print(f"compute: median {np.median(comp):.0f} p10 {np.percentile(comp, 10):.0f} p90 {np.percentile(comp, 90):.0f}")
 print(f"service (total - waits): median {np.median(tot - wr - wl):.0f}")
 deps = eng.last_compile["deps"]
-WPC = int(os.environ.get("FLOW_WPC", "4"))
+WPC = int(os.environ.get("FLOW_WPC", "8"))
 ghz = float(np.median((tot - wr)[gt3 > gt1] / (gt3 - gt1)[gt3 > gt1]))
 print(f"SM clock from clock64 / globaltimer: {ghz:.3f} GHz")
 for side, w, path, got, col in (("right", wr, pr, gt1, 1), ("left", wl, pl, gt2, 0)):      # deps: (left, right)
