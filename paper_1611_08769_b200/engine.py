@@ -835,12 +835,19 @@ class GpuEngine(LevelledNetlist):
             tpl.out_list = oi.tolist()
             tpl.outs_list = tpl.outs.tolist()
         new = self._new_nodes(tpl.out_levels, tpl.out_ests)
-        real = dict(zip(tpl.out_list, new))
-        for i, nd in enumerate(in_nodes):
-            real[i] = nd
         self._macros.append((tpl, list(in_nodes), list(new)))
         if len(self._macros) > 1 or self._pending_ops or self._capturing:
             self._expand_macros()
+        if not hasattr(tpl, "out_fast"):              # per template, once: every output handle an
+            pos = {v: i for i, v in enumerate(tpl.out_list)}    # internal node (the usual case)
+            fast = all(kind == 1 and val in pos for kind, val, _ in tpl.outs_list)
+            tpl.out_fast = [(pos[val], neg) for _, val, neg in tpl.outs_list] if fast else None
+        if tpl.out_fast is not None:
+            n0 = new[0] if len(new) else 0
+            return [GpuBit(self, n0 + i, neg, False, None, -1) for i, neg in tpl.out_fast]
+        real = dict(zip(tpl.out_list, new))
+        for i, nd in enumerate(in_nodes):
+            real[i] = nd
         out = []
         for kind, val, neg in tpl.outs_list:
             out.append(self.constant(val) if kind == 0 else GpuBit(self, real[val], neg, False, None, -1))
@@ -874,12 +881,14 @@ class GpuEngine(LevelledNetlist):
         """Free the slots of inputs / replay outputs nobody holds any more (an ordinary compile
         releases dead nodes itself; replays only run cached programs, so they sweep here)."""
         keep = []
+        slot, refs, free, keep_all = self._slot, self._refs, self._free, self.keep_all
         for nd in self._loose:
-            if self._slot[nd] < 0:
+            sl = slot[nd]
+            if sl < 0:
                 continue
-            if self._refs[nd] <= 0 and not self.keep_all:
-                self._free.append(self._slot[nd])
-                self._slot[nd] = -1
+            if refs[nd] <= 0 and not keep_all:
+                free.append(sl)
+                slot[nd] = -1
             else:
                 keep.append(nd)
         self._loose = keep
